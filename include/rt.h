@@ -1,0 +1,183 @@
+/*
+ * rt.h — C ABI of the B200-native hot path of arXiv 1504.03151 ("Massively Parallel Ray Tracing
+ * Algorithm Using GPU"): per-pixel iterative ray tracing of spheres and planes with
+ * Lambert/Phong point-light shading, one shadow ray per light, and a stack-free
+ * reflection/refraction loop up to max_depth, written to a float RGBA framebuffer.
+ *
+ * Library: paper_1504_03151_b200/libb200rt.so (CUDA, sm_100a). No torch types cross this
+ * boundary; pointers are plain host or device pointers.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n; BJ = BASELINE.json
+ * north_star; §8 = SURVEY.md §8; R#n = DESIGN.md reading n.
+ *
+ * Conventions shared by every entry point:
+ *  - Return value: RT_OK (0) on success, a negative rt_status on error. The library never
+ *    aborts. rt_last_error() returns a message for the last failing call of the calling
+ *    thread ("prim 7: radius <= 0", cf. the ParseError line + reason of S:221).
+ *  - On error, caller-owned outputs are left untouched and library state is unchanged.
+ *  - Ownership: inputs are deep-copied during the call; the caller keeps its arrays. The
+ *    library owns device copies of the scene until the next rt_scene_upload or process exit.
+ *  - Output pointers may be host or device memory (detected with cudaPointerGetAttributes).
+ *    With a host pointer the call returns after the data is complete; with a device pointer
+ *    the call is asynchronous on the library stream (rt_set_stream).
+ *  - One context per process and current CUDA device (one rank = one process = one GPU).
+ *    Calls are not thread-safe.
+ */
+#ifndef B200_RT_H
+#define B200_RT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RT_OK = 0,
+  RT_ERR_INVALID_ARG = -1, /* a parameter or scene element violates the documented contract */
+  RT_ERR_NO_SCENE = -2,    /* rt_render* before a successful rt_scene_upload */
+  RT_ERR_NO_CAMERA = -3,   /* rt_render* before a successful rt_camera_set */
+  RT_ERR_CUDA = -4,        /* CUDA runtime error (message carries cudaGetErrorString) */
+  RT_ERR_OOM = -5,         /* device allocation failed */
+  RT_ERR_STATE = -6        /* call not valid in the current state */
+} rt_status;
+
+enum { RT_PRIM_SPHERE = 0, RT_PRIM_PLANE = 1 };
+/* Material kinds (Fig. 3). */
+enum { RT_MAT_DIFFUSE = 0, RT_MAT_SPECULAR = 1, RT_MAT_REFRACTIVE = 2 };
+
+enum {
+  RT_MAX_LIGHTS = 32,        /* point lights per scene */
+  RT_MAX_PLANES = 32,        /* planes per scene */
+  RT_MAX_SPHERES = 1 << 20,  /* spheres per scene; > RT_CONST_SPHERES uses the global-memory path */
+  RT_CONST_SPHERES = 3072,   /* spheres held in the constant bank (uniform-register operands) */
+  RT_TILE_W = 8,             /* shard tile: 8 x 4 pixels = one warp of primary rays */
+  RT_TILE_H = 4
+};
+
+/* Primitive (S:37-41 sphere; planes per BJ north_star).
+ *   type = RT_PRIM_SPHERE: p = {cx, cy, cz, radius}, radius > 0            (Eq. 9)
+ *   type = RT_PRIM_PLANE:  p = {nx, ny, nz, d}, n != 0, points x with n.x = d (normalised on
+ *                          upload; two-sided)
+ * material indexes the rt_material array. 24 bytes, 4-byte aligned. */
+typedef struct {
+  uint32_t type;
+  uint32_t material;
+  float p[4];
+} rt_primitive;
+
+/* Material (S:199-204 + reading R#3, R#8): albedo rho in [0,1]; emission L_e >= 0 (Eq. 7,
+ * P:128); ior >= 1 (REFRACTIVE); DIFFUSE adds a normalised Phong lobe
+ * ks (s+2)/(2 pi) max(0, r.wo)^s with ks in [0,1], shininess s in [1, 1e4], and mirrors
+ * with weight kr in [0,1] when kr > 0. 48 bytes. */
+typedef struct {
+  uint32_t kind;
+  float albedo[3];
+  float emission[3];
+  float ior;
+  float ks;
+  float shininess;
+  float kr;
+  float _pad;
+} rt_material;
+
+/* Point light (reading R#2): position and RGB intensity I (>= 0); irradiance I cos/d^2
+ * (Eq. 3, for a delta source). 24 bytes. */
+typedef struct {
+  float position[3];
+  float intensity[3];
+} rt_light;
+
+/* Environment (readings R#4, R#5): radiance returned by rays that miss everything, and the
+ * ambient term added as rho * ambient at DIFFUSE hits. NULL = all zero. */
+typedef struct {
+  float background[3];
+  float ambient[3];
+} rt_env;
+
+/* Ray statistics of the last rt_render / rt_render_shard / rt_assemble_tiles (BJ "rt_stats
+ * (rays_cast)"). primary + shadow + secondary = rays cast (BJ metric). sphere_tests and
+ * plane_tests are the algorithmic test counts of SURVEY §8(c).1 step 11 (closest-hit rays
+ * test every primitive; shadow rays stop at the first occluder in index order when planes
+ * precede spheres in the primitive list). last_render_ms: device time of the render kernel
+ * (CUDA events on the library stream; 0 for rt_assemble_tiles). */
+typedef struct {
+  uint64_t primary;
+  uint64_t shadow;
+  uint64_t secondary;
+  uint64_t sphere_tests;
+  uint64_t plane_tests;
+  double last_render_ms;
+} rt_ray_stats;
+
+/* Upload the scene: validates every element, normalises plane
+ * normals, packs spheres into a structure-of-arrays pair layout for the constant bank (or
+ * global memory above RT_CONST_SPHERES), planes and lights into the constant bank, materials
+ * into global memory. Replaces any previous scene. n_prims >= 0, 1 <= n_mats, 0 <= n_lights <=
+ * RT_MAX_LIGHTS. env may be NULL. Errors: RT_ERR_INVALID_ARG (message names the element),
+ * RT_ERR_OOM, RT_ERR_CUDA. */
+int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_material* mats,
+                    int32_t n_mats, const rt_light* lights, int32_t n_lights, const rt_env* env);
+
+/* Pinhole camera: forward = normalize(look_at - eye), right =
+ * normalize(forward x up), up' = right x forward; vfov in (0, 180) degrees. Requires
+ * eye != look_at and up not parallel to the view direction. */
+int rt_camera_set(const float eye[3], const float look_at[3], const float up[3], float vfov_deg);
+
+/* Render one frame: for every pixel (row-major, row 0 =
+ * top) and sample s = 0..spp-1 (stratified n x n when spp = n^2, else Hammersley, R#19):
+ * primary ray -> nearest hit over all primitives -> emission + (DIFFUSE) ambient + per-light
+ * shadow ray and Lambert/Phong term -> stack-free reflection/refraction continuation for up to
+ * max_depth secondary segments. out_rgba receives width*height float4 (R, G, B, 1) = the mean
+ * over samples summed in order s = 0..spp-1; 16 bytes per pixel, caller-owned, host or device.
+ * width, height >= 1; width*height <= 2^31-1; 0 <= max_depth <= 64; 1 <= spp <= 4096. */
+int rt_render(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba);
+
+/* Copy the statistics of the last render into *rays_cast. */
+int rt_stats(rt_ray_stats* rays_cast);
+
+/* ---- helpers (multi-GPU sharding, parity, plumbing) ---------------------------------------- */
+
+/* Bind the library to a cudaStream_t (NULL = legacy default stream). Kernels and copies are
+ * issued on it. */
+int rt_set_stream(void* cuda_stream);
+
+/* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
+int rt_set_seed(uint64_t seed);
+
+/* Message of the last failing call on this thread ("" if none). Owned by the library. */
+const char* rt_last_error(void);
+
+/* Shard layout for `world` ranks: the image is cut into RT_TILE_W x RT_TILE_H tiles; tile t
+ * belongs to rank t % world (cyclic). tiles_per_rank = ceil(n_tiles / world); slab_bytes =
+ * tiles_per_rank * 32 * 16 + 64 (pixel slab, tile-major, then a 64-byte stats record of 8
+ * uint64: primary, shadow, secondary, sphere_tests, plane_tests, 0, 0, 0). */
+int rt_shard_layout(int32_t width, int32_t height, int32_t world, int32_t* tiles_per_rank,
+                    int64_t* slab_bytes);
+
+/* Render this rank's tiles into slab_dev (device pointer, slab_bytes from rt_shard_layout).
+ * Pixels of partial edge tiles outside the image are written as 0. Tiles inside the rank are
+ * taken dynamically by persistent CTAs. The framebuffer assembled from all ranks is
+ * bit-identical to rt_render for any world size. */
+int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank,
+                    int32_t world, float* slab_dev);
+
+/* gathered_dev: world slabs back to back (e.g. the output of an NCCL all-gather / gather).
+ * Writes the row-major framebuffer to out_rgba_dev and sums the ranks' stats records into the
+ * library statistics (rt_stats). Both pointers are device pointers. */
+int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, int32_t world,
+                      float* out_rgba_dev);
+
+/* rt_render plus per-sample records for parity tests: hit_ids[((py*W+px)*spp + s)*(max_depth+1)
+ * + segment] = primitive index hit by that segment, -1 on a miss, -2 if the segment was not
+ * traced; bounces[(py*W+px)*spp + s] = number of secondary rays. Host or device pointers. */
+int rt_render_debug(int32_t width, int32_t height, int32_t max_depth, int32_t spp,
+                    float* out_rgba, int32_t* hit_ids, int32_t* bounces);
+
+/* SPEC tone_map on the device: per channel round_half_up(255 clamp(exposure v, 0,
+ * 1)^(1/gamma)), alpha = 255. rgba: n_px float4 (device); out: n_px * 4 bytes (device). */
+int rt_tonemap_rgba8(const float* rgba, uint8_t* out, int64_t n_px, float exposure, float gamma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200_RT_H */

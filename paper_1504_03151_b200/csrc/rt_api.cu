@@ -1,0 +1,496 @@
+// rt_api.cu — host runtime behind include/rt.h: validation, structure-of-arrays packing,
+// device buffers, stream binding, launches, statistics and error reporting.
+// Every computational step of the path runs in the kernels of rt_kernels.cu; this file only
+// validates, packs and launches.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rt.h"
+#include "rt_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation) return fail(RT_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+  return fail(RT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CU(call, what)                          \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+bool finite3(const float* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t reserve(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * (count ? count : 1));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+};
+
+struct Context {
+  int device = -1;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  unsigned long long seed = 0;
+  // scene
+  bool has_scene = false;
+  bool const_scene = true;
+  int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
+  float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
+  DevBuf<float4> pairs, sph_cr, stage;
+  DevBuf<int> sph_prim, sph_mat;
+  DevBuf<rt::DevMat> mats;
+  DevBuf<rt::DevLight> lights;
+  DevBuf<unsigned int> counter;
+  DevBuf<unsigned long long> stats;
+  DevBuf<int> dbg_hits, dbg_bounces;
+  // camera (double basis)
+  bool has_camera = false;
+  double eye[3], f[3], r[3], u[3], h = 0;
+  // last statistics
+  rt_ray_stats last{};
+  bool stats_pending = false, stats_timed = false;  // resolved lazily by rt_stats
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+Context g_ctx;
+
+int ensure_device() {
+  int dev = 0;
+  CU(cudaGetDevice(&dev), "cudaGetDevice");
+  if (g_ctx.device != dev) {
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    if (prop.major < 10) return fail(RT_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", dev, prop.major, prop.minor);
+    g_ctx = Context();
+    g_ctx.device = dev;
+    g_ctx.num_sms = prop.multiProcessorCount;
+    CU(cudaEventCreate(&g_ctx.ev0), "cudaEventCreate");
+    CU(cudaEventCreate(&g_ctx.ev1), "cudaEventCreate");
+    CU(g_ctx.counter.reserve(1), "cudaMalloc(counter)");
+    CU(g_ctx.stats.reserve(8), "cudaMalloc(stats)");
+  }
+  return RT_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void norm3(double* v) {
+  double l = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  v[0] /= l; v[1] /= l; v[2] /= l;
+}
+
+rt::DevParams make_params(int W, int H, int max_depth, int spp) {
+  rt::DevParams p{};
+  const Context& c = g_ctx;
+  const double aspect = (double)W / (double)H;
+  for (int i = 0; i < 3; ++i) {
+    p.eye[i] = (float)c.eye[i];
+    p.F[i] = (float)c.f[i];
+    p.R[i] = (float)(c.r[i] * c.h * aspect);
+    p.U[i] = (float)(c.u[i] * c.h);
+    p.bg[i] = c.bg[i];
+    p.amb[i] = c.amb[i];
+  }
+  p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
+  p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
+  p.seed = c.seed;
+  p.tiles_x = (W + rt::kTileW - 1) / rt::kTileW;
+  p.n_tiles = p.tiles_x * ((H + rt::kTileH - 1) / rt::kTileH);
+  return p;
+}
+
+int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
+  if (W < 1 || H < 1) return fail(RT_ERR_INVALID_ARG, "width/height must be >= 1 (got %d x %d)", W, H);
+  if ((long long)W * H > 2147483647LL) return fail(RT_ERR_INVALID_ARG, "width*height exceeds 2^31-1");
+  if (D < 0 || D > 64) return fail(RT_ERR_INVALID_ARG, "max_depth must be in [0, 64] (got %d)", D);
+  if (spp < 1 || spp > 4096) return fail(RT_ERR_INVALID_ARG, "spp must be in [1, 4096] (got %d)", spp);
+  if (!g_ctx.has_scene) return fail(RT_ERR_NO_SCENE, "no scene: call rt_scene_upload first");
+  if (!g_ctx.has_camera) return fail(RT_ERR_NO_CAMERA, "no camera: call rt_camera_set first");
+  return RT_OK;
+}
+
+int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_bounces) {
+  Context& c = g_ctx;
+  CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
+  CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
+  rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p};
+  rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces};
+  CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
+  CU(rt::launch_render(p, sc, o, c.const_scene, c.num_sms, c.stream), "render kernel launch");
+  CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
+  return RT_OK;
+}
+
+// Statistics stay on the device until rt_stats (or a host-output render) needs them, so a
+// render into a device buffer is fully asynchronous on the library stream.
+void defer_stats(bool timed) {
+  g_ctx.stats_pending = true;
+  g_ctx.stats_timed = timed;
+}
+
+int collect_stats(bool timed) {
+  Context& c = g_ctx;
+  c.stats_pending = false;
+  unsigned long long h[8];
+  CU(cudaMemcpyAsync(h, c.stats.p, sizeof h, cudaMemcpyDeviceToHost, c.stream), "stats D2H");
+  CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
+  float ms = 0.f;
+  if (timed) CU(cudaEventElapsedTime(&ms, c.ev0, c.ev1), "cudaEventElapsedTime");
+  c.last.primary = h[0];
+  c.last.shadow = h[1];
+  c.last.secondary = h[2];
+  c.last.sphere_tests = h[3];
+  c.last.plane_tests = h[4];
+  c.last.last_render_ms = ms;
+  return RT_OK;
+}
+
+int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba, int32_t* hit_ids,
+                  int32_t* bounces) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (!out_rgba) return fail(RT_ERR_INVALID_ARG, "out_rgba is NULL");
+  rc = check_frame(W, H, D, spp);
+  if (rc) return rc;
+  Context& c = g_ctx;
+  const long long npx = (long long)W * H;
+  const bool dev_out = is_device_ptr(out_rgba);
+  if (dev_out && (reinterpret_cast<uintptr_t>(out_rgba) & 15u) != 0)
+    return fail(RT_ERR_INVALID_ARG, "device out_rgba must be 16-byte aligned");
+  float4* out = reinterpret_cast<float4*>(out_rgba);
+  if (!dev_out) {
+    CU(c.stage.reserve(npx), "cudaMalloc(staging)");
+    out = c.stage.p;
+  }
+  const bool dbg = hit_ids != nullptr;
+  int* dh = nullptr;
+  int* db = nullptr;
+  const long long nsamp = npx * spp;
+  bool dev_dbg = false;
+  if (dbg) {
+    if (!bounces) return fail(RT_ERR_INVALID_ARG, "bounces is NULL");
+    dev_dbg = is_device_ptr(hit_ids) && is_device_ptr(bounces);
+    if (dev_dbg) {
+      dh = hit_ids;
+      db = bounces;
+    } else {
+      CU(c.dbg_hits.reserve(nsamp * (D + 1)), "cudaMalloc(debug)");
+      CU(c.dbg_bounces.reserve(nsamp), "cudaMalloc(debug)");
+      dh = c.dbg_hits.p;
+      db = c.dbg_bounces.p;
+    }
+  }
+  rt::DevParams p = make_params(W, H, D, spp);
+  p.mode = 0;
+  p.n_items = p.n_tiles * rt::kTilePx;
+  rc = run_render(p, out, dh, db);
+  if (rc) return rc;
+  if (!dev_out)
+    CU(cudaMemcpyAsync(out_rgba, out, sizeof(float4) * npx, cudaMemcpyDeviceToHost, c.stream), "framebuffer D2H");
+  if (dbg && !dev_dbg) {
+    CU(cudaMemcpyAsync(hit_ids, dh, sizeof(int) * nsamp * (D + 1), cudaMemcpyDeviceToHost, c.stream), "debug D2H");
+    CU(cudaMemcpyAsync(bounces, db, sizeof(int) * nsamp, cudaMemcpyDeviceToHost, c.stream), "debug D2H");
+  }
+  if (!dev_out || (dbg && !dev_dbg)) return collect_stats(true);  // host outputs: complete on return
+  defer_stats(true);
+  return RT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rt_last_error(void) { return g_err.c_str(); }
+
+int rt_set_stream(void* cuda_stream) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  g_ctx.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return RT_OK;
+}
+
+int rt_set_seed(uint64_t seed) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  g_ctx.seed = seed;
+  return RT_OK;
+}
+
+int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_material* mats, int32_t n_mats,
+                    const rt_light* lights, int32_t n_lights, const rt_env* env) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (n_prims < 0 || (n_prims > 0 && !prims)) return fail(RT_ERR_INVALID_ARG, "prims: NULL or n_prims < 0");
+  if (n_mats < 1 || !mats) return fail(RT_ERR_INVALID_ARG, "mats: need n_mats >= 1");
+  if (n_lights < 0 || n_lights > RT_MAX_LIGHTS || (n_lights > 0 && !lights))
+    return fail(RT_ERR_INVALID_ARG, "lights: need 0 <= n_lights <= %d", (int)RT_MAX_LIGHTS);
+  // validate materials
+  for (int i = 0; i < n_mats; ++i) {
+    const rt_material& m = mats[i];
+    if (m.kind > 2) return fail(RT_ERR_INVALID_ARG, "material %d: kind %u not in {0,1,2}", i, m.kind);
+    for (int k = 0; k < 3; ++k) {
+      if (!(m.albedo[k] >= 0.f && m.albedo[k] <= 1.f)) return fail(RT_ERR_INVALID_ARG, "material %d: albedo outside [0,1]", i);
+      if (!(m.emission[k] >= 0.f) || !std::isfinite(m.emission[k])) return fail(RT_ERR_INVALID_ARG, "material %d: emission must be finite and >= 0", i);
+    }
+    if (m.kind == RT_MAT_REFRACTIVE && !(m.ior >= 1.f && std::isfinite(m.ior))) return fail(RT_ERR_INVALID_ARG, "material %d: ior must be >= 1", i);
+    if (!(m.ks >= 0.f && m.ks <= 1.f)) return fail(RT_ERR_INVALID_ARG, "material %d: ks outside [0,1]", i);
+    if (!(m.shininess >= 1.f && m.shininess <= 1e4f)) return fail(RT_ERR_INVALID_ARG, "material %d: shininess outside [1,1e4]", i);
+    if (!(m.kr >= 0.f && m.kr <= 1.f)) return fail(RT_ERR_INVALID_ARG, "material %d: kr outside [0,1]", i);
+  }
+  int ns = 0, np = 0;
+  for (int i = 0; i < n_prims; ++i) {
+    const rt_primitive& q = prims[i];
+    if (q.material >= (uint32_t)n_mats) return fail(RT_ERR_INVALID_ARG, "prim %d: material %u >= n_mats %d", i, q.material, n_mats);
+    for (int k = 0; k < 4; ++k)
+      if (!std::isfinite(q.p[k])) return fail(RT_ERR_INVALID_ARG, "prim %d: non-finite parameter", i);
+    if (q.type == RT_PRIM_SPHERE) {
+      if (!(q.p[3] > 0.f)) return fail(RT_ERR_INVALID_ARG, "prim %d: radius <= 0", i);
+      ++ns;
+    } else if (q.type == RT_PRIM_PLANE) {
+      if (q.p[0] == 0.f && q.p[1] == 0.f && q.p[2] == 0.f) return fail(RT_ERR_INVALID_ARG, "prim %d: plane normal is zero", i);
+      ++np;
+    } else {
+      return fail(RT_ERR_INVALID_ARG, "prim %d: type %u not in {0 sphere, 1 plane}", i, q.type);
+    }
+  }
+  if (np > RT_MAX_PLANES) return fail(RT_ERR_INVALID_ARG, "too many planes (%d > %d)", np, (int)RT_MAX_PLANES);
+  if (ns > RT_MAX_SPHERES) return fail(RT_ERR_INVALID_ARG, "too many spheres (%d > %d)", ns, (int)RT_MAX_SPHERES);
+  for (int i = 0; i < n_lights; ++i) {
+    if (!finite3(lights[i].position)) return fail(RT_ERR_INVALID_ARG, "light %d: non-finite position", i);
+    for (int k = 0; k < 3; ++k)
+      if (!(lights[i].intensity[k] >= 0.f) || !std::isfinite(lights[i].intensity[k])) return fail(RT_ERR_INVALID_ARG, "light %d: intensity must be finite and >= 0", i);
+  }
+  if (env) {
+    for (int k = 0; k < 3; ++k)
+      if (!(env->background[k] >= 0.f && std::isfinite(env->background[k])) || !(env->ambient[k] >= 0.f && std::isfinite(env->ambient[k])))
+        return fail(RT_ERR_INVALID_ARG, "env: background/ambient must be finite and >= 0");
+  }
+
+  // pack: spheres in index order into AoSoA pairs; planes in index order
+  const int npairs = (ns + 1) / 2;
+  const int npairs_pad = ((npairs + rt::kPairsPerBatch - 1) / rt::kPairsPerBatch) * rt::kPairsPerBatch;
+  std::vector<float4> pairs(2 * (size_t)npairs_pad);
+  for (int q = 0; q < npairs_pad; ++q) {  // dummies: r^2 = -1 never intersects
+    pairs[2 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    pairs[2 * q + 1] = make_float4(0.f, 0.f, -1.f, -1.f);
+  }
+  std::vector<float4> cr(ns > 0 ? ns : 1);
+  std::vector<int> sprim(ns > 0 ? ns : 1), smat(ns > 0 ? ns : 1);
+  std::vector<rt::DevPlane> planes(np > 0 ? np : 1);
+  int ks = 0, kp = 0;
+  for (int i = 0; i < n_prims; ++i) {
+    const rt_primitive& q = prims[i];
+    if (q.type == RT_PRIM_SPHERE) {
+      const float r2 = q.p[3] * q.p[3];
+      float* A = reinterpret_cast<float*>(&pairs[2 * (ks / 2)]);
+      float* B = reinterpret_cast<float*>(&pairs[2 * (ks / 2) + 1]);
+      const int h = ks & 1;
+      A[0 + h] = q.p[0]; A[2 + h] = q.p[1]; B[0 + h] = q.p[2]; B[2 + h] = r2;
+      cr[ks] = make_float4(q.p[0], q.p[1], q.p[2], q.p[3]);
+      sprim[ks] = i;
+      smat[ks] = (int)q.material;
+      ++ks;
+    } else {
+      double n[3] = {q.p[0], q.p[1], q.p[2]};
+      const double l = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+      rt::DevPlane pl{};
+      pl.nx = (float)(n[0] / l); pl.ny = (float)(n[1] / l); pl.nz = (float)(n[2] / l);
+      pl.d = (float)((double)q.p[3] / l);
+      pl.prim = i;
+      pl.mat = (int)q.material;
+      planes[kp++] = pl;
+    }
+  }
+  std::vector<rt::DevMat> dm(n_mats);
+  for (int i = 0; i < n_mats; ++i) {
+    const rt_material& m = mats[i];
+    dm[i] = rt::DevMat{m.albedo[0], m.albedo[1], m.albedo[2], m.emission[0], m.emission[1], m.emission[2],
+                       m.ior, m.ks, m.shininess, m.kr, (int)m.kind, 0.f};
+  }
+  std::vector<rt::DevLight> dl(n_lights > 0 ? n_lights : 1);
+  for (int i = 0; i < n_lights; ++i) {
+    const rt_light& L = lights[i];
+    dl[i] = rt::DevLight{L.position[0], L.position[1], L.position[2], L.intensity[0], L.intensity[1], L.intensity[2], 0.f, 0.f};
+  }
+
+  Context& c = g_ctx;
+  CU(c.pairs.reserve(pairs.size()), "cudaMalloc(pairs)");
+  CU(c.sph_cr.reserve(cr.size()), "cudaMalloc(spheres)");
+  CU(c.sph_prim.reserve(sprim.size()), "cudaMalloc(spheres)");
+  CU(c.sph_mat.reserve(smat.size()), "cudaMalloc(spheres)");
+  CU(c.mats.reserve(dm.size()), "cudaMalloc(materials)");
+  CU(c.lights.reserve(dl.size()), "cudaMalloc(lights)");
+  CU(cudaMemcpyAsync(c.pairs.p, pairs.data(), sizeof(float4) * pairs.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaMemcpyAsync(c.sph_cr.p, cr.data(), sizeof(float4) * cr.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaMemcpyAsync(c.sph_prim.p, sprim.data(), sizeof(int) * sprim.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaMemcpyAsync(c.sph_mat.p, smat.data(), sizeof(int) * smat.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaMemcpyAsync(c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  const bool in_const = npairs_pad <= rt::kMaxConstPairs;
+  CU(rt::upload_const_scene(pairs.data(), in_const ? (int)pairs.size() : 0, planes.data(), np, c.stream), "constant upload");
+  CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
+  c.const_scene = in_const;
+  c.n_spheres = ns;
+  c.n_pairs_pad = npairs_pad;
+  c.n_planes = np;
+  c.n_lights = n_lights;
+  c.n_mats = n_mats;
+  for (int k = 0; k < 3; ++k) {
+    c.bg[k] = env ? env->background[k] : 0.f;
+    c.amb[k] = env ? env->ambient[k] : 0.f;
+  }
+  c.has_scene = true;
+  return RT_OK;
+}
+
+int rt_camera_set(const float eye[3], const float look_at[3], const float up[3], float vfov_deg) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (!eye || !look_at || !up) return fail(RT_ERR_INVALID_ARG, "camera: NULL vector");
+  if (!finite3(eye) || !finite3(look_at) || !finite3(up) || !std::isfinite(vfov_deg))
+    return fail(RT_ERR_INVALID_ARG, "camera: non-finite value");
+  if (!(vfov_deg > 0.f && vfov_deg < 180.f)) return fail(RT_ERR_INVALID_ARG, "camera: vfov must be in (0, 180)");
+  double f[3] = {(double)look_at[0] - eye[0], (double)look_at[1] - eye[1], (double)look_at[2] - eye[2]};
+  double fl = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  if (!(fl > 0.0)) return fail(RT_ERR_INVALID_ARG, "camera: eye == look_at");
+  norm3(f);
+  double u0[3] = {up[0], up[1], up[2]};
+  double r[3] = {f[1] * u0[2] - f[2] * u0[1], f[2] * u0[0] - f[0] * u0[2], f[0] * u0[1] - f[1] * u0[0]};
+  double rl = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  double ul = std::sqrt(u0[0] * u0[0] + u0[1] * u0[1] + u0[2] * u0[2]);
+  if (!(rl > 1e-12 * (ul > 0 ? ul : 1.0))) return fail(RT_ERR_INVALID_ARG, "camera: up is zero or parallel to the view direction");
+  norm3(r);
+  double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+  Context& c = g_ctx;
+  for (int k = 0; k < 3; ++k) { c.eye[k] = eye[k]; c.f[k] = f[k]; c.r[k] = r[k]; c.u[k] = u[k]; }
+  c.h = std::tan(0.5 * (double)vfov_deg * 3.14159265358979323846 / 180.0);
+  c.has_camera = true;
+  return RT_OK;
+}
+
+int rt_render(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba) {
+  g_err.clear();
+  return render_common(width, height, max_depth, spp, out_rgba, nullptr, nullptr);
+}
+
+int rt_render_debug(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba,
+                    int32_t* hit_ids, int32_t* bounces) {
+  g_err.clear();
+  if (!hit_ids || !bounces) return fail(RT_ERR_INVALID_ARG, "hit_ids/bounces must not be NULL");
+  return render_common(width, height, max_depth, spp, out_rgba, hit_ids, bounces);
+}
+
+int rt_stats(rt_ray_stats* rays_cast) {
+  g_err.clear();
+  if (!rays_cast) return fail(RT_ERR_INVALID_ARG, "rays_cast is NULL");
+  if (g_ctx.stats_pending) {
+    int rc = collect_stats(g_ctx.stats_timed);
+    if (rc) return rc;
+  }
+  *rays_cast = g_ctx.last;
+  return RT_OK;
+}
+
+int rt_shard_layout(int32_t width, int32_t height, int32_t world, int32_t* tiles_per_rank, int64_t* slab_bytes) {
+  g_err.clear();
+  if (width < 1 || height < 1 || world < 1) return fail(RT_ERR_INVALID_ARG, "shard layout: width, height, world must be >= 1");
+  const long long tiles = (long long)((width + rt::kTileW - 1) / rt::kTileW) * ((height + rt::kTileH - 1) / rt::kTileH);
+  const long long tpr = (tiles + world - 1) / world;
+  if (tiles_per_rank) *tiles_per_rank = (int32_t)tpr;
+  if (slab_bytes) *slab_bytes = tpr * rt::kTilePx * 16 + 64;
+  return RT_OK;
+}
+
+int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank, int32_t world,
+                    float* slab_dev) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world) return fail(RT_ERR_INVALID_ARG, "shard: need 0 <= rank < world");
+  if (!slab_dev || !is_device_ptr(slab_dev)) return fail(RT_ERR_INVALID_ARG, "shard: slab must be a device pointer");
+  if ((reinterpret_cast<uintptr_t>(slab_dev) & 15u) != 0) return fail(RT_ERR_INVALID_ARG, "shard: slab must be 16-byte aligned");
+  rc = check_frame(width, height, max_depth, spp);
+  if (rc) return rc;
+  int32_t tpr = 0;
+  rt_shard_layout(width, height, world, &tpr, nullptr);
+  rt::DevParams p = make_params(width, height, max_depth, spp);
+  p.mode = 1;
+  p.rank = rank;
+  p.world = world;
+  p.n_items = tpr * rt::kTilePx;
+  Context& c = g_ctx;
+  float4* slab = reinterpret_cast<float4*>(slab_dev);
+  rc = run_render(p, slab, nullptr, nullptr);
+  if (rc) return rc;
+  // stats record at the slab tail (device to device, stays on the stream)
+  CU(cudaMemcpyAsync(slab + (size_t)tpr * rt::kTilePx, c.stats.p, 64, cudaMemcpyDeviceToDevice, c.stream), "stats record");
+  defer_stats(true);
+  return RT_OK;
+}
+
+int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, int32_t world, float* out_rgba_dev) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (width < 1 || height < 1 || world < 1) return fail(RT_ERR_INVALID_ARG, "assemble: width, height, world must be >= 1");
+  if (!gathered_dev || !out_rgba_dev || !is_device_ptr(gathered_dev) || !is_device_ptr(out_rgba_dev))
+    return fail(RT_ERR_INVALID_ARG, "assemble: both pointers must be device pointers");
+  int32_t tpr = 0;
+  rt_shard_layout(width, height, world, &tpr, nullptr);
+  Context& c = g_ctx;
+  CU(rt::launch_assemble(reinterpret_cast<const float4*>(gathered_dev), width, height, world, tpr,
+                         reinterpret_cast<float4*>(out_rgba_dev), c.stats.p, c.stream), "assemble launch");
+  defer_stats(false);
+  return RT_OK;
+}
+
+int rt_tonemap_rgba8(const float* rgba, uint8_t* out, int64_t n_px, float exposure, float gamma) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (n_px < 0 || !rgba || !out) return fail(RT_ERR_INVALID_ARG, "tonemap: NULL pointer or n_px < 0");
+  if (!(exposure > 0.f) || !(gamma > 0.f)) return fail(RT_ERR_INVALID_ARG, "tonemap: exposure and gamma must be > 0");
+  if (!is_device_ptr(rgba) || !is_device_ptr(out)) return fail(RT_ERR_INVALID_ARG, "tonemap: device pointers required");
+  if (n_px == 0) return RT_OK;
+  CU(rt::launch_tonemap(reinterpret_cast<const float4*>(rgba), out, n_px, exposure, gamma, g_ctx.stream), "tonemap launch");
+  return RT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// rt_internal.h — device-side data layout shared by the host runtime (rt_api.cu) and the
+// kernels (rt_kernels.cu). Not part of the public ABI (include/rt.h).
+//
+// HBM / on-chip layout:
+//   spheres : AoSoA pairs, 32 B per pair of spheres: float4 {cxA, cxB, cyA, cyB},
+//             float4 {czA, czB, r2A, r2B}; padded with r2 = -1 dummies to a multiple of
+//             kPairsPerBatch pairs. In the constant bank (<= RT_CONST_SPHERES spheres: loads
+//             become LDCU.128 uniform-register operands of FFMA2) or in global memory.
+//   sph_cr  : float4 {cx, cy, cz, r} per sphere (shading only), global
+//   sph_prim/sph_mat : int per sphere (original primitive index / material), global
+//   planes  : DevPlane[n_planes] in the constant bank (tested before spheres)
+//   lights  : DevLight[n_lights], global (lane-divergent index in the shading code)
+//   mats    : DevMat[n_mats], global
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rt {
+
+constexpr int kWarp = 32;
+constexpr int kPairsPerBatch = 4;   // 8 spheres per unrolled batch of the intersection loop
+constexpr int kMaxConstPairs = 1536;  // 3072 spheres (48 KB of the 64 KB constant bank)
+constexpr int kMaxPlanes = 32;
+constexpr int kMaxLights = 32;
+constexpr int kTileW = 8, kTileH = 4, kTilePx = kTileW * kTileH;
+
+struct DevPlane {
+  float nx, ny, nz, d;  // unit normal, n.x = d
+  int prim, mat, pad0, pad1;
+};
+
+struct DevLight {
+  float px, py, pz, ix, iy, iz, pad0, pad1;
+};
+
+struct DevMat {
+  float ar, ag, ab;     // albedo rho
+  float er, eg, eb;     // emission L_e
+  float ior, ks, shin, kr;
+  int kind;
+  float pad;
+};
+
+struct DevParams {
+  // camera (host computes the basis in double, rounds once): d = F + (2sx-1) R + (1-2sy) U
+  float eye[3], F[3], R[3], U[3];
+  float bg[3], amb[3];
+  int W, H, max_depth, spp;
+  int n_spheres, n_pairs_pad, n_planes, n_lights;
+  unsigned long long seed;
+  // job: full frame (mode 0, tile-major work items, row-major output) or shard (mode 1)
+  int mode, rank, world, tiles_x, n_tiles, n_items;
+};
+
+struct DevScene {
+  const float4* pairs;     // global copy of the pair layout (used when not in the constant bank)
+  const float4* sph_cr;
+  const int* sph_prim;
+  const int* sph_mat;
+  const DevMat* mats;
+  const DevLight* lights;
+};
+
+struct DevOutputs {
+  float4* out;                  // framebuffer (mode 0) or slab (mode 1)
+  unsigned int* work_counter;   // persistent work queue head
+  unsigned long long* stats;    // [5] primary, shadow, secondary, sphere_tests, plane_tests
+  int* dbg_hits;                // optional [n_px * spp * (max_depth+1)]
+  int* dbg_bounces;             // optional [n_px * spp]
+};
+
+// launchers (rt_kernels.cu)
+cudaError_t upload_const_scene(const float4* pairs, int n_pair_float4, const DevPlane* planes,
+                               int n_planes, cudaStream_t st);
+cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
+                          bool const_scene, int num_sms, cudaStream_t st);
+cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
+                            float4* out, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,
+                           float gamma, cudaStream_t st);
+int render_blocks_per_sm(bool const_scene, bool debug);
+
+}  // namespace rt

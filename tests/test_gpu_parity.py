@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Rule: tests/parity.py. Full frames where the oracle finishes in
+seconds; at BASELINE.json's full sizes (C3, C4) the GPU renders the whole frame in the bench's
+launch configuration and the oracle computes a seeded sample of pixels one by one.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import scenegen
+from tests import parity
+from tests.gpu_helpers import gpu_render
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1504_03151_b200 import build
+    build.build()
+    yield
+
+
+def _check(oracle_lib, sc, pixels=None, label=""):
+    g = gpu_render(sc)
+    ref = oracle_lib.render(sc, pixels=pixels)
+    pix = ref.pixels
+    cls = parity.classify(oracle_lib, sc, ref, pixels if pixels is not None else None)
+    rep = parity.compare(g["rgb"][pix], g["ids"][pix], g["bounces"][pix], ref, cls)
+    print(f"[{label or sc.name}] {rep}")
+    assert rep.ok, f"{label or sc.name}: {rep}"
+    if pixels is None:
+        ok, msg = parity.ray_budget_ok(g["stats"], ref.counts, ref, cls, sc.n_lights)
+        print(f"[{label or sc.name}] rays: {msg}")
+        assert ok, msg
+    return g, ref, rep
+
+
+def test_c1_full_frame(oracle_lib):
+    _check(oracle_lib, scenegen.get("C1"))
+
+
+def test_c2_full_frame(oracle_lib):
+    _check(oracle_lib, scenegen.get("C2"))
+
+
+def test_c2_ragged_deeper_supersampled(oracle_lib):
+    # ragged against 8x4 tiles, non-square spp (Hammersley), deeper bounces
+    sc = scenegen.get("C2").with_frame(width=67, height=45, max_depth=6, spp=3)
+    _check(oracle_lib, sc, label="C2-ragged")
+
+
+@pytest.mark.parametrize("seed,W,H,D,spp", [(0, 13, 7, 3, 1), (1, 9, 9, 6, 4), (2, 17, 5, 0, 2),
+                                            (3, 8, 4, 2, 5), (4, 31, 3, 5, 9), (5, 1, 1, 4, 16)])
+def test_tiny_random_scenes(oracle_lib, seed, W, H, D, spp):
+    sc = scenegen.random_tiny(seed, n_spheres=7, n_planes=2, n_lights=3, width=W, height=H, max_depth=D, spp=spp)
+    _check(oracle_lib, sc, label=f"tiny{seed}")
+
+
+def test_c3_full_size_sampled(oracle_lib):
+    sc = scenegen.get("C3")
+    pix = np.random.default_rng(33).choice(sc.width * sc.height, 6000, replace=False)
+    _check(oracle_lib, sc, pixels=pix, label="C3@1080p")
+
+
+def test_c4_full_size_sampled(oracle_lib):
+    sc = scenegen.get("C4")
+    pix = np.random.default_rng(44).choice(sc.width * sc.height, 3000, replace=False)
+    _check(oracle_lib, sc, pixels=pix, label="C4@1080p")
+
+
+def test_c4_full_size_counts_consistent(oracle_lib):
+    # rays-per-pixel statistics of the full-size GPU frame agree with the oracle sample
+    sc = scenegen.get("C4")
+    g = gpu_render(sc, debug=False)
+    st = g["stats"]
+    assert st["primary"] == sc.width * sc.height * sc.spp
+    pix = np.random.default_rng(45).choice(sc.width * sc.height, 3000, replace=False)
+    ref = oracle_lib.render(sc, pixels=pix)
+    for k in ("shadow", "secondary", "sphere_tests"):
+        gpu_rate = st[k] / st["primary"]
+        orc_rate = ref.counts[k] / ref.counts["primary"]
+        assert gpu_rate == pytest.approx(orc_rate, rel=0.1), k
+
+
+def test_worked_examples_on_gpu():
+    # W1, W2, W4 closed forms (tests/golden/worked_examples.json) through the CUDA path
+    b = scenegen.builder()
+    b.sphere((0, 0, 5), 1.0, b.material(scenegen.DIFFUSE, (0.5, 0.5, 0.5)))
+    b.light((0, 0, 0), (16 * math.pi,) * 3)
+    sc = b.build("W1", eye=(0, 0, 0), look_at=(0, 0, 1), up=(0, 1, 0), vfov=60, width=1, height=1,
+                 max_depth=0, spp=1, ambient=(0.1,) * 3)
+    g = gpu_render(sc)
+    assert g["rgb"][0] == pytest.approx([0.55] * 3, rel=2e-6)
+    assert g["stats"]["shadow"] == 1
+    for D in (0, 1, 3, 5, 8):
+        b = scenegen.builder()
+        m = b.material(scenegen.SPECULAR, (0.5, 0.5, 0.5), emission=(1, 1, 1))
+        b.plane((0, 0, 1), 0.0, m)
+        b.plane((0, 0, 1), 10.0, m)
+        sc = b.build("W4", eye=(0, 0, 5), look_at=(0, 0, 6), up=(0, 1, 0), vfov=30, width=1, height=1,
+                     max_depth=D, spp=1)
+        g = gpu_render(sc)
+        assert g["rgb"][0, 0] == 2 - 0.5 ** D  # exact in float32 too
+        assert g["bounces"][0, 0] == D
+
+
+def test_empty_and_planes_only_scenes(oracle_lib):
+    b = scenegen.builder()
+    b.material(scenegen.DIFFUSE, (0.5, 0.5, 0.5))
+    sc = b.build("empty", eye=(0, 0, 0), look_at=(0, 0, 1), up=(0, 1, 0), vfov=60, width=19, height=6,
+                 max_depth=3, spp=2, background=(0.25, 0.5, 0.125))
+    g = gpu_render(sc)
+    assert (g["rgb"] == np.array([0.25, 0.5, 0.125], np.float32)).all()
+    assert (g["rgba"][:, 3] == 1.0).all()
+    assert g["stats"]["primary"] == 19 * 6 * 2 and g["stats"]["secondary"] == 0
+    b = scenegen.builder()
+    b.plane((0, 1, 0), 0.0, b.material(scenegen.DIFFUSE, (0.6, 0.6, 0.6), kr=0.5))
+    b.plane((0, -1, 0), -6.0, b.material(scenegen.SPECULAR, (0.8, 0.8, 0.8)))
+    b.light((0, 3, 4), (50, 50, 50))
+    sc = b.build("planes", eye=(0, 1, -5), look_at=(0, 1, 0), up=(0, 1, 0), vfov=70, width=24, height=20,
+                 max_depth=4, spp=1, background=(0.1, 0.1, 0.1), ambient=(0.05, 0.05, 0.05))
+    _check(oracle_lib, sc, label="planes-only")
+
+
+def test_host_and_device_outputs_identical():
+    import torch
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get("C2")
+    rt.load_scene(sc)
+    dev = torch.empty((sc.height, sc.width, 4), dtype=torch.float32, device="cuda")
+    rt.render(sc.width, sc.height, sc.max_depth, sc.spp, dev)
+    host = np.empty((sc.height, sc.width, 4), np.float32)
+    rt.render(sc.width, sc.height, sc.max_depth, sc.spp, host)
+    torch.cuda.synchronize()
+    assert (dev.cpu().numpy().view(np.uint32) == host.view(np.uint32)).all()
+    again = torch.empty_like(dev)
+    rt.render(sc.width, sc.height, sc.max_depth, sc.spp, again)
+    assert torch.equal(again, dev)  # deterministic
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shards_assemble_bit_identical(world):
+    # SURVEY §4 level (i): every rank's shard rendered on one GPU, gathered by concatenation
+    import torch
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get("C2").with_frame(width=203, height=117, spp=2)
+    rt.load_scene(sc)
+    W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
+    full = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
+    rt.render(W, H, D, S, full)
+    ref_stats = rt.stats()
+    tpr, sb = rt.shard_layout(W, H, world)
+    gathered = torch.zeros(world * sb, dtype=torch.uint8, device="cuda")
+    for r in range(world):
+        rt.render_shard(W, H, D, S, r, world, gathered[r * sb:(r + 1) * sb])
+    out = torch.empty_like(full)
+    rt.assemble_tiles(gathered, W, H, world, out)
+    st = rt.stats()
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+    for k in ("primary", "shadow", "secondary", "sphere_tests", "plane_tests"):
+        assert st[k] == ref_stats[k], k
+
+
+def test_tonemap_kernel_matches_spec():
+    import torch
+    from paper_1504_03151_b200 import rt
+    v = np.random.default_rng(0).uniform(-0.2, 1.3, (1000, 4)).astype(np.float32)
+    v[:5, 0] = [0.0, 0.5, 1.0, 2.0, -1.0]
+    dev = torch.from_numpy(v).cuda()
+    out = torch.empty((1000, 4), dtype=torch.uint8, device="cuda")
+    rt.tonemap_rgba8(dev, out)
+    got = out.cpu().numpy()
+    want = parity.tonemap8(v[:, :3])
+    assert (got[:, :3] == want).all() and (got[:, 3] == 255).all()
+    assert list(got[:5, 0]) == [0, 186, 255, 255, 0]
+
+
+def test_validation_errors():
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get("C1")
+    prims, mats, lights, env = rt.pack_scene(sc)
+    bad = prims.copy()
+    bad["p"][2, 3] = -1.0
+    with pytest.raises(rt.RtError) as e:
+        rt.scene_upload(bad, mats, lights, env)
+    assert e.value.code == -1 and "prim 2" in e.value.msg and "radius" in e.value.msg
+    bad = prims.copy()
+    bad["material"][1] = 99
+    with pytest.raises(rt.RtError) as e:
+        rt.scene_upload(bad, mats, lights, env)
+    assert "prim 1" in e.value.msg
+    badm = mats.copy()
+    badm["albedo"][0, 1] = 1.5
+    with pytest.raises(rt.RtError) as e:
+        rt.scene_upload(prims, badm, lights, env)
+    assert "material 0" in e.value.msg
+    with pytest.raises(rt.RtError) as e:
+        rt.camera_set((0, 0, 0), (0, 0, 0), (0, 1, 0), 60)
+    assert e.value.code == -1
+    with pytest.raises(rt.RtError) as e:
+        rt.camera_set((0, 0, 0), (0, 1, 0), (0, 1, 0), 60)  # up parallel to view
+    with pytest.raises(rt.RtError) as e:
+        rt.camera_set((0, 0, 0), (0, 0, 1), (0, 1, 0), 180)
+    rt.load_scene(sc)
+    import torch
+    out = torch.empty((4, 4, 4), dtype=torch.float32, device="cuda")
+    with pytest.raises(rt.RtError) as e:
+        rt.render(4, 4, -1, 1, out)
+    assert e.value.code == -1
+    with pytest.raises(rt.RtError):
+        rt.render(0, 4, 1, 1, out)
+    with pytest.raises(rt.RtError):
+        rt.render(4, 4, 1, 0, out)
+    with pytest.raises(rt.RtError):
+        rt.render_shard(4, 4, 1, 1, 2, 2, out)  # rank >= world
+    # state is unchanged after errors: a valid render still works
+    rt.render(4, 4, 1, 1, out)
