@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ray-tracing hot path (arXiv 1504.03151) — prints ONE JSON line.
+
+Metric (BASELINE.json): "Mrays/s (primary+shadow+secondary) and fps at 1080p depth 5, 1/2/4/8
+B200". Workload: config C4 (BJ:10) — 1920x1080, 1000 random spheres, 8 point lights,
+max_depth 5, 4 spp, tile-sharded across N GPUs (one process per GPU, NCCL all-gather of the
+tile slabs to rank 0, which assembles the frame). A step = one full frame.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C4]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: W untimed warm-up frames; K timed frames bracketed by barrier + synchronize; each frame
+timed with CUDA events on the launch stream; L2 (126 MB) is flushed with a 256 MiB write before
+every frame, outside the per-frame events; value = rays of all ranks / max-over-ranks time.
+`--impl reference` times the CPU oracle (the plain C reference written from the paper) on the
+host cores with the same metric, on a bounded pixel sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import scenegen  # noqa: E402
+
+METRIC = "Mrays/s (primary+shadow+secondary) and fps at 1080p depth 5, 1/2/4/8 B200"
+FLOP_SPHERE, FLOP_PLANE = 19, 12   # SURVEY.md §8(d).3 counted flops per test
+PEAK_FALLBACK_MHZ = 1965.0
+
+
+# ---------------------------------------------------------------------------------------------
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int, period_ms: int = 50):
+        self.idx, self.period, self.proc, self.lines = gpu_index, period_ms, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 f"-lms", str(self.period), "-i", str(self.idx)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _load_profile_traffic(workload: str):
+    """dram bytes per launch of the render kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_render_kernel.json")
+    try:
+        d = json.load(open(path))
+        ent = d.get(workload)
+        if ent and ent.get("dram_bytes_per_launch"):
+            return float(ent["dram_bytes_per_launch"])
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------------------------
+_SCENES = {}
+
+
+def _oracle_chunk(args):
+    """Worker: oracle on a slice of pixels (runs in a separate process; scene cached)."""
+    name, pixels = args
+    from oracle import pyoracle as po
+    if name not in _SCENES:
+        _SCENES[name] = scenegen.get(name)
+    sc = _SCENES[name]
+    _, counts = po.render_rgb_only(sc, pixels=np.asarray(pixels, np.int64))
+    return counts
+
+
+class OracleTimer:
+    """The CPU oracle, as it stands, on all host cores (pixel slices across processes)."""
+
+    def __init__(self, name: str):
+        import concurrent.futures as cf
+        from oracle import pyoracle as po
+        po.build()
+        self.name = name
+        self.cores = os.cpu_count() or 1
+        self.pool = cf.ProcessPoolExecutor(max_workers=self.cores)
+        list(self.pool.map(_oracle_chunk, [(name, [0])] * self.cores))  # warm the workers
+
+    def run(self, pixels: np.ndarray) -> tuple[float, dict]:
+        chunks = [(self.name, c.tolist()) for c in np.array_split(pixels, self.cores) if len(c)]
+        t0 = time.perf_counter()
+        res = list(self.pool.map(_oracle_chunk, chunks))
+        dt = time.perf_counter() - t0
+        tot = {k: sum(r[k] for r in res) for k in res[0]}
+        return dt, tot
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def cpu_baseline(name: str, target_core_s: float = 20.0, seed: int = 7) -> dict:
+    sc = scenegen.get(name)
+    tm = OracleTimer(name)
+    rng = np.random.default_rng(seed)
+    # calibrate: per-pixel cost on a small sample, then size the sample to ~target_core_s
+    probe = rng.choice(sc.width * sc.height, 64 * tm.cores, replace=False)
+    dt, _ = tm.run(probe)
+    per_px_core = dt * tm.cores / len(probe)
+    n = int(min(sc.width * sc.height, max(len(probe), target_core_s / max(per_px_core, 1e-9))))
+    pix = rng.choice(sc.width * sc.height, n, replace=False)
+    dt, cnt = tm.run(pix)
+    tm.close()
+    rays = cnt["primary"] + cnt["shadow"] + cnt["secondary"]
+    frac = n / (sc.width * sc.height)
+    return {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": tm.cores, "kind": "oracle",
+            "sample": f"{n} random pixels of {name} (all {sc.spp} spp, depth {sc.max_depth}) = {frac:.2%} of the frame, "
+                      f"{dt:.1f} s wall on {tm.cores} processes",
+            "fps_extrapolated": 1.0 / (dt / frac)}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    name = args.config
+    sc = scenegen.get(name)
+    tm = OracleTimer(name)
+    rng = np.random.default_rng(11)
+    n_px = args.ref_pixels
+    for _ in range(args.warmup):
+        tm.run(rng.choice(sc.width * sc.height, n_px, replace=False))
+    tot_t, tot_rays = 0.0, 0
+    for _ in range(args.steps):
+        dt, cnt = tm.run(rng.choice(sc.width * sc.height, n_px, replace=False))
+        tot_t += dt
+        tot_rays += cnt["primary"] + cnt["shadow"] + cnt["secondary"]
+    tm.close()
+    value = tot_rays / tot_t / 1e6
+    frac = n_px / (sc.width * sc.height)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "fps": 1.0 / (tot_t / args.steps / frac),
+        "config": dict(sc.describe(), workload=name, sample_pixels_per_step=n_px),
+        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": tm.cores, "kind": "oracle",
+                         "sample": f"{n_px} random pixels of {name} per step ({frac:.3%} of the frame)"},
+        "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1504_03151_b200 import build as rtbuild
+    from paper_1504_03151_b200 import rt
+    from paper_1504_03151_b200.multigpu import CudaBackend, ShardedRenderer
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    rtbuild.build()  # no-op when the in-tree library is current
+    stream = torch.cuda.current_stream()
+    rt.set_stream(stream)
+
+    sc = scenegen.get(args.config)
+    W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
+    prims, mats, lights, env = rt.pack_scene(sc)
+    rt.load_scene(sc)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    if world > 1:
+        rend = ShardedRenderer(CudaBackend(dev), W, H, D, S)
+        step = rend.render
+        launches_per_step = rend.launches_per_frame
+    else:
+        out = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
+        step = lambda: rt.render(W, H, D, S, out)  # noqa: E731
+        launches_per_step = 1
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3 if args.strict else 0)):
+        flush.zero_()
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    t_wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()                       # L2 flush, outside the frame events
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    barrier()
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    frame_ms = [a.elapsed_time(b) for a, b in evs]
+    my_total = sum(frame_ms)
+    st = rt.stats()  # last frame (rank 0 holds the all-rank sum after assembly)
+    t = torch.tensor([my_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+
+    # e2e: the public C-ABI call with host buffers, H2D of the step's inputs and D2H of the frame
+    e2e = None
+    if world == 1 and rank == 0:
+        host_out = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
+        h2d = prims.nbytes + mats.nbytes + lights.nbytes + env.nbytes
+        d2h = host_out.numel() * 4 + 64
+        ke = max(3, min(args.steps, 20))
+        rt.scene_upload(prims, mats, lights, env)
+        rt.render(W, H, D, S, host_out)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rays_e2e = 0
+        for _ in range(ke):
+            rt.scene_upload(prims, mats, lights, env)
+            rt.camera_set(sc.eye, sc.look_at, sc.up, sc.vfov)
+            rt.render(W, H, D, S, host_out)   # host pointer: returns after the D2H copy
+            s2 = rt.stats()
+            rays_e2e += s2["primary"] + s2["shadow"] + s2["secondary"]
+        dt = time.perf_counter() - t0
+        e2e = {"value": rays_e2e / dt / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": ke, "ms_per_step": 1e3 * dt / ke,
+               "timing": "host wall clock around rt_scene_upload + rt_camera_set + rt_render(host buffer)"}
+
+    if rank == 0:
+        rays = st["primary"] + st["shadow"] + st["secondary"]
+        ms_per_step = total_ms / args.steps
+        value = rays / (ms_per_step * 1e-3) / 1e6
+        # roofline: counted algorithmic flops of the render kernel per launch / its event time
+        flops = FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"]
+        props = torch.cuda.get_device_properties(dev)
+        sms = props.multi_processor_count
+        sm_max = clk.get("sm_max_mhz") or PEAK_FALLBACK_MHZ
+        peak = sms * 128 * 2 * sm_max * 1e6 / 1e12
+        # N=1: the frame events bracket exactly the render kernel (+2 tiny memsets); N>1: the
+        # per-rank share of the flops over the frame time (includes the all-gather + assembly)
+        achieved = flops / world / (ms_per_step * 1e-3) / 1e12
+        traffic = _load_profile_traffic(args.config) if world == 1 else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (FFMA2 filter) + f64 (candidate refinement, shading geometry)",
+            "data": "synthetic (seeded scenegen C4 scene; no dataset)",
+            "fps": 1e3 / ms_per_step,
+            "config": dict(sc.describe(), workload=args.config, parallelism=f"tiles{world}",
+                           l2="flushed (256 MiB write) before every frame, outside the frame events",
+                           rays_per_frame=int(rays), primary=int(st["primary"]), shadow=int(st["shadow"]),
+                           secondary=int(st["secondary"]), sphere_tests=int(st["sphere_tests"]),
+                           plane_tests=int(st["plane_tests"]), wall_s=t_wall),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "render_kernel (persistent megakernel)",
+                         "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (derived, DESIGN.md)",
+                         "flops_basis": "19 flops/sphere test + 12/plane test (SURVEY 8(d).3) x algorithmic test counts"},
+            "clocks": clk,
+            "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.config, target_core_s=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", default="C4", choices=sorted(scenegen.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="core-seconds of oracle work")
+    ap.add_argument("--ref-pixels", type=int, default=1024, help="--impl reference: pixels per step")
+    ap.add_argument("--strict", action="store_true", default=True)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

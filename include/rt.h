@@ -48,8 +48,8 @@ enum { RT_MAT_DIFFUSE = 0, RT_MAT_SPECULAR = 1, RT_MAT_REFRACTIVE = 2 };
 enum {
   RT_MAX_LIGHTS = 32,        /* point lights per scene */
   RT_MAX_PLANES = 32,        /* planes per scene */
-  RT_MAX_SPHERES = 1 << 20,  /* spheres per scene; > RT_CONST_SPHERES uses the global-memory path */
-  RT_CONST_SPHERES = 3072,   /* spheres held in the constant bank (uniform-register operands) */
+  RT_MAX_SPHERES = 1 << 20,  /* spheres per scene; > RT_SMEM_SPHERES uses the global-memory path */
+  RT_SMEM_SPHERES = 10240,   /* spheres staged per CTA in shared memory (TMA bulk copy, 160 KB) */
   RT_TILE_W = 8,             /* shard tile: 8 x 4 pixels = one warp of primary rays */
   RT_TILE_H = 4
 };
@@ -110,10 +110,10 @@ typedef struct {
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane
- * normals, packs spheres into a structure-of-arrays pair layout for the constant bank (or
- * global memory above RT_CONST_SPHERES), planes and lights into the constant bank, materials
- * into global memory. Replaces any previous scene. n_prims >= 0, 1 <= n_mats, 0 <= n_lights <=
- * RT_MAX_LIGHTS. env may be NULL. Errors: RT_ERR_INVALID_ARG (message names the element),
+ * normals, packs spheres into a structure-of-arrays pair layout in device memory (each render
+ * CTA stages it into shared memory with a TMA bulk copy up to RT_SMEM_SPHERES spheres), planes
+ * into the constant bank, materials and lights into global memory. Replaces any previous
+ * scene. n_prims >= 0, 1 <= n_mats, 0 <= n_lights <= RT_MAX_LIGHTS. env may be NULL. Errors: RT_ERR_INVALID_ARG (message names the element),
  * RT_ERR_OOM, RT_ERR_CUDA. */
 int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_material* mats,
                     int32_t n_mats, const rt_light* lights, int32_t n_lights, const rt_env* env);

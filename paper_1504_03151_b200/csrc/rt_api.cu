@@ -64,8 +64,9 @@ struct Context {
   unsigned long long seed = 0;
   // scene
   bool has_scene = false;
-  bool const_scene = true;
+  bool smem_scene = true;
   int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
+  float cmax = 0.f, rmax = 0.f;
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage;
   DevBuf<int> sph_prim, sph_mat;
@@ -119,13 +120,15 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   const Context& c = g_ctx;
   const double aspect = (double)W / (double)H;
   for (int i = 0; i < 3; ++i) {
-    p.eye[i] = (float)c.eye[i];
-    p.F[i] = (float)c.f[i];
-    p.R[i] = (float)(c.r[i] * c.h * aspect);
-    p.U[i] = (float)(c.u[i] * c.h);
+    p.eye[i] = c.eye[i];
+    p.F[i] = c.f[i];
+    p.R[i] = c.r[i] * c.h * aspect;
+    p.U[i] = c.u[i] * c.h;
     p.bg[i] = c.bg[i];
     p.amb[i] = c.amb[i];
   }
+  p.cmax = c.cmax;
+  p.rmax = c.rmax;
   p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
   p.seed = c.seed;
@@ -151,7 +154,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p};
   rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces};
   CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
-  CU(rt::launch_render(p, sc, o, c.const_scene, c.num_sms, c.stream), "render kernel launch");
+  CU(rt::launch_render(p, sc, o, c.smem_scene, c.num_sms, c.stream), "render kernel launch");
   CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
   return RT_OK;
 }
@@ -314,9 +317,13 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   std::vector<int> sprim(ns > 0 ? ns : 1), smat(ns > 0 ? ns : 1);
   std::vector<rt::DevPlane> planes(np > 0 ? np : 1);
   int ks = 0, kp = 0;
+  double cmax = 0.0, rmax = 0.0;
   for (int i = 0; i < n_prims; ++i) {
     const rt_primitive& q = prims[i];
     if (q.type == RT_PRIM_SPHERE) {
+      const double cn = std::fabs((double)q.p[0]) + std::fabs((double)q.p[1]) + std::fabs((double)q.p[2]);
+      if (cn > cmax) cmax = cn;
+      if (q.p[3] > rmax) rmax = q.p[3];
       const float r2 = q.p[3] * q.p[3];
       float* A = reinterpret_cast<float*>(&pairs[2 * (ks / 2)]);
       float* B = reinterpret_cast<float*>(&pairs[2 * (ks / 2) + 1]);
@@ -330,8 +337,8 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
       double n[3] = {q.p[0], q.p[1], q.p[2]};
       const double l = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
       rt::DevPlane pl{};
-      pl.nx = (float)(n[0] / l); pl.ny = (float)(n[1] / l); pl.nz = (float)(n[2] / l);
-      pl.d = (float)((double)q.p[3] / l);
+      pl.nx = n[0] / l; pl.ny = n[1] / l; pl.nz = n[2] / l;
+      pl.d = (double)q.p[3] / l;
       pl.prim = i;
       pl.mat = (int)q.material;
       planes[kp++] = pl;
@@ -362,10 +369,12 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(cudaMemcpyAsync(c.sph_mat.p, smat.data(), sizeof(int) * smat.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  const bool in_const = npairs_pad <= rt::kMaxConstPairs;
-  CU(rt::upload_const_scene(pairs.data(), in_const ? (int)pairs.size() : 0, planes.data(), np, c.stream), "constant upload");
+  const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
+  CU(rt::upload_const_scene(planes.data(), np, c.stream), "constant upload");
   CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
-  c.const_scene = in_const;
+  c.smem_scene = in_smem;
+  c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
+  c.rmax = (float)(rmax * (1.0 + 1e-6));
   c.n_spheres = ns;
   c.n_pairs_pad = npairs_pad;
   c.n_planes = np;

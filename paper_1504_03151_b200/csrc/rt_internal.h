@@ -4,13 +4,18 @@
 // HBM / on-chip layout:
 //   spheres : AoSoA pairs, 32 B per pair of spheres: float4 {cxA, cxB, cyA, cyB},
 //             float4 {czA, czB, r2A, r2B}; padded with r2 = -1 dummies to a multiple of
-//             kPairsPerBatch pairs. In the constant bank (<= RT_CONST_SPHERES spheres: loads
-//             become LDCU.128 uniform-register operands of FFMA2) or in global memory.
+//             kPairsPerBatch pairs. Global memory; staged per CTA into shared memory with one
+//             TMA bulk copy when <= kMaxSmemPairs pairs (warp-uniform LDS.128 broadcasts),
+//             else read from global memory.
 //   sph_cr  : float4 {cx, cy, cz, r} per sphere (shading only), global
 //   sph_prim/sph_mat : int per sphere (original primitive index / material), global
-//   planes  : DevPlane[n_planes] in the constant bank (tested before spheres)
+//   planes  : DevPlane[n_planes] (double) in the constant bank (tested before spheres)
 //   lights  : DevLight[n_lights], global (lane-divergent index in the shading code)
 //   mats    : DevMat[n_mats], global
+//
+// Precision split: the sphere scan is a conservative float32 filter
+// (FFMA2, two spheres per instruction) whose candidates are re-decided in float64 from the exact
+// float inputs; rays, hit points, normals, shadow-ray set-up and the bounce are float64.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -19,13 +24,13 @@ namespace rt {
 
 constexpr int kWarp = 32;
 constexpr int kPairsPerBatch = 4;   // 8 spheres per unrolled batch of the intersection loop
-constexpr int kMaxConstPairs = 1536;  // 3072 spheres (48 KB of the 64 KB constant bank)
+constexpr int kMaxSmemPairs = 5120;  // 10240 spheres = 160 KB of dynamic shared memory per CTA
 constexpr int kMaxPlanes = 32;
 constexpr int kMaxLights = 32;
 constexpr int kTileW = 8, kTileH = 4, kTilePx = kTileW * kTileH;
 
 struct DevPlane {
-  float nx, ny, nz, d;  // unit normal, n.x = d
+  double nx, ny, nz, d;  // unit normal (normalised in double from the float input), n.x = d
   int prim, mat, pad0, pad1;
 };
 
@@ -42,9 +47,11 @@ struct DevMat {
 };
 
 struct DevParams {
-  // camera (host computes the basis in double, rounds once): d = F + (2sx-1) R + (1-2sy) U
-  float eye[3], F[3], R[3], U[3];
+  // camera (basis in double): d = normalize(F + (2sx-1) R + (1-2sy) U)
+  double eye[3], F[3], R[3], U[3];
   float bg[3], amb[3];
+  float cmax;   // max over spheres of |c| (float filter error bound)
+  float rmax;   // max sphere radius
   int W, H, max_depth, spp;
   int n_spheres, n_pairs_pad, n_planes, n_lights;
   unsigned long long seed;
@@ -70,14 +77,12 @@ struct DevOutputs {
 };
 
 // launchers (rt_kernels.cu)
-cudaError_t upload_const_scene(const float4* pairs, int n_pair_float4, const DevPlane* planes,
-                               int n_planes, cudaStream_t st);
+cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
-                          bool const_scene, int num_sms, cudaStream_t st);
+                          bool smem_scene, int num_sms, cudaStream_t st);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,
                            float gamma, cudaStream_t st);
-int render_blocks_per_sm(bool const_scene, bool debug);
 
 }  // namespace rt

@@ -75,6 +75,23 @@ __global__ void k_ffma2(float* out, int iters, float b0, float c0) {
   if (s == 12345.678f) out[0] = s;
 }
 
+__global__ void k_dfma(double* out, int iters, double b0, double c0) {
+  double a[kChains], b[kChains], c[kChains];
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) { a[i] = threadIdx.x * 1e-3 + i; b[i] = b0 + i * 1e-7; c[i] = c0 - i * 1e-7; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int i = 0; i < kChains; ++i) a[i] = fma(a[i], b[i], c[i]);
+    }
+  }
+  double s = 0.;
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 // ---- prototype sphere loops -------------------------------------------------------------
 constexpr int kMaxS = 2048;
 __constant__ float4 c_sph[kMaxS];         // cx, cy, cz, r^2
@@ -209,6 +226,14 @@ int main() {
   printf("FFMA2    : %.3f ms  %.2f TFLOP/s  %.1f FMA-lanes/clk/SM\n", ms, 2 * 2 * fmas / ms / 1e9,
          2 * fmas / (ms * 1e-3) / sms / (clk_khz * 1e3));
 
+  {
+    double* dd; CK(cudaMalloc(&dd, 64));
+    int it2 = iters / 8;
+    double dfmas = double(blocks) * threads * it2 * 16 * kChains;
+    float m = time_ms([&] { k_dfma<<<blocks, threads>>>(dd, it2, 0.999, 0.001); });
+    printf("DFMA     : %.3f ms  %.2f TFLOP/s(fp64)  %.1f DFMA-lanes/clk/SM\n", m, 2 * dfmas / m / 1e9,
+           dfmas / (m * 1e-3) / sms / (clk_khz * 1e3));
+  }
   // sphere field: 1000 spheres in [-30,30]x[-15,15]x[10,70], r in [0.3,1.2]
   int n = 1000;
   std::vector<float4> sph(n), pair(kMaxS);
