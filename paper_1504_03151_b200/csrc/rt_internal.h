@@ -23,7 +23,7 @@
 namespace rt {
 
 constexpr int kWarp = 32;
-constexpr int kPairsPerBatch = 4;   // 8 spheres per unrolled batch of the intersection loop
+constexpr int kPairsPerBatch = 8;   // 16 spheres per unrolled batch of the intersection loop
 constexpr int kMaxSmemPairs = 5120;  // 10240 spheres = 160 KB of dynamic shared memory per CTA
 constexpr int kMaxPlanes = 32;
 constexpr int kMaxLights = 32;

@@ -254,12 +254,19 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
         const float2 nx = make_float2(-x.x, -x.y), ny = make_float2(-y.x, -y.y);
         disc[i] = __ffma2_rn(nx, x, __ffma2_rn(ny, y, R2));
       }
-      unsigned cand = 0u;
+      // candidate detection: one max-reduction per batch (FMNMX3 tree), the per-sphere mask is
+      // only built on the rare path where some lane has a candidate
+      float dmax = fmaxf(disc[0].x, disc[0].y);
 #pragma unroll
-      for (int i = 0; i < kPairsPerBatch; ++i)
-        cand |= ((disc[i].x >= neg_slack) ? 1u : 0u) << (2 * i) | ((disc[i].y >= neg_slack) ? 1u : 0u) << (2 * i + 1);
-      if (!act) cand = 0u;
-      if (__any_sync(kFull, cand != 0u)) {
+      for (int i = 1; i < kPairsPerBatch; ++i) dmax = fmaxf(dmax, fmaxf(disc[i].x, disc[i].y));
+      const bool any_cand = act && dmax >= neg_slack;
+      if (__any_sync(kFull, any_cand)) {
+        unsigned cand = 0u;
+        if (any_cand) {
+#pragma unroll
+          for (int i = 0; i < kPairsPerBatch; ++i)
+            cand |= ((disc[i].x >= neg_slack) ? 1u : 0u) << (2 * i) | ((disc[i].y >= neg_slack) ? 1u : 0u) << (2 * i + 1);
+        }
         while (cand != 0u && act) {  // per-lane candidates, in index order (float64 decision)
           const int i = __ffs(cand) - 1;
           cand &= cand - 1u;
