@@ -1,0 +1,219 @@
+// rt_device.cuh — device helpers shared by the megakernel and the wavefront kernels
+// (included by rt_kernels.cu only: one translation unit, one copy of the constant bank).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "rt_internal.h"
+
+namespace rt {
+
+__constant__ DevPlane c_planes[kMaxPlanes];
+
+constexpr double kEps = 1e-4;          // EPS_T
+constexpr double kInf = 1.0e300;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kInvPi = 0.318309886183790671538f;
+constexpr float kInv2Pi = 0.159154943091895335769f;
+constexpr float kUlp = 5.9604644775390625e-08f;  // 2^-24
+
+enum : int { Q_NONE = 0, Q_CLOSEST = 1, Q_SHADOW = 2 };
+
+struct d3 { double x, y, z; };
+__device__ __forceinline__ d3 mk(double x, double y, double z) { d3 r; r.x = x; r.y = y; r.z = z; return r; }
+__device__ __forceinline__ d3 operator+(d3 a, d3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ d3 operator-(d3 a, d3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ d3 operator*(d3 a, double s) { return mk(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 normalize(d3 a) { return a * (1.0 / sqrt(dot(a, a))); }
+__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__device__ __forceinline__ float3 add(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ float3 mul(float3 a, float3 b) { return f3(a.x * b.x, a.y * b.y, a.z * b.z); }
+
+// splitmix64 finalizer and the per-decision counter RNG
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+__device__ __forceinline__ double rng_u(unsigned long long seed, unsigned long long pix, int s, int depth) {
+  const unsigned long long G = 0x9E3779B97F4A7C15ull;
+  unsigned long long x = seed ^ ((pix + 1ull) * G);
+  x = mix64(x);
+  x = mix64(x ^ ((((unsigned long long)(unsigned)s) << 32) + (unsigned long long)(unsigned)depth) * G);
+  return (double)(x >> 40) * (1.0 / 16777216.0);
+}
+
+// ---- ray generation (a2): §8(c).1 steps 1-2 ------------------------------------
+__device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double& oy) {
+  int n = 1;
+  while ((n + 1) * (n + 1) <= spp) ++n;
+  if (n * n == spp) {
+    const int i = s % n, j = s / n;
+    ox = (i + 0.5) / n;
+    oy = (j + 0.5) / n;
+  } else {
+    const double radinv = (double)__brev((unsigned)s) * (1.0 / 4294967296.0);
+    const double y = radinv + 0.5 / spp;
+    ox = (s + 0.5) / spp;
+    oy = y - floor(y);
+  }
+}
+
+// camera ray of sample s of pixel (px, py): d = normalize(F + (2sx-1) R + (1-2sy) U)
+__device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int s) {
+  double ox, oy;
+  sample_offset(s, P.spp, ox, oy);
+  const double sx = (px + ox) / P.W, sy = (py + oy) / P.H;
+  const double a = 2.0 * sx - 1.0, b = 1.0 - 2.0 * sy;
+  return normalize(mk(P.F[0] + a * P.R[0] + b * P.U[0], P.F[1] + a * P.R[1] + b * P.U[1],
+                      P.F[2] + a * P.R[2] + b * P.U[2]));
+}
+
+// work item w (tile-major, 8x4 tiles; shard mode maps local tile j to global tile j*world+rank)
+// -> pixel; returns false for pixels outside the image / tiles past the end
+__device__ __forceinline__ bool item_pixel(const DevParams& P, int w, int& px, int& py) {
+  int t = w / kTilePx;
+  const int i = w % kTilePx;
+  if (P.mode == 1) {
+    t = t * P.world + P.rank;
+    if (t >= P.n_tiles) return false;
+  }
+  px = (t % P.tiles_x) * kTileW + (i % kTileW);
+  py = (t / P.tiles_x) * kTileH + (i / kTileW);
+  return px < P.W && py < P.H;
+}
+
+__device__ __forceinline__ d3 reflect(d3 d, d3 n) { return d - n * (2.0 * dot(d, n)); }
+
+// ---- scene staging (a1): one TMA bulk copy global -> shared per CTA -------------------------
+// The pair array (32 B per two spheres) is copied into dynamic shared memory with
+// cp.async.bulk (UBLKCP) completing on an mbarrier; every warp then reads each pair as a
+// warp-uniform LDS.128 broadcast. Scenes larger than the shared-memory budget stay in global
+// memory (uniform LDG through L1).
+__device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pairs, uint32_t bytes,
+                                            uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_pairs);
+    constexpr uint32_t kChunk = 1u << 15;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t n = (bytes - off) < kChunk ? (bytes - off) : kChunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+          "l"(reinterpret_cast<const char*>(g_pairs) + off), "r"(n), "r"(mb)
+          : "memory");
+    }
+  }
+  __syncthreads();  // barrier initialised before anyone waits on it
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(mb), "r"(0u)
+        : "memory");
+  }
+}
+
+// ---- intersection (a3 closest-hit + a5 any-hit), one loop for the whole warp -----------------
+extern __shared__ float4 s_pairs[];
+
+template <bool kSmem>
+__device__ __forceinline__ float4 load_pair(const float4* __restrict__ gp, int i) {
+  if constexpr (kSmem) return s_pairs[i];  // warp-uniform address: LDS.128 broadcast
+  else return __ldg(gp + i);
+}
+
+// Exact decision for one sphere (float64, from the float inputs): smallest root >= EPS_T of
+// Eq. 11 with a = 1, precise discriminant r^2 - |oc - (oc.d) d|^2, stable roots.
+__device__ __forceinline__ double sphere_root(const float4 cr, const d3 o, const d3 d) {
+  const d3 oc = o - mk(cr.x, cr.y, cr.z);
+  const double r = cr.w;
+  const double b = dot(oc, d);
+  const d3 perp = oc - d * b;
+  const double disc = r * r - dot(perp, perp);
+  if (disc < 0.0) return -1.0;
+  const double q = sqrt(disc);
+  double t0 = -b - q, t1 = -b + q;
+  // stable form: a root that cancels (origin near the surface) is recomputed from the
+  // product of the roots, c' = |oc|^2 - r^2
+  const double cancel = 1e-3 * fabs(b);
+  if (fabs(t0) < cancel || fabs(t1) < cancel) {
+    const double cprime = dot(oc, oc) - r * r;
+    if (fabs(t0) < cancel) t0 = cprime / t1;
+    else t1 = cprime / t0;
+    if (t0 > t1) { const double tmp = t0; t0 = t1; t1 = tmp; }
+  }
+  return t0 >= kEps ? t0 : t1;
+}
+
+// Float32 filter state of one ray: orthonormal basis (u1, u2) of d
+// (Duff et al. 2017); for each sphere the lateral coordinates x = (c - o).u1, y = (c - o).u2
+// give disc = r^2 - x^2 - y^2 (the precise discriminant of Eq. 11-12 with a = 1). A sphere is a
+// candidate when disc >= -slack; eta bounds the float error of x, y and of tc = (c - o).d.
+struct RayFilter {
+  float dx, dy, dz, u1x, u1y, u1z, u2x, u2y, u2z, ou1, ou2, odf, eta, neg_slack;
+  __device__ __forceinline__ void init(const d3& o, const d3& d, const DevParams& P) {
+    const float ox = (float)o.x, oy = (float)o.y, oz = (float)o.z;
+    dx = (float)d.x; dy = (float)d.y; dz = (float)d.z;
+    const float sg = copysignf(1.0f, dz);
+    const float ia = -1.0f / (sg + dz);
+    const float bb = dx * dy * ia;
+    u1x = fmaf(sg * dx * dx, ia, 1.0f); u1y = sg * bb; u1z = -sg * dx;
+    u2x = bb; u2y = fmaf(dy * dy, ia, sg); u2z = -dy;
+    ou1 = -fmaf(ox, u1x, fmaf(oy, u1y, oz * u1z));
+    ou2 = -fmaf(ox, u2x, fmaf(oy, u2y, oz * u2z));
+    odf = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));
+    eta = 32.0f * kUlp * (fabsf(ox) + fabsf(oy) + fabsf(oz) + P.cmax);
+    neg_slack = -(4.0f * eta * P.rmax + 4.0f * eta * eta + 4.0f * kUlp * P.rmax * P.rmax);
+  }
+  // disc of 16 spheres (pairs base..base+7) with two spheres per FFMA2; returns their max
+  template <bool kSmem>
+  __device__ __forceinline__ float batch(const float4* __restrict__ gp, int base, float2 (&disc)[kPairsPerBatch]) const {
+    const float2 U1x = make_float2(u1x, u1x), U1y = make_float2(u1y, u1y), U1z = make_float2(u1z, u1z);
+    const float2 U2x = make_float2(u2x, u2x), U2y = make_float2(u2y, u2y), U2z = make_float2(u2z, u2z);
+    const float2 OU1 = make_float2(ou1, ou1), OU2 = make_float2(ou2, ou2);
+#pragma unroll
+    for (int i = 0; i < kPairsPerBatch; ++i) {
+      const float4 a = load_pair<kSmem>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSmem>(gp, 2 * (base + i) + 1);
+      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
+      const float2 CZ = make_float2(b.x, b.y), R2 = make_float2(b.z, b.w);
+      const float2 x = __ffma2_rn(CX, U1x, __ffma2_rn(CY, U1y, __ffma2_rn(CZ, U1z, OU1)));
+      const float2 y = __ffma2_rn(CX, U2x, __ffma2_rn(CY, U2y, __ffma2_rn(CZ, U2z, OU2)));
+      const float2 nx = make_float2(-x.x, -x.y), ny = make_float2(-y.x, -y.y);
+      disc[i] = __ffma2_rn(nx, x, __ffma2_rn(ny, y, R2));
+    }
+    float dmax = fmaxf(disc[0].x, disc[0].y);
+#pragma unroll
+    for (int i = 1; i < kPairsPerBatch; ++i) dmax = fmaxf(dmax, fmaxf(disc[i].x, disc[i].y));
+    return dmax;
+  }
+  // float lateral disc, chord centre tc and bounds of one sphere k (rare path)
+  template <bool kSmem>
+  __device__ __forceinline__ void sphere(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
+    const float4 pa = load_pair<kSmem>(gp, 2 * (k >> 1));
+    const float4 pb = load_pair<kSmem>(gp, 2 * (k >> 1) + 1);
+    const bool h = k & 1;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, r2 = h ? pb.w : pb.z;
+    const float lx = fmaf(cx, u1x, fmaf(cy, u1y, fmaf(cz, u1z, ou1)));
+    const float ly = fmaf(cx, u2x, fmaf(cy, u2y, fmaf(cz, u2z, ou2)));
+    dd = fmaf(-lx, lx, fmaf(-ly, ly, r2));  // == the FFMA2 lane value
+    tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, odf)));
+  }
+};
+
+__device__ __forceinline__ unsigned batch_mask(const float2 (&disc)[kPairsPerBatch], float neg_slack) {
+  unsigned cand = 0u;
+#pragma unroll
+  for (int i = 0; i < kPairsPerBatch; ++i)
+    cand |= ((disc[i].x >= neg_slack) ? 1u : 0u) << (2 * i) | ((disc[i].y >= neg_slack) ? 1u : 0u) << (2 * i + 1);
+  return cand;
+}
+
+}  // namespace rt

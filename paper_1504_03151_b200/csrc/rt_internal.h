@@ -76,10 +76,45 @@ struct DevOutputs {
   int* dbg_bounces;             // optional [n_px * spp]
 };
 
+// ---- wavefront variant buffers (rt_wavefront.cuh) ----
+constexpr int kCandMax = 6;  // candidates stored per ray; more -> overflow -> FP64 full scan
+
+struct WfBuffers {
+  double* ray;     // [6][cap]  current ray o, d (next closest query)
+  double* hit;     // [6][cap]  shading point p and facing normal n of the current depth
+  float* T;        // [3][cap]
+  float* Lr;       // [3][cap]  sample radiance
+  int* depth;      // [cap]
+  int* shoff;      // [cap]  first shadow entry of the path at the current depth
+  int* shcnt;      // [cap]
+  int* q[2];       // closest queues (path ids)
+  int* sq_path;    // [scap]
+  int* sq_light;   // [scap]
+  float* sq_c;     // [3][scap] contribution f_r I cos/d^2 * T
+  int* ccand;      // [cap * kCandMax]
+  int* cn;         // [cap]
+  int* scand;      // [scap * kCandMax]
+  int* sn;         // [scap]
+  int* srob;       // [scap] robust occluder: sphere index, -1 none, -2-j plane j
+  unsigned* ctr;   // counters, see wf_ctr_*
+  int cap, scap;
+};
+
+// counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
+__host__ __device__ constexpr int wf_ctr_q(int d) { return 4 * d; }
+__host__ __device__ constexpr int wf_ctr_s(int d) { return 4 * d + 1; }
+__host__ __device__ constexpr int wf_ctr_wc(int d) { return 4 * d + 2; }
+__host__ __device__ constexpr int wf_ctr_ws(int d) { return 4 * d + 3; }
+constexpr int kWfCtrPerDepth = 4;
+
 // launchers (rt_kernels.cu)
 cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
+size_t wf_bytes(int cap, int scap);
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr);
+cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
+                                    int num_sms, WfBuffers& B, cudaStream_t st);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,

@@ -19,46 +19,10 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
-#include "rt_internal.h"
+#include "rt_device.cuh"
+#include "rt_wavefront.cuh"
 
 namespace rt {
-
-__constant__ DevPlane c_planes[kMaxPlanes];
-
-constexpr double kEps = 1e-4;          // EPS_T
-constexpr double kInf = 1.0e300;
-constexpr unsigned kFull = 0xffffffffu;
-constexpr float kInvPi = 0.318309886183790671538f;
-constexpr float kInv2Pi = 0.159154943091895335769f;
-constexpr float kUlp = 5.9604644775390625e-08f;  // 2^-24
-
-enum : int { Q_NONE = 0, Q_CLOSEST = 1, Q_SHADOW = 2 };
-
-struct d3 { double x, y, z; };
-__device__ __forceinline__ d3 mk(double x, double y, double z) { d3 r; r.x = x; r.y = y; r.z = z; return r; }
-__device__ __forceinline__ d3 operator+(d3 a, d3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ d3 operator-(d3 a, d3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
-__device__ __forceinline__ d3 operator*(d3 a, double s) { return mk(a.x * s, a.y * s, a.z * s); }
-__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ d3 normalize(d3 a) { return a * (1.0 / sqrt(dot(a, a))); }
-__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
-__device__ __forceinline__ float3 add(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ float3 mul(float3 a, float3 b) { return f3(a.x * b.x, a.y * b.y, a.z * b.z); }
-
-// splitmix64 finalizer and the per-decision counter RNG
-__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
-  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
-  x ^= x >> 27; x *= 0x94D049BB133111EBull;
-  x ^= x >> 31;
-  return x;
-}
-__device__ __forceinline__ double rng_u(unsigned long long seed, unsigned long long pix, int s, int depth) {
-  const unsigned long long G = 0x9E3779B97F4A7C15ull;
-  unsigned long long x = seed ^ ((pix + 1ull) * G);
-  x = mix64(x);
-  x = mix64(x ^ ((((unsigned long long)(unsigned)s) << 32) + (unsigned long long)(unsigned)depth) * G);
-  return (double)(x >> 40) * (1.0 / 16777216.0);
-}
 
 // ---- per-lane state ------------------------------------------------------------------------
 struct Lane {
@@ -79,22 +43,6 @@ struct Lane {
   unsigned n_primary, n_shadow, n_secondary;
   unsigned long long n_stests, n_ptests;
 };
-
-// ---- ray generation (a2): §8(c).1 steps 1-2 ------------------------------------
-__device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double& oy) {
-  int n = 1;
-  while ((n + 1) * (n + 1) <= spp) ++n;
-  if (n * n == spp) {
-    const int i = s % n, j = s / n;
-    ox = (i + 0.5) / n;
-    oy = (j + 0.5) / n;
-  } else {
-    const double radinv = (double)__brev((unsigned)s) * (1.0 / 4294967296.0);
-    const double y = radinv + 0.5 / spp;
-    ox = (s + 0.5) / spp;
-    oy = y - floor(y);
-  }
-}
 
 __device__ __forceinline__ void start_sample(Lane& L, const DevParams& P) {
   double ox, oy;
@@ -130,69 +78,6 @@ __device__ __forceinline__ bool start_item(Lane& L, const DevParams& P, int w, f
   L.Lpix = f3(0.f, 0.f, 0.f);
   start_sample(L, P);
   return true;
-}
-
-// ---- scene staging (a1): one TMA bulk copy global -> shared per CTA -------------------------
-// The pair array (32 B per two spheres) is copied into dynamic shared memory with
-// cp.async.bulk (UBLKCP) completing on an mbarrier; every warp then reads each pair as a
-// warp-uniform LDS.128 broadcast. Scenes larger than the shared-memory budget stay in global
-// memory (uniform LDG through L1).
-__device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pairs, uint32_t bytes,
-                                            uint64_t* mbar) {
-  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_pairs);
-    constexpr uint32_t kChunk = 1u << 15;
-    for (uint32_t off = 0; off < bytes; off += kChunk) {
-      const uint32_t n = (bytes - off) < kChunk ? (bytes - off) : kChunk;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
-          "l"(reinterpret_cast<const char*>(g_pairs) + off), "r"(n), "r"(mb)
-          : "memory");
-    }
-  }
-  __syncthreads();  // barrier initialised before anyone waits on it
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(mb), "r"(0u)
-        : "memory");
-  }
-}
-
-// ---- intersection (a3 closest-hit + a5 any-hit), one loop for the whole warp -----------------
-template <bool kSmem>
-__device__ __forceinline__ float4 load_pair(const float4* __restrict__ sp, int i) {
-  if constexpr (kSmem) return sp[i];     // warp-uniform address: LDS.128 broadcast
-  else return __ldg(sp + i);
-}
-
-// Exact decision for one sphere (float64, from the float inputs): smallest root >= EPS_T of
-// Eq. 11 with a = 1, precise discriminant r^2 - |oc - (oc.d) d|^2, stable roots.
-__device__ __forceinline__ double sphere_root(const float4 cr, const d3 o, const d3 d) {
-  const d3 oc = o - mk(cr.x, cr.y, cr.z);
-  const double r = cr.w;
-  const double b = dot(oc, d);
-  const d3 perp = oc - d * b;
-  const double disc = r * r - dot(perp, perp);
-  if (disc < 0.0) return -1.0;
-  const double q = sqrt(disc);
-  const double cprime = dot(oc, oc) - r * r;
-  double t0, t1;
-  if (b < 0.0) {
-    t1 = -b + q;
-    t0 = t1 != 0.0 ? cprime / t1 : -b - q;
-  } else {
-    t0 = -b - q;
-    t1 = t0 != 0.0 ? cprime / t0 : -b + q;
-  }
-  if (t0 > t1) { const double tmp = t0; t0 = t1; t1 = tmp; }
-  return t0 >= kEps ? t0 : t1;
 }
 
 template <bool kSmem>
@@ -233,12 +118,52 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
   const float ou1 = -fmaf(ox, u1x, fmaf(oy, u1y, oz * u1z));
   const float ou2 = -fmaf(ox, u2x, fmaf(oy, u2y, oz * u2z));
   const float eta = 32.0f * kUlp * (fabsf(ox) + fabsf(oy) + fabsf(oz) + P.cmax);
+  const float odf = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));
   const float neg_slack = -(4.0f * eta * P.rmax + 4.0f * eta * eta + 4.0f * kUlp * P.rmax * P.rmax);
   const float2 U1x = make_float2(u1x, u1x), U1y = make_float2(u1y, u1y), U1z = make_float2(u1z, u1z);
   const float2 U2x = make_float2(u2x, u2x), U2y = make_float2(u2y, u2y), U2z = make_float2(u2z, u2z);
   const float2 OU1 = make_float2(ou1, ou1), OU2 = make_float2(ou2, ou2);
-  // a warp without closest-hit lanes may leave the loop once every shadow lane found an occluder
+  // Candidates of one 16-sphere batch (mask bit i = sphere 2*base + i), in index order:
+  // float range prefilter (the chord [tc - q, tc + q] lies before EPS_T or beyond tmax with
+  // margin: tc error <= eta, q <= sqrt(disc_f + slack)), then the float64 decision.
+  auto process = [&](unsigned cand, int base) {
+    const float tmax_hi = (float)tmax * 1.000001f + eta;
+    while (cand != 0u && act) {
+      const int i = __ffs(cand) - 1;
+      cand &= cand - 1u;
+      const int k = 2 * base + i;  // pair (base + i/2), half i&1
+      if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds r^2 = 1)
+      const float4 pa = load_pair<kSmem>(pairs, 2 * (base + (i >> 1)));
+      const float4 pb = load_pair<kSmem>(pairs, 2 * (base + (i >> 1)) + 1);
+      const float cx = (i & 1) ? pa.y : pa.x, cy = (i & 1) ? pa.w : pa.z, cz = (i & 1) ? pb.y : pb.x;
+      const float r2 = (i & 1) ? pb.w : pb.z;
+      const float lx = fmaf(cx, u1x, fmaf(cy, u1y, fmaf(cz, u1z, ou1)));
+      const float ly = fmaf(cx, u2x, fmaf(cy, u2y, fmaf(cz, u2z, ou2)));
+      const float dd = fmaf(-lx, lx, fmaf(-ly, ly, r2));  // == the FFMA2 lane value
+      const float tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, odf)));
+      const float qh = sqrtf(fmaxf(dd - neg_slack, 0.f));
+      if (tc + qh < (float)kEps - eta || tc - qh > tmax_hi) continue;
+      const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
+      if (t >= kEps && t < tmax) {
+        hs = k; hp = -1;
+        if (shadow) act = false; else tmax = t;
+      }
+    }
+  };
+  // A warp without closest-hit lanes decides candidates inside the loop and leaves it once
+  // every shadow lane found an occluder (Alg. 1 `break`). Otherwise the loop runs over the whole
+  // scene for the closest-hit lanes anyway, so candidates are queued (batch | mask, FIFO of 4)
+  // and decided after the loop with all lanes in parallel instead of one batch at a time.
   const bool may_exit = !__any_sync(kFull, L.qkind == Q_CLOSEST);
+  unsigned long long qa = 0ull, qb = 0ull;
+  int nq = 0;
+  auto pop = [&]() -> unsigned {
+    const unsigned e = (unsigned)qa;
+    qa = (qa >> 32) | (qb << 32);
+    qb >>= 32;
+    --nq;
+    return e;
+  };
 
   if (__any_sync(kFull, act)) {
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
@@ -261,25 +186,28 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       for (int i = 1; i < kPairsPerBatch; ++i) dmax = fmaxf(dmax, fmaxf(disc[i].x, disc[i].y));
       const bool any_cand = act && dmax >= neg_slack;
       if (__any_sync(kFull, any_cand)) {
-        unsigned cand = 0u;
         if (any_cand) {
+          unsigned cand = 0u;
 #pragma unroll
           for (int i = 0; i < kPairsPerBatch; ++i)
             cand |= ((disc[i].x >= neg_slack) ? 1u : 0u) << (2 * i) | ((disc[i].y >= neg_slack) ? 1u : 0u) << (2 * i + 1);
-        }
-        while (cand != 0u && act) {  // per-lane candidates, in index order (float64 decision)
-          const int i = __ffs(cand) - 1;
-          cand &= cand - 1u;
-          const int k = 2 * base + i;  // pair (base + i/2), half i&1
-          if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds r^2 = 1)
-          const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
-          if (t >= kEps && t < tmax) {
-            hs = k; hp = -1;
-            if (shadow) act = false; else tmax = t;
+          if (may_exit) {
+            process(cand, base);
+          } else {
+            if (nq == 4) {  // FIFO full (rare): decide the queued batches now
+              while (nq > 0) { const unsigned e = pop(); process(e & 0xffffu, (int)(e >> 16) * kPairsPerBatch); }
+            }
+            const unsigned long long e = ((unsigned long long)(base / kPairsPerBatch) << 16) | cand;
+            if (nq < 2) qa |= e << (32 * nq); else qb |= e << (32 * (nq - 2));
+            ++nq;
           }
         }
       }
       if (may_exit && !__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
+    }
+    while (nq > 0) {  // deferred candidates, in index order
+      const unsigned e = pop();
+      process(e & 0xffffu, (int)(e >> 16) * kPairsPerBatch);
     }
   }
   // algorithmic test counts
@@ -320,8 +248,6 @@ __device__ void finish_sample(Lane& L, const DevParams& P, const DevOutputs& O) 
   L.item = -1;
   L.qkind = Q_NONE;
 }
-
-__device__ __forceinline__ d3 reflect(d3 d, d3 n) { return d - n * (2.0 * dot(d, n)); }
 
 template <bool kDebug>
 __device__ void bounce(Lane& L, const DevParams& P, const DevScene& S, const DevOutputs& O) {
@@ -447,13 +373,15 @@ __device__ __forceinline__ void advance(Lane& L, const DevParams& P, const DevSc
 }
 
 // ---- the persistent megakernel --------------------------------------------------------------
+#ifndef RT_MIN_BLOCKS
+#define RT_MIN_BLOCKS 2
+#endif
 template <bool kSmem, bool kDebug>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, RT_MIN_BLOCKS)
 render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
-  extern __shared__ float4 s_pairs[];
   __shared__ uint64_t s_mbar;
   if constexpr (kSmem) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
-  const float4* pairs = kSmem ? s_pairs : S.pairs;
+  const float4* pairs = S.pairs;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   Lane L;
@@ -595,6 +523,82 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
   if (grid < 1) grid = 1;
   tonemap_kernel<<<grid, 256, 0, st>>>(rgba, reinterpret_cast<uchar4*>(out), n, exposure, 1.0f / gamma);
   return cudaGetLastError();
+}
+
+// ---- wavefront launcher ---------------------------------------------------------------------
+size_t wf_bytes(int cap, int scap) {
+  return (size_t)cap * (12 * 8 + 6 * 4 + 3 * 4 + 2 * 4 + kCandMax * 4 + 4) +
+         (size_t)scap * (4 + 4 + 12 + kCandMax * 4 + 4 + 4);
+}
+
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
+  char* p = static_cast<char*>(base);
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
+  B.cap = cap;
+  B.scap = scap;
+  B.ray = reinterpret_cast<double*>(take(6 * 8 * (size_t)cap));
+  B.hit = reinterpret_cast<double*>(take(6 * 8 * (size_t)cap));
+  B.T = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
+  B.Lr = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
+  B.depth = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.shoff = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.shcnt = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.q[0] = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.q[1] = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.ccand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * cap));
+  B.cn = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.sq_path = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sq_light = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sq_c = reinterpret_cast<float*>(take(3 * 4 * (size_t)scap));
+  B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * scap));
+  B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.ctr = ctr;
+}
+
+template <bool kSmem>
+static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
+                          WfBuffers& B, cudaStream_t st) {
+  const bool dbg = o.dbg_hits != nullptr;
+  const size_t smem = kSmem ? (size_t)p.n_pairs_pad * 32u : 0u;
+  cudaError_t e;
+  int occ_c = 0, occ_s = 0;
+  for (auto fn : {wf_isect<kSmem, false>, wf_isect<kSmem, true>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
+    if (e != cudaSuccess) return e;
+  }
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSmem, false>, 256, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSmem, true>, 256, smem)) != cudaSuccess) return e;
+  const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
+  const int grid_l = num_sms * 8;
+  const int items_per_chunk = B.cap / p.spp;
+  if (dbg) {
+    const long long nh = (long long)p.W * p.H * p.spp * (p.max_depth + 1);
+    fill_int<<<num_sms * 8, 256, 0, st>>>(o.dbg_hits, nh, -2);
+  }
+  for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk) {
+    const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
+    const int npaths = nw * p.spp;
+    const long long g0 = (long long)w0 * p.spp;
+    if ((e = cudaMemsetAsync(B.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
+    const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
+    wf_raygen<<<grid_r, 256, 0, st>>>(p, B, g0, npaths, o.stats);
+    for (int d = 0; d <= p.max_depth; ++d) {
+      wf_isect<kSmem, false><<<grid_c, 256, smem, st>>>(p, sc, B, d);
+      if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
+      else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
+      wf_isect<kSmem, true><<<grid_s, 256, smem, st>>>(p, sc, B, d);
+      wf_accumulate<<<grid_l, 256, 0, st>>>(p, sc, B, d, o.stats);
+    }
+    const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
+    wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
+                                    int num_sms, WfBuffers& B, cudaStream_t st) {
+  return smem_scene ? wf_run<true>(p, sc, o, num_sms, B, st) : wf_run<false>(p, sc, o, num_sms, B, st);
 }
 
 }  // namespace rt

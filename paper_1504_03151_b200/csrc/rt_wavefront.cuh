@@ -1,0 +1,461 @@
+// rt_wavefront.cuh — wavefront variant of the hot path (included by rt_kernels.cu).
+//
+// The megakernel keeps every lane's path state in registers and runs one divergent state
+// machine per round. The wavefront variant splits the same computation
+// into kernels over compacted queues in HBM, so the FP32 intersection loop runs at high
+// occupancy with no divergent logic inside, and the FP64 logic runs at full SIMD width:
+//
+//   raygen            paths of a chunk of pixels -> closest queue Q[0]              (a2)
+//   per depth d = 0..max_depth:
+//     isect_closest   Q[d]: FP32 FFMA2 filter over all spheres -> candidate lists     (a3)
+//     shade           Q[d]: FP64 nearest hit (planes + candidates), emission/ambient,
+//                     shadow entries with their Lambert/Phong contribution, bounce   (a4, a6)
+//                     -> Q[d+1]
+//     isect_shadow    shadow entries: FP64 planes, FP32 filter with early exit on a
+//                     robust (float-certain) occluder -> candidate lists             (a5)
+//     accumulate      Q[d]: FP64 occlusion decisions in light order, L += contribution
+//   resolve           sum of the spp sample radiances in order s = 0..spp-1 -> float4 (a7)
+//
+// Per path the radiance receives the same terms in the same order as the megakernel
+// (emission, ambient, lights 0..L-1 of depth 0, then depth 1, ...), so the two variants
+// produce bit-identical framebuffers.
+#pragma once
+#include "rt_device.cuh"
+
+namespace rt {
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// warp-aggregated reservation of `cnt` slots on a global counter (ballot/popc/shfl)
+__device__ __forceinline__ unsigned warp_reserve(unsigned cnt, unsigned* counter) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  unsigned incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned v = __shfl_up_sync(act, incl, off);
+    if (lane >= off && (act >> (lane - off)) & 1u) incl += v;
+  }
+  const int last = 31 - __clz(act);
+  const unsigned total = __shfl_sync(act, incl, last);
+  const int leader = __ffs(act) - 1;
+  unsigned base = 0;
+  if (lane == leader && total) base = atomicAdd(counter, total);
+  base = __shfl_sync(act, base, leader);
+  return base + incl - cnt;
+}
+
+__device__ __forceinline__ void warp_stat(unsigned long long* stats, int k, unsigned long long v) {
+  const unsigned act = __activemask();
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(act, v, off);
+  if ((threadIdx.x & 31) == (__ffs(act) - 1) && v) atomicAdd(stats + k, v);
+}
+
+__device__ __forceinline__ d3 ld3(const double* a, int cap, int i, int c0) {
+  return mk(a[(c0 + 0) * (size_t)cap + i], a[(c0 + 1) * (size_t)cap + i], a[(c0 + 2) * (size_t)cap + i]);
+}
+__device__ __forceinline__ void st3(double* a, int cap, int i, int c0, d3 v) {
+  a[(c0 + 0) * (size_t)cap + i] = v.x;
+  a[(c0 + 1) * (size_t)cap + i] = v.y;
+  a[(c0 + 2) * (size_t)cap + i] = v.z;
+}
+__device__ __forceinline__ float3 lf3(const float* a, int cap, int i) {
+  return f3(a[i], a[(size_t)cap + i], a[2 * (size_t)cap + i]);
+}
+__device__ __forceinline__ void sf3(float* a, int cap, int i, float3 v) {
+  a[i] = v.x;
+  a[(size_t)cap + i] = v.y;
+  a[2 * (size_t)cap + i] = v.z;
+}
+
+// shadow ray of light l from the shading point: o = p + EPS_T n toward the light
+__device__ __forceinline__ void shadow_ray(const DevScene& S, d3 p, d3 n, int l, d3& os, d3& ds, double& tl) {
+  const DevLight lt = S.lights[l];
+  os = p + n * kEps;
+  const d3 ws = mk(lt.px, lt.py, lt.pz) - os;
+  tl = sqrt(dot(ws, ws));
+  ds = ws * (1.0 / tl);
+}
+
+// ---- a2: ray generation ---------------------------------------------------------------------
+__global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
+                                                 unsigned long long* stats) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const long long g = g0 + i;
+    const int w = (int)(g / P.spp), s = (int)(g % P.spp);
+    int px = 0, py = 0;
+    const bool valid = item_pixel(P, w, px, py);
+    sf3(B.Lr, B.cap, i, f3(0.f, 0.f, 0.f));
+    if (valid) {
+      st3(B.ray, B.cap, i, 0, mk(P.eye[0], P.eye[1], P.eye[2]));
+      st3(B.ray, B.cap, i, 3, camera_dir(P, px, py, s));
+      sf3(B.T, B.cap, i, f3(1.f, 1.f, 1.f));
+      B.depth[i] = 0;
+      B.shcnt[i] = 0;
+    }
+    const unsigned slot = warp_reserve(valid ? 1u : 0u, B.ctr + wf_ctr_q(0));
+    if (valid) B.q[0][slot] = i;
+    warp_stat(stats, 0, valid ? 1ull : 0ull);
+  }
+}
+
+// ---- a3 / a5: FP32 filter over all spheres (persistent, one warp = 32 rays) -----------------
+template <bool kSmem, bool kShadow>
+__global__ void __launch_bounds__(256, 3)
+wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  __shared__ uint64_t s_mbar;
+  if constexpr (kSmem) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
+  const float4* gp = S.pairs;
+  const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
+  const int* q = B.q[d & 1];
+  int* cand = kShadow ? B.scand : B.ccand;
+  int* cn = kShadow ? B.sn : B.cn;
+  const int lane = threadIdx.x & 31;
+  const float eps_f = (float)kEps;
+  while (true) {
+    unsigned e0 = 0;
+    if (lane == 0) e0 = atomicAdd(work, 32u);
+    e0 = __shfl_sync(kFull, e0, 0);
+    if (e0 >= n) break;
+    const unsigned e = e0 + lane;
+    bool act = e < n;
+    d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+    double tl = 0.0;
+    int rob = -1;
+    if (act) {
+      if constexpr (kShadow) {
+        const int path = B.sq_path[e];
+        shadow_ray(S, ld3(B.hit, B.cap, path, 0), ld3(B.hit, B.cap, path, 3), B.sq_light[e], o, dir, tl);
+        // planes first, exactly (FP64): the first plane in index order that occludes decides
+        for (int j = 0; j < P.n_planes; ++j) {
+          const DevPlane pl = c_planes[j];
+          const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+          if (fabs(den) >= 1e-12) {
+            const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+            if (t >= kEps && t < tl) { rob = -2 - j; act = false; break; }
+          }
+        }
+      } else {
+        const int path = q[e];
+        o = ld3(B.ray, B.cap, path, 0);
+        dir = ld3(B.ray, B.cap, path, 3);
+      }
+    }
+    RayFilter F;
+    F.init(o, dir, P);
+    const float tl_f = (float)tl;
+    float tub = 3.0e38f;  // closest: certain upper bound of the nearest accepted root
+    int nc = 0;
+    for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
+      float2 disc[kPairsPerBatch];
+      const float dmax = F.batch<kSmem>(gp, base, disc);
+      const bool any = act && dmax >= F.neg_slack;
+      if (__any_sync(kFull, any)) {
+        if (any) {
+          unsigned m = batch_mask(disc, F.neg_slack);
+          while (m != 0u) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1u;
+            const int k = 2 * base + i;
+            if (k >= P.n_spheres) break;
+            float dd, tc;
+            F.sphere<kSmem>(gp, k, dd, tc);
+            const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
+            const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
+            const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
+            if (tc + qh < eps_f - F.eta) continue;                  // chord certainly behind
+            if constexpr (kShadow) {
+              if (tc - qh - F.eta >= tl_f * 1.000001f) continue;   // certainly beyond the light
+              if (sure) {
+                const float t0lo = tc - qh - F.eta, t0hi = tc - ql + F.eta;
+                const float t1lo = tc + ql - F.eta, t1hi = tc + qh + F.eta;
+                const float tlo = tl_f * 0.999999f;
+                if ((t0lo >= eps_f && t0hi < tlo) || (t0hi < eps_f && t1lo >= eps_f && t1hi < tlo)) {
+                  rob = k;  // certain occluder: earlier ambiguous candidates are decided in FP64 later
+                  act = false;
+                  break;
+                }
+              }
+            } else {
+              if (tc - qh - F.eta > tub) continue;  // certainly farther than a certain hit
+              if (sure) {
+                const float t0lo = tc - qh - F.eta, t0hi = tc - ql + F.eta;
+                const float t1lo = tc + ql - F.eta, t1hi = tc + qh + F.eta;
+                if (t0lo >= eps_f) tub = fminf(tub, t0hi);
+                else if (t0hi < eps_f && t1lo >= eps_f) tub = fminf(tub, t1hi);
+              }
+            }
+            if (nc < kCandMax) cand[(size_t)e * kCandMax + nc] = k;
+            ++nc;
+          }
+        }
+      }
+      if constexpr (kShadow) {
+        if (!__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
+      }
+    }
+    if (e < n) {
+      cn[e] = nc;
+      if constexpr (kShadow) B.srob[e] = rob;
+    }
+  }
+}
+
+// FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
+// the list overflowed
+__device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScene& S, const int* cand, int nc,
+                                               d3 o, d3 d, double& tbest, int& hs, int& hp) {
+  if (nc <= kCandMax) {
+    for (int c = 0; c < nc; ++c) {
+      const int k = cand[c];
+      const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
+      if (t >= kEps && t < tbest) { tbest = t; hs = k; hp = -1; }
+    }
+  } else {
+    for (int k = 0; k < P.n_spheres; ++k) {
+      const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
+      if (t >= kEps && t < tbest) { tbest = t; hs = k; hp = -1; }
+    }
+  }
+}
+
+// ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
+template <bool kDebug>
+__global__ void __launch_bounds__(256) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
+                                                long long g0, unsigned long long* stats, int* dbg_hits,
+                                                int* dbg_bounces) {
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  const int* q = B.q[d & 1];
+  int* qn = B.q[(d + 1) & 1];
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int path = q[e];
+    const d3 o = ld3(B.ray, B.cap, path, 0), dir = ld3(B.ray, B.cap, path, 3);
+    double tbest = kInf;
+    int hs = -1, hp = -1;
+    for (int j = 0; j < P.n_planes; ++j) {
+      const DevPlane pl = c_planes[j];
+      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+      if (fabs(den) >= 1e-12) {
+        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+        if (t >= kEps && t < tbest) { tbest = t; hp = j; }
+      }
+    }
+    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], o, dir, tbest, hs, hp);
+    const int depth = B.depth[path];
+    int prim = -1;
+    if (hp >= 0) prim = c_planes[hp].prim;
+    else if (hs >= 0) prim = S.sph_prim[hs];
+    long long si = 0;
+    if constexpr (kDebug) {
+      const long long g = g0 + path;
+      int px = 0, py = 0;
+      item_pixel(P, (int)(g / P.spp), px, py);
+      si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
+      dbg_hits[si * (P.max_depth + 1) + depth] = prim;
+    }
+    float3 T = lf3(B.T, B.cap, path);
+    float3 L = lf3(B.Lr, B.cap, path);
+    bool cont = false;
+    unsigned nsh = 0;
+    d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
+    int mi = 0;
+    bool entering = false;
+    // part 1: hit geometry, emission/ambient, number of shadow rays
+    if (prim < 0) {  // miss -> background
+      L = add(L, mul(T, f3(P.bg[0], P.bg[1], P.bg[2])));
+    } else {
+      p = o + dir * tbest;
+      if (hp >= 0) {
+        const DevPlane pl = c_planes[hp];
+        ng = mk(pl.nx, pl.ny, pl.nz);
+        mi = pl.mat;
+      } else {
+        const float4 cr = __ldg(S.sph_cr + hs);
+        ng = (p - mk(cr.x, cr.y, cr.z)) * (1.0 / (double)cr.w);
+        mi = S.sph_mat[hs];
+      }
+      entering = dot(dir, ng) < 0.0;
+      nrm = entering ? ng : ng * -1.0;
+      const DevMat m = S.mats[mi];
+      L = add(L, mul(T, f3(m.er, m.eg, m.eb)));  // Eq. 7 emission
+      if (m.kind == 0) {
+        L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
+        for (int l = 0; l < P.n_lights; ++l) {  // count shadow rays (none if cos <= 0)
+          const DevLight lt = S.lights[l];
+          const d3 w = mk(lt.px, lt.py, lt.pz) - p;
+          const double d2 = dot(w, w);
+          if (d2 < 1e-12) continue;
+          if (dot(nrm, w * (1.0 / sqrt(d2))) <= 0.0) continue;
+          ++nsh;
+        }
+      }
+    }
+    const unsigned off = warp_reserve(nsh, B.ctr + wf_ctr_s(d));  // converged: ballot/scan/atomic
+    // part 2: shadow entries with their contribution T f_r I cos / d^2 (Eq. 3, 5, 6)
+    if (nsh) {
+      const DevMat m = S.mats[mi];
+      st3(B.hit, B.cap, path, 0, p);
+      st3(B.hit, B.cap, path, 3, nrm);
+      unsigned k = off;
+      for (int l = 0; l < P.n_lights; ++l) {
+        const DevLight lt = S.lights[l];
+        const d3 w = mk(lt.px, lt.py, lt.pz) - p;
+        const double d2 = dot(w, w);
+        if (d2 < 1e-12) continue;
+        const d3 wi = w * (1.0 / sqrt(d2));
+        const double cosT = dot(nrm, wi);
+        if (cosT <= 0.0) continue;
+        // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3)
+        const d3 rl = nrm * (2.0 * cosT) - wi;
+        const float alpha = (float)fmax(0.0, -dot(rl, dir));
+        const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+        const float g = (float)(cosT / d2);
+        B.sq_path[k] = path;
+        B.sq_light[k] = l;
+        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * lt.ix * g, fmaf(m.ag, kInvPi, spec) * lt.iy * g,
+                                       fmaf(m.ab, kInvPi, spec) * lt.iz * g)));
+        ++k;
+      }
+    }
+    B.shoff[path] = (int)off;
+    // part 3: stack-free continuation
+    if (prim >= 0 && depth < P.max_depth) {
+      const DevMat m = S.mats[mi];
+      d3 dn = mk(0, 0, 0);
+      if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
+        dn = reflect(dir, nrm);
+        T = mul(T, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
+        if (m.kr > 0.f) {
+          dn = reflect(dir, nrm);
+          T = f3(T.x * m.kr, T.y * m.kr, T.z * m.kr);
+          cont = true;
+        }
+      } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
+        const double ior = m.ior;
+        const double eta = entering ? 1.0 / ior : ior;
+        const double ci = -dot(dir, nrm);
+        const double sin2t = eta * eta * (1.0 - ci * ci);
+        bool refl = sin2t > 1.0;
+        if (!refl) {
+          const double cosT = sqrt(1.0 - sin2t);
+          const double c = entering ? ci : cosT;
+          double r0 = (1.0 - ior) / (1.0 + ior);
+          r0 *= r0;
+          const double mm = 1.0 - c;
+          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
+          const long long g = g0 + path;
+          int px = 0, py = 0;
+          item_pixel(P, (int)(g / P.spp), px, py);
+          const double u = rng_u(P.seed, (unsigned long long)py * P.W + px, (int)(g % P.spp), depth);
+          refl = u < F;
+          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
+        }
+        if (refl) dn = reflect(dir, nrm);
+        T = mul(T, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      }
+      if (cont) {
+        st3(B.ray, B.cap, path, 0, p);
+        st3(B.ray, B.cap, path, 3, normalize(dn));
+        B.depth[path] = depth + 1;
+      }
+    }
+    B.shcnt[path] = (int)nsh;
+    sf3(B.T, B.cap, path, T);
+    sf3(B.Lr, B.cap, path, L);
+    if constexpr (kDebug) {
+      if (!cont) dbg_bounces[si] = depth;
+    }
+    const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
+    if (cont) qn[slot] = path;
+    warp_stat(stats, 1, nsh);
+    warp_stat(stats, 2, cont ? 1ull : 0ull);
+    warp_stat(stats, 3, (unsigned long long)P.n_spheres);
+    warp_stat(stats, 4, (unsigned long long)P.n_planes);
+  }
+}
+
+// ---- a5 decision + accumulation of the visible lights, in light order ----------------------
+__global__ void __launch_bounds__(256) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
+                                                     unsigned long long* stats) {
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  const int* q = B.q[d & 1];
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int path = q[e];
+    const int cnt = B.shcnt[path];
+    unsigned long long st_sph = 0, st_pl = 0;
+    if (cnt > 0) {
+      const int off = B.shoff[path];
+      const d3 p = ld3(B.hit, B.cap, path, 0), nrm = ld3(B.hit, B.cap, path, 3);
+      float3 L = lf3(B.Lr, B.cap, path);
+      for (int j = off; j < off + cnt; ++j) {
+        const int rob = B.srob[j];
+        bool occluded = false;
+        if (rob <= -2) {  // plane -2-rob occludes (planes are tested first, in index order)
+          occluded = true;
+          st_pl += (unsigned long long)(-2 - rob + 1);
+        } else {
+          st_pl += (unsigned long long)P.n_planes;
+          d3 os, ds;
+          double tl;
+          shadow_ray(S, p, nrm, B.sq_light[j], os, ds, tl);
+          const int nc = B.sn[j];
+          int first = -1;
+          if (nc <= kCandMax) {
+            const int* c = B.scand + (size_t)j * kCandMax;
+            for (int i = 0; i < nc; ++i) {
+              const double t = sphere_root(__ldg(S.sph_cr + c[i]), os, ds);
+              if (t >= kEps && t < tl) { first = c[i]; break; }
+            }
+            if (first < 0) first = rob;
+          } else {
+            for (int k = 0; k < P.n_spheres; ++k) {
+              const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
+              if (t >= kEps && t < tl) { first = k; break; }
+            }
+          }
+          occluded = first >= 0;
+          st_sph += occluded ? (unsigned long long)(first + 1) : (unsigned long long)P.n_spheres;
+        }
+        if (!occluded) L = add(L, lf3(B.sq_c, B.scap, j));
+      }
+      sf3(B.Lr, B.cap, path, L);
+    }
+    warp_stat(stats, 3, st_sph);
+    warp_stat(stats, 4, st_pl);
+  }
+}
+
+// ---- a7: mean over samples in order, 16-byte store ------------------------------------------
+__global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
+    const int w = w0 + i;
+    int px = 0, py = 0;
+    const bool valid = item_pixel(P, w, px, py);
+    if (!valid) {
+      if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    float3 acc = f3(0.f, 0.f, 0.f);
+    for (int s = 0; s < P.spp; ++s) acc = add(acc, lf3(B.Lr, B.cap, i * P.spp + s));
+    const float inv = 1.0f / (float)P.spp;
+    const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, 1.0f);
+    if (P.mode == 0) out[(long long)py * P.W + px] = v;
+    else out[w] = v;
+  }
+}
+
+__global__ void fill_int(int* p, long long n, int v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace rt

@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb200rt.so")
+LIB_PATH = os.environ.get("B200RT_LIB", os.path.join(HERE, "libb200rt.so"))  # override: A/B builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rt.h")
 
 RT_OK = 0
@@ -68,6 +68,7 @@ def lib() -> C.CDLL:
         "rt_stats": [C.POINTER(RayStats)],
         "rt_set_stream": [vp],
         "rt_set_seed": [C.c_uint64],
+        "rt_set_variant": [i32],
         "rt_shard_layout": [i32, i32, i32, C.POINTER(i32), C.POINTER(i64)],
         "rt_render_shard": [i32, i32, i32, i32, i32, i32, vp],
         "rt_assemble_tiles": [vp, i32, i32, i32, vp],
@@ -138,6 +139,14 @@ def camera_set(eye, look_at, up, vfov_deg: float):
 
 def set_seed(seed: int):
     _check("rt_set_seed", lib().rt_set_seed(int(seed)))
+
+
+VARIANTS = {"auto": -1, "megakernel": 0, "wavefront": 1}
+
+
+def set_variant(name: str):
+    """Kernel organisation: "auto" (default), "wavefront" or "megakernel" (bit-identical results)."""
+    _check("rt_set_variant", lib().rt_set_variant(VARIANTS[name]))
 
 
 def set_stream(stream):

@@ -4,13 +4,14 @@ from __future__ import annotations
 import numpy as np
 
 
-def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None):
+def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None, variant="wavefront"):
     import torch
     from paper_1504_03151_b200 import rt
     W = sc.width if width is None else width
     H = sc.height if height is None else height
     D = sc.max_depth if max_depth is None else max_depth
     S = sc.spp if spp is None else spp
+    rt.set_variant(variant)
     rt.load_scene(sc)
     out = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
     if debug:

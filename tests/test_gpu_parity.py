@@ -26,8 +26,8 @@ def _cuda():
     yield
 
 
-def _check(oracle_lib, sc, pixels=None, label=""):
-    g = gpu_render(sc)
+def _check(oracle_lib, sc, pixels=None, label="", variant="wavefront"):
+    g = gpu_render(sc, variant=variant)
     ref = oracle_lib.render(sc, pixels=pixels)
     pix = ref.pixels
     cls = parity.classify(oracle_lib, sc, ref, pixels if pixels is not None else None)
@@ -41,12 +41,31 @@ def _check(oracle_lib, sc, pixels=None, label=""):
     return g, ref, rep
 
 
-def test_c1_full_frame(oracle_lib):
-    _check(oracle_lib, scenegen.get("C1"))
+VARIANTS = ["wavefront", "megakernel"]
 
 
-def test_c2_full_frame(oracle_lib):
-    _check(oracle_lib, scenegen.get("C2"))
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c1_full_frame(oracle_lib, variant):
+    _check(oracle_lib, scenegen.get("C1"), variant=variant, label=f"C1/{variant}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c2_full_frame(oracle_lib, variant):
+    _check(oracle_lib, scenegen.get("C2"), variant=variant, label=f"C2/{variant}")
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_variants_bit_identical(name):
+    # the wavefront and megakernel organisations compute the same terms in the same order
+    sc = scenegen.get(name)
+    if name in ("C3", "C4"):
+        sc = sc.with_frame(width=480, height=270)
+    a = gpu_render(sc, variant="wavefront")
+    b = gpu_render(sc, variant="megakernel")
+    assert (a["rgba"].view(np.uint32) == b["rgba"].view(np.uint32)).all()
+    assert (a["ids"] == b["ids"]).all() and (a["bounces"] == b["bounces"]).all()
+    for k in ("primary", "shadow", "secondary", "sphere_tests", "plane_tests"):
+        assert a["stats"][k] == b["stats"][k], k
 
 
 def test_c2_ragged_deeper_supersampled(oracle_lib):
@@ -55,11 +74,12 @@ def test_c2_ragged_deeper_supersampled(oracle_lib):
     _check(oracle_lib, sc, label="C2-ragged")
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("seed,W,H,D,spp", [(0, 13, 7, 3, 1), (1, 9, 9, 6, 4), (2, 17, 5, 0, 2),
                                             (3, 8, 4, 2, 5), (4, 31, 3, 5, 9), (5, 1, 1, 4, 16)])
-def test_tiny_random_scenes(oracle_lib, seed, W, H, D, spp):
+def test_tiny_random_scenes(oracle_lib, seed, W, H, D, spp, variant):
     sc = scenegen.random_tiny(seed, n_spheres=7, n_planes=2, n_lights=3, width=W, height=H, max_depth=D, spp=spp)
-    _check(oracle_lib, sc, label=f"tiny{seed}")
+    _check(oracle_lib, sc, label=f"tiny{seed}/{variant}", variant=variant)
 
 
 def test_c3_full_size_sampled(oracle_lib):
@@ -68,10 +88,11 @@ def test_c3_full_size_sampled(oracle_lib):
     _check(oracle_lib, sc, pixels=pix, label="C3@1080p")
 
 
-def test_c4_full_size_sampled(oracle_lib):
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c4_full_size_sampled(oracle_lib, variant):
     sc = scenegen.get("C4")
     pix = np.random.default_rng(44).choice(sc.width * sc.height, 3000, replace=False)
-    _check(oracle_lib, sc, pixels=pix, label="C4@1080p")
+    _check(oracle_lib, sc, pixels=pix, label=f"C4@1080p/{variant}", variant=variant)
 
 
 def test_c4_full_size_counts_consistent(oracle_lib):
