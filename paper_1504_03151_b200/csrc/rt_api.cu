@@ -170,11 +170,10 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     if (items < 1) items = 1;
     const int cap = items * p.spp;
     const int scap = cap * (c.n_lights > 0 ? c.n_lights : 1);
-    if (c.wf.cap < cap || c.wf.scap < scap) {
-      CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap) + 64 * 256), "cudaMalloc(wavefront)");
-      CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-      rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
-    }
+    // (re)carve for this frame's cap: per-light queues are indexed l * cap + slot
+    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap) + 64 * 256), "cudaMalloc(wavefront)");
+    CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
+    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
     CU(rt::launch_render_wavefront(p, sc, o, c.smem_scene, c.num_sms, c.wf, c.stream), "wavefront launch");
     CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
