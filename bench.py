@@ -236,24 +236,26 @@ def run_b200(args):
     if world > 1:
         rend = ShardedRenderer(CudaBackend(dev), W, H, D, S)
         step = rend.render
-        launches_per_step = rend.launches_per_frame
     else:
         out = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
         step = lambda: rt.render(W, H, D, S, out)  # noqa: E731
-        launches_per_step = 1
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3 if args.strict else 0)):
+    for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step()
+    if world > 1:  # kernels per frame on this rank: the shard render (+ assembly on rank 0)
+        rt.render_shard(W, H, D, S, rank, world, rend.slab)
+        launches_per_step = rt.stats()["launches"] + (2 if rank == 0 else 0)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    per_frame = []
     barrier()
     t_wall0 = time.perf_counter()
     for i in range(args.steps):
@@ -261,12 +263,16 @@ def run_b200(args):
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)
+        if world == 1:
+            per_frame.append(rt.stats())    # per-kernel event times of this frame (host sync only)
     barrier()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
     frame_ms = [a.elapsed_time(b) for a, b in evs]
     my_total = sum(frame_ms)
     st = rt.stats()  # last frame (rank 0 holds the all-rank sum after assembly)
+    if world == 1:
+        launches_per_step = per_frame[-1]["launches"]
     t = torch.tensor([my_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -299,16 +305,29 @@ def run_b200(args):
         rays = st["primary"] + st["shadow"] + st["secondary"]
         ms_per_step = total_ms / args.steps
         value = rays / (ms_per_step * 1e-3) / 1e6
-        # roofline: counted algorithmic flops of the render kernel per launch / its event time
-        flops = FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"]
+        # roofline of the dominant kernel (19 flops per ray-sphere test, 12 per
+        # ray-plane test) = algorithmic flops per launch / its CUDA-event launch time
         props = torch.cuda.get_device_properties(dev)
         sms = props.multi_processor_count
         sm_max = clk.get("sm_max_mhz") or PEAK_FALLBACK_MHZ
         peak = sms * 128 * 2 * sm_max * 1e6 / 1e12
-        # N=1: the frame events bracket exactly the render kernel (+2 tiny memsets); N>1: the
-        # per-rank share of the flops over the frame time (includes the all-gather + assembly)
-        achieved = flops / world / (ms_per_step * 1e-3) / 1e12
         traffic = _load_profile_traffic(args.config) if world == 1 else None
+        if world == 1 and per_frame[-1]["variant"] == 1:
+            tc = sum(f["isect_closest_ms"] for f in per_frame)
+            ts = sum(f["isect_shadow_ms"] for f in per_frame)
+            nc = sum(f["closest_sphere_tests"] for f in per_frame)
+            ns = sum(f["sphere_tests"] - f["closest_sphere_tests"] for f in per_frame)
+            achieved = FLOP_SPHERE * nc / (tc * 1e-3) / 1e12
+            kernel = "wf_isect<closest> (FP32 FFMA2 sphere scan of closest-hit rays; 41% of the frame in the ncu launch list)"
+            extra = {"share_of_frame": tc / total_ms,
+                     "shadow_kernel": {"achieved": FLOP_SPHERE * ns / (ts * 1e-3) / 1e12, "share_of_frame": ts / total_ms},
+                     "whole_frame_achieved": (FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"])
+                     / (ms_per_step * 1e-3) / 1e12}
+        else:
+            flops = FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"]
+            achieved = flops / world / (total_ms / args.steps * 1e-3) / 1e12
+            kernel = "render_kernel (megakernel)" if world == 1 else "whole shard frame incl. all-gather"
+            extra = {}
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -321,8 +340,7 @@ def run_b200(args):
                            secondary=int(st["secondary"]), sphere_tests=int(st["sphere_tests"]),
                            plane_tests=int(st["plane_tests"]), wall_s=t_wall),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "render_kernel (persistent megakernel)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel, **extra,
                          "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (derived, DESIGN.md)",
                          "flops_basis": "19 flops/sphere test + 12/plane test (SURVEY 8(d).3) x algorithmic test counts"},
             "clocks": clk,

@@ -99,7 +99,7 @@ typedef struct {
  * plane_tests are the algorithmic test counts of SURVEY §8(c).1 step 11 (closest-hit rays
  * test every primitive; shadow rays stop at the first occluder in index order when planes
  * precede spheres in the primitive list). last_render_ms: device time of the render kernel
- * (CUDA events on the library stream; 0 for rt_assemble_tiles). */
+ * (CUDA events on the library stream; 0 for rt_assemble_tiles). 80 bytes. */
 typedef struct {
   uint64_t primary;
   uint64_t shadow;
@@ -107,6 +107,12 @@ typedef struct {
   uint64_t sphere_tests;
   uint64_t plane_tests;
   double last_render_ms;
+  uint64_t closest_sphere_tests; /* part of sphere_tests done by closest-hit (primary/secondary) rays */
+  double isect_closest_ms;       /* wavefront: summed device time of the closest-hit intersection
+                                    kernels (CUDA events around each launch); 0 for the megakernel */
+  double isect_shadow_ms;        /* wavefront: same for the shadow-ray intersection kernels */
+  uint32_t launches;             /* kernels of this library launched by the call */
+  int32_t variant;               /* RT_VARIANT_MEGAKERNEL or RT_VARIANT_WAVEFRONT actually used */
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane
@@ -158,7 +164,7 @@ const char* rt_last_error(void);
 /* Shard layout for `world` ranks: the image is cut into RT_TILE_W x RT_TILE_H tiles; tile t
  * belongs to rank t % world (cyclic). tiles_per_rank = ceil(n_tiles / world); slab_bytes =
  * tiles_per_rank * 32 * 16 + 64 (pixel slab, tile-major, then a 64-byte stats record of 8
- * uint64: primary, shadow, secondary, sphere_tests, plane_tests, 0, 0, 0). */
+ * uint64: primary, shadow, secondary, sphere_tests, plane_tests, closest_sphere_tests, 0, 0). */
 int rt_shard_layout(int32_t width, int32_t height, int32_t world, int32_t* tiles_per_rank,
                     int64_t* slab_bytes);
 

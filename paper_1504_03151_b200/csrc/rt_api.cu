@@ -80,6 +80,8 @@ struct Context {
   DevBuf<unsigned char> wf_mem;
   DevBuf<unsigned> wf_ctr;
   rt::WfBuffers wf{};
+  std::vector<cudaEvent_t> ev_c, ev_s;  // per-launch intersection timing (wavefront)
+  int n_timed = 0, last_launches = 0, last_variant = 0;
   // camera (double basis)
   bool has_camera = false;
   double eye[3], f[3], r[3], u[3], h = 0;
@@ -174,14 +176,29 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap) + 64 * 256), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
     rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
+    const int pairs = rt::wf_timing_pairs(p, cap);
+    while ((int)c.ev_c.size() < 2 * pairs) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a), "cudaEventCreate");
+      CU(cudaEventCreate(&b), "cudaEventCreate");
+      c.ev_c.push_back(a);
+      c.ev_s.push_back(b);
+    }
+    rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
-    CU(rt::launch_render_wavefront(p, sc, o, c.smem_scene, c.num_sms, c.wf, c.stream), "wavefront launch");
+    CU(rt::launch_render_wavefront(p, sc, o, c.smem_scene, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
     CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
+    c.n_timed = tm.n;
+    c.last_launches = tm.launches;
+    c.last_variant = RT_VARIANT_WAVEFRONT;
     return RT_OK;
   }
   CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
   CU(rt::launch_render(p, sc, o, c.smem_scene, c.num_sms, c.stream), "render kernel launch");
   CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
+  c.n_timed = 0;
+  c.last_launches = 1;
+  c.last_variant = RT_VARIANT_MEGAKERNEL;
   return RT_OK;
 }
 
@@ -205,7 +222,22 @@ int collect_stats(bool timed) {
   c.last.secondary = h[2];
   c.last.sphere_tests = h[3];
   c.last.plane_tests = h[4];
+  c.last.closest_sphere_tests = h[5];
   c.last.last_render_ms = ms;
+  double tc = 0.0, ts = 0.0;
+  if (timed) {
+    for (int i = 0; i < c.n_timed; ++i) {
+      float a = 0.f, b = 0.f;
+      CU(cudaEventElapsedTime(&a, c.ev_c[2 * i], c.ev_c[2 * i + 1]), "cudaEventElapsedTime");
+      CU(cudaEventElapsedTime(&b, c.ev_s[2 * i], c.ev_s[2 * i + 1]), "cudaEventElapsedTime");
+      tc += a;
+      ts += b;
+    }
+  }
+  c.last.isect_closest_ms = tc;
+  c.last.isect_shadow_ms = ts;
+  c.last.launches = timed ? (uint32_t)c.last_launches : 2u;
+  c.last.variant = c.last_variant;
   return RT_OK;
 }
 

@@ -71,7 +71,8 @@ struct DevScene {
 struct DevOutputs {
   float4* out;                  // framebuffer (mode 0) or slab (mode 1)
   unsigned int* work_counter;   // persistent work queue head
-  unsigned long long* stats;    // [5] primary, shadow, secondary, sphere_tests, plane_tests
+  unsigned long long* stats;    // [6] primary, shadow, secondary, sphere_tests, plane_tests,
+                                //     closest_sphere_tests
   int* dbg_hits;                // optional [n_px * spp * (max_depth+1)]
   int* dbg_bounces;             // optional [n_px * spp]
 };
@@ -113,8 +114,17 @@ cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutpu
                           bool smem_scene, int num_sms, cudaStream_t st);
 size_t wf_bytes(int cap, int scap);
 void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr);
+// per-launch CUDA events around the intersection kernels (pairs: [2i] before, [2i+1] after)
+struct WfTiming {
+  cudaEvent_t* closest;
+  cudaEvent_t* shadow;
+  int cap;        // pairs available in each array
+  int n;          // pairs recorded (output)
+  int launches;   // kernels launched (output)
+};
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
-                                    int num_sms, WfBuffers& B, cudaStream_t st);
+                                    int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st);
+int wf_timing_pairs(const DevParams& p, int cap_paths);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,

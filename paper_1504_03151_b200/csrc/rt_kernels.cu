@@ -41,7 +41,7 @@ struct Lane {
   float3 contrib;
   // stats
   unsigned n_primary, n_shadow, n_secondary;
-  unsigned long long n_stests, n_ptests;
+  unsigned long long n_stests, n_ptests, n_ctests;
 };
 
 __device__ __forceinline__ void start_sample(Lane& L, const DevParams& P) {
@@ -213,6 +213,7 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
   // algorithmic test counts
   if (L.qkind == Q_CLOSEST) {
     L.n_stests += (unsigned)P.n_spheres;
+    L.n_ctests += (unsigned)P.n_spheres;
     L.n_ptests += (unsigned)P.n_planes;
   } else if (L.qkind == Q_SHADOW) {
     if (hp >= 0) {
@@ -387,7 +388,7 @@ render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
   Lane L;
   L.item = -1; L.qkind = Q_NONE;
   L.n_primary = L.n_shadow = L.n_secondary = 0;
-  L.n_stests = L.n_ptests = 0ull;
+  L.n_stests = L.n_ptests = L.n_ctests = 0ull;
   L.hit_sph = L.hit_pl = -1;
   bool exhausted = false;
 
@@ -412,15 +413,15 @@ render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
   }
 
   // stats: warp reduction, one atomic per warp
-  unsigned long long v[5] = {L.n_primary, L.n_shadow, L.n_secondary, L.n_stests, L.n_ptests};
+  unsigned long long v[6] = {L.n_primary, L.n_shadow, L.n_secondary, L.n_stests, L.n_ptests, L.n_ctests};
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < 6; ++k) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(kFull, v[k], off);
   }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 5; ++k) atomicAdd(O.stats + k, v[k]);
+    for (int k = 0; k < 6; ++k) atomicAdd(O.stats + k, v[k]);
   }
 }
 
@@ -441,7 +442,7 @@ __global__ void assemble_kernel(const float4* __restrict__ g, int W, int H, int 
 
 __global__ void sum_stats_kernel(const float4* __restrict__ g, int world, int tpr,
                                  unsigned long long* stats) {
-  if (threadIdx.x < 5) {
+  if (threadIdx.x < 6) {
     const long long slab_f4 = (long long)tpr * kTilePx + 4;
     unsigned long long s = 0;
     for (int r = 0; r < world; ++r) {
@@ -556,9 +557,15 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.ctr = ctr;
 }
 
+int wf_timing_pairs(const DevParams& p, int cap_paths) {
+  const int items_per_chunk = cap_paths / p.spp;
+  const int chunks = (p.n_items + items_per_chunk - 1) / items_per_chunk;
+  return chunks * (p.max_depth + 1);
+}
+
 template <bool kSmem>
 static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
-                          WfBuffers& B, cudaStream_t st) {
+                          WfBuffers& B, WfTiming& tm, cudaStream_t st) {
   const bool dbg = o.dbg_hits != nullptr;
   const size_t smem = kSmem ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
@@ -572,9 +579,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
   const int grid_l = num_sms * 8;
   const int items_per_chunk = B.cap / p.spp;
+  tm.n = 0;
+  tm.launches = 0;
   if (dbg) {
     const long long nh = (long long)p.W * p.H * p.spp * (p.max_depth + 1);
     fill_int<<<num_sms * 8, 256, 0, st>>>(o.dbg_hits, nh, -2);
+    ++tm.launches;
   }
   for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk) {
     const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
@@ -584,21 +594,29 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
     wf_raygen<<<grid_r, 256, 0, st>>>(p, B, g0, npaths, o.stats);
     for (int d = 0; d <= p.max_depth; ++d) {
+      const bool rec = tm.n < tm.cap;
+      if (rec) cudaEventRecord(tm.closest[2 * tm.n], st);
       wf_isect<kSmem, false><<<grid_c, 256, smem, st>>>(p, sc, B, d);
+      if (rec) cudaEventRecord(tm.closest[2 * tm.n + 1], st);
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
+      if (rec) cudaEventRecord(tm.shadow[2 * tm.n], st);
       wf_isect<kSmem, true><<<grid_s, 256, smem, st>>>(p, sc, B, d);
+      if (rec) cudaEventRecord(tm.shadow[2 * tm.n + 1], st);
       wf_accumulate<<<grid_l, 256, 0, st>>>(p, sc, B, d, o.stats);
+      if (rec) ++tm.n;
+      tm.launches += 4;
     }
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
     wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out);
+    tm.launches += 2;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
-                                    int num_sms, WfBuffers& B, cudaStream_t st) {
-  return smem_scene ? wf_run<true>(p, sc, o, num_sms, B, st) : wf_run<false>(p, sc, o, num_sms, B, st);
+                                    int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st) {
+  return smem_scene ? wf_run<true>(p, sc, o, num_sms, B, tm, st) : wf_run<false>(p, sc, o, num_sms, B, tm, st);
 }
 
 }  // namespace rt

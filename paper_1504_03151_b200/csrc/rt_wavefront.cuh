@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(256) wf_shade(const DevParams P, const DevScen
     warp_stat(stats, 2, cont ? 1ull : 0ull);
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
+    warp_stat(stats, 5, (unsigned long long)P.n_spheres);
   }
 }
 
