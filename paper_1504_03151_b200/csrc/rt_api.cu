@@ -65,6 +65,7 @@ struct Context {
   // scene
   bool has_scene = false;
   bool smem_scene = true;
+  bool const_scene = true;
   int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
   float cmax = 0.f, rmax = 0.f;
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
@@ -186,7 +187,11 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     }
     rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
-    CU(rt::launch_render_wavefront(p, sc, o, c.smem_scene, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    #ifndef RT_WF_PREFER_CONST
+#define RT_WF_PREFER_CONST 0
+#endif
+    const int src = (RT_WF_PREFER_CONST && c.const_scene) ? 2 : (c.smem_scene ? 1 : 0);
+    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
     CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
     c.n_timed = tm.n;
     c.last_launches = tm.launches;
@@ -437,9 +442,12 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(cudaMemcpyAsync(c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
-  CU(rt::upload_const_scene(planes.data(), np, c.stream), "constant upload");
+  const bool in_const = npairs_pad <= rt::kMaxConstPairs;
+  CU(rt::upload_const_scene(planes.data(), np, pairs.data(), in_const ? (int)pairs.size() : 0, c.stream),
+     "constant upload");
   CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
   c.smem_scene = in_smem;
+  c.const_scene = in_const;
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
   c.rmax = (float)(rmax * (1.0 + 1e-6));
   c.n_spheres = ns;

@@ -123,9 +123,14 @@ __device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pai
 // ---- intersection (a3 closest-hit + a5 any-hit), one loop for the whole warp -----------------
 extern __shared__ float4 s_pairs[];
 
-template <bool kSmem>
+// where the sphere-pair array is read from inside the scans
+enum : int { SRC_GLOBAL = 0, SRC_SMEM = 1, SRC_CONST = 2 };
+__constant__ float4 c_pairs[2 * kMaxConstPairs];
+
+template <int kSrc>
 __device__ __forceinline__ float4 load_pair(const float4* __restrict__ gp, int i) {
-  if constexpr (kSmem) return s_pairs[i];  // warp-uniform address: LDS.128 broadcast
+  if constexpr (kSrc == SRC_SMEM) return s_pairs[i];       // warp-uniform address: LDS.128 broadcast
+  else if constexpr (kSrc == SRC_CONST) return c_pairs[i];  // uniform index: LDCU.128 -> UR operands
   else return __ldg(gp + i);
 }
 
@@ -173,15 +178,15 @@ struct RayFilter {
     neg_slack = -(4.0f * eta * P.rmax + 4.0f * eta * eta + 4.0f * kUlp * P.rmax * P.rmax);
   }
   // disc of 16 spheres (pairs base..base+7) with two spheres per FFMA2; returns their max
-  template <bool kSmem>
+  template <int kSrc>
   __device__ __forceinline__ float batch(const float4* __restrict__ gp, int base, float2 (&disc)[kPairsPerBatch]) const {
     const float2 U1x = make_float2(u1x, u1x), U1y = make_float2(u1y, u1y), U1z = make_float2(u1z, u1z);
     const float2 U2x = make_float2(u2x, u2x), U2y = make_float2(u2y, u2y), U2z = make_float2(u2z, u2z);
     const float2 OU1 = make_float2(ou1, ou1), OU2 = make_float2(ou2, ou2);
 #pragma unroll
     for (int i = 0; i < kPairsPerBatch; ++i) {
-      const float4 a = load_pair<kSmem>(gp, 2 * (base + i));
-      const float4 b = load_pair<kSmem>(gp, 2 * (base + i) + 1);
+      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
       const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
       const float2 CZ = make_float2(b.x, b.y), R2 = make_float2(b.z, b.w);
       const float2 x = __ffma2_rn(CX, U1x, __ffma2_rn(CY, U1y, __ffma2_rn(CZ, U1z, OU1)));
@@ -195,10 +200,10 @@ struct RayFilter {
     return dmax;
   }
   // float lateral disc, chord centre tc and bounds of one sphere k (rare path)
-  template <bool kSmem>
+  template <int kSrc>
   __device__ __forceinline__ void sphere(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
-    const float4 pa = load_pair<kSmem>(gp, 2 * (k >> 1));
-    const float4 pb = load_pair<kSmem>(gp, 2 * (k >> 1) + 1);
+    const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
+    const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
     const bool h = k & 1;
     const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, r2 = h ? pb.w : pb.z;
     const float lx = fmaf(cx, u1x, fmaf(cy, u1y, fmaf(cz, u1z, ou1)));

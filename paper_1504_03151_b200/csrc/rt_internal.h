@@ -25,6 +25,7 @@ namespace rt {
 constexpr int kWarp = 32;
 constexpr int kPairsPerBatch = 8;   // 16 spheres per unrolled batch of the intersection loop
 constexpr int kMaxSmemPairs = 5120;  // 10240 spheres = 160 KB of dynamic shared memory per CTA
+constexpr int kMaxConstPairs = 1536; // 3072 spheres = 48 KB of the 64 KB constant bank
 constexpr int kMaxPlanes = 32;
 constexpr int kMaxLights = 32;
 constexpr int kTileW = 8, kTileH = 4, kTilePx = kTileW * kTileH;
@@ -109,7 +110,8 @@ __host__ __device__ constexpr int wf_ctr_ws(int d) { return 4 * d + 3; }
 constexpr int kWfCtrPerDepth = 4;
 
 // launchers (rt_kernels.cu)
-cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, cudaStream_t st);
+cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float4* pairs, int n_pair_float4,
+                               cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
 size_t wf_bytes(int cap, int scap);
@@ -122,7 +124,8 @@ struct WfTiming {
   int n;          // pairs recorded (output)
   int launches;   // kernels launched (output)
 };
-cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
+// scene source of the wavefront intersection kernels: 0 global, 1 shared memory, 2 constant bank
+cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st);
 int wf_timing_pairs(const DevParams& p, int cap_paths);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,

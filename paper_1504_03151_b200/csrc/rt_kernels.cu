@@ -133,8 +133,8 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       cand &= cand - 1u;
       const int k = 2 * base + i;  // pair (base + i/2), half i&1
       if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds r^2 = 1)
-      const float4 pa = load_pair<kSmem>(pairs, 2 * (base + (i >> 1)));
-      const float4 pb = load_pair<kSmem>(pairs, 2 * (base + (i >> 1)) + 1);
+      const float4 pa = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + (i >> 1)));
+      const float4 pb = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + (i >> 1)) + 1);
       const float cx = (i & 1) ? pa.y : pa.x, cy = (i & 1) ? pa.w : pa.z, cz = (i & 1) ? pb.y : pb.x;
       const float r2 = (i & 1) ? pb.w : pb.z;
       const float lx = fmaf(cx, u1x, fmaf(cy, u1y, fmaf(cz, u1z, ou1)));
@@ -170,8 +170,8 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       float2 disc[kPairsPerBatch];
 #pragma unroll
       for (int i = 0; i < kPairsPerBatch; ++i) {
-        const float4 a = load_pair<kSmem>(pairs, 2 * (base + i));
-        const float4 b = load_pair<kSmem>(pairs, 2 * (base + i) + 1);
+        const float4 a = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + i));
+        const float4 b = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + i) + 1);
         const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
         const float2 CZ = make_float2(b.x, b.y), R2 = make_float2(b.z, b.w);
         const float2 x = __ffma2_rn(CX, U1x, __ffma2_rn(CY, U1y, __ffma2_rn(CZ, U1z, OU1)));
@@ -469,9 +469,12 @@ __global__ void tonemap_kernel(const float4* __restrict__ in, uchar4* __restrict
 }
 
 // ---- launchers ------------------------------------------------------------------------------
-cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, cudaStream_t st) {
+cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float4* pairs, int n_pair_float4,
+                               cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  if (n_planes > 0)
+  if (n_pair_float4 > 0)
+    e = cudaMemcpyToSymbolAsync(c_pairs, pairs, sizeof(float4) * n_pair_float4, 0, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && n_planes > 0)
     e = cudaMemcpyToSymbolAsync(c_planes, planes, sizeof(DevPlane) * n_planes, 0,
                                 cudaMemcpyHostToDevice, st);
   return e;
@@ -563,19 +566,19 @@ int wf_timing_pairs(const DevParams& p, int cap_paths) {
   return chunks * (p.max_depth + 1);
 }
 
-template <bool kSmem>
+template <int kSrc>
 static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
                           WfBuffers& B, WfTiming& tm, cudaStream_t st) {
   const bool dbg = o.dbg_hits != nullptr;
-  const size_t smem = kSmem ? (size_t)p.n_pairs_pad * 32u : 0u;
+  const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
   int occ_c = 0, occ_s = 0;
-  for (auto fn : {wf_isect<kSmem, false>, wf_isect<kSmem, true>}) {
+  for (auto fn : {wf_isect<kSrc, false>, wf_isect<kSrc, true>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSmem, false>, 256, smem)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSmem, true>, 256, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSrc, false>, 256, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
   const int grid_l = num_sms * 8;
   const int items_per_chunk = B.cap / p.spp;
@@ -596,12 +599,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     for (int d = 0; d <= p.max_depth; ++d) {
       const bool rec = tm.n < tm.cap;
       if (rec) cudaEventRecord(tm.closest[2 * tm.n], st);
-      wf_isect<kSmem, false><<<grid_c, 256, smem, st>>>(p, sc, B, d);
+      wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, d);
       if (rec) cudaEventRecord(tm.closest[2 * tm.n + 1], st);
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
       if (rec) cudaEventRecord(tm.shadow[2 * tm.n], st);
-      wf_isect<kSmem, true><<<grid_s, 256, smem, st>>>(p, sc, B, d);
+      wf_isect<kSrc, true><<<grid_s, 256, smem, st>>>(p, sc, B, d);
       if (rec) cudaEventRecord(tm.shadow[2 * tm.n + 1], st);
       wf_accumulate<<<grid_l, 256, 0, st>>>(p, sc, B, d, o.stats);
       if (rec) ++tm.n;
@@ -614,9 +617,11 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   return cudaGetLastError();
 }
 
-cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
+cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st) {
-  return smem_scene ? wf_run<true>(p, sc, o, num_sms, B, tm, st) : wf_run<false>(p, sc, o, num_sms, B, tm, st);
+  if (src == SRC_CONST) return wf_run<SRC_CONST>(p, sc, o, num_sms, B, tm, st);
+  if (src == SRC_SMEM) return wf_run<SRC_SMEM>(p, sc, o, num_sms, B, tm, st);
+  return wf_run<SRC_GLOBAL>(p, sc, o, num_sms, B, tm, st);
 }
 
 }  // namespace rt

@@ -105,11 +105,11 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
 }
 
 // ---- a3 / a5: FP32 filter over all spheres (persistent, one warp = 32 rays) -----------------
-template <bool kSmem, bool kShadow>
+template <int kSrc, bool kShadow>
 __global__ void __launch_bounds__(256, 3)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   __shared__ uint64_t s_mbar;
-  if constexpr (kSmem) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
+  if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
   const float4* gp = S.pairs;
   const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
   unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
@@ -154,7 +154,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     int nc = 0;
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
-      const float dmax = F.batch<kSmem>(gp, base, disc);
+      const float dmax = F.batch<kSrc>(gp, base, disc);
       const bool any = act && dmax >= F.neg_slack;
       if (__any_sync(kFull, any)) {
         if (any) {
@@ -165,7 +165,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
             const int k = 2 * base + i;
             if (k >= P.n_spheres) break;
             float dd, tc;
-            F.sphere<kSmem>(gp, k, dd, tc);
+            F.sphere<kSrc>(gp, k, dd, tc);
             const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
             const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
             const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
