@@ -68,6 +68,7 @@ struct Context {
   bool const_scene = true;
   int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
   float cmax = 0.f, rmax = 0.f;
+  double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage;
   DevBuf<int> sph_prim, sph_mat;
@@ -140,6 +141,7 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   }
   p.cmax = c.cmax;
   p.rmax = c.rmax;
+  for (int i = 0; i < 3; ++i) p.centre[i] = c.centre[i];
   p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
   p.seed = c.seed;
@@ -381,9 +383,20 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   const int npairs = (ns + 1) / 2;
   const int npairs_pad = ((npairs + rt::kPairsPerBatch - 1) / rt::kPairsPerBatch) * rt::kPairsPerBatch;
   std::vector<float4> pairs(2 * (size_t)npairs_pad);
-  for (int q = 0; q < npairs_pad; ++q) {  // dummies: r^2 = -1 never intersects
+  // filter frame: centre of the spheres' bounding box (expanded form works in c' = c - centre)
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int i = 0; i < n_prims; ++i)
+    if (prims[i].type == RT_PRIM_SPHERE)
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = std::fmin(lo[k], (double)prims[i].p[k]);
+        hi[k] = std::fmax(hi[k], (double)prims[i].p[k]);
+      }
+  double centre[3] = {0, 0, 0};
+  if (ns > 0)
+    for (int k = 0; k < 3; ++k) centre[k] = (double)(float)(0.5 * (lo[k] + hi[k]));
+  for (int q = 0; q < npairs_pad; ++q) {  // dummies never pass the filter
     pairs[2 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    pairs[2 * q + 1] = make_float4(0.f, 0.f, -1.f, -1.f);
+    pairs[2 * q + 1] = RT_FILTER_EXPANDED ? make_float4(0.f, 0.f, -1e30f, -1e30f) : make_float4(0.f, 0.f, -1.f, -1.f);
   }
   std::vector<float4> cr(ns > 0 ? ns : 1);
   std::vector<int> sprim(ns > 0 ? ns : 1), smat(ns > 0 ? ns : 1);
@@ -393,14 +406,26 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   for (int i = 0; i < n_prims; ++i) {
     const rt_primitive& q = prims[i];
     if (q.type == RT_PRIM_SPHERE) {
-      const double cn = std::fabs((double)q.p[0]) + std::fabs((double)q.p[1]) + std::fabs((double)q.p[2]);
-      if (cn > cmax) cmax = cn;
       if (q.p[3] > rmax) rmax = q.p[3];
-      const float r2 = q.p[3] * q.p[3];
+      float f0, f1, f2, f3;
+#if RT_FILTER_EXPANDED
+      // c' = c - centre (float), K = r^2 - |c'|^2 (double, rounded once)
+      f0 = (float)((double)q.p[0] - centre[0]);
+      f1 = (float)((double)q.p[1] - centre[1]);
+      f2 = (float)((double)q.p[2] - centre[2]);
+      const double r = q.p[3];
+      f3 = (float)(r * r - ((double)f0 * f0 + (double)f1 * f1 + (double)f2 * f2));
+      const double cn = std::sqrt((double)f0 * f0 + (double)f1 * f1 + (double)f2 * f2);
+#else
+      f0 = q.p[0]; f1 = q.p[1]; f2 = q.p[2];
+      f3 = q.p[3] * q.p[3];
+      const double cn = std::fabs((double)q.p[0]) + std::fabs((double)q.p[1]) + std::fabs((double)q.p[2]);
+#endif
+      if (cn > cmax) cmax = cn;
       float* A = reinterpret_cast<float*>(&pairs[2 * (ks / 2)]);
       float* B = reinterpret_cast<float*>(&pairs[2 * (ks / 2) + 1]);
       const int h = ks & 1;
-      A[0 + h] = q.p[0]; A[2 + h] = q.p[1]; B[0 + h] = q.p[2]; B[2 + h] = r2;
+      A[0 + h] = f0; A[2 + h] = f1; B[0 + h] = f2; B[2 + h] = f3;
       cr[ks] = make_float4(q.p[0], q.p[1], q.p[2], q.p[3]);
       sprim[ks] = i;
       smat[ks] = (int)q.material;
@@ -449,6 +474,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   c.smem_scene = in_smem;
   c.const_scene = in_const;
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
+  for (int k = 0; k < 3; ++k) c.centre[k] = RT_FILTER_EXPANDED ? centre[k] : 0.0;
   c.rmax = (float)(rmax * (1.0 + 1e-6));
   c.n_spheres = ns;
   c.n_pairs_pad = npairs_pad;

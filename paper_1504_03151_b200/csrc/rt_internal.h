@@ -20,6 +20,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef RT_FILTER_EXPANDED
+#define RT_FILTER_EXPANDED 1  // float32 filter form, see RayFilter (rt_device.cuh)
+#endif
+
 namespace rt {
 
 constexpr int kWarp = 32;
@@ -51,7 +55,9 @@ struct DevParams {
   // camera (basis in double): d = normalize(F + (2sx-1) R + (1-2sy) U)
   double eye[3], F[3], R[3], U[3];
   float bg[3], amb[3];
-  float cmax;   // max over spheres of |c| (float filter error bound)
+  double centre[3];  // scene centre (bounding box of the spheres): origin of the filter frame
+  float cmax;   // filter error bound: max over spheres of |c'| (expanded form, c' = c - centre)
+                //   or of |c|_1 (projected form)
   float rmax;   // max sphere radius
   int W, H, max_depth, spp;
   int n_spheres, n_pairs_pad, n_planes, n_lights;

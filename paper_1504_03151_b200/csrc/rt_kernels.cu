@@ -104,45 +104,24 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
     }
   }
 
-  // Spheres, float32 filter: orthonormal basis (u1, u2) of d (Duff et al. 2017); lateral
-  // coordinates x = (c - o).u1, y = (c - o).u2 of each centre; disc = r^2 - x^2 - y^2 (the
-  // precise discriminant of Eq. 11-12 with a = 1), two spheres per FFMA2. A sphere is a
-  // candidate when disc >= -slack, slack bounding the float error.
-  const float ox = (float)o.x, oy = (float)o.y, oz = (float)o.z;
-  const float dx = (float)d.x, dy = (float)d.y, dz = (float)d.z;
-  const float sg = copysignf(1.0f, dz);
-  const float ia = -1.0f / (sg + dz);
-  const float bb = dx * dy * ia;
-  const float u1x = fmaf(sg * dx * dx, ia, 1.0f), u1y = sg * bb, u1z = -sg * dx;
-  const float u2x = bb, u2y = fmaf(dy * dy, ia, sg), u2z = -dy;
-  const float ou1 = -fmaf(ox, u1x, fmaf(oy, u1y, oz * u1z));
-  const float ou2 = -fmaf(ox, u2x, fmaf(oy, u2y, oz * u2z));
-  const float eta = 32.0f * kUlp * (fabsf(ox) + fabsf(oy) + fabsf(oz) + P.cmax);
-  const float odf = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));
-  const float neg_slack = -(4.0f * eta * P.rmax + 4.0f * eta * eta + 4.0f * kUlp * P.rmax * P.rmax);
-  const float2 U1x = make_float2(u1x, u1x), U1y = make_float2(u1y, u1y), U1z = make_float2(u1z, u1z);
-  const float2 U2x = make_float2(u2x, u2x), U2y = make_float2(u2y, u2y), U2z = make_float2(u2z, u2z);
-  const float2 OU1 = make_float2(ou1, ou1), OU2 = make_float2(ou2, ou2);
+  // Spheres: float32 filter (RayFilter), candidates decided in float64.
+  RayFilter F;
+  F.init(o, d, P);
+  constexpr int kSrc = kSmem ? SRC_SMEM : SRC_GLOBAL;
   // Candidates of one 16-sphere batch (mask bit i = sphere 2*base + i), in index order:
   // float range prefilter (the chord [tc - q, tc + q] lies before EPS_T or beyond tmax with
   // margin: tc error <= eta, q <= sqrt(disc_f + slack)), then the float64 decision.
   auto process = [&](unsigned cand, int base) {
-    const float tmax_hi = (float)tmax * 1.000001f + eta;
+    const float tmax_hi = (float)tmax * 1.000001f + F.eta;
     while (cand != 0u && act) {
       const int i = __ffs(cand) - 1;
       cand &= cand - 1u;
       const int k = 2 * base + i;  // pair (base + i/2), half i&1
-      if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds r^2 = 1)
-      const float4 pa = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + (i >> 1)));
-      const float4 pb = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + (i >> 1)) + 1);
-      const float cx = (i & 1) ? pa.y : pa.x, cy = (i & 1) ? pa.w : pa.z, cz = (i & 1) ? pb.y : pb.x;
-      const float r2 = (i & 1) ? pb.w : pb.z;
-      const float lx = fmaf(cx, u1x, fmaf(cy, u1y, fmaf(cz, u1z, ou1)));
-      const float ly = fmaf(cx, u2x, fmaf(cy, u2y, fmaf(cz, u2z, ou2)));
-      const float dd = fmaf(-lx, lx, fmaf(-ly, ly, r2));  // == the FFMA2 lane value
-      const float tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, odf)));
-      const float qh = sqrtf(fmaxf(dd - neg_slack, 0.f));
-      if (tc + qh < (float)kEps - eta || tc - qh > tmax_hi) continue;
+      if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds the dummy margin)
+      float dd, tc;
+      F.sphere<kSrc>(pairs, k, dd, tc);
+      const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));
+      if (tc + qh < (float)kEps - F.eta || tc - qh > tmax_hi) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
       if (t >= kEps && t < tmax) {
         hs = k; hp = -1;
@@ -168,29 +147,11 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
   if (__any_sync(kFull, act)) {
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
-#pragma unroll
-      for (int i = 0; i < kPairsPerBatch; ++i) {
-        const float4 a = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + i));
-        const float4 b = load_pair<kSmem ? SRC_SMEM : SRC_GLOBAL>(pairs, 2 * (base + i) + 1);
-        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-        const float2 CZ = make_float2(b.x, b.y), R2 = make_float2(b.z, b.w);
-        const float2 x = __ffma2_rn(CX, U1x, __ffma2_rn(CY, U1y, __ffma2_rn(CZ, U1z, OU1)));
-        const float2 y = __ffma2_rn(CX, U2x, __ffma2_rn(CY, U2y, __ffma2_rn(CZ, U2z, OU2)));
-        const float2 nx = make_float2(-x.x, -x.y), ny = make_float2(-y.x, -y.y);
-        disc[i] = __ffma2_rn(nx, x, __ffma2_rn(ny, y, R2));
-      }
-      // candidate detection: one max-reduction per batch (FMNMX3 tree), the per-sphere mask is
-      // only built on the rare path where some lane has a candidate
-      float dmax = fmaxf(disc[0].x, disc[0].y);
-#pragma unroll
-      for (int i = 1; i < kPairsPerBatch; ++i) dmax = fmaxf(dmax, fmaxf(disc[i].x, disc[i].y));
-      const bool any_cand = act && dmax >= neg_slack;
+      const float dmax = F.batch<kSrc>(pairs, base, disc);
+      const bool any_cand = act && dmax >= F.cut;
       if (__any_sync(kFull, any_cand)) {
         if (any_cand) {
-          unsigned cand = 0u;
-#pragma unroll
-          for (int i = 0; i < kPairsPerBatch; ++i)
-            cand |= ((disc[i].x >= neg_slack) ? 1u : 0u) << (2 * i) | ((disc[i].y >= neg_slack) ? 1u : 0u) << (2 * i + 1);
+          const unsigned cand = batch_mask(disc, F.cut);
           if (may_exit) {
             process(cand, base);
           } else {

@@ -155,10 +155,10 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
       const float dmax = F.batch<kSrc>(gp, base, disc);
-      const bool any = act && dmax >= F.neg_slack;
+      const bool any = act && dmax >= F.cut;
       if (__any_sync(kFull, any)) {
         if (any) {
-          unsigned m = batch_mask(disc, F.neg_slack);
+          unsigned m = batch_mask(disc, F.cut);
           while (m != 0u) {
             const int i = __ffs(m) - 1;
             m &= m - 1u;
