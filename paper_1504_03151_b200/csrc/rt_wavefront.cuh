@@ -30,23 +30,22 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// warp-aggregated reservation of `cnt` slots on a global counter (ballot/popc/shfl)
+// warp-aggregated reservation of `cnt` (< 64) slots on a global counter: exclusive prefix of
+// the counts by bit-plane ballots (valid for any set of active lanes), one atomicAdd per warp
 __device__ __forceinline__ unsigned warp_reserve(unsigned cnt, unsigned* counter) {
   const unsigned act = __activemask();
-  const int lane = threadIdx.x & 31;
-  unsigned incl = cnt;
+  const unsigned lt = lanemask_lt();
+  unsigned prefix = 0, total = 0;
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned v = __shfl_up_sync(act, incl, off);
-    if (lane >= off && (act >> (lane - off)) & 1u) incl += v;
+  for (int b = 0; b < 6; ++b) {
+    const unsigned m = __ballot_sync(act, (cnt >> b) & 1u);
+    prefix += (unsigned)__popc(m & lt) << b;
+    total += (unsigned)__popc(m) << b;
   }
-  const int last = 31 - __clz(act);
-  const unsigned total = __shfl_sync(act, incl, last);
   const int leader = __ffs(act) - 1;
   unsigned base = 0;
-  if (lane == leader && total) base = atomicAdd(counter, total);
-  base = __shfl_sync(act, base, leader);
-  return base + incl - cnt;
+  if ((int)(threadIdx.x & 31) == leader && total) base = atomicAdd(counter, total);
+  return __shfl_sync(act, base, leader) + prefix;
 }
 
 __device__ __forceinline__ void warp_stat(unsigned long long* stats, int k, unsigned long long v) {
@@ -226,8 +225,11 @@ __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScen
 }
 
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
+#ifndef RT_LOGIC_MIN_BLOCKS
+#define RT_LOGIC_MIN_BLOCKS 4
+#endif
 template <bool kDebug>
-__global__ void __launch_bounds__(256) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
+__global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(256) wf_shade(const DevParams P, const DevScen
 }
 
 // ---- a5 decision + accumulation of the visible lights, in light order ----------------------
-__global__ void __launch_bounds__(256) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
+__global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const int* q = B.q[d & 1];
