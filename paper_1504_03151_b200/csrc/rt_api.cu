@@ -241,6 +241,15 @@ int collect_stats(bool timed) {
       ts += b;
     }
   }
+#ifdef RT_SIMD_PROBE
+  if (c.wf_ctr.p) {
+    unsigned pr[4];
+    cudaMemcpy(pr, c.wf_ctr.p + 70 * rt::kWfCtrPerDepth, sizeof pr, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "SIMD probe: closest batches %u lanes %u (%.3f) | shadow batches %u lanes %u (%.3f)\n", pr[0], pr[1],
+            pr[1] / (32.0 * pr[0] + 1e-9), pr[2], pr[3], pr[3] / (32.0 * pr[2] + 1e-9));
+    cudaMemset(c.wf_ctr.p + 70 * rt::kWfCtrPerDepth, 0, sizeof pr);
+  }
+#endif
   c.last.isect_closest_ms = tc;
   c.last.isect_shadow_ms = ts;
   c.last.launches = timed ? (uint32_t)c.last_launches : 2u;

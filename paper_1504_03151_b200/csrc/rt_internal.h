@@ -93,6 +93,9 @@ struct WfBuffers {
   float* T;        // [3][cap]
   float* Lr;       // [3][cap]  sample radiance
   int* depth;      // [cap]
+  int* skip_c;     // [cap]  sphere the current ray leaves (provably not hit: convexity) or -1
+  int* hit_out;    // [cap]  sphere hit from outside at the current depth (shadow rays leaving it
+                   //        cannot hit it) or -1
   int* shoff;      // [cap]  first shadow entry of the path at the current depth
   int* shcnt;      // [cap]
   int* q[2];       // closest queues (path ids)

@@ -492,7 +492,7 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 
 // ---- wavefront launcher ---------------------------------------------------------------------
 size_t wf_bytes(int cap, int scap) {
-  return (size_t)cap * (12 * 8 + 6 * 4 + 3 * 4 + 2 * 4 + kCandMax * 4 + 4) +
+  return (size_t)cap * (12 * 8 + 6 * 4 + 5 * 4 + 2 * 4 + kCandMax * 4 + 4) +
          (size_t)scap * (4 + 4 + 12 + kCandMax * 4 + 4 + 4);
 }
 
@@ -506,6 +506,8 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.T = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
   B.Lr = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
   B.depth = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.skip_c = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.hit_out = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.shoff = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.shcnt = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.q[0] = reinterpret_cast<int*>(take(4 * (size_t)cap));

@@ -81,6 +81,10 @@ __device__ __forceinline__ void shadow_ray(const DevScene& S, d3 p, d3 n, int l,
   ds = ws * (1.0 / tl);
 }
 
+// A shadow ray from a point hit on the outside of sphere `out` (origin p + EPS_T n, outside)
+// that heads away from it (n.d > 0) cannot hit it (convexity): that sphere is skipped exactly.
+__device__ __forceinline__ int shadow_skip(int out, d3 n, d3 ds) { return (out >= 0 && dot(n, ds) > 0.0) ? out : -1; }
+
 // ---- a2: ray generation ---------------------------------------------------------------------
 __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
                                                  unsigned long long* stats) {
@@ -96,6 +100,7 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
       sf3(B.T, B.cap, i, f3(1.f, 1.f, 1.f));
       B.depth[i] = 0;
       B.shcnt[i] = 0;
+      B.skip_c[i] = -1;
     }
     const unsigned slot = warp_reserve(valid ? 1u : 0u, B.ctr + wf_ctr_q(0));
     if (valid) B.q[0][slot] = i;
@@ -126,11 +131,13 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     bool act = e < n;
     d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
     double tl = 0.0;
-    int rob = -1;
+    int rob = -1, skip = -1;
     if (act) {
       if constexpr (kShadow) {
         const int path = B.sq_path[e];
-        shadow_ray(S, ld3(B.hit, B.cap, path, 0), ld3(B.hit, B.cap, path, 3), B.sq_light[e], o, dir, tl);
+        const d3 nrm = ld3(B.hit, B.cap, path, 3);
+        shadow_ray(S, ld3(B.hit, B.cap, path, 0), nrm, B.sq_light[e], o, dir, tl);
+        skip = shadow_skip(B.hit_out[path], nrm, dir);
         // planes first, exactly (FP64): the first plane in index order that occludes decides
         for (int j = 0; j < P.n_planes; ++j) {
           const DevPlane pl = c_planes[j];
@@ -144,6 +151,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         const int path = q[e];
         o = ld3(B.ray, B.cap, path, 0);
         dir = ld3(B.ray, B.cap, path, 3);
+        skip = B.skip_c[path];
       }
     }
     RayFilter F;
@@ -163,6 +171,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
             m &= m - 1u;
             const int k = 2 * base + i;
             if (k >= P.n_spheres) break;
+            if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
             float dd, tc;
             F.sphere<kSrc>(gp, k, dd, tc);
             const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
@@ -195,6 +204,15 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
           }
         }
       }
+#ifdef RT_SIMD_PROBE
+      {
+        const unsigned nact = (unsigned)__popc(__ballot_sync(kFull, act));
+        if ((threadIdx.x & 31) == 0) {
+          atomicAdd(B.ctr + 70 * kWfCtrPerDepth + (kShadow ? 2 : 0), 1u);
+          atomicAdd(B.ctr + 70 * kWfCtrPerDepth + (kShadow ? 3 : 1), nact);
+        }
+      }
+#endif
       if constexpr (kShadow) {
         if (!__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
       }
@@ -209,7 +227,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
 // the list overflowed
 __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScene& S, const int* cand, int nc,
-                                               d3 o, d3 d, double& tbest, int& hs, int& hp) {
+                                               int skip, d3 o, d3 d, double& tbest, int& hs, int& hp) {
   if (nc <= kCandMax) {
     for (int c = 0; c < nc; ++c) {
       const int k = cand[c];
@@ -218,6 +236,7 @@ __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScen
     }
   } else {
     for (int k = 0; k < P.n_spheres; ++k) {
+      if (k == skip) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
       if (t >= kEps && t < tbest) { tbest = t; hs = k; hp = -1; }
     }
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         if (t >= kEps && t < tbest) { tbest = t; hp = j; }
       }
     }
-    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], o, dir, tbest, hs, hp);
+    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], B.skip_c[path], o, dir, tbest, hs, hp);
     const int depth = B.depth[path];
     int prim = -1;
     if (hp >= 0) prim = c_planes[hp].prim;
@@ -284,6 +303,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
       entering = dot(dir, ng) < 0.0;
       nrm = entering ? ng : ng * -1.0;
+      B.hit_out[path] = (hs >= 0 && entering) ? hs : -1;
       const DevMat m = S.mats[mi];
       L = add(L, mul(T, f3(m.er, m.eg, m.eb)));  // Eq. 7 emission
       if (m.kind == 0) {
@@ -365,9 +385,13 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         cont = true;
       }
       if (cont) {
+        const d3 dnn = normalize(dn);
         st3(B.ray, B.cap, path, 0, p);
-        st3(B.ray, B.cap, path, 3, normalize(dn));
+        st3(B.ray, B.cap, path, 3, dnn);
         B.depth[path] = depth + 1;
+        // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
+        // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
+        B.skip_c[path] = (hs >= 0 && dot(dnn, ng) > 0.0) ? hs : -1;
       }
     }
     B.shcnt[path] = (int)nsh;
@@ -410,6 +434,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
           d3 os, ds;
           double tl;
           shadow_ray(S, p, nrm, B.sq_light[j], os, ds, tl);
+          const int skip = shadow_skip(B.hit_out[path], nrm, ds);
           const int nc = B.sn[j];
           int first = -1;
           if (nc <= kCandMax) {
@@ -421,6 +446,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
             if (first < 0) first = rob;
           } else {
             for (int k = 0; k < P.n_spheres; ++k) {
+              if (k == skip) continue;
               const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
               if (t >= kEps && t < tl) { first = k; break; }
             }
