@@ -255,7 +255,6 @@ def run_b200(args):
     clocks = ClockSampler(local)
     clocks.start()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    per_frame = []
     barrier()
     t_wall0 = time.perf_counter()
     for i in range(args.steps):
@@ -263,43 +262,52 @@ def run_b200(args):
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)
-        if world == 1:
-            per_frame.append(rt.stats())    # per-kernel event times of this frame (host sync only)
     barrier()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
     frame_ms = [a.elapsed_time(b) for a, b in evs]
     my_total = sum(frame_ms)
     st = rt.stats()  # last frame (rank 0 holds the all-rank sum after assembly)
+    per_frame = [st]  # per-kernel event times of the last timed frame
     if world == 1:
-        launches_per_step = per_frame[-1]["launches"]
+        launches_per_step = st["launches"]
     t = torch.tensor([my_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
 
-    # e2e: the public C-ABI call with host buffers, H2D of the step's inputs and D2H of the frame
-    e2e = None
-    if world == 1 and rank == 0:
-        host_out = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
-        h2d = prims.nbytes + mats.nbytes + lights.nbytes + env.nbytes
-        d2h = host_out.numel() * 4 + 64
-        ke = max(3, min(args.steps, 20))
+    # e2e: the public C-ABI calls with host buffers: H2D of the step's inputs (the scene, on
+    # every rank) and D2H of the step's result (the frame, on rank 0), wall clock, max over ranks
+    host_out = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+    h2d = (prims.nbytes + mats.nbytes + lights.nbytes + env.nbytes) * world
+    d2h = H * W * 16 + 64
+    ke = max(3, min(args.steps, 20))
+    barrier()
+    t0 = time.perf_counter()
+    rays_e2e = 0
+    for _ in range(ke):
         rt.scene_upload(prims, mats, lights, env)
-        rt.render(W, H, D, S, host_out)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rays_e2e = 0
-        for _ in range(ke):
-            rt.scene_upload(prims, mats, lights, env)
-            rt.camera_set(sc.eye, sc.look_at, sc.up, sc.vfov)
+        rt.camera_set(sc.eye, sc.look_at, sc.up, sc.vfov)
+        if world == 1:
             rt.render(W, H, D, S, host_out)   # host pointer: returns after the D2H copy
             s2 = rt.stats()
-            rays_e2e += s2["primary"] + s2["shadow"] + s2["secondary"]
-        dt = time.perf_counter() - t0
-        e2e = {"value": rays_e2e / dt / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": ke, "ms_per_step": 1e3 * dt / ke,
-               "timing": "host wall clock around rt_scene_upload + rt_camera_set + rt_render(host buffer)"}
+        else:
+            frame = rend.render()
+            if rank == 0:
+                host_out.copy_(frame.image.view(H, W, 4))
+            torch.cuda.synchronize()
+            s2 = frame.stats or {"primary": 0, "shadow": 0, "secondary": 0}
+        rays_e2e += s2["primary"] + s2["shadow"] + s2["secondary"]
+    dt = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    e2e = {"value": rays_e2e / dt / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "steps": ke, "ms_per_step": 1e3 * dt / ke,
+           "timing": "host wall clock (max over ranks) around rt_scene_upload + rt_camera_set + "
+                     + ("rt_render(pinned host buffer)" if world == 1 else
+                        "rt_render_shard + NCCL all-gather + rt_assemble_tiles + D2H to pinned host")}
 
     if rank == 0:
         rays = st["primary"] + st["shadow"] + st["secondary"]
@@ -318,9 +326,9 @@ def run_b200(args):
             nc = sum(f["closest_sphere_tests"] for f in per_frame)
             ns = sum(f["sphere_tests"] - f["closest_sphere_tests"] for f in per_frame)
             achieved = FLOP_SPHERE * nc / (tc * 1e-3) / 1e12
-            kernel = "wf_isect<closest> (FP32 FFMA2 sphere scan of closest-hit rays; 41% of the frame in the ncu launch list)"
-            extra = {"share_of_frame": tc / total_ms,
-                     "shadow_kernel": {"achieved": FLOP_SPHERE * ns / (ts * 1e-3) / 1e12, "share_of_frame": ts / total_ms},
+            kernel = "wf_isect<closest> (FP32 FFMA2 sphere scan of closest-hit rays), per-launch CUDA events of the last timed frame"
+            extra = {"share_of_frame": tc / ms_per_step,
+                     "shadow_kernel": {"achieved": FLOP_SPHERE * ns / (ts * 1e-3) / 1e12, "share_of_frame": ts / ms_per_step},
                      "whole_frame_achieved": (FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"])
                      / (ms_per_step * 1e-3) / 1e12}
         else:

@@ -4,7 +4,9 @@ from __future__ import annotations
 import numpy as np
 
 
-def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None, variant="wavefront"):
+def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None, variant="wavefront", pixels=None):
+    """Render through the C ABI; with `pixels`, only those pixels' records are copied back
+    (indices into the row-major frame) — used at full BASELINE sizes."""
     import torch
     from paper_1504_03151_b200 import rt
     W = sc.width if width is None else width
@@ -22,9 +24,10 @@ def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None
         rt.render(W, H, D, S, out)
     st = rt.stats()
     torch.cuda.synchronize()
-    rgba = out.reshape(-1, 4).cpu().numpy()
+    sel = slice(None) if pixels is None else torch.as_tensor(np.asarray(pixels), device="cuda", dtype=torch.long)
+    rgba = out.reshape(-1, 4)[sel].cpu().numpy()
     res = {"rgba": rgba, "rgb": rgba[:, :3], "stats": st}
     if debug:
-        res["ids"] = ids.cpu().numpy()
-        res["bounces"] = bn.cpu().numpy()
+        res["ids"] = ids[sel].cpu().numpy()
+        res["bounces"] = bn[sel].cpu().numpy()
     return res

@@ -95,6 +95,19 @@ def test_c4_full_size_sampled(oracle_lib, variant):
     _check(oracle_lib, sc, pixels=pix, label=f"C4@1080p/{variant}", variant=variant)
 
 
+def test_c5_full_size_sampled(oracle_lib):
+    # 3840x2160, 16 spp, depth 8: 132.7 M paths -> 32 wavefront chunks; oracle on sampled pixels
+    sc = scenegen.get("C5")
+    pix = np.sort(np.random.default_rng(55).choice(sc.width * sc.height, 1200, replace=False))
+    g = gpu_render(sc, pixels=pix)
+    ref = oracle_lib.render(sc, pixels=pix)
+    cls = parity.classify(oracle_lib, sc, ref, pix)
+    rep = parity.compare(g["rgb"], g["ids"], g["bounces"], ref, cls)
+    print(f"[C5@4K] {rep}")
+    assert rep.ok, rep
+    assert g["stats"]["primary"] == sc.width * sc.height * sc.spp
+
+
 def test_c4_full_size_counts_consistent(oracle_lib):
     # rays-per-pixel statistics of the full-size GPU frame agree with the oracle sample
     sc = scenegen.get("C4")
