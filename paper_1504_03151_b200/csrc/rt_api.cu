@@ -67,7 +67,7 @@ struct Context {
   bool smem_scene = true;
   bool const_scene = true;
   int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
-  float cmax = 0.f, rmax = 0.f;
+  float cmax = 0.f, rmax = 0.f, cmax_abs = 0.f;
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage;
@@ -141,6 +141,7 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   }
   p.cmax = c.cmax;
   p.rmax = c.rmax;
+  p.cmax_abs = c.cmax_abs;
   for (int i = 0; i < 3; ++i) p.centre[i] = c.centre[i];
   p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
@@ -450,6 +451,21 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
       planes[kp++] = pl;
     }
   }
+  // constant-bank copy in the projected form {c, r^2} (RayFilterT<false>), dummies r^2 = -1
+  std::vector<float4> cpairs(2 * (size_t)npairs_pad);
+  double cmax_abs = 0.0;
+  for (int q = 0; q < npairs_pad; ++q) {
+    cpairs[2 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    cpairs[2 * q + 1] = make_float4(0.f, 0.f, -1.f, -1.f);
+  }
+  for (int k = 0; k < ns; ++k) {
+    float* A = reinterpret_cast<float*>(&cpairs[2 * (k / 2)]);
+    float* B = reinterpret_cast<float*>(&cpairs[2 * (k / 2) + 1]);
+    const int h = k & 1;
+    A[0 + h] = cr[k].x; A[2 + h] = cr[k].y; B[0 + h] = cr[k].z; B[2 + h] = cr[k].w * cr[k].w;
+    const double cn = std::fabs((double)cr[k].x) + std::fabs((double)cr[k].y) + std::fabs((double)cr[k].z);
+    if (cn > cmax_abs) cmax_abs = cn;
+  }
   std::vector<rt::DevMat> dm(n_mats);
   for (int i = 0; i < n_mats; ++i) {
     const rt_material& m = mats[i];
@@ -477,7 +493,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
   const bool in_const = npairs_pad <= rt::kMaxConstPairs;
-  CU(rt::upload_const_scene(planes.data(), np, pairs.data(), in_const ? (int)pairs.size() : 0, c.stream),
+  CU(rt::upload_const_scene(planes.data(), np, cpairs.data(), in_const ? (int)cpairs.size() : 0, c.stream),
      "constant upload");
   CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
   c.smem_scene = in_smem;
@@ -485,6 +501,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
   for (int k = 0; k < 3; ++k) c.centre[k] = RT_FILTER_EXPANDED ? centre[k] : 0.0;
   c.rmax = (float)(rmax * (1.0 + 1e-6));
+  c.cmax_abs = (float)(cmax_abs * (1.0 + 1e-6));
   c.n_spheres = ns;
   c.n_pairs_pad = npairs_pad;
   c.n_planes = np;

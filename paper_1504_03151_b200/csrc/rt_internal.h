@@ -27,7 +27,10 @@
 namespace rt {
 
 constexpr int kWarp = 32;
-constexpr int kPairsPerBatch = 8;   // 16 spheres per unrolled batch of the intersection loop
+#ifndef RT_PAIRS_PER_BATCH
+#define RT_PAIRS_PER_BATCH 8
+#endif
+constexpr int kPairsPerBatch = RT_PAIRS_PER_BATCH;  // 2x spheres per unrolled batch of the scans
 constexpr int kMaxSmemPairs = 5120;  // 10240 spheres = 160 KB of dynamic shared memory per CTA
 constexpr int kMaxConstPairs = 1536; // 3072 spheres = 48 KB of the 64 KB constant bank
 constexpr int kMaxPlanes = 32;
@@ -59,6 +62,7 @@ struct DevParams {
   float cmax;   // filter error bound: max over spheres of |c'| (expanded form, c' = c - centre)
                 //   or of |c|_1 (projected form)
   float rmax;   // max sphere radius
+  float cmax_abs;  // max over spheres of |c|_1 (projected form in the constant bank)
   int W, H, max_depth, spp;
   int n_spheres, n_pairs_pad, n_planes, n_lights;
   unsigned long long seed;

@@ -119,7 +119,7 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       const int k = 2 * base + i;  // pair (base + i/2), half i&1
       if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds the dummy margin)
       float dd, tc;
-      F.sphere<kSrc>(pairs, k, dd, tc);
+      F.sphere<kSrc>(pairs, S.sph_cr, k, dd, tc);
       const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));
       if (tc + qh < (float)kEps - F.eta || tc - qh > tmax_hi) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);

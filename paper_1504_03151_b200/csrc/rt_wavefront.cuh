@@ -109,8 +109,11 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
 }
 
 // ---- a3 / a5: FP32 filter over all spheres (persistent, one warp = 32 rays) -----------------
+#ifndef RT_ISECT_MIN_BLOCKS
+#define RT_ISECT_MIN_BLOCKS 3
+#endif
 template <int kSrc, bool kShadow>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   __shared__ uint64_t s_mbar;
   if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
@@ -154,7 +157,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         skip = B.skip_c[path];
       }
     }
-    RayFilter F;
+    RayFilterFor<kSrc> F;
     F.init(o, dir, P);
     const float tl_f = (float)tl;
     float tub = 3.0e38f;  // closest: certain upper bound of the nearest accepted root
@@ -173,7 +176,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
             if (k >= P.n_spheres) break;
             if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
             float dd, tc;
-            F.sphere<kSrc>(gp, k, dd, tc);
+            F.sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
             const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
             const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
             const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
