@@ -23,12 +23,21 @@ __global__ void k(float* out, int iters, float s0) {
         if (kMode == 1) a[i] = __ffma2_rn(b[i], make_float2(sc[i], sc[i]), a[i]);         // pair x scalar + pair
         if (kMode == 2) a[i] = __ffma2_rn(b[(i + u) % kC], make_float2(sc[i], sc[i]), a[i]);  // rotating pair x scalar
         if (kMode == 3) a[i] = __ffma2_rn(b[i], make_float2(sc[u % kC], sc[u % kC]), a[i]);   // same scalar for all chains
+        if (kMode == 4) {  // FFMA2 chain + independent scalar FFMA chain (does scalar FFMA co-issue on the lite pipe?)
+          a[i] = __ffma2_rn(b[i], make_float2(sc[i], sc[i]), a[i]);
+          sc[i] = fmaf(sc[i], 1.0001f, 0.5f);
+        }
+        if (kMode == 5) {  // 2 FFMA2 + 1 scalar FFMA
+          a[i] = __ffma2_rn(b[i], make_float2(sc[i], sc[i]), a[i]);
+          b[i] = __ffma2_rn(a[i], make_float2(sc[i], sc[i]), b[i]);
+          sc[i] = fmaf(sc[i], 1.0001f, 0.5f);
+        }
       }
     }
   }
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < kC; ++i) s += a[i].x + a[i].y;
+  for (int i = 0; i < kC; ++i) s += a[i].x + a[i].y + sc[i] + b[i].x;
   if (s == 12345.678f) out[0] = s;
 }
 int main() {
@@ -37,8 +46,8 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const int blocks = sms * 8, threads = 256, iters = 2048;
-  double fmas = 2.0 * blocks * threads * iters * 16 * kC;
-  auto run = [&](auto kern, const char* name) {
+  auto run = [&](auto kern, const char* name, double per = 2.0) {
+    const double fmas = per * blocks * threads * iters * 16 * kC;
     kern<<<blocks, threads>>>(d, iters, 0.999f);
     cudaDeviceSynchronize();
     float best = 1e30f;
@@ -52,5 +61,7 @@ int main() {
   run(k<1>, "pair*scalar+pair");
   run(k<2>, "rot pair*scalar+pair");
   run(k<3>, "pair*shared-scalar+pair");
+  run(k<4>, "FFMA2 + scalar FFMA-imm", 3.0);
+  run(k<5>, "2 FFMA2 + scalar FFMA-imm", 5.0);
   return 0;
 }
