@@ -140,6 +140,44 @@ int orc_refract(const double d[3], const double n[3], double eta, double out[3])
  * Radiometry (Eq. 3, 5-7)
  * -------------------------------------------------------------------------------------- */
 
+/* ----------------------------------------------------------------------------------------
+ * Light-surface and diffuse-bounce sampling
+ * -------------------------------------------------------------------------------------- */
+
+/* sample_light_point (Fig. 2 "sampling points on the surface of light source"):
+ * uniform on the whole sphere: cos(theta) = 1 - 2 u1, phi = 2 pi u2, pole = +z. */
+double orc_sample_sphere(const double c[3], double r, double u1, double u2, double x[3],
+                         double nl[3]) {
+  double ct = 1.0 - 2.0 * u1;
+  double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  double ph = 2.0 * PI * u2;
+  nl[0] = st * cos(ph);
+  nl[1] = st * sin(ph);
+  nl[2] = ct;
+  for (int i = 0; i < 3; ++i) x[i] = c[i] + r * nl[i];
+  return 1.0 / (4.0 * PI * r * r);
+}
+
+/* Orthonormal basis of unit n (Duff et al. 2017, "Building an Orthonormal Basis, Revisited"):
+ * s = sign(n.z) (sign(-0) = -1), a = -1 / (s + n.z), b = n.x n.y a,
+ * t1 = (1 + s n.x^2 a, s b, -s n.x), t2 = (b, s + n.y^2 a, -n.y). */
+void orc_onb(const double n[3], double t1[3], double t2[3]) {
+  double sg = copysign(1.0, n[2]);
+  double a = -1.0 / (sg + n[2]);
+  double b = n[0] * n[1] * a;
+  t1[0] = 1.0 + sg * n[0] * n[0] * a; t1[1] = sg * b; t1[2] = -sg * n[0];
+  t2[0] = b; t2[1] = sg + n[1] * n[1] * a; t2[2] = -n[1];
+}
+
+/* cosine_weighted_direction: pdf cos(theta)/pi about n. */
+void orc_cosine_direction(const double n[3], double u1, double u2, double out[3]) {
+  double t1[3], t2[3];
+  orc_onb(n, t1, t2);
+  double rr = sqrt(u1), ph = 2.0 * PI * u2;
+  double lx = rr * cos(ph), ly = rr * sin(ph), lz = sqrt(fmax(0.0, 1.0 - u1));
+  for (int i = 0; i < 3; ++i) out[i] = t1[i] * lx + t2[i] * ly + n[i] * lz;
+}
+
 /* f_r (Eq. 5): DIFFUSE = rho/pi + normalised Phong ks (s+2)/(2 pi) max(0, r.wo)^s with
  * r = 2 (n.wi) n - wi (reading R#3); delta materials -> 0. */
 void orc_brdf(int32_t kind, const double albedo[3], double ks, double shininess,
@@ -180,6 +218,17 @@ double orc_rng(uint64_t seed, uint64_t pixel_index, uint32_t sample, uint32_t de
   return (double)(x >> 40) * (1.0 / 16777216.0); /* exact in float and double */
 }
 
+/* Further draws of the same (pixel, sample, depth): stream k in bits 8..31 of the counter
+ * word (reading R#42); k = 0 reproduces orc_rng. */
+double orc_rng_stream(uint64_t seed, uint64_t pixel_index, uint32_t sample, uint32_t depth,
+                      uint32_t stream) {
+  uint64_t x = seed ^ ((pixel_index + 1ULL) * GOLDEN);
+  x = orc_mix64(x);
+  uint64_t word = ((uint64_t)sample << 32) + ((uint64_t)stream << 8) + (uint64_t)depth;
+  x = orc_mix64(x ^ (word * GOLDEN));
+  return (double)(x >> 40) * (1.0 / 16777216.0);
+}
+
 /* ----------------------------------------------------------------------------------------
  * Camera (§8(c).1 steps 1-2)
  * -------------------------------------------------------------------------------------- */
@@ -216,16 +265,21 @@ static camera build_camera(const orc_scene* sc) {
 }
 
 /* generate_camera_ray: pinhole, vertical fov, aspect W/H, py = 0 is the top row. */
-static void camera_ray(const camera* cam, int32_t W, int32_t H, int32_t px, int32_t py,
-                       int32_t s, int32_t spp, v3* o, v3* d) {
-  double ox, oy;
-  orc_sample_offset(s, spp, &ox, &oy);
+static void camera_ray_at(const camera* cam, int32_t W, int32_t H, int32_t px, int32_t py,
+                          double ox, double oy, v3* o, v3* d) {
   double sx = (px + ox) / W, sy = (py + oy) / H;
   double aspect = (double)W / (double)H;
   v3 dir = add(cam->f, add(scl(cam->r, (2.0 * sx - 1.0) * cam->h * aspect),
                            scl(cam->u, (1.0 - 2.0 * sy) * cam->h)));
   *o = cam->eye;
   *d = normalize(dir);
+}
+
+static void camera_ray(const camera* cam, int32_t W, int32_t H, int32_t px, int32_t py,
+                       int32_t s, int32_t spp, v3* o, v3* d) {
+  double ox, oy;
+  orc_sample_offset(s, spp, &ox, &oy);
+  camera_ray_at(cam, W, H, px, py, ox, oy, o, d);
 }
 
 void orc_camera_ray(const orc_scene* scene, int32_t width, int32_t height, int32_t px,
@@ -257,6 +311,8 @@ typedef struct {
   v3* c;      /* sphere centre, or plane normal */
   double* r;  /* sphere radius, or plane d */
   double* cn; /* |centre| (classification scales) */
+  int n_emit;     /* emissive spheres, in prim index order (R#41) */
+  int* emit;      /* [n_emit] prim index */
 } prims;
 
 static void prims_load(prims* P, const orc_scene* sc) {
@@ -286,10 +342,16 @@ static void prims_load(prims* P, const orc_scene* sc) {
       P->n_spheres++;
     }
   }
+  P->n_emit = 0;
+  P->emit = (int*)malloc(sizeof(int) * (P->n + 1));
+  for (int k = 0; k < P->n; ++k) {
+    const float* le = sc->mat_emission + 3 * P->mat[k];
+    if (P->type[k] == 0 && (le[0] > 0.0f || le[1] > 0.0f || le[2] > 0.0f)) P->emit[P->n_emit++] = k;
+  }
 }
 
 static void prims_free(prims* P) {
-  free(P->type); free(P->mat); free(P->c); free(P->r); free(P->cn);
+  free(P->type); free(P->mat); free(P->c); free(P->r); free(P->cn); free(P->emit);
 }
 
 static int prim_hit(const prims* P, int k, v3 o, v3 d, double* t) {
@@ -408,11 +470,12 @@ static double shadow_prim_margin(const prims* P, int k, v3 o, v3 d, double tmax,
 
 /* Occluded -> robust if at least one occluder is robust; visible -> robust if every prim is. */
 static double shadow_margin(const prims* P, v3 o, v3 d, double tmax, double Ps, double Ad,
-                            double El, int self, int self_inside) {
+                            double El, int self, int self_inside, int emitter) {
   double m_vis = INFINITY, m_occ = 0.0;
   int any = 0;
   for (int k = 0; k < P->n; ++k) {
     if (k == self && !self_inside) continue;
+    if (k == emitter) continue; /* the sampled emitter never blocks its own sample (R#41) */
     int occ;
     double mk_ = shadow_prim_margin(P, k, o, d, tmax, Ps, Ad, El, &occ);
     if (occ) { any = 1; if (mk_ > m_occ) m_occ = mk_; }
@@ -447,8 +510,17 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
   const orc_scene* sc = P->sc;
   sample_result res;
   uint64_t pixel_index = (uint64_t)py * (uint64_t)fr->width + (uint64_t)px;
+  /* the sample's global index keys every random draw (progressive passes, R#42) */
+  const uint32_t sg = (uint32_t)(fr->sample_base + s);
   v3 o, d;
-  camera_ray(cam, fr->width, fr->height, px, py, s, fr->spp, &o, &d); /* step 2 */
+  if (fr->jitter) { /* random sub-pixel offset from streams 1, 2 (R#42) */
+    double ox = orc_rng_stream(fr->seed, pixel_index, sg, 0, 1);
+    double oy = orc_rng_stream(fr->seed, pixel_index, sg, 0, 2);
+    camera_ray_at(cam, fr->width, fr->height, px, py, ox, oy, &o, &d); /* step 2 */
+  } else {
+    camera_ray(cam, fr->width, fr->height, px, py, s, fr->spp, &o, &d); /* step 2 */
+  }
+  int prev_diffuse = 0; /* the current ray left a DIFFUSE hit by a cosine-weighted bounce */
   v3 T = mk(1, 1, 1);  /* throughput */
   v3 L = mk(0, 0, 0);  /* radiance */
   v3 bg = ld3(sc->background), amb = ld3(sc->ambient);
@@ -459,7 +531,7 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
   double margin = INFINITY;
   double Ps = len(o) + 1.0, Ad = 1.0;
   int self = -1, self_inside = 0;
-  uint64_t pkey = fr->perturb_seed ^ orc_mix64(pixel_index * 0x100000001B3ULL + (uint64_t)s);
+  uint64_t pkey = fr->perturb_seed ^ orc_mix64(pixel_index * 0x100000001B3ULL + (uint64_t)sg);
 
   for (int depth = 0; depth <= fr->max_depth; ++depth) {
     if (hit_ids) hit_ids[depth] = -1;
@@ -495,8 +567,15 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
     double Phit = Ps + tbest * Ad + len(p) + 1.0;
     double An = P->type[best] == 1 ? 1.0 : (Phit + P->cn[best]) / P->r[best];
 
-    /* step 6: emission at every hit (Eq. 7; reading R#6) */
-    L = add(L, mulv(T, ld3(sc->mat_emission + 3 * mi)));
+    /* step 6: emission at every hit (Eq. 7; reading R#6) — except an
+     * emitter that next-event estimation already sampled from the previous diffuse bounce
+     * (S:299 double-count rule; R#43) */
+    {
+      int sampled_emitter = 0;
+      if (fr->area_lights && prev_diffuse)
+        for (int e = 0; e < P->n_emit; ++e) sampled_emitter |= (P->emit[e] == best);
+      if (!sampled_emitter) L = add(L, mulv(T, ld3(sc->mat_emission + 3 * mi)));
+    }
 
     /* step 7: direct lighting at DIFFUSE hits (Alg. 1; Eq. 3, 5, 6) */
     if (kind == 0) {
@@ -531,7 +610,7 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
         if (want_margin) {
           int self_in = (P->type[best] == 0) && !entering; /* shading from inside a sphere */
           margin = fmin2(margin, shadow_margin(P, os, ds, tmax, Phit + EPS_T, (Phit + El) / tmax,
-                                               El, best, self_in));
+                                               El, best, self_in, -1));
         }
         if (!occluded) {
           double f[3], wi_a[3], wo_a[3], n_a[3], alb[3];
@@ -543,6 +622,58 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
           L = add(L, mulv(T, scl(mulv(mk(f[0], f[1], f[2]), I), g)));
         }
       }
+      /* spherical area lights (NEXT-1; Eq. 8 as a one-sample estimator, Fig. 2):
+       * one uniform surface point per emitter, in emitter order after the point lights */
+      for (int e = 0; fr->area_lights && e < P->n_emit; ++e) {
+        int ke = P->emit[e];
+        double u1 = orc_rng_stream(fr->seed, pixel_index, sg, (uint32_t)depth, 5u + 2u * e);
+        double u2 = orc_rng_stream(fr->seed, pixel_index, sg, (uint32_t)depth, 6u + 2u * e);
+        double ca[3], xa[3], nla[3];
+        st3(ca, P->c[ke]);
+        double pdf = orc_sample_sphere(ca, P->r[ke], u1, u2, xa, nla);
+        v3 X = ldd(xa), NL = ldd(nla);
+        v3 w = sub(X, p);
+        double d2 = dot(w, w);
+        if (d2 < 1e-12) continue;
+        v3 wi = scl(w, 1.0 / sqrt(d2));
+        double cos_s = dot(n, wi);      /* cos(theta) at the shading point (Eq. 3) */
+        double cos_l = -dot(wi, NL);    /* cos(theta) at the light sample */
+        double El = len(X) + 1.0;
+        margin = fmin2(margin, fabs(cos_s) / (An + (Phit + El) / sqrt(d2)));
+        margin = fmin2(margin, fabs(cos_l) / (1.0 + (Phit + El) / sqrt(d2)));
+        if (cos_s <= 0.0 || cos_l <= 0.0) continue; /* no shadow ray (S:160 analogue) */
+        v3 os = add(p, scl(n, EPS_T));
+        v3 ws = sub(X, os);
+        double tmax = len(ws);
+        v3 ds = scl(ws, 1.0 / tmax);
+        if (fr->perturb > 0.0) {
+          uint64_t key = pkey + 0xA5E1ULL * (uint64_t)(depth * 4096 + e + 1);
+          os = perturb_v3(os, fr->perturb, key);
+          ds = normalize(perturb_v3(ds, fr->perturb, key + 7));
+        }
+        cnt->shadow++;
+        int occluded = 0;
+        for (int k = 0; k < P->n; ++k) { /* index order, break at the first occluder */
+          double t;
+          if (k == ke) continue; /* the emitter itself is not tested (S:174 ledger) */
+          if (P->type[k] == 1) cnt->plane_tests++; else cnt->sphere_tests++;
+          if (prim_hit(P, k, os, ds, &t) && t < tmax) { occluded = 1; break; }
+        }
+        if (want_margin) {
+          int self_in = (P->type[best] == 0) && !entering;
+          margin = fmin2(margin, shadow_margin(P, os, ds, tmax, Phit + EPS_T, (Phit + El) / tmax,
+                                               El, best, self_in, ke));
+        }
+        if (!occluded) {
+          double f[3], wi_a[3], wo_a[3], n_a[3], alb[3];
+          st3(wi_a, wi); st3(wo_a, wo); st3(n_a, n); st3(alb, rho);
+          orc_brdf(kind, alb, (double)sc->mat_ks[mi], (double)sc->mat_shininess[mi], wi_a, wo_a,
+                   n_a, f);
+          v3 Le = ld3(sc->mat_emission + 3 * P->mat[ke]);
+          double g = cos_s * cos_l / (d2 * pdf); /* f L_e cos_s cos_l / (dist^2 pdf_area) */
+          L = add(L, mulv(T, scl(mulv(mk(f[0], f[1], f[2]), Le), g)));
+        }
+      }
     }
 
     /* step 8: stack-free continuation */
@@ -552,6 +683,16 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
     if (kind == 1) { /* SPECULAR: mirror, T *= rho */
       dn = reflect(d, n);
       T = mulv(T, rho);
+      An_next = Ad + 2.0 * An;
+    } else if (kind == 0 && fr->integrator == 1) { /* global: cosine-weighted (NEXT-2, R#40) */
+      double u1 = orc_rng_stream(fr->seed, pixel_index, sg, (uint32_t)depth, 3u);
+      double u2 = orc_rng_stream(fr->seed, pixel_index, sg, (uint32_t)depth, 4u);
+      double n_a[3], dn_a[3];
+      st3(n_a, n);
+      margin = fmin2(margin, fabs(n.z) / An); /* sign(n.z) selects the basis branch */
+      orc_cosine_direction(n_a, u1, u2, dn_a);
+      dn = ldd(dn_a);
+      T = mulv(T, rho); /* f_r cos / pdf = albedo */
       An_next = Ad + 2.0 * An;
     } else if (kind == 0) { /* DIFFUSE: mirror iff kr > 0 (reading R#8) */
       double kr = (double)sc->mat_kr[mi];
@@ -570,7 +711,7 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
       } else {
         double c = entering ? ci : sqrt(1.0 - sin2t);
         double F = orc_schlick(ior, c);
-        double u = orc_rng(fr->seed, pixel_index, (uint32_t)s, (uint32_t)depth);
+        double u = orc_rng(fr->seed, pixel_index, sg, (uint32_t)depth);
         margin = fmin2(margin, fabs(u - F) / (5.0 * (Ad + An)));
         if (u < F) dn = reflect(d, n);
         else refract(d, n, eta, &dn);
@@ -581,6 +722,7 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
     /* new ray: o' = p (no offset; EPS_T rejects self hits), d' normalised */
     o = p;
     d = normalize(dn);
+    prev_diffuse = (kind == 0 && fr->integrator == 1);
     bounces++;
     cnt->secondary++;
     self = best;
@@ -599,7 +741,8 @@ int orc_render(const orc_scene* scene, const orc_frame* frame, const int64_t* pi
                int64_t n_pixels, double* rgb, int32_t* hit_ids, int32_t* bounces,
                double* margin, double* sample_rgb, orc_counts* counts) {
   if (!scene || !frame || frame->width < 1 || frame->height < 1 || frame->max_depth < 0 ||
-      frame->spp < 1)
+      frame->spp < 1 || frame->max_depth > 255 || frame->sample_base < 0 ||
+      frame->sample_base + frame->spp > 4294967296LL)
     return -1;
   int64_t npx_total = (int64_t)frame->width * frame->height;
   if (!pixels) n_pixels = npx_total;

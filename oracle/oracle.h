@@ -18,6 +18,10 @@
  * brute-force bisection of Eq. 9 along the ray, BRDF/Phong hemisphere normalisation
  * quadrature, splitmix64 reference vector, invariants (miss -> background bit-exact,
  * linearity, depth monotonicity, partition invariance).
+ * NEXT-1 / NEXT-2 extensions (tests/test_oracle_next.py): sphere-irradiance closed form and an
+ * independent quadrature for the area-light estimator, cosine-lobe moments, furnace and
+ * constant-sky closed forms for the global bounce, SPEC S:148-150 / S:166-168 / S:302-303
+ * examples, the NEE double-count rule, progressive resume.
  */
 #ifndef RT_ORACLE_H
 #define RT_ORACLE_H
@@ -63,6 +67,20 @@ typedef struct {
    * (Monte Carlo arithmetic). perturb = 0 is the method exactly. */
   double perturb;
   uint64_t perturb_seed;
+  /* SURVEY §8(f) NEXT-1 / NEXT-2 (0 = the §8(a) hot path exactly):
+   * integrator  0 Whitted (DIFFUSE stops unless kr > 0); 1 global: DIFFUSE continues with a
+   *             cosine-weighted direction, T *= albedo (R#40)
+   * area_lights 1: every emissive sphere is also sampled as a light, one uniform point on its
+   *             surface per emitter per shading point (R#41)
+   * jitter      0: stratified / Hammersley sub-pixel offsets; 1: random offsets from the
+   *             pixel's RNG stream (progressive passes; R#42)
+   * sample_base global index of sample 0: sample s of this call is sample (pass)
+   *             sample_base + s of the pixel's sequence (keys every RNG draw) */
+  int32_t integrator;
+  int32_t area_lights;
+  int32_t jitter;
+  int32_t pad_;
+  int64_t sample_base;
 } orc_frame;
 
 typedef struct {
@@ -94,6 +112,20 @@ void orc_camera_ray(const orc_scene* scene, int32_t width, int32_t height, int32
                     int32_t py, int32_t s, int32_t spp, double o[3], double d[3]);
 uint64_t orc_mix64(uint64_t x);
 double orc_rng(uint64_t seed, uint64_t pixel_index, uint32_t sample, uint32_t depth);
+/* stream k of the counter-based RNG: counter word (sample << 32) + (k << 8) + depth, depth <
+ * 256; k = 0 is orc_rng (R#42). Streams: 0 Fresnel, 1/2 jitter x/y, 3/4 diffuse bounce,
+ * 5 + 2e / 6 + 2e the surface sample of emitter e. */
+double orc_rng_stream(uint64_t seed, uint64_t pixel_index, uint32_t sample, uint32_t depth,
+                      uint32_t stream);
+/* uniform point on a sphere: cos(theta) = 1 - 2 u1, phi = 2 pi u2, z = pole;
+ * writes the point and the outward unit normal, returns pdf_area = 1 / (4 pi r^2) */
+double orc_sample_sphere(const double c[3], double r, double u1, double u2, double x[3],
+                         double nl[3]);
+/* orthonormal basis (t1, t2, n) of a unit vector n (branchless form, Duff et al. 2017) */
+void orc_onb(const double n[3], double t1[3], double t2[3]);
+/* cosine-weighted direction about unit n: r = sqrt(u1), phi = 2 pi u2,
+ * local (r cos phi, r sin phi, sqrt(1 - u1)) in orc_onb(n); pdf = cos(theta) / pi */
+void orc_cosine_direction(const double n[3], double u1, double u2, double out[3]);
 void orc_brdf(int32_t kind, const double albedo[3], double ks, double shininess,
               const double wi[3], const double wo[3], const double n[3], double f[3]);
 double orc_schlick(double ior, double cos_outside);

@@ -45,7 +45,8 @@ class _Scene(C.Structure):
 class _Frame(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("max_depth", C.c_int32),
                 ("spp", C.c_int32), ("seed", C.c_uint64), ("perturb", C.c_double),
-                ("perturb_seed", C.c_uint64)]
+                ("perturb_seed", C.c_uint64), ("integrator", C.c_int32), ("area_lights", C.c_int32),
+                ("jitter", C.c_int32), ("pad_", C.c_int32), ("sample_base", C.c_int64)]
 
 
 class _Counts(C.Structure):
@@ -77,6 +78,12 @@ def lib():
         _lib.orc_mix64.argtypes = [C.c_uint64]
         _lib.orc_rng.restype = C.c_double
         _lib.orc_rng.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]
+        _lib.orc_rng_stream.restype = C.c_double
+        _lib.orc_rng_stream.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
+        _lib.orc_sample_sphere.restype = C.c_double
+        _lib.orc_sample_sphere.argtypes = [dp, C.c_double, C.c_double, C.c_double, dp, dp]
+        _lib.orc_onb.argtypes = [dp, dp, dp]
+        _lib.orc_cosine_direction.argtypes = [dp, C.c_double, C.c_double, dp]
         _lib.orc_brdf.argtypes = [C.c_int32, dp, C.c_double, C.c_double, dp, dp, dp, dp]
         _lib.orc_schlick.restype = C.c_double
         _lib.orc_schlick.argtypes = [C.c_double, C.c_double]
@@ -129,7 +136,8 @@ class OracleResult:
 
 
 def render(sc, pixels=None, perturb: float = 0.0, perturb_seed: int = 0,
-           width=None, height=None, max_depth=None, spp=None, seed=None) -> OracleResult:
+           width=None, height=None, max_depth=None, spp=None, seed=None,
+           integrator: int = 0, area_lights: int = 0, jitter: int = 0, sample_base: int = 0) -> OracleResult:
     L = lib()
     W = sc.width if width is None else width
     H = sc.height if height is None else height
@@ -137,7 +145,8 @@ def render(sc, pixels=None, perturb: float = 0.0, perturb_seed: int = 0,
     S = sc.spp if spp is None else spp
     sd = sc.seed if seed is None else seed
     holder = _SceneHolder(sc)
-    fr = _Frame(width=W, height=H, max_depth=D, spp=S, seed=sd, perturb=perturb, perturb_seed=perturb_seed)
+    fr = _Frame(width=W, height=H, max_depth=D, spp=S, seed=sd, perturb=perturb, perturb_seed=perturb_seed,
+                integrator=integrator, area_lights=area_lights, jitter=jitter, sample_base=sample_base)
     if pixels is None:
         pix = np.arange(W * H, dtype=np.int64)
         ppix = None
@@ -159,12 +168,14 @@ def render(sc, pixels=None, perturb: float = 0.0, perturb_seed: int = 0,
     return OracleResult(rgb, ids, bn, mg, srgb, counts, pix)
 
 
-def render_rgb_only(sc, pixels=None, **kw) -> tuple:
+def render_rgb_only(sc, pixels=None, integrator: int = 0, area_lights: int = 0, jitter: int = 0,
+                    sample_base: int = 0) -> tuple:
     """Cheaper call for timing (cpu baseline): only the image and the counts."""
     L = lib()
     W, H = sc.width, sc.height
     holder = _SceneHolder(sc)
-    fr = _Frame(width=W, height=H, max_depth=sc.max_depth, spp=sc.spp, seed=sc.seed, perturb=0.0, perturb_seed=0)
+    fr = _Frame(width=W, height=H, max_depth=sc.max_depth, spp=sc.spp, seed=sc.seed, perturb=0.0, perturb_seed=0,
+                integrator=integrator, area_lights=area_lights, jitter=jitter, sample_base=sample_base)
     if pixels is None:
         n, ppix = W * H, None
     else:
@@ -230,6 +241,28 @@ def mix64(x):
 
 def rng(seed, pixel, sample, depth):
     return float(lib().orc_rng(seed, pixel, sample, depth))
+
+
+def rng_stream(seed, pixel, sample, depth, stream):
+    return float(lib().orc_rng_stream(seed, pixel, sample, depth, stream))
+
+
+def sample_sphere(c, r, u1, u2):
+    x, nl = (C.c_double * 3)(), (C.c_double * 3)()
+    pdf = lib().orc_sample_sphere(_d3(c), r, u1, u2, x, nl)
+    return np.array(list(x)), np.array(list(nl)), float(pdf)
+
+
+def onb(n):
+    t1, t2 = (C.c_double * 3)(), (C.c_double * 3)()
+    lib().orc_onb(_d3(n), t1, t2)
+    return np.array(list(t1)), np.array(list(t2))
+
+
+def cosine_direction(n, u1, u2):
+    out = (C.c_double * 3)()
+    lib().orc_cosine_direction(_d3(n), u1, u2, out)
+    return np.array(list(out))
 
 
 def brdf(kind, albedo, ks, shininess, wi, wo, n):

@@ -306,7 +306,30 @@ def config_c5(seed: int = 5) -> Scene:
                    background=(0.05, 0.07, 0.12), ambient=(0.02, 0.02, 0.02))
 
 
-CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C5": config_c5}
+def config_c0() -> Scene:
+    """Paper-shaped workload for NEXT-1 / NEXT-2 (SURVEY §8(d).1 "C0", §8(f) NEXT-2): a Cornell
+    box of 5 planes + 3 spheres + 1 spherical area light at 640x480, depth 6 (P:241, P:275,
+    P:290), rendered with the global integrator and area lights in progressive passes. No point
+    lights, no ambient, black background: all light comes from the emitter."""
+    b = _Builder()
+    white = b.material(DIFFUSE, (0.75, 0.75, 0.75))
+    red = b.material(DIFFUSE, (0.75, 0.25, 0.25))
+    green = b.material(DIFFUSE, (0.25, 0.75, 0.25))
+    b.plane((0, 1, 0), 0.0, white)      # floor y = 0
+    b.plane((0, -1, 0), -5.0, white)    # ceiling y = 5
+    b.plane((1, 0, 0), -2.5, red)       # left wall x = -2.5
+    b.plane((-1, 0, 0), -2.5, green)    # right wall x = 2.5
+    b.plane((0, 0, -1), -5.0, white)    # back wall z = 5
+    b.sphere((-1.1, 0.9, 3.2), 0.9, b.material(SPECULAR, (0.95, 0.95, 0.95)))
+    b.sphere((1.1, 0.9, 2.0), 0.9, b.material(REFRACTIVE, (1.0, 1.0, 1.0), ior=1.5))
+    b.sphere((0.6, 0.5, 4.2), 0.5, b.material(DIFFUSE, (0.6, 0.6, 0.9), ks=0.3, shininess=32.0))
+    b.sphere((0.0, 4.3, 2.8), 0.4, b.material(DIFFUSE, (0.0, 0.0, 0.0), emission=(25.0, 25.0, 25.0)))
+    return b.build("C0", eye=(0, 2.5, -6.5), look_at=(0, 2.5, 0), up=(0, 1, 0), vfov=45,
+                   width=640, height=480, max_depth=6, spp=1, background=(0, 0, 0), ambient=(0, 0, 0),
+                   notes="Cornell box; render with integrator=global, area_lights=1, progressive passes")
+
+
+CONFIGS = {"C0": config_c0, "C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C5": config_c5}
 
 
 def get(name: str) -> Scene:
@@ -314,7 +337,8 @@ def get(name: str) -> Scene:
 
 
 def random_tiny(seed: int, n_spheres: int = 6, n_planes: int = 1, n_lights: int = 2,
-                width: int = 12, height: int = 9, max_depth: int = 3, spp: int = 1) -> Scene:
+                width: int = 12, height: int = 9, max_depth: int = 3, spp: int = 1,
+                n_emitters: int = 0) -> Scene:
     """Tiny random scenes for brute-force and randomized parity tests (all material kinds)."""
     g = SplitMix64(0xC0FFEE ^ seed)
     b = _Builder()
@@ -327,6 +351,11 @@ def random_tiny(seed: int, n_spheres: int = 6, n_planes: int = 1, n_lights: int 
         r = _f32(g.uniform(0.3, 1.5))
         c = (_f32(g.uniform(-4, 4)), _f32(g.uniform(0.2, 3)), _f32(g.uniform(2, 9)))
         b.sphere(c, r, _mixed_material(b, g, 0.5))
+    for _ in range(n_emitters):  # spherical area lights (NEXT-1): emissive DIFFUSE spheres
+        r = _f32(g.uniform(0.2, 0.6))
+        c = (_f32(g.uniform(-4, 4)), _f32(g.uniform(3, 6)), _f32(g.uniform(1, 8)))
+        le = _f32(g.uniform(5, 20))
+        b.sphere(c, r, b.material(DIFFUSE, (_f32(g.uniform(0, 0.5)),) * 3, emission=(le, le * 0.9, le * 0.7)))
     for _ in range(n_lights):
         I = _f32(g.uniform(20, 80))
         b.light((_f32(g.uniform(-5, 5)), _f32(g.uniform(4, 8)), _f32(g.uniform(-2, 6))), (I, I * 0.9, I * 0.8))
