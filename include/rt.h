@@ -47,6 +47,7 @@ enum { RT_MAT_DIFFUSE = 0, RT_MAT_SPECULAR = 1, RT_MAT_REFRACTIVE = 2 };
 
 enum {
   RT_MAX_LIGHTS = 32,        /* point lights per scene */
+  RT_MAX_EMITTERS = 64,      /* emissive spheres sampled as area lights (rt_set_integrator) */
   RT_MAX_PLANES = 32,        /* planes per scene */
   RT_MAX_SPHERES = 1 << 20,  /* spheres per scene; > RT_SMEM_SPHERES uses the global-memory path */
   RT_SMEM_SPHERES = 10240,   /* spheres staged per CTA in shared memory (TMA bulk copy, 160 KB) */
@@ -186,6 +187,39 @@ int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, 
  * traced; bounces[(py*W+px)*spp + s] = number of secondary rays. Host or device pointers. */
 int rt_render_debug(int32_t width, int32_t height, int32_t max_depth, int32_t spp,
                     float* out_rgba, int32_t* hit_ids, int32_t* bounces);
+
+/* ---- area lights, global illumination, progressive passes ----
+ * Integrator for every following render call (R#40-R#43):
+ *   integrator RT_INTEGRATOR_WHITTED (default): the §8(a) hot path — DIFFUSE hits stop unless
+ *     kr > 0 (mirror term); RT_INTEGRATOR_GLOBAL: DIFFUSE hits continue with a cosine-weighted
+ *     direction (pdf cos/pi), T *= albedo (Fig. 7 P:290 "global illumination").
+ *   area_lights 1: every sphere whose material emits (emission > 0 in some channel; at most
+ *     RT_MAX_EMITTERS) is also a light: one uniform point on its surface per shading point
+ *     (pdf 1/(4 pi r^2)), contribution f_r L_e cos_s cos_l / (d^2 pdf), shadow ray to the point
+ *     with the emitter itself non-blocking (Eq. 8, Fig. 2). A cosine bounce that
+ *     hits a sampled emitter does not add its emission again.
+ * Non-default settings run the wavefront kernels (RT_VARIANT_MEGAKERNEL is overridden).
+ * Errors: RT_ERR_INVALID_ARG for values outside the enums. */
+enum { RT_INTEGRATOR_WHITTED = 0, RT_INTEGRATOR_GLOBAL = 1 };
+int rt_set_integrator(int32_t integrator, int32_t area_lights);
+
+/* Progressive passes (§IV.A P:226-229 "the same kernel function should be launched
+ * iteratively", "overlapping new color value onto the pixel"). Pass p traces one
+ * camera ray per pixel with a random sub-pixel offset and random light / bounce samples, all
+ * keyed by (seed, pixel, p) (R#42). For p = pass_begin .. pass_begin + n_passes - 1, in order:
+ *   accum_rgb[(py*W + px)*3 + c] += radiance of pass p   (double, device pointer, caller-owned;
+ *                                                         zero it before pass 0)
+ * then, if out_rgba != NULL (host or device, float4 row-major), out = accum / (pass_begin +
+ * n_passes), alpha 1. Splitting a run of passes over several calls is bit-identical to one
+ * call. 1 <= n_passes <= 4096, pass_begin + n_passes <= 2^32. Stats (rt_stats) cover this
+ * call's passes. Asynchronous unless out_rgba is a host pointer. */
+int rt_render_passes(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin,
+                     int32_t n_passes, double* accum_rgb, float* out_rgba);
+/* rt_render_passes plus the per-sample records of rt_render_debug (sample index = pass -
+ * pass_begin). out_rgba, hit_ids, bounces must not be NULL. */
+int rt_render_passes_debug(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin,
+                           int32_t n_passes, double* accum_rgb, float* out_rgba, int32_t* hit_ids,
+                           int32_t* bounces);
 
 /* SPEC tone_map on the device: per channel round_half_up(255 clamp(exposure v, 0,
  * 1)^(1/gamma)), alpha = 255. rgba: n_px float4 (device); out: n_px * 4 bytes (device). */

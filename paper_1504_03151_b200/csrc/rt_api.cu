@@ -71,7 +71,10 @@ struct Context {
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage;
-  DevBuf<int> sph_prim, sph_mat;
+  DevBuf<int> sph_prim, sph_mat, emit_sph;
+  int n_emitters = 0;  // emissive spheres (prim order)
+  // integrator settings (rt_set_integrator)
+  int integrator = RT_INTEGRATOR_WHITTED, area_lights = 0;
   DevBuf<rt::DevMat> mats;
   DevBuf<rt::DevLight> lights;
   DevBuf<unsigned int> counter;
@@ -146,6 +149,8 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
   p.seed = c.seed;
+  p.integrator = c.integrator;
+  p.n_emitters = c.area_lights ? c.n_emitters : 0;
   p.tiles_x = (W + rt::kTileW - 1) / rt::kTileW;
   p.n_tiles = p.tiles_x * ((H + rt::kTileH - 1) / rt::kTileH);
   return p;
@@ -161,13 +166,16 @@ int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
   return RT_OK;
 }
 
-int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_bounces) {
+int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_bounces, double* accum = nullptr) {
   Context& c = g_ctx;
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
-  rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p};
-  rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces};
-  const bool wavefront = c.variant == RT_VARIANT_WAVEFRONT ||
+  rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p};
+  rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces, accum};
+  // the NEXT-1 / NEXT-2 modes (global integrator, area lights, progressive passes) exist in the
+  // wavefront kernels only; the megakernel implements the §8(a) hot path
+  const bool extended = p.integrator != 0 || p.n_emitters > 0 || p.jitter != 0 || accum != nullptr;
+  const bool wavefront = extended || c.variant == RT_VARIANT_WAVEFRONT ||
                          (c.variant == RT_VARIANT_AUTO && c.n_spheres >= kAutoWavefrontSpheres);
   if (wavefront) {
     // chunk of whole pixels: at most 2^22 paths; shadow entries: paths x lights
@@ -175,11 +183,13 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     int items = (int)((want < (1ll << 22) ? want : (1ll << 22)) / p.spp);
     if (items < 1) items = 1;
     const int cap = items * p.spp;
-    const int scap = cap * (c.n_lights > 0 ? c.n_lights : 1);
-    // (re)carve for this frame's cap: per-light queues are indexed l * cap + slot
-    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap) + 64 * 256), "cudaMalloc(wavefront)");
+    const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
+    const int scap = cap * (n_src > 0 ? n_src : 1);
+    const bool with_x = p.n_emitters > 0;
+    // (re)carve for this frame's cap
+    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, with_x) + 64 * 256), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
+    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, with_x, c.wf_ctr.p);
     const int pairs = rt::wf_timing_pairs(p, cap);
     while ((int)c.ev_c.size() < 2 * pairs) {
       cudaEvent_t a, b;
@@ -259,14 +269,31 @@ int collect_stats(bool timed) {
 }
 
 int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba, int32_t* hit_ids,
-                  int32_t* bounces) {
+                  int32_t* bounces, double* accum = nullptr, long long sample_base = 0) {
   int rc = ensure_device();
   if (rc) return rc;
-  if (!out_rgba) return fail(RT_ERR_INVALID_ARG, "out_rgba is NULL");
+  if (!out_rgba && !accum) return fail(RT_ERR_INVALID_ARG, "out_rgba is NULL");
   rc = check_frame(W, H, D, spp);
   if (rc) return rc;
   Context& c = g_ctx;
   const long long npx = (long long)W * H;
+  if (accum) {
+    if (!is_device_ptr(accum)) return fail(RT_ERR_INVALID_ARG, "accum_rgb must be a device pointer");
+    if ((reinterpret_cast<uintptr_t>(accum) & 7u) != 0) return fail(RT_ERR_INVALID_ARG, "accum_rgb must be 8-byte aligned");
+    if (sample_base < 0 || sample_base + spp > 4294967296LL)
+      return fail(RT_ERR_INVALID_ARG, "passes: need 0 <= pass_begin and pass_begin + n_passes <= 2^32");
+  }
+  if (!out_rgba) {  // accumulation only: resolve writes no framebuffer
+    rt::DevParams p = make_params(W, H, D, spp);
+    p.mode = 0;
+    p.n_items = p.n_tiles * rt::kTilePx;
+    p.jitter = 1;
+    p.sample_base = sample_base;
+    rc = run_render(p, nullptr, nullptr, nullptr, accum);
+    if (rc) return rc;
+    defer_stats(true);
+    return RT_OK;
+  }
   const bool dev_out = is_device_ptr(out_rgba);
   if (dev_out && (reinterpret_cast<uintptr_t>(out_rgba) & 15u) != 0)
     return fail(RT_ERR_INVALID_ARG, "device out_rgba must be 16-byte aligned");
@@ -296,7 +323,11 @@ int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba,
   rt::DevParams p = make_params(W, H, D, spp);
   p.mode = 0;
   p.n_items = p.n_tiles * rt::kTilePx;
-  rc = run_render(p, out, dh, db);
+  if (accum) {  // progressive passes (R#42)
+    p.jitter = 1;
+    p.sample_base = sample_base;
+  }
+  rc = run_render(p, out, dh, db, accum);
   if (rc) return rc;
   if (!dev_out)
     CU(cudaMemcpyAsync(out_rgba, out, sizeof(float4) * npx, cudaMemcpyDeviceToHost, c.stream), "framebuffer D2H");
@@ -329,6 +360,32 @@ int rt_set_variant(int32_t variant) {
     return fail(RT_ERR_INVALID_ARG, "variant %d not in {-1 auto, 0 megakernel, 1 wavefront}", variant);
   g_ctx.variant = variant;
   return RT_OK;
+}
+
+int rt_set_integrator(int32_t integrator, int32_t area_lights) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (integrator != RT_INTEGRATOR_WHITTED && integrator != RT_INTEGRATOR_GLOBAL)
+    return fail(RT_ERR_INVALID_ARG, "integrator %d not in {0 whitted, 1 global}", integrator);
+  if (area_lights != 0 && area_lights != 1) return fail(RT_ERR_INVALID_ARG, "area_lights must be 0 or 1");
+  g_ctx.integrator = integrator;
+  g_ctx.area_lights = area_lights;
+  return RT_OK;
+}
+
+int rt_render_passes(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin, int32_t n_passes,
+                     double* accum_rgb, float* out_rgba) {
+  g_err.clear();
+  if (!accum_rgb) return fail(RT_ERR_INVALID_ARG, "accum_rgb is NULL");
+  return render_common(width, height, max_depth, n_passes, out_rgba, nullptr, nullptr, accum_rgb, pass_begin);
+}
+
+int rt_render_passes_debug(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin, int32_t n_passes,
+                           double* accum_rgb, float* out_rgba, int32_t* hit_ids, int32_t* bounces) {
+  g_err.clear();
+  if (!accum_rgb) return fail(RT_ERR_INVALID_ARG, "accum_rgb is NULL");
+  if (!out_rgba || !hit_ids || !bounces) return fail(RT_ERR_INVALID_ARG, "out_rgba/hit_ids/bounces must not be NULL");
+  return render_common(width, height, max_depth, n_passes, out_rgba, hit_ids, bounces, accum_rgb, pass_begin);
 }
 
 int rt_set_seed(uint64_t seed) {
@@ -466,6 +523,14 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     const double cn = std::fabs((double)cr[k].x) + std::fabs((double)cr[k].y) + std::fabs((double)cr[k].z);
     if (cn > cmax_abs) cmax_abs = cn;
   }
+  // emitters (R#41): spheres whose material emits in some channel, in prim (= sphere) order
+  std::vector<int> emit;
+  for (int k = 0; k < ns; ++k) {
+    const rt_material& m = mats[smat[k]];
+    if (m.emission[0] > 0.f || m.emission[1] > 0.f || m.emission[2] > 0.f) emit.push_back(k);
+  }
+  if (emit.size() > (size_t)RT_MAX_EMITTERS)
+    return fail(RT_ERR_INVALID_ARG, "too many emissive spheres (%d > %d)", (int)emit.size(), (int)RT_MAX_EMITTERS);
   std::vector<rt::DevMat> dm(n_mats);
   for (int i = 0; i < n_mats; ++i) {
     const rt_material& m = mats[i];
@@ -485,6 +550,9 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(c.sph_mat.reserve(smat.size()), "cudaMalloc(spheres)");
   CU(c.mats.reserve(dm.size()), "cudaMalloc(materials)");
   CU(c.lights.reserve(dl.size()), "cudaMalloc(lights)");
+  CU(c.emit_sph.reserve(emit.size() > 0 ? emit.size() : 1), "cudaMalloc(emitters)");
+  if (!emit.empty())
+    CU(cudaMemcpyAsync(c.emit_sph.p, emit.data(), sizeof(int) * emit.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.pairs.p, pairs.data(), sizeof(float4) * pairs.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.sph_cr.p, cr.data(), sizeof(float4) * cr.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.sph_prim.p, sprim.data(), sizeof(int) * sprim.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
@@ -506,6 +574,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   c.n_pairs_pad = npairs_pad;
   c.n_planes = np;
   c.n_lights = n_lights;
+  c.n_emitters = (int)emit.size();
   c.n_mats = n_mats;
   for (int k = 0; k < 3; ++k) {
     c.bg[k] = env ? env->background[k] : 0.f;

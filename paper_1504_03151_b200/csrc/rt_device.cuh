@@ -45,6 +45,39 @@ __device__ __forceinline__ double rng_u(unsigned long long seed, unsigned long l
   return (double)(x >> 40) * (1.0 / 16777216.0);
 }
 
+// draw k of (pixel, sample, depth): counter word s*2^32 + k*2^8 + depth (R#42);
+// stream 0 is rng_u. Streams: 1/2 jitter, 3/4 diffuse bounce, 5+2e/6+2e emitter e's point.
+__device__ __forceinline__ double rng_stream(unsigned long long seed, unsigned long long pix, unsigned s,
+                                             int depth, unsigned k) {
+  const unsigned long long G = 0x9E3779B97F4A7C15ull;
+  unsigned long long x = seed ^ ((pix + 1ull) * G);
+  x = mix64(x);
+  x = mix64(x ^ (((unsigned long long)s << 32) + ((unsigned long long)k << 8) + (unsigned long long)(unsigned)depth) * G);
+  return (double)(x >> 40) * (1.0 / 16777216.0);
+}
+
+// uniform point on a sphere (R#41): cos(theta) = 1 - 2 u1, phi = 2 pi u2, pole +z
+__device__ __forceinline__ d3 sphere_point(double u1, double u2) {
+  const double ct = 1.0 - 2.0 * u1;
+  const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  double sp, cp;
+  sincospi(2.0 * u2, &sp, &cp);
+  return mk(st * cp, st * sp, ct);
+}
+
+// cosine-weighted direction about unit n in the Duff et al. (2017) basis (R#40)
+__device__ __forceinline__ d3 cosine_dir(d3 n, double u1, double u2) {
+  const double sg = copysign(1.0, n.z);
+  const double a = -1.0 / (sg + n.z);
+  const double b = n.x * n.y * a;
+  const d3 t1 = mk(1.0 + sg * n.x * n.x * a, sg * b, -sg * n.x);
+  const d3 t2 = mk(b, sg + n.y * n.y * a, -n.y);
+  const double rr = sqrt(u1);
+  double sp, cp;
+  sincospi(2.0 * u2, &sp, &cp);
+  return t1 * (rr * cp) + t2 * (rr * sp) + n * sqrt(fmax(0.0, 1.0 - u1));
+}
+
 // ---- ray generation (a2): §8(c).1 steps 1-2 ------------------------------------
 __device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double& oy) {
   int n = 1;
@@ -64,7 +97,14 @@ __device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double
 // camera ray of sample s of pixel (px, py): d = normalize(F + (2sx-1) R + (1-2sy) U)
 __device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int s) {
   double ox, oy;
-  sample_offset(s, P.spp, ox, oy);
+  if (P.jitter) {  // progressive passes: random offset of sample (pass) sample_base + s (R#42)
+    const unsigned long long pix = (unsigned long long)py * P.W + px;
+    const unsigned sg = (unsigned)(P.sample_base + s);
+    ox = rng_stream(P.seed, pix, sg, 0, 1u);
+    oy = rng_stream(P.seed, pix, sg, 0, 2u);
+  } else {
+    sample_offset(s, P.spp, ox, oy);
+  }
   const double sx = (px + ox) / P.W, sy = (py + oy) / P.H;
   const double a = 2.0 * sx - 1.0, b = 1.0 - 2.0 * sy;
   return normalize(mk(P.F[0] + a * P.R[0] + b * P.U[0], P.F[1] + a * P.R[1] + b * P.U[1],

@@ -66,6 +66,12 @@ struct DevParams {
   int W, H, max_depth, spp;
   int n_spheres, n_pairs_pad, n_planes, n_lights;
   unsigned long long seed;
+  // SURVEY §8(f) NEXT-1 / NEXT-2 (all zero = the §8(a) hot path; R#40-R#43)
+  int integrator;     // 0 Whitted, 1 global (cosine-weighted diffuse bounce)
+  int n_emitters;     // emissive spheres sampled as area lights (0 = area lights off)
+  int jitter;         // 1: random sub-pixel offsets from RNG streams 1/2 (progressive passes)
+  int pad_;
+  long long sample_base;  // global index of sample 0 (pass index of the first pass)
   // job: full frame (mode 0, tile-major work items, row-major output) or shard (mode 1)
   int mode, rank, world, tiles_x, n_tiles, n_items;
 };
@@ -77,6 +83,7 @@ struct DevScene {
   const int* sph_mat;
   const DevMat* mats;
   const DevLight* lights;
+  const int* emit_sph;     // [n_emitters] sphere index of emitter e (prim order), or null
 };
 
 struct DevOutputs {
@@ -86,6 +93,7 @@ struct DevOutputs {
                                 //     closest_sphere_tests
   int* dbg_hits;                // optional [n_px * spp * (max_depth+1)]
   int* dbg_bounces;             // optional [n_px * spp]
+  double* accum;                // optional [H][W][3] progressive sums (rt_render_passes)
 };
 
 // ---- wavefront variant buffers (rt_wavefront.cuh) ----
@@ -96,7 +104,7 @@ struct WfBuffers {
   double* hit;     // [6][cap]  shading point p and facing normal n of the current depth
   float* T;        // [3][cap]
   float* Lr;       // [3][cap]  sample radiance
-  int* depth;      // [cap]
+  int* depth;      // [cap]  segment depth | kPrevDiffuse when the ray left a cosine bounce
   int* skip_c;     // [cap]  sphere the current ray leaves (provably not hit: convexity) or -1
   int* hit_out;    // [cap]  sphere hit from outside at the current depth (shadow rays leaving it
                    //        cannot hit it) or -1
@@ -106,6 +114,7 @@ struct WfBuffers {
   int* sq_path;    // [scap]
   int* sq_light;   // [scap]
   float* sq_c;     // [3][scap] contribution f_r I cos/d^2 * T
+  double* sq_x;    // [3][scap] sampled point of an emitter entry (sq_light >= n_lights), or null
   int* ccand;      // [cap * kCandMax]
   int* cn;         // [cap]
   int* scand;      // [scap * kCandMax]
@@ -121,14 +130,15 @@ __host__ __device__ constexpr int wf_ctr_s(int d) { return 4 * d + 1; }
 __host__ __device__ constexpr int wf_ctr_wc(int d) { return 4 * d + 2; }
 __host__ __device__ constexpr int wf_ctr_ws(int d) { return 4 * d + 3; }
 constexpr int kWfCtrPerDepth = 4;
+constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
 // launchers (rt_kernels.cu)
 cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float4* pairs, int n_pair_float4,
                                cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
-size_t wf_bytes(int cap, int scap);
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr);
+size_t wf_bytes(int cap, int scap, bool with_x);
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, bool with_x, unsigned* ctr);
 // per-launch CUDA events around the intersection kernels (pairs: [2i] before, [2i+1] after)
 struct WfTiming {
   cudaEvent_t* closest;

@@ -491,12 +491,12 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 }
 
 // ---- wavefront launcher ---------------------------------------------------------------------
-size_t wf_bytes(int cap, int scap) {
+size_t wf_bytes(int cap, int scap, bool with_x) {
   return (size_t)cap * (12 * 8 + 6 * 4 + 5 * 4 + 2 * 4 + kCandMax * 4 + 4) +
-         (size_t)scap * (4 + 4 + 12 + kCandMax * 4 + 4 + 4);
+         (size_t)scap * (4 + 4 + 12 + kCandMax * 4 + 4 + 4 + (with_x ? 24 : 0));
 }
 
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, bool with_x, unsigned* ctr) {
   char* p = static_cast<char*>(base);
   auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
   B.cap = cap;
@@ -520,6 +520,7 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * scap));
   B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sq_x = with_x ? reinterpret_cast<double*>(take(3 * 8 * (size_t)scap)) : nullptr;
   B.ctr = ctr;
 }
 
@@ -574,7 +575,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       tm.launches += 4;
     }
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
-    wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out);
+    wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out, o.accum);
     tm.launches += 2;
   }
   return cudaGetLastError();

@@ -85,6 +85,70 @@ __device__ __forceinline__ void shadow_ray(const DevScene& S, d3 p, d3 n, int l,
 // that heads away from it (n.d > 0) cannot hit it (convexity): that sphere is skipped exactly.
 __device__ __forceinline__ int shadow_skip(int out, d3 n, d3 ds) { return (out >= 0 && dot(n, ds) > 0.0) ? out : -1; }
 
+// shadow ray toward a sampled emitter point x (R#41): o = p + EPS_T n, t_max = |x - o|
+__device__ __forceinline__ void shadow_ray_to(d3 p, d3 n, d3 x, d3& os, d3& ds, double& tl) {
+  os = p + n * kEps;
+  const d3 ws = x - os;
+  tl = sqrt(dot(ws, ws));
+  ds = ws * (1.0 / tl);
+}
+
+// the shadow ray of entry j and the emitter sphere it must not test (-1 for point lights)
+__device__ __forceinline__ int entry_ray(const DevParams& P, const DevScene& S, const WfBuffers& B, int j, d3 p, d3 n,
+                                         d3& os, d3& ds, double& tl) {
+  const int l = B.sq_light[j];
+  if (l < P.n_lights) {
+    shadow_ray(S, p, n, l, os, ds, tl);
+    return -1;
+  }
+  shadow_ray_to(p, n, mk(B.sq_x[j], B.sq_x[(size_t)B.scap + j], B.sq_x[2 * (size_t)B.scap + j]), os, ds, tl);
+  return S.emit_sph[l - P.n_lights];
+}
+
+// Light l seen from shading point p: point light l < n_lights (R#2: g = cos / d^2), else
+// emitter e = l - n_lights with one uniform surface point (R#41: g = cos_s cos_l / (d^2 pdf)).
+// False when it sends no shadow ray (d^2 < 1e-12, cos_s <= 0, or cos_l <= 0 for an emitter).
+struct LightSample {
+  d3 x, wi;
+  double cos_s, g;
+  float ir, ig, ib;
+};
+constexpr double kPiD = 3.14159265358979323846;
+__device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene& S, int l, d3 p, d3 nrm,
+                                             unsigned long long pix, unsigned sg, int depth, LightSample& ls) {
+  d3 nl = mk(0, 0, 0);
+  double r = 0.0;
+  const bool emitter = l >= P.n_lights;
+  if (!emitter) {
+    const DevLight lt = S.lights[l];
+    ls.x = mk(lt.px, lt.py, lt.pz);
+    ls.ir = lt.ix; ls.ig = lt.iy; ls.ib = lt.iz;
+  } else {
+    const unsigned e = (unsigned)(l - P.n_lights);
+    const int ks = S.emit_sph[e];
+    const float4 cr = __ldg(S.sph_cr + ks);
+    nl = sphere_point(rng_stream(P.seed, pix, sg, depth, 5u + 2u * e), rng_stream(P.seed, pix, sg, depth, 6u + 2u * e));
+    r = (double)cr.w;
+    ls.x = mk((double)cr.x + r * nl.x, (double)cr.y + r * nl.y, (double)cr.z + r * nl.z);
+    const DevMat m = S.mats[S.sph_mat[ks]];
+    ls.ir = m.er; ls.ig = m.eg; ls.ib = m.eb;
+  }
+  const d3 w = ls.x - p;
+  const double d2 = dot(w, w);
+  if (d2 < 1e-12) return false;
+  ls.wi = w * (1.0 / sqrt(d2));
+  ls.cos_s = dot(nrm, ls.wi);
+  if (ls.cos_s <= 0.0) return false;  // no shadow ray
+  if (emitter) {
+    const double cos_l = -dot(ls.wi, nl);
+    if (cos_l <= 0.0) return false;
+    ls.g = ls.cos_s * cos_l / (d2 * (1.0 / (4.0 * kPiD * r * r)));
+  } else {
+    ls.g = ls.cos_s / d2;
+  }
+  return true;
+}
+
 // ---- a2: ray generation ---------------------------------------------------------------------
 __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
                                                  unsigned long long* stats) {
@@ -134,12 +198,12 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     bool act = e < n;
     d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
     double tl = 0.0;
-    int rob = -1, skip = -1;
+    int rob = -1, skip = -1, skip2 = -1;  // skip2: the emitter a shadow ray aims at (R#41)
     if (act) {
       if constexpr (kShadow) {
         const int path = B.sq_path[e];
         const d3 nrm = ld3(B.hit, B.cap, path, 3);
-        shadow_ray(S, ld3(B.hit, B.cap, path, 0), nrm, B.sq_light[e], o, dir, tl);
+        skip2 = entry_ray(P, S, B, (int)e, ld3(B.hit, B.cap, path, 0), nrm, o, dir, tl);
         skip = shadow_skip(B.hit_out[path], nrm, dir);
         // planes first, exactly (FP64): the first plane in index order that occludes decides
         for (int j = 0; j < P.n_planes; ++j) {
@@ -164,7 +228,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     int nc = 0;
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
-      const float dmax = F.batch<kSrc>(gp, base, disc);
+      const float dmax = F.template batch<kSrc>(gp, base, disc);
       const bool any = act && dmax >= F.cut;
       if (__any_sync(kFull, any)) {
         if (any) {
@@ -175,8 +239,9 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
             const int k = 2 * base + i;
             if (k >= P.n_spheres) break;
             if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
+            if (kShadow && k == skip2) continue;
             float dd, tc;
-            F.sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
+            F.template sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
             const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
             const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
             const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
@@ -271,7 +336,8 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], B.skip_c[path], o, dir, tbest, hs, hp);
-    const int depth = B.depth[path];
+    const int dword = B.depth[path];
+    const int depth = dword & 0xff;
     int prim = -1;
     if (hp >= 0) prim = c_planes[hp].prim;
     else if (hs >= 0) prim = S.sph_prim[hs];
@@ -286,6 +352,16 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     float3 T = lf3(B.T, B.cap, path);
     float3 L = lf3(B.Lr, B.cap, path);
     bool cont = false;
+    const int n_src = P.n_lights + P.n_emitters;  // point lights, then emitters (R#41)
+    unsigned long long pix = 0;
+    unsigned sg = 0;
+    {
+      const long long g = g0 + path;
+      int px = 0, py = 0;
+      item_pixel(P, (int)(g / P.spp), px, py);
+      pix = (unsigned long long)py * P.W + px;
+      sg = (unsigned)(P.sample_base + (int)(g % P.spp));  // R#42
+    }
     unsigned nsh = 0;
     d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
     int mi = 0;
@@ -308,16 +384,14 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       nrm = entering ? ng : ng * -1.0;
       B.hit_out[path] = (hs >= 0 && entering) ? hs : -1;
       const DevMat m = S.mats[mi];
-      L = add(L, mul(T, f3(m.er, m.eg, m.eb)));  // Eq. 7 emission
+      // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
+      const bool sampled = (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
+      if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
       if (m.kind == 0) {
         L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
-        for (int l = 0; l < P.n_lights; ++l) {  // count shadow rays (none if cos <= 0)
-          const DevLight lt = S.lights[l];
-          const d3 w = mk(lt.px, lt.py, lt.pz) - p;
-          const double d2 = dot(w, w);
-          if (d2 < 1e-12) continue;
-          if (dot(nrm, w * (1.0 / sqrt(d2))) <= 0.0) continue;
-          ++nsh;
+        for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
+          LightSample ls;
+          if (light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) ++nsh;
         }
       }
     }
@@ -328,23 +402,24 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       st3(B.hit, B.cap, path, 0, p);
       st3(B.hit, B.cap, path, 3, nrm);
       unsigned k = off;
-      for (int l = 0; l < P.n_lights; ++l) {
-        const DevLight lt = S.lights[l];
-        const d3 w = mk(lt.px, lt.py, lt.pz) - p;
-        const double d2 = dot(w, w);
-        if (d2 < 1e-12) continue;
-        const d3 wi = w * (1.0 / sqrt(d2));
-        const double cosT = dot(nrm, wi);
-        if (cosT <= 0.0) continue;
-        // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3)
-        const d3 rl = nrm * (2.0 * cosT) - wi;
+      for (int l = 0; l < n_src; ++l) {
+        LightSample ls;
+        if (!light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) continue;
+        // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3),
+        // or L_e cos_s cos_l / (d^2 pdf) for an emitter sample (Eq. 8, R#41)
+        const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
         const float alpha = (float)fmax(0.0, -dot(rl, dir));
         const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
-        const float g = (float)(cosT / d2);
+        const float g = (float)ls.g;
         B.sq_path[k] = path;
         B.sq_light[k] = l;
-        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * lt.ix * g, fmaf(m.ag, kInvPi, spec) * lt.iy * g,
-                                       fmaf(m.ab, kInvPi, spec) * lt.iz * g)));
+        if (l >= P.n_lights) {
+          B.sq_x[k] = ls.x.x;
+          B.sq_x[(size_t)B.scap + k] = ls.x.y;
+          B.sq_x[2 * (size_t)B.scap + k] = ls.x.z;
+        }
+        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
+                                       fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
         ++k;
       }
     }
@@ -355,6 +430,10 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       d3 dn = mk(0, 0, 0);
       if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
         dn = reflect(dir, nrm);
+        T = mul(T, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
+        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
         T = mul(T, f3(m.ar, m.ag, m.ab));
         cont = true;
       } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
@@ -376,10 +455,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
           r0 *= r0;
           const double mm = 1.0 - c;
           const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-          const long long g = g0 + path;
-          int px = 0, py = 0;
-          item_pixel(P, (int)(g / P.spp), px, py);
-          const double u = rng_u(P.seed, (unsigned long long)py * P.W + px, (int)(g % P.spp), depth);
+          const double u = rng_u(P.seed, pix, (int)sg, depth);
           refl = u < F;
           if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
         }
@@ -391,7 +467,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         const d3 dnn = normalize(dn);
         st3(B.ray, B.cap, path, 0, p);
         st3(B.ray, B.cap, path, 3, dnn);
-        B.depth[path] = depth + 1;
+        B.depth[path] = (depth + 1) | ((m.kind == 0 && P.integrator == 1) ? kPrevDiffuse : 0);
         // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
         // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
         B.skip_c[path] = (hs >= 0 && dot(dnn, ng) > 0.0) ? hs : -1;
@@ -436,7 +512,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
           st_pl += (unsigned long long)P.n_planes;
           d3 os, ds;
           double tl;
-          shadow_ray(S, p, nrm, B.sq_light[j], os, ds, tl);
+          const int skip2 = entry_ray(P, S, B, j, p, nrm, os, ds, tl);
           const int skip = shadow_skip(B.hit_out[path], nrm, ds);
           const int nc = B.sn[j];
           int first = -1;
@@ -449,13 +525,15 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
             if (first < 0) first = rob;
           } else {
             for (int k = 0; k < P.n_spheres; ++k) {
-              if (k == skip) continue;
+              if (k == skip || k == skip2) continue;
               const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
               if (t >= kEps && t < tl) { first = k; break; }
             }
           }
           occluded = first >= 0;
-          st_sph += occluded ? (unsigned long long)(first + 1) : (unsigned long long)P.n_spheres;
+          // tests up to the first occluder in index order; the aimed-at emitter is not tested
+          const unsigned long long nsk = (skip2 >= 0 && (!occluded || skip2 < first)) ? 1ull : 0ull;
+          st_sph += (occluded ? (unsigned long long)(first + 1) : (unsigned long long)P.n_spheres) - nsk;
         }
         if (!occluded) L = add(L, lf3(B.sq_c, B.scap, j));
       }
@@ -467,13 +545,30 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
 }
 
 // ---- a7: mean over samples in order, 16-byte store ------------------------------------------
-__global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out) {
+__global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out,
+                                                  double* accum) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
     const int w = w0 + i;
     int px = 0, py = 0;
     const bool valid = item_pixel(P, w, px, py);
     if (!valid) {
       if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    if (accum) {  // progressive passes: double sums in pass order, mean = sum / passes so far
+      double* a = accum + 3 * ((long long)py * P.W + px);
+      double a0 = a[0], a1 = a[1], a2 = a[2];
+      for (int s = 0; s < P.spp; ++s) {
+        const float3 v = lf3(B.Lr, B.cap, i * P.spp + s);
+        a0 += (double)v.x;
+        a1 += (double)v.y;
+        a2 += (double)v.z;
+      }
+      a[0] = a0; a[1] = a1; a[2] = a2;
+      if (out) {
+        const double inv = 1.0 / (double)(P.sample_base + P.spp);
+        out[(long long)py * P.W + px] = make_float4((float)(a0 * inv), (float)(a1 * inv), (float)(a2 * inv), 1.0f);
+      }
       continue;
     }
     float3 acc = f3(0.f, 0.f, 0.f);

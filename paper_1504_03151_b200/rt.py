@@ -76,6 +76,9 @@ def lib() -> C.CDLL:
         "rt_assemble_tiles": [vp, i32, i32, i32, vp],
         "rt_render_debug": [i32, i32, i32, i32, vp, vp, vp],
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
+        "rt_set_integrator": [i32, i32],
+        "rt_render_passes": [i32, i32, i32, i64, i32, vp, vp],
+        "rt_render_passes_debug": [i32, i32, i32, i64, i32, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -174,6 +177,29 @@ def render_debug(width, height, max_depth, spp, out, hit_ids, bounces):
     _check("rt_render_debug", lib().rt_render_debug(width, height, max_depth, spp, _ptr(out), _ptr(hit_ids),
                                                     _ptr(bounces)))
     return out, hit_ids, bounces
+
+
+INTEGRATORS = {"whitted": 0, "global": 1}
+
+
+def set_integrator(name: str = "whitted", area_lights: bool = False):
+    """NEXT-1 / NEXT-2 (include/rt.h rt_set_integrator): "whitted" (the hot path) or "global"
+    (cosine-weighted diffuse bounce); area_lights samples every emissive sphere as a light."""
+    _check("rt_set_integrator", lib().rt_set_integrator(INTEGRATORS[name], 1 if area_lights else 0))
+
+
+def render_passes(width, height, max_depth, pass_begin, n_passes, accum, out=None):
+    """Progressive passes: accum (float64 CUDA tensor [H, W, 3], zeroed before pass 0) += the
+    radiance of passes pass_begin .. pass_begin + n_passes - 1; out (optional) = the mean."""
+    _check("rt_render_passes", lib().rt_render_passes(width, height, max_depth, int(pass_begin), n_passes,
+                                                      _ptr(accum), _ptr(out) if out is not None else None))
+    return accum
+
+
+def render_passes_debug(width, height, max_depth, pass_begin, n_passes, accum, out, hit_ids, bounces):
+    _check("rt_render_passes_debug", lib().rt_render_passes_debug(
+        width, height, max_depth, int(pass_begin), n_passes, _ptr(accum), _ptr(out), _ptr(hit_ids), _ptr(bounces)))
+    return accum, out, hit_ids, bounces
 
 
 def stats() -> dict:

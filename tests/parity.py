@@ -45,11 +45,13 @@ class Classified:
     cond_ok: np.ndarray
 
 
-def classify(oracle_mod, sc, ref, pixels, n_replicas=2) -> Classified:
+def classify(oracle_mod, sc, ref, pixels, n_replicas=2, **okw) -> Classified:
+    """okw: the oracle's mode arguments of `ref` (integrator, area_lights, jitter, sample_base,
+    spp ...), repeated for the perturbed replicas."""
     margin_ok = (ref.margin >= MARGIN_THR).all(axis=1)
     cond_ok = np.ones(len(ref.rgb), bool)
     for k in range(n_replicas):
-        rp = oracle_mod.render(sc, pixels=pixels, perturb=PERTURB, perturb_seed=1 + k)
+        rp = oracle_mod.render(sc, pixels=pixels, perturb=PERTURB, perturb_seed=1 + k, **okw)
         same_ids = (rp.hit_ids == ref.hit_ids).all(axis=(1, 2))
         rel = (np.abs(rp.rgb - ref.rgb) / (np.abs(ref.rgb) + 1e-6)).max(axis=1)
         cond_ok &= same_ids & (rel <= COND_REL_THR)

@@ -1,0 +1,164 @@
+"""GPU parity of the NEXT-1 / NEXT-2 modes: spherical area lights, the global
+(cosine-bounce) integrator and progressive passes, through the C ABI, against the oracle with
+the same parity rule as the hot path (tests/parity.py), plus closed forms the kernels must hit
+and the progressive resume property."""
+import numpy as np
+import pytest
+
+import scenegen
+from scenegen import DIFFUSE
+from tests import parity
+from tests.gpu_helpers import gpu_passes, gpu_render
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1504_03151_b200 import build
+    build.build()
+    yield
+
+
+@pytest.fixture(autouse=True)
+def _reset():
+    yield
+    from paper_1504_03151_b200 import rt
+    rt.set_integrator("whitted", False)
+    rt.set_variant("auto")
+
+
+def _n_src(sc, area):
+    n_emit = 0
+    if area:
+        em = sc.mat_emission[sc.prim_mat]
+        n_emit = int(((sc.prim_type == scenegen.SPHERE) & (em > 0).any(axis=1)).sum())
+    return sc.n_lights + n_emit
+
+
+def _check_frame(oracle_lib, sc, integrator, area, label):
+    g = gpu_render(sc, integrator=integrator, area_lights=area)
+    okw = dict(integrator=1 if integrator == "global" else 0, area_lights=int(area))
+    ref = oracle_lib.render(sc, **okw)
+    cls = parity.classify(oracle_lib, sc, ref, None, **okw)
+    rep = parity.compare(g["rgb"], g["ids"], g["bounces"], ref, cls)
+    print(f"[{label}] {rep}")
+    assert rep.ok, f"{label}: {rep}"
+    ok, msg = parity.ray_budget_ok(g["stats"], ref.counts, ref, cls, _n_src(sc, area))
+    print(f"[{label}] rays: {msg}")
+    assert ok, msg
+    assert g["stats"]["variant"] == 1  # extended modes run the wavefront kernels
+    return g, ref
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("integrator,area", [("whitted", True), ("global", False), ("global", True)])
+def test_tiny_random_with_emitters(oracle_lib, seed, integrator, area):
+    sc = scenegen.random_tiny(seed, n_spheres=7, n_planes=2, n_lights=2, n_emitters=2, width=37, height=23,
+                              max_depth=4, spp=3)
+    _check_frame(oracle_lib, sc, integrator, area, f"tiny{seed}/{integrator}/area={area}")
+
+
+def test_c0_reduced_frame_global_area(oracle_lib):
+    sc = scenegen.get("C0").with_frame(width=80, height=60, spp=2)
+    g, ref = _check_frame(oracle_lib, sc, "global", True, "C0 80x60")
+    assert ref.rgb.mean() > 0.01  # lit by the emitter only
+
+
+def test_megakernel_setting_is_overridden_by_extended_modes(oracle_lib):
+    sc = scenegen.random_tiny(4, n_spheres=4, n_emitters=1, width=16, height=12, max_depth=2)
+    g = gpu_render(sc, variant="megakernel", integrator="global", area_lights=True)
+    assert g["stats"]["variant"] == 1
+    w = gpu_render(sc, variant="megakernel")
+    assert w["stats"]["variant"] == 0
+
+
+def test_emitters_ignored_without_area_lights():
+    """area_lights off: the emitters are ordinary emissive geometry, same frame as the hot path."""
+    sc = scenegen.random_tiny(5, n_spheres=5, n_emitters=2, width=24, height=16, max_depth=3, spp=2)
+    a = gpu_render(sc, integrator="whitted", area_lights=False, variant="wavefront")
+    b = gpu_render(sc, variant="megakernel")
+    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+
+
+# ---- closed forms on the GPU ----------------------------------------------------------------
+def test_gpu_furnace_geometric_series():
+    rho, Le, D = 0.5, 2.0, 5
+    b = scenegen.builder()
+    b.sphere((0, 0, 0), 10.0, b.material(DIFFUSE, (rho, rho, rho), emission=(Le, Le, Le)))
+    sc = b.build("furnace", eye=(1, 2, 3), look_at=(0, 0, 9), up=(0, 1, 0), vfov=60, width=16, height=12,
+                 max_depth=D, spp=4, background=(7, 7, 7))
+    g = gpu_render(sc, integrator="global")
+    expected = Le * (1 - rho ** (D + 1)) / (1 - rho)
+    assert np.allclose(g["rgb"], expected, rtol=2e-6)
+    assert (g["bounces"] == D).all() and (g["ids"] == 0).all()
+    assert g["stats"]["secondary"] == 16 * 12 * 4 * D
+
+
+def test_gpu_diffuse_plane_under_constant_sky():
+    b = scenegen.builder()
+    b.plane((0, 1, 0), 0.0, b.material(DIFFUSE, (0.25, 0.5, 0.75)))
+    sc = b.build("sky", eye=(0, 2, -3), look_at=(0, 0, 2), up=(0, 1, 0), vfov=40, width=24, height=16,
+                 max_depth=3, spp=2, background=(2.0, 4.0, 8.0))
+    g = gpu_render(sc, integrator="global")
+    assert np.allclose(g["rgb"], np.array([0.5, 2.0, 6.0]), rtol=1e-6)
+    assert (g["bounces"] == 1).all()
+
+
+# ---- progressive passes ---------------------------------------------------------------------
+def test_progressive_passes_parity_and_mean(oracle_lib):
+    sc = scenegen.get("C0").with_frame(width=48, height=36)
+    n = 4
+    g = gpu_passes(sc, 0, n)
+    okw = dict(integrator=1, area_lights=1, jitter=1, sample_base=0, spp=n)
+    ref = oracle_lib.render(sc, **okw)
+    cls = parity.classify(oracle_lib, sc, ref, None, **okw)
+    rep = parity.compare(g["accum_np"] / n, g["ids"], g["bounces"], ref, cls)
+    print(f"[C0 passes] {rep}")
+    assert rep.ok, str(rep)
+    ok, msg = parity.ray_budget_ok(g["stats"], ref.counts, ref, cls, 1)
+    assert ok, msg
+    assert np.array_equal(g["rgba"][:, :3], (g["accum_np"] / n).astype(np.float32))
+    assert (g["rgba"][:, 3] == 1.0).all()
+
+
+def test_progressive_resume_bit_identical():
+    sc = scenegen.get("C0").with_frame(width=64, height=48)
+    one = gpu_passes(sc, 0, 6, debug=False)
+    part = gpu_passes(sc, 0, 2, debug=False)
+    part = gpu_passes(sc, 2, 3, accum=part["accum"], debug=False)
+    part = gpu_passes(sc, 5, 1, accum=part["accum"], debug=False)
+    assert np.array_equal(one["accum_np"], part["accum_np"])
+    assert np.array_equal(one["rgba"], part["rgba"])
+
+
+def test_progressive_later_passes_match_oracle(oracle_lib):
+    """Passes 7..9 of a pixel sample: the RNG is keyed by the global pass index."""
+    sc = scenegen.random_tiny(6, n_spheres=6, n_emitters=2, n_lights=1, width=20, height=14, max_depth=3)
+    g = gpu_passes(sc, 7, 3)
+    okw = dict(integrator=1, area_lights=1, jitter=1, sample_base=7, spp=3)
+    ref = oracle_lib.render(sc, **okw)
+    cls = parity.classify(oracle_lib, sc, ref, None, **okw)
+    rep = parity.compare(g["accum_np"] / 3, g["ids"], g["bounces"], ref, cls)
+    assert rep.ok, str(rep)
+
+
+def test_extended_mode_validation():
+    import torch
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get("C1")
+    rt.load_scene(sc)
+    with pytest.raises(rt.RtError) as e:
+        rt._check("rt_set_integrator", rt.lib().rt_set_integrator(7, 0))
+    assert e.value.code == -1
+    with pytest.raises(rt.RtError):
+        rt._check("rt_set_integrator", rt.lib().rt_set_integrator(1, 2))
+    host = np.zeros((8, 8, 3))
+    with pytest.raises(rt.RtError):
+        rt.render_passes(8, 8, 1, 0, 1, host)
+    acc = torch.zeros((8, 8, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(rt.RtError):
+        rt.render_passes(8, 8, 1, 2 ** 32 - 1, 2, acc)
