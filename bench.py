@@ -14,6 +14,10 @@ timed with CUDA events on the launch stream; L2 (126 MB) is flushed with a 256 M
 every frame, outside the per-frame events; value = rays of all ranks / max-over-ranks time.
 `--impl reference` times the CPU oracle (the plain C reference written from the paper) on the
 host cores with the same metric, on a bounded pixel sample per step.
+
+`--mode progressive` (auxiliary; 1 GPU): the paper-shaped Cornell
+box C0 (640x480, depth 6) with the global integrator and its spherical area light, a step =
+one rt_render_passes call of --passes passes accumulated into a device float64 buffer.
 """
 from __future__ import annotations
 
@@ -119,29 +123,34 @@ _SCENES = {}
 
 def _oracle_chunk(args):
     """Worker: oracle on a slice of pixels (runs in a separate process; scene cached)."""
-    name, pixels = args
+    name, pixels, okw = args
     from oracle import pyoracle as po
     if name not in _SCENES:
         _SCENES[name] = scenegen.get(name)
     sc = _SCENES[name]
-    _, counts = po.render_rgb_only(sc, pixels=np.asarray(pixels, np.int64))
+    if okw.get("spp"):
+        sc = sc.with_frame(spp=okw["spp"])
+    okw = {k: v for k, v in okw.items() if k != "spp"}
+    _, counts = po.render_rgb_only(sc, pixels=np.asarray(pixels, np.int64), **okw)
     return counts
 
 
 class OracleTimer:
-    """The CPU oracle, as it stands, on all host cores (pixel slices across processes)."""
+    """The CPU oracle, as it stands, on all host cores (pixel slices across processes).
+    okw: oracle mode arguments (progressive mode: integrator, area_lights, jitter, spp)."""
 
-    def __init__(self, name: str):
+    def __init__(self, name: str, okw: dict | None = None):
         import concurrent.futures as cf
         from oracle import pyoracle as po
         po.build()
         self.name = name
+        self.okw = dict(okw or {})
         self.cores = os.cpu_count() or 1
         self.pool = cf.ProcessPoolExecutor(max_workers=self.cores)
-        list(self.pool.map(_oracle_chunk, [(name, [0])] * self.cores))  # warm the workers
+        list(self.pool.map(_oracle_chunk, [(name, [0], self.okw)] * self.cores))  # warm the workers
 
     def run(self, pixels: np.ndarray) -> tuple[float, dict]:
-        chunks = [(self.name, c.tolist()) for c in np.array_split(pixels, self.cores) if len(c)]
+        chunks = [(self.name, c.tolist(), self.okw) for c in np.array_split(pixels, self.cores) if len(c)]
         t0 = time.perf_counter()
         res = list(self.pool.map(_oracle_chunk, chunks))
         dt = time.perf_counter() - t0
@@ -152,9 +161,11 @@ class OracleTimer:
         self.pool.shutdown()
 
 
-def cpu_baseline(name: str, target_core_s: float = 20.0, seed: int = 7) -> dict:
+def cpu_baseline(name: str, target_core_s: float = 20.0, seed: int = 7, okw: dict | None = None) -> dict:
     sc = scenegen.get(name)
-    tm = OracleTimer(name)
+    if okw and okw.get("spp"):
+        sc = sc.with_frame(spp=okw["spp"])
+    tm = OracleTimer(name, okw)
     rng = np.random.default_rng(seed)
     # calibrate: per-pixel cost on a small sample, then size the sample to ~target_core_s
     probe = rng.choice(sc.width * sc.height, 64 * tm.cores, replace=False)
@@ -166,8 +177,9 @@ def cpu_baseline(name: str, target_core_s: float = 20.0, seed: int = 7) -> dict:
     tm.close()
     rays = cnt["primary"] + cnt["shadow"] + cnt["secondary"]
     frac = n / (sc.width * sc.height)
+    what = f"all {sc.spp} spp" if not okw else f"{sc.spp} progressive passes, global integrator + area lights"
     return {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": tm.cores, "kind": "oracle",
-            "sample": f"{n} random pixels of {name} (all {sc.spp} spp, depth {sc.max_depth}) = {frac:.2%} of the frame, "
+            "sample": f"{n} random pixels of {name} ({what}, depth {sc.max_depth}) = {frac:.2%} of the frame, "
                       f"{dt:.1f} s wall on {tm.cores} processes",
             "fps_extrapolated": 1.0 / (dt / frac)}
 
@@ -364,6 +376,114 @@ def run_b200(args):
     return 0
 
 
+def run_progressive(args):
+    """NEXT-1/NEXT-2 measurement: progressive passes of C0 with the global integrator and area
+    lights. A step = one rt_render_passes call of args.passes passes (pass indices continue
+    across steps, the float64 accumulation buffer stays on the device)."""
+    import torch
+    from paper_1504_03151_b200 import build as rtbuild
+    from paper_1504_03151_b200 import rt
+    if _env_int("WORLD_SIZE", 1) != 1:
+        raise SystemExit("--mode progressive runs on one GPU (rt_render_passes is a full-frame call)")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    rtbuild.build()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    rt.set_stream(stream)
+    name = args.config if args.config != "C4" else "C0"
+    sc = scenegen.get(name)
+    W, H, D, P = sc.width, sc.height, sc.max_depth, args.passes
+    prims, mats, lights, env = rt.pack_scene(sc)
+    rt.load_scene(sc)
+    rt.set_integrator("global", True)
+    accum = torch.zeros((H, W, 3), dtype=torch.float64, device=dev)
+    out = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    nxt = [0]
+
+    def step():
+        rt.render_passes(W, H, D, nxt[0], P, accum, out)
+        nxt[0] += P
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    first = nxt[0]
+    clocks = ClockSampler(0)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    st_last = rt.stats()
+    # exact ray counts of the timed steps: replay the same pass indices (deterministic) untimed
+    acc2 = torch.zeros_like(accum)
+    rays = tests_c = tests_s = tests_p = 0
+    for i in range(args.steps):
+        rt.render_passes(W, H, D, first + i * P, P, acc2, None)
+        s2 = rt.stats()
+        rays += s2["primary"] + s2["shadow"] + s2["secondary"]
+        tests_c += s2["closest_sphere_tests"]
+        tests_s += s2["sphere_tests"] - s2["closest_sphere_tests"]
+        tests_p += s2["plane_tests"]
+    ms_per_step = total_ms / args.steps
+    value = rays / (total_ms * 1e-3) / 1e6
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = clk.get("sm_max_mhz") or PEAK_FALLBACK_MHZ
+    peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    whole = (FLOP_SPHERE * (tests_c + tests_s) + FLOP_PLANE * tests_p) / (total_ms * 1e-3) / 1e12
+    tc = st_last["isect_closest_ms"]
+    # e2e through the public API with host buffers: scene H2D, P passes, mean frame D2H
+    host_out = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
+    ke = max(3, min(args.steps, 10))
+    acc3 = torch.zeros_like(accum)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rays_e2e = 0
+    for i in range(ke):
+        rt.scene_upload(prims, mats, lights, env)
+        rt.camera_set(sc.eye, sc.look_at, sc.up, sc.vfov)
+        rt.render_passes(W, H, D, i * P, P, acc3, host_out)
+        s3 = rt.stats()
+        rays_e2e += s3["primary"] + s3["shadow"] + s3["secondary"]
+    dt = time.perf_counter() - t0
+    rt.set_integrator("whitted", False)
+    line = {
+        "metric": "Mrays/s (primary+shadow+secondary), progressive passes, global illumination + area light",
+        "value": value, "unit": "Mrays/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (FFMA2 filter, radiance) + f64 (decisions, geometry, accumulation)",
+        "data": f"synthetic (seeded scenegen {name} Cornell box; no dataset)",
+        "passes_per_s": P / (ms_per_step * 1e-3),
+        "config": dict(sc.describe(), workload=name, mode="progressive", integrator="global", area_lights=True,
+                       passes_per_step=P, l2="flushed (256 MiB write) before every step, outside the events",
+                       rays_per_step=int(rays / args.steps)),
+        "roofline": {"bound": "alu", "achieved": whole, "peak": peak, "unit": "TFLOP/s", "frac": whole / peak,
+                     "traffic": None, "kernel": "whole step (counted test flops / step time; the sphere scan is "
+                     "not dominant at 4 spheres + 5 planes, see profiles/r01_launches_c0_progressive_summary.txt)",
+                     "closest_scan_share_of_step": tc / ms_per_step},
+        "clocks": clk,
+        "gpu_launches": st_last["launches"] * args.steps,
+        "e2e": {"value": rays_e2e / dt / 1e6, "unit": "Mrays/s",
+                "h2d_bytes_per_step": int(prims.nbytes + mats.nbytes + lights.nbytes + env.nbytes),
+                "d2h_bytes_per_step": H * W * 16, "steps": ke, "ms_per_step": 1e3 * dt / ke,
+                "timing": "host wall clock around rt_scene_upload + rt_camera_set + rt_render_passes(pinned host out)"},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, target_core_s=args.cpu_seconds,
+                                            okw=dict(integrator=1, area_lights=1, jitter=1, spp=P))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -375,9 +495,14 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="core-seconds of oracle work")
     ap.add_argument("--ref-pixels", type=int, default=1024, help="--impl reference: pixels per step")
     ap.add_argument("--strict", action="store_true", default=True)
+    ap.add_argument("--mode", choices=["hot", "progressive"], default="hot",
+                    help="hot: the §8(a) path on C4 (default); progressive: NEXT-1/2 passes on C0")
+    ap.add_argument("--passes", type=int, default=16, help="--mode progressive: passes per step")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "progressive":
+        return run_progressive(args)
     return run_b200(args)
 
 

@@ -689,7 +689,9 @@ static sample_result trace_sample(const prims* P, const camera* cam, const orc_f
       double u2 = orc_rng_stream(fr->seed, pixel_index, sg, (uint32_t)depth, 4u);
       double n_a[3], dn_a[3];
       st3(n_a, n);
-      margin = fmin2(margin, fabs(n.z) / An); /* sign(n.z) selects the basis branch */
+      /* sign(n.z) selects the basis branch: a decision for a sphere normal; a plane's normal is
+       * exact on both sides (normalised from the same floats), signed zero included */
+      if (P->type[best] == 0) margin = fmin2(margin, fabs(n.z) / An);
       orc_cosine_direction(n_a, u1, u2, dn_a);
       dn = ldd(dn_a);
       T = mulv(T, rho); /* f_r cos / pdf = albedo */

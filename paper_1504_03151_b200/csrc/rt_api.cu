@@ -172,11 +172,12 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
   rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p};
   rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces, accum};
-  // the NEXT-1 / NEXT-2 modes (global integrator, area lights, progressive passes) exist in the
-  // wavefront kernels only; the megakernel implements the §8(a) hot path
+  // AUTO: the wavefront kernels for large scenes, and for the NEXT-1 / NEXT-2 modes, whose long
+  // divergent paths (every diffuse hit continues; one lane per pixel walks all its passes) leave
+  // the megakernel's lanes idle (C0 progressive, 16 passes: 9.7 ms wavefront, 15.2 ms megakernel)
   const bool extended = p.integrator != 0 || p.n_emitters > 0 || p.jitter != 0 || accum != nullptr;
-  const bool wavefront = extended || c.variant == RT_VARIANT_WAVEFRONT ||
-                         (c.variant == RT_VARIANT_AUTO && c.n_spheres >= kAutoWavefrontSpheres);
+  const bool wavefront = c.variant == RT_VARIANT_WAVEFRONT ||
+                         (c.variant == RT_VARIANT_AUTO && (extended || c.n_spheres >= kAutoWavefrontSpheres));
   if (wavefront) {
     // chunk of whole pixels: at most 2^22 paths; shadow entries: paths x lights
     const long long want = (long long)p.n_items * p.spp;

@@ -39,23 +39,23 @@ struct Lane {
   double tmax;
   int qs, qp;               // query result: packed sphere / plane index (-1 none)
   float3 contrib;
+  // NEXT-1 / NEXT-2 (kExt kernels only): emitter a shadow query must not test, cosine-bounce
+  // flag (R#43), float64 progressive sums of the pixel (R#42)
+  int qskip, prevd;
+  double acc0, acc1, acc2;
   // stats
   unsigned n_primary, n_shadow, n_secondary;
   unsigned long long n_stests, n_ptests, n_ctests;
 };
 
 __device__ __forceinline__ void start_sample(Lane& L, const DevParams& P) {
-  double ox, oy;
-  sample_offset(L.s, P.spp, ox, oy);
-  const double sx = (L.px + ox) / P.W, sy = (L.py + oy) / P.H;
-  const double a = 2.0 * sx - 1.0, b = 1.0 - 2.0 * sy;
-  const d3 dir = mk(P.F[0] + a * P.R[0] + b * P.U[0], P.F[1] + a * P.R[1] + b * P.U[1],
-                    P.F[2] + a * P.R[2] + b * P.U[2]);
   L.o = mk(P.eye[0], P.eye[1], P.eye[2]);
-  L.d = normalize(dir);
+  L.d = camera_dir(P, L.px, L.py, L.s);  // stratified / Hammersley, or random jitter (R#42)
   L.T = f3(1.f, 1.f, 1.f);
   L.Ls = f3(0.f, 0.f, 0.f);
   L.depth = 0;
+  L.prevd = 0;
+  L.qskip = -1;
   L.qkind = Q_CLOSEST;
   L.qo = L.o; L.qd = L.d; L.tmax = kInf;
   L.n_primary++;
@@ -80,7 +80,17 @@ __device__ __forceinline__ bool start_item(Lane& L, const DevParams& P, int w, f
   return true;
 }
 
-template <bool kSmem>
+template <bool kExt>
+__device__ __forceinline__ void load_accum(Lane& L, const DevParams& P, const DevOutputs& O) {
+  if constexpr (kExt) {
+    if (O.accum) {
+      const double* a = O.accum + 3 * ((long long)L.py * P.W + L.px);
+      L.acc0 = a[0]; L.acc1 = a[1]; L.acc2 = a[2];
+    }
+  }
+}
+
+template <bool kSmem, bool kExt>
 __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const DevScene& S,
                                           const float4* __restrict__ pairs) {
   bool act = (L.qkind != Q_NONE);
@@ -118,6 +128,7 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       cand &= cand - 1u;
       const int k = 2 * base + i;  // pair (base + i/2), half i&1
       if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds the dummy margin)
+      if (kExt && shadow && k == L.qskip) continue;  // the emitter a shadow ray aims at (R#41)
       float dd, tc;
       F.sphere<kSrc>(pairs, S.sph_cr, k, dd, tc);
       const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));
@@ -181,7 +192,9 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       L.n_ptests += (unsigned)(hp + 1);
     } else {
       L.n_ptests += (unsigned)P.n_planes;
-      L.n_stests += (unsigned)(hs >= 0 ? hs + 1 : P.n_spheres);
+      unsigned nt = (unsigned)(hs >= 0 ? hs + 1 : P.n_spheres);
+      if (kExt && L.qskip >= 0 && (hs < 0 || L.qskip < hs)) --nt;  // the emitter is not tested
+      L.n_stests += nt;
     }
   }
   L.tmax = tmax;
@@ -190,9 +203,14 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
 }
 
 // ---- shading, shadow setup, continuation (a4-a7) --------------------------------------------
-template <bool kDebug>
+template <bool kDebug, bool kExt>
 __device__ void finish_sample(Lane& L, const DevParams& P, const DevOutputs& O) {
   L.Lpix = add(L.Lpix, L.Ls);
+  if constexpr (kExt) {  // progressive sums in pass order, as wf_resolve
+    L.acc0 += (double)L.Ls.x;
+    L.acc1 += (double)L.Ls.y;
+    L.acc2 += (double)L.Ls.z;
+  }
   if constexpr (kDebug) {
     const long long si = ((long long)L.py * P.W + L.px) * P.spp + L.s;
     O.dbg_bounces[si] = L.depth;  // secondary rays traced = depth of the last segment
@@ -203,6 +221,20 @@ __device__ void finish_sample(Lane& L, const DevParams& P, const DevOutputs& O) 
     start_sample(L, P);
     return;
   }
+  if constexpr (kExt) {
+    if (O.accum) {
+      const long long pix = (long long)L.py * P.W + L.px;
+      double* a = O.accum + 3 * pix;
+      a[0] = L.acc0; a[1] = L.acc1; a[2] = L.acc2;
+      if (O.out) {
+        const double inv = 1.0 / (double)(P.sample_base + P.spp);
+        O.out[pix] = make_float4((float)(L.acc0 * inv), (float)(L.acc1 * inv), (float)(L.acc2 * inv), 1.0f);
+      }
+      L.item = -1;
+      L.qkind = Q_NONE;
+      return;
+    }
+  }
   const float inv = 1.0f / (float)P.spp;
   const float4 v = make_float4(L.Lpix.x * inv, L.Lpix.y * inv, L.Lpix.z * inv, 1.0f);
   if (P.mode == 0) O.out[(long long)L.py * P.W + L.px] = v;  // 16-byte vector store
@@ -211,16 +243,23 @@ __device__ void finish_sample(Lane& L, const DevParams& P, const DevOutputs& O) 
   L.qkind = Q_NONE;
 }
 
-template <bool kDebug>
+template <bool kDebug, bool kExt>
 __device__ void bounce(Lane& L, const DevParams& P, const DevScene& S, const DevOutputs& O) {
-  if (L.depth == P.max_depth) { finish_sample<kDebug>(L, P, O); return; }
+  if (L.depth == P.max_depth) { finish_sample<kDebug, kExt>(L, P, O); return; }
   const DevMat m = S.mats[L.mat];
+  const unsigned long long pix = (unsigned long long)L.py * P.W + L.px;
+  const unsigned sg = (unsigned)(P.sample_base + L.s);  // R#42
   d3 dn;
+  bool cosine = false;
   if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
     dn = reflect(L.d, L.n);
     L.T = mul(L.T, f3(m.ar, m.ag, m.ab));
+  } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
+    dn = cosine_dir(L.n, rng_stream(P.seed, pix, sg, L.depth, 3u), rng_stream(P.seed, pix, sg, L.depth, 4u));
+    L.T = mul(L.T, f3(m.ar, m.ag, m.ab));
+    cosine = true;
   } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
-    if (!(m.kr > 0.f)) { finish_sample<kDebug>(L, P, O); return; }
+    if (!(m.kr > 0.f)) { finish_sample<kDebug, kExt>(L, P, O); return; }
     dn = reflect(L.d, L.n);
     L.T = f3(L.T.x * m.kr, L.T.y * m.kr, L.T.z * m.kr);
   } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
@@ -236,7 +275,7 @@ __device__ void bounce(Lane& L, const DevParams& P, const DevScene& S, const Dev
       r0 *= r0;
       const double mm = 1.0 - c;
       const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-      const double u = rng_u(P.seed, (unsigned long long)L.py * P.W + L.px, L.s, L.depth);
+      const double u = rng_u(P.seed, pix, (int)sg, L.depth);
       refl = u < F;
       if (!refl) dn = L.d * eta + L.n * (eta * ci - cosT);
     }
@@ -246,16 +285,46 @@ __device__ void bounce(Lane& L, const DevParams& P, const DevScene& S, const Dev
   L.o = L.p;
   L.d = normalize(dn);
   L.depth++;
+  L.prevd = cosine ? 1 : 0;
   L.n_secondary++;
   L.qkind = Q_CLOSEST;
   L.qo = L.o; L.qd = L.d; L.tmax = kInf;
 }
 
-template <bool kDebug>
+template <bool kDebug, bool kExt>
 __device__ void next_light_or_bounce(Lane& L, const DevParams& P, const DevScene& S,
                                      const DevOutputs& O) {
   const DevMat m = S.mats[L.mat];
-  if (m.kind == 0) {
+  if (kExt && m.kind == 0) {  // point lights, then one surface sample per emitter (R#41)
+    const unsigned long long pix = (unsigned long long)L.py * P.W + L.px;
+    const unsigned sg = (unsigned)(P.sample_base + L.s);
+    while (L.light < P.n_lights + P.n_emitters) {
+      const int l = L.light++;
+      LightSample ls;
+      if (!light_sample(P, S, l, L.p, L.n, pix, sg, L.depth, ls)) continue;
+      double tl;
+      d3 os, ds;
+      if (l < P.n_lights) {
+        shadow_ray(S, L.p, L.n, l, os, ds, tl);
+        L.qskip = -1;
+      } else {
+        shadow_ray_to(L.p, L.n, ls.x, os, ds, tl);
+        L.qskip = S.emit_sph[l - P.n_lights];
+      }
+      L.qo = os;
+      L.qd = ds;
+      L.tmax = tl;
+      L.qkind = Q_SHADOW;
+      L.n_shadow++;
+      const d3 rl = L.n * (2.0 * ls.cos_s) - ls.wi;
+      const float alpha = (float)fmax(0.0, -dot(rl, L.d));
+      const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+      const float g = (float)ls.g;
+      L.contrib = mul(L.T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
+                              fmaf(m.ab, kInvPi, spec) * ls.ib * g));
+      return;
+    }
+  } else if (m.kind == 0) {
     while (L.light < P.n_lights) {
       const DevLight lt = S.lights[L.light];
       L.light++;
@@ -285,10 +354,10 @@ __device__ void next_light_or_bounce(Lane& L, const DevParams& P, const DevScene
       return;
     }
   }
-  bounce<kDebug>(L, P, S, O);
+  bounce<kDebug, kExt>(L, P, S, O);
 }
 
-template <bool kDebug>
+template <bool kDebug, bool kExt>
 __device__ void on_closest(Lane& L, const DevParams& P, const DevScene& S, const DevOutputs& O) {
   const int hs = L.qs, hp = L.qp;
   int prim = -1;
@@ -300,7 +369,7 @@ __device__ void on_closest(Lane& L, const DevParams& P, const DevScene& S, const
   }
   if (prim < 0) {  // miss -> background
     L.Ls = add(L.Ls, mul(L.T, f3(P.bg[0], P.bg[1], P.bg[2])));
-    finish_sample<kDebug>(L, P, O);
+    finish_sample<kDebug, kExt>(L, P, O);
     return;
   }
   L.p = L.o + L.d * L.tmax;
@@ -318,19 +387,20 @@ __device__ void on_closest(Lane& L, const DevParams& P, const DevScene& S, const
   L.entering = dot(L.d, ng) < 0.0;
   L.n = L.entering ? ng : ng * -1.0;
   const DevMat m = S.mats[L.mat];
-  L.Ls = add(L.Ls, mul(L.T, f3(m.er, m.eg, m.eb)));             // Eq. 7 emission
+  // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
+  if (!(kExt && L.prevd && P.n_emitters > 0 && hs >= 0)) L.Ls = add(L.Ls, mul(L.T, f3(m.er, m.eg, m.eb)));
   if (m.kind == 0) L.Ls = add(L.Ls, mul(L.T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
   L.light = 0;
-  next_light_or_bounce<kDebug>(L, P, S, O);
+  next_light_or_bounce<kDebug, kExt>(L, P, S, O);
 }
 
-template <bool kDebug>
+template <bool kDebug, bool kExt>
 __device__ __forceinline__ void advance(Lane& L, const DevParams& P, const DevScene& S, const DevOutputs& O) {
   if (L.qkind == Q_CLOSEST) {
-    on_closest<kDebug>(L, P, S, O);
+    on_closest<kDebug, kExt>(L, P, S, O);
   } else if (L.qkind == Q_SHADOW) {
     if (L.qs < 0 && L.qp < 0) L.Ls = add(L.Ls, L.contrib);  // visible: add f_r I cos / d^2
-    next_light_or_bounce<kDebug>(L, P, S, O);
+    next_light_or_bounce<kDebug, kExt>(L, P, S, O);
   }
 }
 
@@ -338,7 +408,7 @@ __device__ __forceinline__ void advance(Lane& L, const DevParams& P, const DevSc
 #ifndef RT_MIN_BLOCKS
 #define RT_MIN_BLOCKS 2
 #endif
-template <bool kSmem, bool kDebug>
+template <bool kSmem, bool kDebug, bool kExt>
 __global__ void __launch_bounds__(256, RT_MIN_BLOCKS)
 render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
   __shared__ uint64_t s_mbar;
@@ -365,12 +435,12 @@ render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
       if (need & (1u << lane)) {
         const unsigned w = base + __popc(need & lt_mask);
         if (w >= (unsigned)P.n_items) exhausted = true;
-        else start_item(L, P, (int)w, O.out);
+        else if (start_item(L, P, (int)w, O.out)) load_accum<kExt>(L, P, O);
       }
     }
     if (!__any_sync(kFull, L.qkind != Q_NONE)) break;
-    intersect<kSmem>(L, P, S, pairs);
-    advance<kDebug>(L, P, S, O);
+    intersect<kSmem, kExt>(L, P, S, pairs);
+    advance<kDebug, kExt>(L, P, S, O);
   }
 
   // stats: warp reduction, one atomic per warp
@@ -441,32 +511,41 @@ cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float
   return e;
 }
 
-template <bool kSmem, bool kDebug>
+template <bool kSmem, bool kDebug, bool kExt>
 static cudaError_t launch_t(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
                            cudaStream_t st, int* blocks_per_sm_out) {
   const size_t smem = kSmem ? (size_t)p.n_pairs_pad * 32u : 0u;
-  cudaError_t e = cudaFuncSetAttribute(render_kernel<kSmem, kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(smem > 0 ? smem : 1));
+  auto kern = render_kernel<kSmem, kDebug, kExt>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
   if (e != cudaSuccess) return e;
   int bps = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, render_kernel<kSmem, kDebug>, 256, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, smem);
   if (e != cudaSuccess) return e;
   if (bps < 1) bps = 1;
   if (blocks_per_sm_out) *blocks_per_sm_out = bps;
   const long long want = (long long)num_sms * bps;
   const long long max_useful = ((long long)p.n_items + 255) / 256;  // no idle CTAs on tiny frames
   const int grid = (int)(want < max_useful ? want : (max_useful > 0 ? max_useful : 1));
-  render_kernel<kSmem, kDebug><<<grid, 256, smem, st>>>(p, sc, o);
+  kern<<<grid, 256, smem, st>>>(p, sc, o);
   return cudaGetLastError();
 }
 
+template <bool kExt>
+static cudaError_t launch_x(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene, int num_sms,
+                            cudaStream_t st) {
+  const bool dbg = o.dbg_hits != nullptr;
+  if (smem_scene) return dbg ? launch_t<true, true, kExt>(p, sc, o, num_sms, st, nullptr)
+                             : launch_t<true, false, kExt>(p, sc, o, num_sms, st, nullptr);
+  return dbg ? launch_t<false, true, kExt>(p, sc, o, num_sms, st, nullptr)
+             : launch_t<false, false, kExt>(p, sc, o, num_sms, st, nullptr);
+}
+
+// kExt: the NEXT-1 / NEXT-2 modes (global integrator, area lights, progressive passes); the
+// plain instantiation keeps the hot path's register budget
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene,
                           int num_sms, cudaStream_t st) {
-  const bool dbg = o.dbg_hits != nullptr;
-  if (smem_scene) return dbg ? launch_t<true, true>(p, sc, o, num_sms, st, nullptr)
-                             : launch_t<true, false>(p, sc, o, num_sms, st, nullptr);
-  return dbg ? launch_t<false, true>(p, sc, o, num_sms, st, nullptr)
-             : launch_t<false, false>(p, sc, o, num_sms, st, nullptr);
+  const bool ext = p.integrator != 0 || p.n_emitters > 0 || p.jitter != 0 || o.accum != nullptr;
+  return ext ? launch_x<true>(p, sc, o, smem_scene, num_sms, st) : launch_x<false>(p, sc, o, smem_scene, num_sms, st);
 }
 
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,

@@ -36,14 +36,14 @@ def gpu_render(sc, debug=True, width=None, height=None, max_depth=None, spp=None
 
 
 def gpu_passes(sc, pass_begin, n_passes, accum=None, debug=True, integrator="global", area_lights=True,
-               width=None, height=None, max_depth=None):
+               width=None, height=None, max_depth=None, variant="auto"):
     """Progressive passes through rt_render_passes(_debug); returns host copies."""
     import torch
     from paper_1504_03151_b200 import rt
     W = sc.width if width is None else width
     H = sc.height if height is None else height
     D = sc.max_depth if max_depth is None else max_depth
-    rt.set_variant("auto")
+    rt.set_variant(variant)
     rt.set_integrator(integrator, area_lights)
     rt.load_scene(sc)
     if accum is None:
