@@ -104,6 +104,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _measured_peak(key: str, fallback: float) -> float:
+    """Driver-written MEASURED_PEAKS.json (this pool's B200s), else the profiling guide's figure."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))[key])
+    except (OSError, ValueError, KeyError):
+        return fallback
+
+
 def _load_profile_traffic(workload: str):
     """dram bytes per launch of the render kernel from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "ncu_render_kernel.json")
@@ -427,6 +435,7 @@ def run_progressive(args):
     # exact ray counts of the timed steps: replay the same pass indices (deterministic) untimed
     acc2 = torch.zeros_like(accum)
     rays = tests_c = tests_s = tests_p = 0
+    n_closest = n_shadow = n_secondary = 0
     for i in range(args.steps):
         rt.render_passes(W, H, D, first + i * P, P, acc2, None)
         s2 = rt.stats()
@@ -434,6 +443,9 @@ def run_progressive(args):
         tests_c += s2["closest_sphere_tests"]
         tests_s += s2["sphere_tests"] - s2["closest_sphere_tests"]
         tests_p += s2["plane_tests"]
+        n_closest += s2["primary"] + s2["secondary"]
+        n_shadow += s2["shadow"]
+        n_secondary += s2["secondary"]
     ms_per_step = total_ms / args.steps
     value = rays / (total_ms * 1e-3) / 1e6
     props = torch.cuda.get_device_properties(dev)
@@ -441,6 +453,16 @@ def run_progressive(args):
     peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
     whole = (FLOP_SPHERE * (tests_c + tests_s) + FLOP_PLANE * tests_p) / (total_ms * 1e-3) / 1e12
     tc = st_last["isect_closest_ms"]
+    # dominant kernel here: wf_shade (profiles/r01_launches_c0_progressive_summary.txt). Its
+    # algorithmic HBM bytes: 124 B per shaded path (queue id, ray, candidate count,
+    # skip, depth, T, L in; T, L, shadow offset/count, exit sphere out) + 44 B per shadow entry
+    # (path, light, contribution, sampled emitter point; C0 has no point lights) + 60 B per
+    # continuation (ray, depth, skip, queue slot). Timed per launch with CUDA events in the library.
+    shade_ms = st_last["shade_ms"]
+    last_closest = st_last["primary"] + st_last["secondary"]
+    shade_bytes = 124 * last_closest + 44 * st_last["shadow"] + 60 * st_last["secondary"]
+    hbm_peak = _measured_peak("hbm_gbs", 6549.1)
+    shade_gbs = shade_bytes / (shade_ms * 1e-3) / 1e9 if shade_ms > 0 else 0.0
     # e2e through the public API with host buffers: scene H2D, P passes, mean frame D2H
     host_out = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
     ke = max(3, min(args.steps, 10))
@@ -466,10 +488,14 @@ def run_progressive(args):
         "config": dict(sc.describe(), workload=name, mode="progressive", integrator="global", area_lights=True,
                        passes_per_step=P, l2="flushed (256 MiB write) before every step, outside the events",
                        rays_per_step=int(rays / args.steps)),
-        "roofline": {"bound": "alu", "achieved": whole, "peak": peak, "unit": "TFLOP/s", "frac": whole / peak,
-                     "traffic": None, "kernel": "whole step (counted test flops / step time; the sphere scan is "
-                     "not dominant at 4 spheres + 5 planes, see profiles/r01_launches_c0_progressive_summary.txt)",
-                     "closest_scan_share_of_step": tc / ms_per_step},
+        "roofline": {"bound": "hbm", "achieved": shade_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": shade_gbs / hbm_peak, "traffic": _load_profile_traffic("C0"),
+                     "kernel": "wf_shade (FP64 nearest hit + shading + light sampling + bounce), per-launch CUDA "
+                               "events of the last timed step; algorithmic bytes per DESIGN.md §7",
+                     "share_of_step": shade_ms / ms_per_step,
+                     "peak_basis": "MEASURED_PEAKS.json hbm_gbs (burst copy bandwidth)",
+                     "closest_scan": {"bound": "alu", "share_of_step": tc / ms_per_step},
+                     "whole_step_test_flops_tflops": whole, "alu_peak_tflops": peak},
         "clocks": clk,
         "gpu_launches": st_last["launches"] * args.steps,
         "e2e": {"value": rays_e2e / dt / 1e6, "unit": "Mrays/s",

@@ -100,7 +100,7 @@ typedef struct {
  * plane_tests are the algorithmic test counts of SURVEY §8(c).1 step 11 (closest-hit rays
  * test every primitive; shadow rays stop at the first occluder in index order when planes
  * precede spheres in the primitive list). last_render_ms: device time of the render kernel
- * (CUDA events on the library stream; 0 for rt_assemble_tiles). 80 bytes. */
+ * (CUDA events on the library stream; 0 for rt_assemble_tiles). 88 bytes. */
 typedef struct {
   uint64_t primary;
   uint64_t shadow;
@@ -114,6 +114,8 @@ typedef struct {
   double isect_shadow_ms;        /* wavefront: same for the shadow-ray intersection kernels */
   uint32_t launches;             /* kernels of this library launched by the call */
   int32_t variant;               /* RT_VARIANT_MEGAKERNEL or RT_VARIANT_WAVEFRONT actually used */
+  double shade_ms;               /* wavefront: summed device time of the wf_shade launches (a4/a6:
+                                    FP64 nearest hit, shading, shadow set-up, bounce) */
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane

@@ -243,14 +243,17 @@ int collect_stats(bool timed) {
   c.last.plane_tests = h[4];
   c.last.closest_sphere_tests = h[5];
   c.last.last_render_ms = ms;
-  double tc = 0.0, ts = 0.0;
+  double tc = 0.0, ts = 0.0, tsh = 0.0;
   if (timed) {
     for (int i = 0; i < c.n_timed; ++i) {
-      float a = 0.f, b = 0.f;
+      float a = 0.f, b = 0.f, m = 0.f;
       CU(cudaEventElapsedTime(&a, c.ev_c[2 * i], c.ev_c[2 * i + 1]), "cudaEventElapsedTime");
       CU(cudaEventElapsedTime(&b, c.ev_s[2 * i], c.ev_s[2 * i + 1]), "cudaEventElapsedTime");
+      // wf_shade is the only launch between the closest-hit scan's end and the shadow scan's start
+      CU(cudaEventElapsedTime(&m, c.ev_c[2 * i + 1], c.ev_s[2 * i]), "cudaEventElapsedTime");
       tc += a;
       ts += b;
+      tsh += m;
     }
   }
 #ifdef RT_SIMD_PROBE
@@ -264,6 +267,7 @@ int collect_stats(bool timed) {
 #endif
   c.last.isect_closest_ms = tc;
   c.last.isect_shadow_ms = ts;
+  c.last.shade_ms = tsh;
   c.last.launches = timed ? (uint32_t)c.last_launches : 2u;
   c.last.variant = c.last_variant;
   return RT_OK;

@@ -41,7 +41,8 @@ class RayStats(C.Structure):
     _fields_ = [("primary", C.c_uint64), ("shadow", C.c_uint64), ("secondary", C.c_uint64),
                 ("sphere_tests", C.c_uint64), ("plane_tests", C.c_uint64), ("last_render_ms", C.c_double),
                 ("closest_sphere_tests", C.c_uint64), ("isect_closest_ms", C.c_double),
-                ("isect_shadow_ms", C.c_double), ("launches", C.c_uint32), ("variant", C.c_int32)]
+                ("isect_shadow_ms", C.c_double), ("launches", C.c_uint32), ("variant", C.c_int32),
+                ("shade_ms", C.c_double)]
 
 
 _lib = None
