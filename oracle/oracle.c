@@ -775,3 +775,113 @@ int orc_render(const orc_scene* scene, const orc_frame* frame, const int64_t* pi
   if (counts) *counts = cnt;
   return 0;
 }
+
+/* ----------------------------------------------------------------------------------------
+ * NEXT-3: the literal Alg. 1 light-grid form. Test infrastructure that
+ * cross-checks the one-sample estimator of trace_sample (NEXT-1) against the paper's serial
+ * quadrature over "each sampling point of each source light".
+ * -------------------------------------------------------------------------------------- */
+int orc_render_local_grid(const orc_scene* scene, int32_t width, int32_t height, int32_t light_grid,
+                          int32_t rays_per_pixel, double* rgb) {
+  if (!scene || !rgb || width < 1 || height < 1 || light_grid < 1 || rays_per_pixel < 1) return -1;
+  prims P;
+  prims_load(&P, scene);
+  camera cam = build_camera(scene);
+  const int n = light_grid;
+  for (int32_t py = 0; py < height; ++py) {
+    for (int32_t px = 0; px < width; ++px) {
+      v3 acc = mk(0, 0, 0);
+      for (int32_t s = 0; s < rays_per_pixel; ++s) { /* Alg. 1 line 1: each light of each pixel */
+        v3 o, d;
+        camera_ray(&cam, width, height, px, py, s, rays_per_pixel, &o, &d);
+        int best = -1; /* lines 2-3: each object, nearest intersection */
+        double tbest = INFINITY;
+        for (int k = 0; k < P.n; ++k) {
+          double t;
+          if (prim_hit(&P, k, o, d, &t) && t < tbest) { tbest = t; best = k; }
+        }
+        v3 col = mk(0, 0, 0);
+        if (best < 0) {
+          col = ld3(scene->background);
+        } else {
+          v3 p = add(o, scl(d, tbest));
+          v3 ng = P.type[best] == 1 ? P.c[best] : scl(sub(p, P.c[best]), 1.0 / P.r[best]);
+          v3 nrm = dot(d, ng) < 0.0 ? ng : scl(ng, -1.0);
+          v3 wo = scl(d, -1.0);
+          int mi = P.mat[best];
+          int kind = scene->mat_kind[mi];
+          v3 rho = ld3(scene->mat_albedo + 3 * mi);
+          col = ld3(scene->mat_emission + 3 * mi); /* Eq. 7 */
+          if (kind == 0) {
+            double f[3], wi_a[3], wo_a[3], n_a[3], alb[3];
+            st3(wo_a, wo); st3(n_a, nrm); st3(alb, rho);
+            col = add(col, mulv(rho, ld3(scene->ambient)));
+            v3 os = add(p, scl(nrm, EPS_T));
+            for (int l = 0; l < scene->n_lights; ++l) { /* point lights, as orc_render */
+              v3 Pl = ld3(scene->light_pos + 3 * l);
+              v3 w = sub(Pl, p);
+              double d2 = dot(w, w);
+              if (d2 < 1e-12) continue;
+              v3 wi = scl(w, 1.0 / sqrt(d2));
+              double cs = dot(nrm, wi);
+              if (cs <= 0.0) continue;
+              v3 ws = sub(Pl, os);
+              double tmax = len(ws);
+              v3 ds = scl(ws, 1.0 / tmax);
+              int occ = 0;
+              for (int k = 0; k < P.n; ++k) {
+                double t;
+                if (prim_hit(&P, k, os, ds, &t) && t < tmax) { occ = 1; break; }
+              }
+              if (occ) continue;
+              st3(wi_a, wi);
+              orc_brdf(kind, alb, (double)scene->mat_ks[mi], (double)scene->mat_shininess[mi], wi_a, wo_a, n_a, f);
+              col = add(col, scl(mulv(mk(f[0], f[1], f[2]), ld3(scene->light_intensity + 3 * l)), cs / d2));
+            }
+            for (int e = 0; e < P.n_emit; ++e) { /* line 4: each sampling point of each source light */
+              int ke = P.emit[e];
+              v3 c = P.c[ke];
+              double r = P.r[ke];
+              v3 Le = ld3(scene->mat_emission + 3 * P.mat[ke]);
+              for (int i = 0; i < n; ++i) {
+                double th0 = PI * i / n, th1 = PI * (i + 1) / n, thm = 0.5 * (th0 + th1);
+                for (int j = 0; j < n; ++j) {
+                  double phm = 2.0 * PI * (j + 0.5) / n;
+                  double dA = r * r * (cos(th0) - cos(th1)) * (2.0 * PI / n); /* exact cell area */
+                  v3 nl = mk(sin(thm) * cos(phm), sin(thm) * sin(phm), cos(thm));
+                  v3 X = add(c, scl(nl, r));
+                  v3 w = sub(X, p);
+                  double d2 = dot(w, w);
+                  if (d2 < 1e-12) continue;
+                  v3 wi = scl(w, 1.0 / sqrt(d2));
+                  double cs = dot(nrm, wi), cl = -dot(wi, nl);
+                  if (cs <= 0.0 || cl <= 0.0) continue;
+                  v3 ws = sub(X, os); /* line 5: emit a shadow light r from p to that point */
+                  double tmax = len(ws);
+                  v3 ds = scl(ws, 1.0 / tmax);
+                  int occ = 0;
+                  for (int k = 0; k < P.n; ++k) { /* lines 6-11: break at an occluder */
+                    double t;
+                    if (k == ke) continue;
+                    if (prim_hit(&P, k, os, ds, &t) && t < tmax) { occ = 1; break; }
+                  }
+                  if (occ) continue;
+                  st3(wi_a, wi);
+                  orc_brdf(kind, alb, (double)scene->mat_ks[mi], (double)scene->mat_shininess[mi], wi_a, wo_a,
+                           n_a, f);
+                  /* Eq. 8 over the cell, accumulated (line 12) */
+                  col = add(col, scl(mulv(mk(f[0], f[1], f[2]), Le), cs * cl / d2 * dA));
+                }
+              }
+            }
+          }
+        }
+        acc = add(acc, col); /* line 16: accumulate the colour of each light */
+      }
+      st3(rgb + 3 * ((int64_t)py * width + px), scl(acc, 1.0 / rays_per_pixel)); /* line 18: average */
+    }
+  }
+  prims_free(&P);
+  return 0;
+}
+

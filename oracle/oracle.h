@@ -99,6 +99,18 @@ int orc_render(const orc_scene* scene, const orc_frame* frame, const int64_t* pi
                int64_t n_pixels, double* rgb, int32_t* hit_ids, int32_t* bounces,
                double* margin, double* sample_rgb, orc_counts* counts);
 
+/* Literal Alg. 1 (SPEC oracle_render_local S:416-423): local
+ * illumination, serial nested loops. Per pixel, per ray (rays_per_pixel sub-pixel offsets of
+ * orc_sample_offset), nearest hit; emission of the hit; at DIFFUSE hits ambient, the point
+ * lights (as orc_render) and, per emissive sphere, per cell of a light_grid x light_grid
+ * latitude-longitude grid (theta in [i pi/n, (i+1) pi/n], phi in [2 pi j/n, 2 pi (j+1)/n],
+ * pole +z): a shadow ray to the cell's midpoint (the emitter itself does not block; `break` at
+ * the first occluder) and the Eq. 8 term f_r L_e cos_s cos_l / d^2 times the cell's exact area
+ * r^2 (cos theta_i - cos theta_i+1) dphi. No continuation (local mode = depth 0). Mean over the
+ * rays of the pixel. rgb: [width*height][3]. Returns 0, or -1 on invalid arguments. */
+int orc_render_local_grid(const orc_scene* scene, int32_t width, int32_t height, int32_t light_grid,
+                          int32_t rays_per_pixel, double* rgb);
+
 /* Building blocks, exported for the unit pins. */
 int orc_solve_quadratic(double a, double b, double c, double roots[2]);
 int orc_intersect_sphere(const double o[3], const double d[3], const double c[3], double r,

@@ -84,6 +84,9 @@ def lib():
         _lib.orc_sample_sphere.argtypes = [dp, C.c_double, C.c_double, C.c_double, dp, dp]
         _lib.orc_onb.argtypes = [dp, dp, dp]
         _lib.orc_cosine_direction.argtypes = [dp, C.c_double, C.c_double, dp]
+        _lib.orc_render_local_grid.restype = C.c_int
+        _lib.orc_render_local_grid.argtypes = [C.POINTER(_Scene), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                               C.c_void_p]
         _lib.orc_brdf.argtypes = [C.c_int32, dp, C.c_double, C.c_double, dp, dp, dp, dp]
         _lib.orc_schlick.restype = C.c_double
         _lib.orc_schlick.argtypes = [C.c_double, C.c_double]
@@ -166,6 +169,18 @@ def render(sc, pixels=None, perturb: float = 0.0, perturb_seed: int = 0,
         raise ValueError(f"orc_render failed rc={rc}")
     counts = {k: int(getattr(cnt, k)) for k, _ in _Counts._fields_}
     return OracleResult(rgb, ids, bn, mg, srgb, counts, pix)
+
+
+def render_local_grid(sc, light_grid: int, rays_per_pixel: int, width=None, height=None) -> np.ndarray:
+    """NEXT-3: the literal Alg. 1 light-grid quadrature (local illumination); [H*W, 3] float64."""
+    W = sc.width if width is None else width
+    H = sc.height if height is None else height
+    holder = _SceneHolder(sc)
+    rgb = np.zeros((W * H, 3), np.float64)
+    rc = lib().orc_render_local_grid(C.byref(holder.s), W, H, light_grid, rays_per_pixel, _ptr(rgb))
+    if rc != 0:
+        raise ValueError(f"orc_render_local_grid failed rc={rc}")
+    return rgb
 
 
 def render_rgb_only(sc, pixels=None, integrator: int = 0, area_lights: int = 0, jitter: int = 0,
