@@ -38,7 +38,9 @@ typedef enum {
   RT_ERR_NO_CAMERA = -3,   /* rt_render* before a successful rt_camera_set */
   RT_ERR_CUDA = -4,        /* CUDA runtime error (message carries cudaGetErrorString) */
   RT_ERR_OOM = -5,         /* device allocation failed */
-  RT_ERR_STATE = -6        /* call not valid in the current state */
+  RT_ERR_STATE = -6,       /* call not valid in the current state */
+  RT_ERR_PARSE = -7,       /* scene text: rt_last_error() = "line N: reason" */
+  RT_ERR_IO = -8           /* file could not be read or written */
 } rt_status;
 
 enum { RT_PRIM_SPHERE = 0, RT_PRIM_PLANE = 1 };
@@ -222,6 +224,31 @@ int rt_render_passes(int32_t width, int32_t height, int32_t max_depth, int64_t p
 int rt_render_passes_debug(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin,
                            int32_t n_passes, double* accum_rgb, float* out_rgba, int32_t* hit_ids,
                            int32_t* bounces);
+
+/* ---- scene files and images ---------------------------------------------
+ * Scene text (extended to the primitives of this library), one
+ * directive per line, fields separated by whitespace, '#' comments and blank lines ignored:
+ *   camera ex ey ez  lx ly lz  ux uy uz  vfov                         (exactly one)
+ *   sphere radius  cx cy cz  er eg eb  ar ag ab  kind [ior] [opts]     (SPEC grammar)
+ *   plane  nx ny nz d  er eg eb  ar ag ab  kind [ior] [opts]           (n.x = d)
+ *   light  px py pz  ir ig ib                                          (point light)
+ *   background r g b | ambient r g b
+ * kind in {diffuse, specular, refractive}; ior (refractive only) defaults to 1.5; opts are
+ * ks=K shininess=S kr=R (defaults 0, 1, 0). Numbers are read as float32 (strtof). Every
+ * sphere/plane line defines its own material. The whole text is parsed and validated before any
+ * device call; then the scene is uploaded (rt_scene_upload) and the camera set (rt_camera_set).
+ * Errors: RT_ERR_PARSE with rt_last_error() = "line N: reason" (unknown directive, bad arity,
+ * non-numeric or non-finite field, radius <= 0, albedo outside [0,1], emission < 0, ior < 1,
+ * unknown kind or option, zero plane normal, missing camera, duplicate camera, invalid camera);
+ * errors of rt_scene_upload / rt_camera_set otherwise. Never reads past text[n_bytes - 1]. */
+int rt_scene_parse(const char* text, int64_t n_bytes);
+/* rt_scene_parse of a file's bytes. RT_ERR_IO if it cannot be read (message names the path). */
+int rt_scene_load(const char* path);
+/* SPEC write_ppm: binary PPM P6, header "P6\n<W> <H>\n255\n", then W*H RGB bytes,
+ * row 0 = top, tone-mapped on the device (rt_tonemap_rgba8). rgba: W*H float4, device pointer.
+ * RT_ERR_IO if the file cannot be written. */
+int rt_write_ppm(const float* rgba, int32_t width, int32_t height, float exposure, float gamma,
+                 const char* path);
 
 /* SPEC tone_map on the device: per channel round_half_up(255 clamp(exposure v, 0,
  * 1)^(1/gamma)), alpha = 255. rgba: n_px float4 (device); out: n_px * 4 bytes (device). */

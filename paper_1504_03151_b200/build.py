@@ -9,8 +9,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libb200rt.so")
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("rt_api.cu", "rt_kernels.cu")]
-DEPS = SRCS + [os.path.join(HERE, "csrc", "rt_internal.h"), os.path.join(ROOT, "include", "rt.h")]
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("rt_api.cu", "rt_kernels.cu", "rt_scene_io.cpp")]
+DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))] + \
+    [os.path.join(ROOT, "include", "rt.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -34,6 +34,17 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(RT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+}  // namespace
+
+// shared with rt_scene_io.cpp (declared in rt_internal.h)
+int rt_fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+void rt_clear_error() { g_err.clear(); }
+
+namespace {
+
 #define CU(call, what)                          \
   do {                                          \
     cudaError_t e_ = (call);                    \

@@ -157,3 +157,7 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
                            float gamma, cudaStream_t st);
 
 }  // namespace rt
+
+// host-side error reporting shared by the runtime translation units (rt_api.cu, rt_scene_io.cpp)
+int rt_fail(int code, const char* msg);
+void rt_clear_error();

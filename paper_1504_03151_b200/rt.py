@@ -19,7 +19,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "rt.h")
 
 RT_OK = 0
 STATUS = {0: "RT_OK", -1: "RT_ERR_INVALID_ARG", -2: "RT_ERR_NO_SCENE", -3: "RT_ERR_NO_CAMERA",
-          -4: "RT_ERR_CUDA", -5: "RT_ERR_OOM", -6: "RT_ERR_STATE"}
+          -4: "RT_ERR_CUDA", -5: "RT_ERR_OOM", -6: "RT_ERR_STATE", -7: "RT_ERR_PARSE", -8: "RT_ERR_IO"}
 TILE_W, TILE_H = 8, 4
 
 PRIM_DTYPE = np.dtype([("type", "<u4"), ("material", "<u4"), ("p", "<f4", (4,))])
@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
         "rt_render_debug": [i32, i32, i32, i32, vp, vp, vp],
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
         "rt_set_integrator": [i32, i32],
+        "rt_scene_parse": [C.c_char_p, i64],
+        "rt_scene_load": [C.c_char_p],
+        "rt_write_ppm": [vp, i32, i32, C.c_float, C.c_float, C.c_char_p],
         "rt_render_passes": [i32, i32, i32, i64, i32, vp, vp],
         "rt_render_passes_debug": [i32, i32, i32, i64, i32, vp, vp, vp, vp],
     }
@@ -93,7 +96,7 @@ def lib() -> C.CDLL:
 
 def _check(fn: str, rc: int):
     if rc != RT_OK:
-        raise RtError(fn, rc, lib().rt_last_error().decode())
+        raise RtError(fn, rc, lib().rt_last_error().decode(errors="replace"))
 
 
 def _ptr(buf) -> int:
@@ -178,6 +181,21 @@ def render_debug(width, height, max_depth, spp, out, hit_ids, bounces):
     _check("rt_render_debug", lib().rt_render_debug(width, height, max_depth, spp, _ptr(out), _ptr(hit_ids),
                                                     _ptr(bounces)))
     return out, hit_ids, bounces
+
+
+def scene_parse(text):
+    """NEXT-4: parse scene text (grammar in include/rt.h), upload it and set its camera."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    _check("rt_scene_parse", lib().rt_scene_parse(b, len(b)))
+
+
+def scene_load(path: str):
+    _check("rt_scene_load", lib().rt_scene_load(os.fsencode(path)))
+
+
+def write_ppm(rgba, width: int, height: int, path: str, exposure: float = 1.0, gamma: float = 2.2):
+    """rgba: float32 CUDA tensor of width*height*4 (tone-mapped on the device)."""
+    _check("rt_write_ppm", lib().rt_write_ppm(_ptr(rgba), width, height, exposure, gamma, os.fsencode(path)))
 
 
 INTEGRATORS = {"whitted": 0, "global": 1}

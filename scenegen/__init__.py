@@ -364,6 +364,37 @@ def random_tiny(seed: int, n_spheres: int = 6, n_planes: int = 1, n_lights: int 
                    background=(0.1, 0.2, 0.3), ambient=(0.03, 0.03, 0.03), seed=seed)
 
 
+_KIND_NAMES = {DIFFUSE: "diffuse", SPECULAR: "specular", REFRACTIVE: "refractive"}
+
+
+def _g(x) -> str:
+    """float32 value as the shortest decimal that round-trips through strtof (%.9g)."""
+    return "%.9g" % float(np.float32(x))
+
+
+def to_text(sc: Scene) -> str:
+    """Scene -> the text format of include/rt.h (rt_scene_parse; SPEC S:246-249 grammar extended
+    with planes, point lights and environment). Every value is printed so that strtof returns the
+    same float32, so parsing the text reproduces the scene exactly (one material per primitive)."""
+    out = [f"# {sc.name}: {sc.notes}".rstrip(": ") if sc.notes else f"# {sc.name}",
+           "camera " + "  ".join(" ".join(_g(v) for v in vec) for vec in (sc.eye, sc.look_at, sc.up)) + "  " + _g(sc.vfov),
+           "background " + " ".join(_g(v) for v in sc.background),
+           "ambient " + " ".join(_g(v) for v in sc.ambient)]
+    for p, I in zip(sc.light_pos, sc.light_intensity):
+        out.append("light " + " ".join(_g(v) for v in p) + "  " + " ".join(_g(v) for v in I))
+    for t, m, q in zip(sc.prim_type, sc.prim_mat, sc.prim_p):
+        geo = (f"sphere {_g(q[3])}  {_g(q[0])} {_g(q[1])} {_g(q[2])}" if t == SPHERE
+               else f"plane {_g(q[0])} {_g(q[1])} {_g(q[2])} {_g(q[3])}")
+        kind = int(sc.mat_kind[m])
+        mat = (" ".join(_g(v) for v in sc.mat_emission[m]) + "  " + " ".join(_g(v) for v in sc.mat_albedo[m])
+               + "  " + _KIND_NAMES[kind])
+        if kind == REFRACTIVE:
+            mat += " " + _g(sc.mat_ior[m])
+        mat += f" ks={_g(sc.mat_ks[m])} shininess={_g(sc.mat_shininess[m])} kr={_g(sc.mat_kr[m])}"
+        out.append(geo + "  " + mat)
+    return "\n".join(out) + "\n"
+
+
 def builder() -> _Builder:
     """Hand-authoring entry point for worked examples in tests."""
     return _Builder()
