@@ -197,11 +197,10 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     const int cap = items * p.spp;
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
     const int scap = cap * (n_src > 0 ? n_src : 1);
-    const bool with_x = p.n_emitters > 0;
     // (re)carve for this frame's cap
-    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, with_x) + 64 * 256), "cudaMalloc(wavefront)");
+    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap)), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, with_x, c.wf_ctr.p);
+    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
     const int pairs = rt::wf_timing_pairs(p, cap);
     while ((int)c.ev_c.size() < 2 * pairs) {
       cudaEvent_t a, b;

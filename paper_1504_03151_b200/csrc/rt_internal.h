@@ -99,24 +99,29 @@ struct DevOutputs {
 // ---- wavefront variant buffers (rt_wavefront.cuh) ----
 constexpr int kCandMax = 6;  // candidates stored per ray; more -> overflow -> FP64 full scan
 
+// Closest-hit queue of one depth, compacted by copy: entry e carries its path's whole state, so
+// every wavefront kernel reads and writes its entries with coalesced accesses.
+struct WfQueue {
+  int* path;       // [cap]     path id (chunk-local: g0 + path = pixel item * spp + sample)
+  double* ray;     // [6][cap]  o, d
+  float* T;        // [3][cap]  throughput
+  float* L;        // [3][cap]  radiance so far
+  int* depth;      // [cap]     segment depth | kPrevDiffuse when the ray left a cosine bounce
+  int* skip;       // [cap]     sphere the ray leaves (provably not hit: convexity) or -1
+};
+
 struct WfBuffers {
-  double* ray;     // [6][cap]  current ray o, d (next closest query)
-  double* hit;     // [6][cap]  shading point p and facing normal n of the current depth
-  float* T;        // [3][cap]
-  float* Lr;       // [3][cap]  sample radiance
-  int* depth;      // [cap]  segment depth | kPrevDiffuse when the ray left a cosine bounce
-  int* skip_c;     // [cap]  sphere the current ray leaves (provably not hit: convexity) or -1
-  int* hit_out;    // [cap]  sphere hit from outside at the current depth (shadow rays leaving it
-                   //        cannot hit it) or -1
-  int* shoff;      // [cap]  first shadow entry of the path at the current depth
-  int* shcnt;      // [cap]
-  int* q[2];       // closest queues (path ids)
-  int* sq_path;    // [scap]
-  int* sq_light;   // [scap]
-  float* sq_c;     // [3][scap] contribution f_r I cos/d^2 * T
-  double* sq_x;    // [3][scap] sampled point of an emitter entry (sq_light >= n_lights), or null
-  int* ccand;      // [cap * kCandMax]
+  WfQueue q[2];    // Q[d & 1]: the closest-hit rays of depth d
+  float* Lr;       // [3][cap]  final radiance per path (written when the path ends)
+  int* nxt;        // [cap]  per entry of Q[d]: its slot in Q[d+1], or -1 - path if the path ended
+  int* shoff;      // [cap]  per entry of Q[d]: first shadow entry
+  int* shcnt;      // [cap]  per entry of Q[d]: number of shadow entries (lights in order)
+  int* ccand;      // [cap * kCandMax] closest-hit candidates per entry of Q[d]
   int* cn;         // [cap]
+  double* sray;    // [7][scap] shadow entry: o_s (3), d_s (3), t_max
+  int* sskip;      // [scap] sphere the shadow ray leaves (exact skip) or -1
+  int* sskip2;     // [scap] emitter sphere the ray aims at (not tested, R#41) or -1
+  float* sq_c;     // [3][scap] contribution T f_r I cos / d^2 (or the emitter estimator)
   int* scand;      // [scap * kCandMax]
   int* sn;         // [scap]
   int* srob;       // [scap] robust occluder: sphere index, -1 none, -2-j plane j
@@ -137,8 +142,8 @@ cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float
                                cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
-size_t wf_bytes(int cap, int scap, bool with_x);
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, bool with_x, unsigned* ctr);
+size_t wf_bytes(int cap, int scap);
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr);
 // per-launch CUDA events around the intersection kernels (pairs: [2i] before, [2i+1] after)
 struct WfTiming {
   cudaEvent_t* closest;

@@ -570,36 +570,39 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 }
 
 // ---- wavefront launcher ---------------------------------------------------------------------
-size_t wf_bytes(int cap, int scap, bool with_x) {
-  return (size_t)cap * (12 * 8 + 6 * 4 + 5 * 4 + 2 * 4 + kCandMax * 4 + 4) +
-         (size_t)scap * (4 + 4 + 12 + kCandMax * 4 + 4 + 4 + (with_x ? 24 : 0));
+size_t wf_bytes(int cap, int scap) {
+  const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
+  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + kCandMax * 4) +
+         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4) + 32 * 256;
 }
 
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, bool with_x, unsigned* ctr) {
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   char* p = static_cast<char*>(base);
   auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
   B.cap = cap;
   B.scap = scap;
-  B.ray = reinterpret_cast<double*>(take(6 * 8 * (size_t)cap));
-  B.hit = reinterpret_cast<double*>(take(6 * 8 * (size_t)cap));
-  B.T = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
+  for (int k = 0; k < 2; ++k) {
+    WfQueue& Q = B.q[k];
+    Q.path = reinterpret_cast<int*>(take(4 * (size_t)cap));
+    Q.ray = reinterpret_cast<double*>(take(6 * 8 * (size_t)cap));
+    Q.T = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
+    Q.L = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
+    Q.depth = reinterpret_cast<int*>(take(4 * (size_t)cap));
+    Q.skip = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  }
   B.Lr = reinterpret_cast<float*>(take(3 * 4 * (size_t)cap));
-  B.depth = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.skip_c = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.hit_out = reinterpret_cast<int*>(take(4 * (size_t)cap));
+  B.nxt = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.shoff = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.shcnt = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.q[0] = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.q[1] = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.ccand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * cap));
   B.cn = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.sq_path = reinterpret_cast<int*>(take(4 * (size_t)scap));
-  B.sq_light = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sray = reinterpret_cast<double*>(take(7 * 8 * (size_t)scap));
+  B.sskip = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sskip2 = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.sq_c = reinterpret_cast<float*>(take(3 * 4 * (size_t)scap));
   B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * scap));
   B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
-  B.sq_x = with_x ? reinterpret_cast<double*>(take(3 * 8 * (size_t)scap)) : nullptr;
   B.ctr = ctr;
 }
 

@@ -93,18 +93,6 @@ __device__ __forceinline__ void shadow_ray_to(d3 p, d3 n, d3 x, d3& os, d3& ds, 
   ds = ws * (1.0 / tl);
 }
 
-// the shadow ray of entry j and the emitter sphere it must not test (-1 for point lights)
-__device__ __forceinline__ int entry_ray(const DevParams& P, const DevScene& S, const WfBuffers& B, int j, d3 p, d3 n,
-                                         d3& os, d3& ds, double& tl) {
-  const int l = B.sq_light[j];
-  if (l < P.n_lights) {
-    shadow_ray(S, p, n, l, os, ds, tl);
-    return -1;
-  }
-  shadow_ray_to(p, n, mk(B.sq_x[j], B.sq_x[(size_t)B.scap + j], B.sq_x[2 * (size_t)B.scap + j]), os, ds, tl);
-  return S.emit_sph[l - P.n_lights];
-}
-
 // Light l seen from shading point p: point light l < n_lights (R#2: g = cos / d^2), else
 // emitter e = l - n_lights with one uniform surface point (R#41: g = cos_s cos_l / (d^2 pdf)).
 // False when it sends no shadow ray (d^2 < 1e-12, cos_s <= 0, or cos_l <= 0 for an emitter).
@@ -149,25 +137,25 @@ __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene&
   return true;
 }
 
-// ---- a2: ray generation ---------------------------------------------------------------------
+// ---- a2: ray generation -> Q[0] ------------------------------------------------------------
 __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
                                                  unsigned long long* stats) {
+  const WfQueue Q = B.q[0];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long g = g0 + i;
     const int w = (int)(g / P.spp), s = (int)(g % P.spp);
     int px = 0, py = 0;
     const bool valid = item_pixel(P, w, px, py);
-    sf3(B.Lr, B.cap, i, f3(0.f, 0.f, 0.f));
-    if (valid) {
-      st3(B.ray, B.cap, i, 0, mk(P.eye[0], P.eye[1], P.eye[2]));
-      st3(B.ray, B.cap, i, 3, camera_dir(P, px, py, s));
-      sf3(B.T, B.cap, i, f3(1.f, 1.f, 1.f));
-      B.depth[i] = 0;
-      B.shcnt[i] = 0;
-      B.skip_c[i] = -1;
-    }
     const unsigned slot = warp_reserve(valid ? 1u : 0u, B.ctr + wf_ctr_q(0));
-    if (valid) B.q[0][slot] = i;
+    if (valid) {
+      Q.path[slot] = i;
+      st3(Q.ray, B.cap, slot, 0, mk(P.eye[0], P.eye[1], P.eye[2]));
+      st3(Q.ray, B.cap, slot, 3, camera_dir(P, px, py, s));
+      sf3(Q.T, B.cap, slot, f3(1.f, 1.f, 1.f));
+      sf3(Q.L, B.cap, slot, f3(0.f, 0.f, 0.f));
+      Q.depth[slot] = 0;
+      Q.skip[slot] = -1;
+    }
     warp_stat(stats, 0, valid ? 1ull : 0ull);
   }
 }
@@ -184,7 +172,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   const float4* gp = S.pairs;
   const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
   unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
-  const int* q = B.q[d & 1];
+  const WfQueue Q = B.q[d & 1];
   int* cand = kShadow ? B.scand : B.ccand;
   int* cn = kShadow ? B.sn : B.cn;
   const int lane = threadIdx.x & 31;
@@ -201,10 +189,11 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     int rob = -1, skip = -1, skip2 = -1;  // skip2: the emitter a shadow ray aims at (R#41)
     if (act) {
       if constexpr (kShadow) {
-        const int path = B.sq_path[e];
-        const d3 nrm = ld3(B.hit, B.cap, path, 3);
-        skip2 = entry_ray(P, S, B, (int)e, ld3(B.hit, B.cap, path, 0), nrm, o, dir, tl);
-        skip = shadow_skip(B.hit_out[path], nrm, dir);
+        o = ld3(B.sray, B.scap, (int)e, 0);
+        dir = ld3(B.sray, B.scap, (int)e, 3);
+        tl = B.sray[6 * (size_t)B.scap + e];
+        skip = B.sskip[e];
+        skip2 = B.sskip2[e];
         // planes first, exactly (FP64): the first plane in index order that occludes decides
         for (int j = 0; j < P.n_planes; ++j) {
           const DevPlane pl = c_planes[j];
@@ -215,10 +204,9 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
           }
         }
       } else {
-        const int path = q[e];
-        o = ld3(B.ray, B.cap, path, 0);
-        dir = ld3(B.ray, B.cap, path, 3);
-        skip = B.skip_c[path];
+        o = ld3(Q.ray, B.cap, (int)e, 0);
+        dir = ld3(Q.ray, B.cap, (int)e, 3);
+        skip = Q.skip[e];
       }
     }
     RayFilterFor<kSrc> F;
@@ -320,11 +308,10 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
-  const int* q = B.q[d & 1];
-  int* qn = B.q[(d + 1) & 1];
+  const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const int path = q[e];
-    const d3 o = ld3(B.ray, B.cap, path, 0), dir = ld3(B.ray, B.cap, path, 3);
+    const int path = Q.path[e];
+    const d3 o = ld3(Q.ray, B.cap, (int)e, 0), dir = ld3(Q.ray, B.cap, (int)e, 3);
     double tbest = kInf;
     int hs = -1, hp = -1;
     for (int j = 0; j < P.n_planes; ++j) {
@@ -335,8 +322,8 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         if (t >= kEps && t < tbest) { tbest = t; hp = j; }
       }
     }
-    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], B.skip_c[path], o, dir, tbest, hs, hp);
-    const int dword = B.depth[path];
+    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], Q.skip[e], o, dir, tbest, hs, hp);
+    const int dword = Q.depth[e];
     const int depth = dword & 0xff;
     int prim = -1;
     if (hp >= 0) prim = c_planes[hp].prim;
@@ -349,10 +336,11 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
       dbg_hits[si * (P.max_depth + 1) + depth] = prim;
     }
-    float3 T = lf3(B.T, B.cap, path);
-    float3 L = lf3(B.Lr, B.cap, path);
+    float3 T = lf3(Q.T, B.cap, (int)e);
+    float3 L = lf3(Q.L, B.cap, (int)e);
     bool cont = false;
     const int n_src = P.n_lights + P.n_emitters;  // point lights, then emitters (R#41)
+    unsigned long long lmask = 0ull;              // sources 0..63 that send a shadow ray
     unsigned long long pix = 0;
     unsigned sg = 0;
     {
@@ -382,7 +370,6 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
       entering = dot(dir, ng) < 0.0;
       nrm = entering ? ng : ng * -1.0;
-      B.hit_out[path] = (hs >= 0 && entering) ? hs : -1;
       const DevMat m = S.mats[mi];
       // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
       const bool sampled = (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
@@ -391,18 +378,22 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
         for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
           LightSample ls;
-          if (light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) ++nsh;
+          if (light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) {
+            ++nsh;
+            if (l < 64) lmask |= 1ull << l;
+          }
         }
       }
     }
     const unsigned off = warp_reserve(nsh, B.ctr + wf_ctr_s(d));  // converged: ballot/scan/atomic
-    // part 2: shadow entries with their contribution T f_r I cos / d^2 (Eq. 3, 5, 6)
+    // part 2: shadow entries — the shadow ray itself and the contribution T f_r I cos / d^2
+    // (Eq. 3, 5, 6); a shadow ray leaving a sphere hit from outside skips it exactly (convexity)
     if (nsh) {
       const DevMat m = S.mats[mi];
-      st3(B.hit, B.cap, path, 0, p);
-      st3(B.hit, B.cap, path, 3, nrm);
+      const int out_sph = (hs >= 0 && entering) ? hs : -1;
       unsigned k = off;
       for (int l = 0; l < n_src; ++l) {
+        if (l < 64 && !((lmask >> l) & 1ull)) continue;  // no shadow ray (decided in the count pass)
         LightSample ls;
         if (!light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) continue;
         // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3),
@@ -411,23 +402,27 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         const float alpha = (float)fmax(0.0, -dot(rl, dir));
         const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
         const float g = (float)ls.g;
-        B.sq_path[k] = path;
-        B.sq_light[k] = l;
-        if (l >= P.n_lights) {
-          B.sq_x[k] = ls.x.x;
-          B.sq_x[(size_t)B.scap + k] = ls.x.y;
-          B.sq_x[2 * (size_t)B.scap + k] = ls.x.z;
-        }
+        d3 os, ds;
+        double tl;
+        if (l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
+        else shadow_ray_to(p, nrm, ls.x, os, ds, tl);
+        st3(B.sray, B.scap, (int)k, 0, os);
+        st3(B.sray, B.scap, (int)k, 3, ds);
+        B.sray[6 * (size_t)B.scap + k] = tl;
+        B.sskip[k] = shadow_skip(out_sph, nrm, ds);
+        B.sskip2[k] = l >= P.n_lights ? S.emit_sph[l - P.n_lights] : -1;
         sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
                                        fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
         ++k;
       }
     }
-    B.shoff[path] = (int)off;
+    B.shoff[e] = (int)off;
     // part 3: stack-free continuation
+    d3 dn = mk(0, 0, 0);
+    bool mi_kind_diffuse_global = false;
     if (prim >= 0 && depth < P.max_depth) {
       const DevMat m = S.mats[mi];
-      d3 dn = mk(0, 0, 0);
+      mi_kind_diffuse_global = m.kind == 0 && P.integrator == 1;
       if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
         dn = reflect(dir, nrm);
         T = mul(T, f3(m.ar, m.ag, m.ab));
@@ -463,24 +458,28 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         T = mul(T, f3(m.ar, m.ag, m.ab));
         cont = true;
       }
-      if (cont) {
-        const d3 dnn = normalize(dn);
-        st3(B.ray, B.cap, path, 0, p);
-        st3(B.ray, B.cap, path, 3, dnn);
-        B.depth[path] = (depth + 1) | ((m.kind == 0 && P.integrator == 1) ? kPrevDiffuse : 0);
-        // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
-        // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
-        B.skip_c[path] = (hs >= 0 && dot(dnn, ng) > 0.0) ? hs : -1;
-      }
+      if (cont) dn = normalize(dn);
     }
-    B.shcnt[path] = (int)nsh;
-    sf3(B.T, B.cap, path, T);
-    sf3(B.Lr, B.cap, path, L);
+    B.shcnt[e] = (int)nsh;
     if constexpr (kDebug) {
       if (!cont) dbg_bounces[si] = depth;
     }
     const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
-    if (cont) qn[slot] = path;
+    if (cont) {  // the path moves to slot `slot` of Q[d+1] with its whole state
+      Qn.path[slot] = path;
+      st3(Qn.ray, B.cap, (int)slot, 0, p);
+      st3(Qn.ray, B.cap, (int)slot, 3, dn);
+      sf3(Qn.T, B.cap, (int)slot, T);
+      sf3(Qn.L, B.cap, (int)slot, L);
+      Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
+      // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
+      // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
+      Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
+      B.nxt[e] = (int)slot;
+    } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
+      sf3(B.Lr, B.cap, path, L);
+      B.nxt[e] = -1 - path;
+    }
     warp_stat(stats, 1, nsh);
     warp_stat(stats, 2, cont ? 1ull : 0ull);
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
@@ -493,15 +492,16 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
 __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
-  const int* q = B.q[d & 1];
+  const WfQueue Qn = B.q[(d + 1) & 1];
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const int path = q[e];
-    const int cnt = B.shcnt[path];
+    const int cnt = B.shcnt[e];
     unsigned long long st_sph = 0, st_pl = 0;
     if (cnt > 0) {
-      const int off = B.shoff[path];
-      const d3 p = ld3(B.hit, B.cap, path, 0), nrm = ld3(B.hit, B.cap, path, 3);
-      float3 L = lf3(B.Lr, B.cap, path);
+      const int off = B.shoff[e];
+      const int loc = B.nxt[e];  // where the path's radiance lives now: Q[d+1] slot or Lr[path]
+      float* Ls = loc >= 0 ? Qn.L : B.Lr;
+      const int li = loc >= 0 ? loc : -1 - loc;
+      float3 L = lf3(Ls, B.cap, li);
       for (int j = off; j < off + cnt; ++j) {
         const int rob = B.srob[j];
         bool occluded = false;
@@ -510,24 +510,26 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
           st_pl += (unsigned long long)(-2 - rob + 1);
         } else {
           st_pl += (unsigned long long)P.n_planes;
-          d3 os, ds;
-          double tl;
-          const int skip2 = entry_ray(P, S, B, j, p, nrm, os, ds, tl);
-          const int skip = shadow_skip(B.hit_out[path], nrm, ds);
+          const int skip2 = B.sskip2[j];
           const int nc = B.sn[j];
           int first = -1;
-          if (nc <= kCandMax) {
-            const int* c = B.scand + (size_t)j * kCandMax;
-            for (int i = 0; i < nc; ++i) {
-              const double t = sphere_root(__ldg(S.sph_cr + c[i]), os, ds);
-              if (t >= kEps && t < tl) { first = c[i]; break; }
-            }
-            if (first < 0) first = rob;
-          } else {
-            for (int k = 0; k < P.n_spheres; ++k) {
-              if (k == skip || k == skip2) continue;
-              const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
-              if (t >= kEps && t < tl) { first = k; break; }
+          if (nc > 0 || rob >= 0) {
+            const d3 os = ld3(B.sray, B.scap, j, 0), ds = ld3(B.sray, B.scap, j, 3);
+            const double tl = B.sray[6 * (size_t)B.scap + j];
+            if (nc <= kCandMax) {
+              const int* c = B.scand + (size_t)j * kCandMax;
+              for (int i = 0; i < nc; ++i) {
+                const double t = sphere_root(__ldg(S.sph_cr + c[i]), os, ds);
+                if (t >= kEps && t < tl) { first = c[i]; break; }
+              }
+              if (first < 0) first = rob;
+            } else {
+              const int skip = B.sskip[j];
+              for (int k = 0; k < P.n_spheres; ++k) {
+                if (k == skip || k == skip2) continue;
+                const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
+                if (t >= kEps && t < tl) { first = k; break; }
+              }
             }
           }
           occluded = first >= 0;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
         }
         if (!occluded) L = add(L, lf3(B.sq_c, B.scap, j));
       }
-      sf3(B.Lr, B.cap, path, L);
+      sf3(Ls, B.cap, li, L);
     }
     warp_stat(stats, 3, st_sph);
     warp_stat(stats, 4, st_pl);
