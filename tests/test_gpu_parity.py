@@ -256,3 +256,24 @@ def test_validation_errors():
         rt.render_shard(4, 4, 1, 1, 2, 2, out)  # rank >= world
     # state is unchanged after errors: a valid render still works
     rt.render(4, 4, 1, 1, out)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_scene_beyond_shared_memory(oracle_lib, variant):
+    """12 000 spheres > RT_SMEM_SPHERES (10 240): the scans read the scene from global memory
+    (L2-resident) instead of the TMA-staged shared-memory copy; sampled parity vs the oracle."""
+    g = scenegen.SplitMix64(77)
+    b = scenegen.builder()
+    mats = [b.material(scenegen.DIFFUSE, (0.7, 0.5, 0.3), ks=0.2, shininess=16.0),
+            b.material(scenegen.SPECULAR, (0.9, 0.9, 0.9)),
+            b.material(scenegen.REFRACTIVE, (1, 1, 1), ior=1.5),
+            b.material(scenegen.DIFFUSE, (0.4, 0.6, 0.8), kr=0.4)]
+    for i in range(12000):
+        c = (g.uniform(-40, 40), g.uniform(-20, 20), g.uniform(10, 90))
+        b.sphere(tuple(float(np.float32(x)) for x in c), float(np.float32(g.uniform(0.2, 0.8))), mats[i % 4])
+    b.light((0, 30, 50), (3000, 3000, 3000))
+    b.light((-20, 0, 0), (800, 800, 800))
+    sc = b.build("big", eye=(0, 0, 0), look_at=(0, 0, 1), up=(0, 1, 0), vfov=60, width=160, height=90,
+                 max_depth=3, spp=1, background=(0.1, 0.1, 0.2))
+    pix = np.random.default_rng(5).choice(sc.width * sc.height, 300, replace=False)
+    _check(oracle_lib, sc, pixels=pix, label=f"12k spheres/{variant}", variant=variant)
