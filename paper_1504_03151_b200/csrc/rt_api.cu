@@ -105,6 +105,10 @@ struct Context {
   rt_ray_stats last{};
   bool stats_pending = false, stats_timed = false;  // resolved lazily by rt_stats
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // host framebuffers: finished rows are copied on a second stream while later chunks render
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+  std::vector<int> chunk_items;
 };
 
 Context g_ctx;
@@ -177,7 +181,12 @@ int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
   return RT_OK;
 }
 
-int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_bounces, double* accum = nullptr) {
+// host_out (optional): the caller's host framebuffer for a mode-0 render into the staging buffer
+// `out`; the wavefront variant then copies each chunk's finished rows as soon as it resolves
+// (RT_OK with *copied = true), else the caller copies the whole frame after the render
+int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_bounces, double* accum = nullptr,
+               float* host_out = nullptr, bool* copied = nullptr) {
+  if (copied) *copied = false;
   Context& c = g_ctx;
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
@@ -192,7 +201,13 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   if (wavefront) {
     // chunk of whole pixels: at most 2^22 paths; shadow entries: paths x lights
     const long long want = (long long)p.n_items * p.spp;
-    int items = (int)((want < (1ll << 22) ? want : (1ll << 22)) / p.spp);
+    // chunks of at most 2^22 paths (host framebuffers: 2^RT_HOST_CHUNK_LOG2; smaller chunks hide
+    // more of the row copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21)
+#ifndef RT_HOST_CHUNK_LOG2
+#define RT_HOST_CHUNK_LOG2 22
+#endif
+    const long long chunk = (host_out != nullptr && p.mode == 0) ? (1ll << RT_HOST_CHUNK_LOG2) : (1ll << 22);
+    int items = (int)((want < chunk ? want : chunk) / p.spp);
     if (items < 1) items = 1;
     const int cap = items * p.spp;
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
@@ -210,6 +225,20 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       c.ev_s.push_back(b);
     }
     rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
+    const bool overlap = host_out != nullptr && p.mode == 0;
+    if (overlap) {
+      const int max_chunks = (p.n_items + items - 1) / items;
+      if (!c.copy_stream) CU(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      while ((int)c.ev_chunk.size() < max_chunks) {
+        cudaEvent_t ev;
+        CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        c.ev_chunk.push_back(ev);
+      }
+      c.chunk_items.assign(max_chunks, 0);
+      tm.chunk_done = c.ev_chunk.data();
+      tm.chunk_items = c.chunk_items.data();
+      tm.chunk_cap = max_chunks;
+    }
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
     #ifndef RT_WF_PREFER_CONST
 #define RT_WF_PREFER_CONST 0
@@ -217,6 +246,21 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     const int src = (RT_WF_PREFER_CONST && c.const_scene) ? 2 : (c.smem_scene ? 1 : 0);
     CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
     CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
+    if (overlap) {  // rows of complete tile rows, in order, each after its chunk's resolve
+      const long long row_items = (long long)p.tiles_x * rt::kTilePx;
+      int rows_done = 0;
+      for (int k = 0; k < tm.n_chunks; ++k) {
+        long long rows = (long long)(tm.chunk_items[k] / row_items) * rt::kTileH;
+        if (k == tm.n_chunks - 1 || rows > p.H) rows = p.H;
+        if (rows <= rows_done) continue;
+        CU(cudaStreamWaitEvent(c.copy_stream, c.ev_chunk[k], 0), "cudaStreamWaitEvent");
+        CU(cudaMemcpyAsync(host_out + (size_t)rows_done * p.W * 4, out + (size_t)rows_done * p.W,
+                           sizeof(float4) * (size_t)(rows - rows_done) * p.W, cudaMemcpyDeviceToHost, c.copy_stream),
+           "framebuffer D2H");
+        rows_done = (int)rows;
+      }
+      if (copied) *copied = rows_done == p.H;
+    }
     c.n_timed = tm.n;
     c.last_launches = tm.launches;
     c.last_variant = RT_VARIANT_WAVEFRONT;
@@ -342,10 +386,12 @@ int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba,
     p.jitter = 1;
     p.sample_base = sample_base;
   }
-  rc = run_render(p, out, dh, db, accum);
+  bool copied = false;
+  rc = run_render(p, out, dh, db, accum, (!dev_out && !dbg && !accum) ? out_rgba : nullptr, &copied);
   if (rc) return rc;
-  if (!dev_out)
+  if (!dev_out && !copied)
     CU(cudaMemcpyAsync(out_rgba, out, sizeof(float4) * npx, cudaMemcpyDeviceToHost, c.stream), "framebuffer D2H");
+  if (copied) CU(cudaStreamSynchronize(c.copy_stream), "cudaStreamSynchronize(copy)");
   if (dbg && !dev_dbg) {
     CU(cudaMemcpyAsync(hit_ids, dh, sizeof(int) * nsamp * (D + 1), cudaMemcpyDeviceToHost, c.stream), "debug D2H");
     CU(cudaMemcpyAsync(bounces, db, sizeof(int) * nsamp, cudaMemcpyDeviceToHost, c.stream), "debug D2H");

@@ -151,6 +151,12 @@ struct WfTiming {
   int cap;        // pairs available in each array
   int n;          // pairs recorded (output)
   int launches;   // kernels launched (output)
+  // optional: an event recorded after each chunk's resolve, and the work items resolved so far,
+  // so the host can copy finished framebuffer rows while later chunks render
+  cudaEvent_t* chunk_done = nullptr;
+  int* chunk_items = nullptr;
+  int chunk_cap = 0;
+  int n_chunks = 0;  // output
 };
 // scene source of the wavefront intersection kernels: 0 global, 1 shared memory, 2 constant bank
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,

@@ -630,6 +630,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const int items_per_chunk = B.cap / p.spp;
   tm.n = 0;
   tm.launches = 0;
+  tm.n_chunks = 0;
   if (dbg) {
     const long long nh = (long long)p.W * p.H * p.spp * (p.max_depth + 1);
     fill_int<<<num_sms * 8, 256, 0, st>>>(o.dbg_hits, nh, -2);
@@ -659,6 +660,11 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
     wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out, o.accum);
     tm.launches += 2;
+    if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
+      cudaEventRecord(tm.chunk_done[tm.n_chunks], st);
+      tm.chunk_items[tm.n_chunks] = w0 + nw;
+      ++tm.n_chunks;
+    }
   }
   return cudaGetLastError();
 }

@@ -162,10 +162,17 @@ def test_empty_and_planes_only_scenes(oracle_lib):
     _check(oracle_lib, sc, label="planes-only")
 
 
-def test_host_and_device_outputs_identical():
+@pytest.mark.parametrize("name,variant", [("C2", "auto"), ("C2", "wavefront"), ("C4", "wavefront"),
+                                          ("C5", "wavefront")])
+def test_host_and_device_outputs_identical(name, variant):
+    """Host framebuffers (the wavefront copies each chunk's finished rows on a second stream while
+    later chunks render; C4 = 2 chunks, C5 = 32) equal device ones bit for bit."""
     import torch
     from paper_1504_03151_b200 import rt
-    sc = scenegen.get("C2")
+    sc = scenegen.get(name)
+    if name == "C5":
+        sc = sc.with_frame(spp=4, max_depth=2)
+    rt.set_variant(variant)
     rt.load_scene(sc)
     dev = torch.empty((sc.height, sc.width, 4), dtype=torch.float32, device="cuda")
     rt.render(sc.width, sc.height, sc.max_depth, sc.spp, dev)
@@ -176,6 +183,7 @@ def test_host_and_device_outputs_identical():
     again = torch.empty_like(dev)
     rt.render(sc.width, sc.height, sc.max_depth, sc.spp, again)
     assert torch.equal(again, dev)  # deterministic
+    rt.set_variant("auto")
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
