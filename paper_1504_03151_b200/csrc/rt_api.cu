@@ -96,7 +96,9 @@ struct Context {
   DevBuf<unsigned char> wf_mem;
   DevBuf<unsigned> wf_ctr;
   rt::WfBuffers wf{};
-  std::vector<cudaEvent_t> ev_c, ev_s;  // per-launch intersection timing (wavefront)
+  std::vector<cudaEvent_t> ev_c, ev_s, ev_h;  // per-launch scan / shade timing (wavefront)
+  cudaStream_t side_stream = nullptr;           // shadow scans || next closest scan
+  std::vector<cudaEvent_t> ev_fork, ev_join;
   int n_timed = 0, last_launches = 0, last_variant = 0;
   // camera (double basis)
   bool has_camera = false;
@@ -218,13 +220,32 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
     const int pairs = rt::wf_timing_pairs(p, cap);
     while ((int)c.ev_c.size() < 2 * pairs) {
-      cudaEvent_t a, b;
+      cudaEvent_t a, b, h;
       CU(cudaEventCreate(&a), "cudaEventCreate");
       CU(cudaEventCreate(&b), "cudaEventCreate");
+      CU(cudaEventCreate(&h), "cudaEventCreate");
       c.ev_c.push_back(a);
       c.ev_s.push_back(b);
+      c.ev_h.push_back(h);
+    }
+    if (!c.side_stream) CU(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    while ((int)c.ev_fork.size() < p.max_depth + 1) {
+      cudaEvent_t f, j;
+      CU(cudaEventCreateWithFlags(&f, cudaEventDisableTiming), "cudaEventCreate");
+      CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "cudaEventCreate");
+      c.ev_fork.push_back(f);
+      c.ev_join.push_back(j);
     }
     rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
+    tm.shade = c.ev_h.data();
+#ifndef RT_WF_CONCURRENT
+#define RT_WF_CONCURRENT 1
+#endif
+    if (RT_WF_CONCURRENT) {
+      tm.side = c.side_stream;
+      tm.fork = c.ev_fork.data();
+      tm.join = c.ev_join.data();
+    }
     const bool overlap = host_out != nullptr && p.mode == 0;
     if (overlap) {
       const int max_chunks = (p.n_items + items - 1) / items;
@@ -303,8 +324,7 @@ int collect_stats(bool timed) {
       float a = 0.f, b = 0.f, m = 0.f;
       CU(cudaEventElapsedTime(&a, c.ev_c[2 * i], c.ev_c[2 * i + 1]), "cudaEventElapsedTime");
       CU(cudaEventElapsedTime(&b, c.ev_s[2 * i], c.ev_s[2 * i + 1]), "cudaEventElapsedTime");
-      // wf_shade is the only launch between the closest-hit scan's end and the shadow scan's start
-      CU(cudaEventElapsedTime(&m, c.ev_c[2 * i + 1], c.ev_s[2 * i]), "cudaEventElapsedTime");
+      CU(cudaEventElapsedTime(&m, c.ev_h[2 * i], c.ev_h[2 * i + 1]), "cudaEventElapsedTime");
       tc += a;
       ts += b;
       tsh += m;

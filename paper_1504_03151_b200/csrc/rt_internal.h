@@ -151,6 +151,12 @@ struct WfTiming {
   int cap;        // pairs available in each array
   int n;          // pairs recorded (output)
   int launches;   // kernels launched (output)
+  cudaEvent_t* shade = nullptr;  // [2 * cap] events around each wf_shade launch
+  // second stream: the shadow scan + accumulate of depth d run on it, concurrently with the
+  // closest-hit scan of depth d + 1 on the main stream (fork/join events per depth)
+  cudaStream_t side = nullptr;
+  cudaEvent_t* fork = nullptr;   // [max_depth + 1]
+  cudaEvent_t* join = nullptr;   // [max_depth + 1]
   // optional: an event recorded after each chunk's resolve, and the work items resolved so far,
   // so the host can copy finished framebuffer rows while later chunks render
   cudaEvent_t* chunk_done = nullptr;

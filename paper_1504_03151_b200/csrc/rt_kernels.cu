@@ -643,20 +643,44 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     if ((e = cudaMemsetAsync(B.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
     const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
     wf_raygen<<<grid_r, 256, 0, st>>>(p, B, g0, npaths, o.stats);
+    // per depth d: closest scan (d) -> shade (d) -> { shadow scan (d) -> accumulate (d) on the side
+    // stream  ||  closest scan (d + 1) on the main stream } -> join -> shade (d + 1) ...
+    // (independent: the shadow side reads the shadow entries and writes L into Q[d+1]; the closest
+    // scan reads Q[d+1]'s rays and writes the candidate lists)
+    const int t0 = tm.n;
+    auto closest_scan = [&](int dd) {
+      const int ti = t0 + dd;
+      const bool rec = ti < tm.cap;
+      if (rec) cudaEventRecord(tm.closest[2 * ti], st);
+      wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+      if (rec) cudaEventRecord(tm.closest[2 * ti + 1], st);
+    };
+    closest_scan(0);
     for (int d = 0; d <= p.max_depth; ++d) {
-      const bool rec = tm.n < tm.cap;
-      if (rec) cudaEventRecord(tm.closest[2 * tm.n], st);
-      wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, d);
-      if (rec) cudaEventRecord(tm.closest[2 * tm.n + 1], st);
+      const int ti = t0 + d;
+      const bool rec = ti < tm.cap;
+      if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti], st);
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
-      if (rec) cudaEventRecord(tm.shadow[2 * tm.n], st);
-      wf_isect<kSrc, true><<<grid_s, 256, smem, st>>>(p, sc, B, d);
-      if (rec) cudaEventRecord(tm.shadow[2 * tm.n + 1], st);
-      wf_accumulate<<<grid_l, 256, 0, st>>>(p, sc, B, d, o.stats);
-      if (rec) ++tm.n;
+      if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti + 1], st);
+      cudaStream_t ss = st;
+      if (tm.side) {
+        cudaEventRecord(tm.fork[d], st);
+        cudaStreamWaitEvent(tm.side, tm.fork[d], 0);
+        ss = tm.side;
+      }
+      if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
+      wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+      if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
+      wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
+      if (d < p.max_depth) closest_scan(d + 1);
+      if (tm.side) {
+        cudaEventRecord(tm.join[d], tm.side);
+        cudaStreamWaitEvent(st, tm.join[d], 0);
+      }
       tm.launches += 4;
     }
+    tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
     wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out, o.accum);
     tm.launches += 2;
