@@ -168,9 +168,12 @@ template <int kSrc, bool kShadow>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   __shared__ uint64_t s_mbar;
+  const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
+  // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
+  if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
   if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
   const float4* gp = S.pairs;
-  const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
   unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
   const WfQueue Q = B.q[d & 1];
   int* cand = kShadow ? B.scand : B.ccand;
