@@ -519,7 +519,7 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(scenegen.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="core-seconds of oracle work")
-    ap.add_argument("--ref-pixels", type=int, default=1024, help="--impl reference: pixels per step")
+    ap.add_argument("--ref-pixels", type=int, default=4096, help="--impl reference: pixels per step")
     ap.add_argument("--strict", action="store_true", default=True)
     ap.add_argument("--mode", choices=["hot", "progressive"], default="hot",
                     help="hot: the §8(a) path on C4 (default); progressive: NEXT-1/2 passes on C0")
