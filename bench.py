@@ -232,7 +232,7 @@ def run_b200(args):
     import torch.distributed as dist
     from paper_1504_03151_b200 import build as rtbuild
     from paper_1504_03151_b200 import rt
-    from paper_1504_03151_b200.multigpu import CudaBackend, ShardedRenderer
+    from paper_1504_03151_b200.multigpu import CudaBackend, P2PRenderer, ShardedRenderer
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -253,9 +253,25 @@ def run_b200(args):
     rt.load_scene(sc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    collective = None
     if world > 1:
-        rend = ShardedRenderer(CudaBackend(dev), W, H, D, S)
-        step = rend.render
+        rend = None
+        if args.collective == "p2p":  # fused render + gather: pixels stored into rank 0's frame over NVLink
+            try:
+                rend = P2PRenderer(W, H, D, S)
+                collective = "p2p (resolve kernels store into rank 0's frame over NVLink peer memory)"
+
+                def step():
+                    rend.render()
+                    rend.release()
+            except RuntimeError as ex:
+                if rank == 0:
+                    print(f"bench.py: {ex}; falling back to the NCCL all-gather", file=sys.stderr)
+                rend = None
+        if rend is None:
+            rend = ShardedRenderer(CudaBackend(dev), W, H, D, S)
+            step = rend.render
+            collective = "allgather (NCCL all_gather_into_tensor of the tile slabs + rank-0 assembly)"
     else:
         out = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
         step = lambda: rt.render(W, H, D, S, out)  # noqa: E731
@@ -268,9 +284,12 @@ def run_b200(args):
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step()
-    if world > 1:  # kernels per frame on this rank: the shard render (+ assembly on rank 0)
-        rt.render_shard(W, H, D, S, rank, world, rend.slab)
-        launches_per_step = rt.stats()["launches"] + (2 if rank == 0 else 0)
+    if world > 1:  # kernels per frame on this rank: the shard render (+ assembly or stats sum on rank 0)
+        probe = torch.empty(rt.shard_layout(W, H, world)[1], dtype=torch.uint8, device=dev)
+        rt.render_shard(W, H, D, S, rank, world, probe)  # same launches as the direct shard
+        extra = (2 if isinstance(rend, ShardedRenderer) else 1) if rank == 0 else 0
+        launches_per_step = rt.stats()["launches"] + extra
+        del probe
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -316,6 +335,8 @@ def run_b200(args):
             if rank == 0:
                 host_out.copy_(frame.image.view(H, W, 4))
             torch.cuda.synchronize()
+            if isinstance(rend, P2PRenderer):
+                rend.release()
             s2 = frame.stats or {"primary": 0, "shadow": 0, "secondary": 0}
         rays_e2e += s2["primary"] + s2["shadow"] + s2["secondary"]
     dt = time.perf_counter() - t0
@@ -362,7 +383,7 @@ def run_b200(args):
             "vs_baseline": None, "dtype": "f32 (FFMA2 filter) + f64 (candidate refinement, shading geometry)",
             "data": "synthetic (seeded scenegen C4 scene; no dataset)",
             "fps": 1e3 / ms_per_step,
-            "config": dict(sc.describe(), workload=args.config, parallelism=f"tiles{world}",
+            "config": dict(sc.describe(), workload=args.config, parallelism=f"tiles{world}", collective=collective,
                            l2="flushed (256 MiB write) before every frame, outside the frame events",
                            rays_per_frame=int(rays), primary=int(st["primary"]), shadow=int(st["shadow"]),
                            secondary=int(st["secondary"]), sphere_tests=int(st["sphere_tests"]),
@@ -524,6 +545,9 @@ def main():
     ap.add_argument("--mode", choices=["hot", "progressive"], default="hot",
                     help="hot: the §8(a) path on C4 (default); progressive: NEXT-1/2 passes on C0")
     ap.add_argument("--passes", type=int, default=16, help="--mode progressive: passes per step")
+    ap.add_argument("--collective", choices=["p2p", "allgather"], default="p2p",
+                    help="N>1: fused render+gather into rank 0's frame over peer memory (default, falls back to "
+                         "allgather if CUDA IPC / peer access is unavailable) or the NCCL all-gather of slabs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -186,6 +186,25 @@ int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t sp
 int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, int32_t world,
                       float* out_rgba_dev);
 
+/* ---- fused render + gather over NVLink peer memory (SURVEY §8(e) ablation) -------------------
+ * Direct shard: render this rank's tiles (the cyclic assignment of rt_shard_layout) and store
+ * each finished pixel straight into the row-major frame `frame_dev` — rank 0's framebuffer, a
+ * peer pointer (rt_ipc_open) on the other ranks, so the pixels cross NVLink inside the resolve
+ * kernel instead of through a slab and an all-gather. The rank's 8-uint64 stats record goes to
+ * records_dev[8 * rank ..]. No pixel of another rank is touched; after every rank's call has
+ * completed (a barrier), the frame equals rt_render's bit for bit. Rank 0 then calls
+ * rt_sum_shard_stats(records_dev, world) so rt_stats reports the whole frame. */
+int rt_render_shard_direct(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank,
+                           int32_t world, float* frame_dev, uint64_t* records_dev);
+int rt_sum_shard_stats(const uint64_t* records_dev, int32_t world);
+/* CUDA IPC for the direct shard (one process per GPU): rt_ipc_alloc cudaMallocs `bytes` and
+ * returns the pointer and its 64-byte handle; another process maps it with rt_ipc_open (peer
+ * access enabled lazily) and unmaps with rt_ipc_close; the owner frees with rt_ipc_free. */
+int rt_ipc_alloc(int64_t bytes, void** dev_ptr, uint8_t handle[64]);
+int rt_ipc_open(const uint8_t handle[64], void** dev_ptr);
+int rt_ipc_close(void* dev_ptr);
+int rt_ipc_free(void* dev_ptr);
+
 /* rt_render plus per-sample records for parity tests: hit_ids[((py*W+px)*spp + s)*(max_depth+1)
  * + segment] = primitive index hit by that segment, -1 on a miss, -2 if the segment was not
  * traced; bounces[(py*W+px)*spp + s] = number of secondary rays. Host or device pointers. */

@@ -751,6 +751,89 @@ int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t sp
   return RT_OK;
 }
 
+int rt_render_shard_direct(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank,
+                           int32_t world, float* frame_dev, uint64_t* records_dev) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world) return fail(RT_ERR_INVALID_ARG, "shard: need 0 <= rank < world");
+  if (!frame_dev || !records_dev || !is_device_ptr(frame_dev) || !is_device_ptr(records_dev))
+    return fail(RT_ERR_INVALID_ARG, "direct shard: frame and records must be device (or peer) pointers");
+  if ((reinterpret_cast<uintptr_t>(frame_dev) & 15u) != 0 || (reinterpret_cast<uintptr_t>(records_dev) & 7u) != 0)
+    return fail(RT_ERR_INVALID_ARG, "direct shard: frame must be 16-byte and records 8-byte aligned");
+  rc = check_frame(width, height, max_depth, spp);
+  if (rc) return rc;
+  int32_t tpr = 0;
+  rt_shard_layout(width, height, world, &tpr, nullptr);
+  rt::DevParams p = make_params(width, height, max_depth, spp);
+  p.mode = 2;
+  p.rank = rank;
+  p.world = world;
+  p.n_items = tpr * rt::kTilePx;
+  Context& c = g_ctx;
+  rc = run_render(p, reinterpret_cast<float4*>(frame_dev), nullptr, nullptr);
+  if (rc) return rc;
+  // this rank's 8-uint64 stats record into slot `rank` (peer memory over NVLink when remote)
+  CU(cudaMemcpyAsync(records_dev + 8 * (size_t)rank, c.stats.p, 64, cudaMemcpyDefault, c.stream), "stats record");
+  defer_stats(true);
+  return RT_OK;
+}
+
+int rt_sum_shard_stats(const uint64_t* records_dev, int32_t world) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (world < 1 || !records_dev || !is_device_ptr(records_dev)) return fail(RT_ERR_INVALID_ARG, "records: device pointer, world >= 1");
+  CU(rt::launch_sum_records(reinterpret_cast<const unsigned long long*>(records_dev), world, g_ctx.stats.p, g_ctx.stream),
+     "sum stats records");
+  defer_stats(false);
+  return RT_OK;
+}
+
+int rt_ipc_alloc(int64_t bytes, void** dev_ptr, uint8_t handle[64]) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (bytes < 1 || !dev_ptr || !handle) return fail(RT_ERR_INVALID_ARG, "ipc_alloc: bytes >= 1 and non-NULL outputs");
+  void* p = nullptr;
+  CU(cudaMalloc(&p, (size_t)bytes), "cudaMalloc(ipc)");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  *dev_ptr = p;
+  return RT_OK;
+}
+
+int rt_ipc_open(const uint8_t handle[64], void** dev_ptr) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (!handle || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "ipc_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CU(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return RT_OK;
+}
+
+int rt_ipc_close(void* dev_ptr) {
+  g_err.clear();
+  if (!dev_ptr) return fail(RT_ERR_INVALID_ARG, "ipc_close: NULL");
+  CU(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+  return RT_OK;
+}
+
+int rt_ipc_free(void* dev_ptr) {
+  g_err.clear();
+  if (!dev_ptr) return fail(RT_ERR_INVALID_ARG, "ipc_free: NULL");
+  CU(cudaFree(dev_ptr), "cudaFree(ipc)");
+  return RT_OK;
+}
+
 int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, int32_t world, float* out_rgba_dev) {
   g_err.clear();
   int rc = ensure_device();

@@ -116,7 +116,7 @@ __device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int
 __device__ __forceinline__ bool item_pixel(const DevParams& P, int w, int& px, int& py) {
   int t = w / kTilePx;
   const int i = w % kTilePx;
-  if (P.mode == 1) {
+  if (P.mode >= 1) {  // shard (1) or direct shard (2): local tile j is global tile j*world + rank
     t = t * P.world + P.rank;
     if (t >= P.n_tiles) return false;
   }

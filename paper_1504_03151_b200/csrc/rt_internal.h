@@ -73,6 +73,8 @@ struct DevParams {
   int pad_;
   long long sample_base;  // global index of sample 0 (pass index of the first pass)
   // job: full frame (mode 0, tile-major work items, row-major output) or shard (mode 1)
+  // mode 0: full frame, tile-major items, row-major output; 1: shard, slab output (tile-major);
+  // 2: direct shard, the rank's tiles stored row-major into a (possibly peer) frame
   int mode, rank, world, tiles_x, n_tiles, n_items;
 };
 
@@ -170,6 +172,7 @@ cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, cons
 int wf_timing_pairs(const DevParams& p, int cap_paths);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,
                            float gamma, cudaStream_t st);
 

@@ -64,9 +64,12 @@ __device__ __forceinline__ void start_sample(Lane& L, const DevParams& P) {
 __device__ __forceinline__ bool start_item(Lane& L, const DevParams& P, int w, float4* out) {
   int t = w / kTilePx;
   const int i = w % kTilePx;
-  if (P.mode == 1) {
+  if (P.mode >= 1) {
     t = t * P.world + P.rank;
-    if (t >= P.n_tiles) { out[w] = make_float4(0.f, 0.f, 0.f, 0.f); return false; }
+    if (t >= P.n_tiles) {
+      if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+      return false;
+    }
   }
   const int px = (t % P.tiles_x) * kTileW + (i % kTileW);
   const int py = (t / P.tiles_x) * kTileH + (i / kTileW);
@@ -237,7 +240,7 @@ __device__ void finish_sample(Lane& L, const DevParams& P, const DevOutputs& O) 
   }
   const float inv = 1.0f / (float)P.spp;
   const float4 v = make_float4(L.Lpix.x * inv, L.Lpix.y * inv, L.Lpix.z * inv, 1.0f);
-  if (P.mode == 0) O.out[(long long)L.py * P.W + L.px] = v;  // 16-byte vector store
+  if (P.mode != 1) O.out[(long long)L.py * P.W + L.px] = v;  // 16-byte vector store (row-major)
   else O.out[L.item] = v;
   L.item = -1;
   L.qkind = Q_NONE;
@@ -557,6 +560,19 @@ cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int
   if (grid < 1) grid = 1;
   assemble_kernel<<<grid, 256, 0, st>>>(gathered, W, H, world, tiles_per_rank, tiles_x, out);
   sum_stats_kernel<<<1, 32, 0, st>>>(gathered, world, tiles_per_rank, stats);
+  return cudaGetLastError();
+}
+
+__global__ void sum_records_kernel(const unsigned long long* __restrict__ rec, int world, unsigned long long* stats) {
+  if (threadIdx.x < 8) {
+    unsigned long long v = 0;
+    for (int r = 0; r < world; ++r) v += rec[r * 8 + threadIdx.x];
+    stats[threadIdx.x] = v;
+  }
+}
+
+cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigned long long* stats, cudaStream_t st) {
+  sum_records_kernel<<<1, 32, 0, st>>>(rec, world, stats);
   return cudaGetLastError();
 }
 

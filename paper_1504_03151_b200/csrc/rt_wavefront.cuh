@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
     for (int s = 0; s < P.spp; ++s) acc = add(acc, lf3(B.Lr, B.cap, i * P.spp + s));
     const float inv = 1.0f / (float)P.spp;
     const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, 1.0f);
-    if (P.mode == 0) out[(long long)py * P.W + px] = v;
+    if (P.mode != 1) out[(long long)py * P.W + px] = v;  // frame (mode 0) or peer frame (mode 2)
     else out[w] = v;
   }
 }

@@ -43,6 +43,76 @@ def rank_tiles(width: int, height: int, rank: int, world: int) -> list[int]:
     return [j * world + rank for j in range(tpr) if j * world + rank < nt]
 
 
+class P2PRenderer:
+    """Fused render + gather over NVLink peer memory (SURVEY §8(e) ablation; include/rt.h
+    rt_render_shard_direct). Rank 0 owns the frame and a world x 8 uint64 stats-record array,
+    allocated for CUDA IPC; the handles travel once over the process group and every other rank
+    maps them (peer access over NVLink / NVSwitch). Each frame, every rank's resolve kernel
+    stores its pixels straight into rank 0's frame — no slab, no all-gather, no assembly kernel —
+    then one barrier orders the frame before rank 0 uses it, and a second (`release`) before the
+    next frame may overwrite it."""
+
+    def __init__(self, width: int, height: int, max_depth: int, spp: int, group=None):
+        self.W, self.H, self.D, self.spp = width, height, max_depth, spp
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.frame_ptr = self.rec_ptr = None
+        handles = [None, None]
+        if self.rank == 0:
+            try:
+                self.frame_ptr, hf = rt.ipc_alloc(width * height * 16)
+                self.rec_ptr, hr = rt.ipc_alloc(self.world * 64)
+                handles = [hf, hr]
+            except rt.RtError:
+                handles = [None, None]
+        if self.world > 1:
+            dist.broadcast_object_list(handles, src=0, group=self.group)
+        ok = handles[0] is not None
+        if ok and self.rank != 0:
+            try:
+                self.frame_ptr = rt.ipc_open(handles[0])
+                self.rec_ptr = rt.ipc_open(handles[1])
+            except rt.RtError:
+                ok = False
+        if self.world > 1:  # every rank agrees, so a failure raises everywhere (no one waits forever)
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            ok = bool(flag.item())
+        if not ok:
+            self.close()
+            raise RuntimeError("peer-memory frame unavailable (CUDA IPC / peer access failed on some rank)")
+        self.image = None
+        if self.rank == 0:
+            self.image = torch.as_tensor(rt.DeviceArray(self.frame_ptr, (height, width, 4), "<f4"), device="cuda")
+
+    def _barrier(self):
+        torch.cuda.current_stream().synchronize()  # this rank's stores (and stats record) issued and done
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def render(self) -> Frame:
+        rt.render_shard_direct(self.W, self.H, self.D, self.spp, self.rank, self.world, self.frame_ptr, self.rec_ptr)
+        self._barrier()
+        if self.rank == 0:
+            rt.sum_shard_stats(self.rec_ptr, self.world)
+            return Frame(self.image, rt.stats())
+        return Frame(None, None)
+
+    def release(self):
+        """Rank 0 is done with the frame: the next render may overwrite it."""
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def close(self):
+        self.image = None
+        for ptr in (self.frame_ptr, self.rec_ptr):
+            if ptr:
+                (rt.ipc_free if self.rank == 0 else rt.ipc_close)(ptr)
+        self.frame_ptr = self.rec_ptr = None
+
+
 class CudaBackend:
     """The product path: libb200rt.so through the ctypes binding."""
 

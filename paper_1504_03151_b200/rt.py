@@ -78,6 +78,12 @@ def lib() -> C.CDLL:
         "rt_render_debug": [i32, i32, i32, i32, vp, vp, vp],
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
         "rt_set_integrator": [i32, i32],
+        "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
+        "rt_sum_shard_stats": [vp, i32],
+        "rt_ipc_alloc": [i64, C.POINTER(vp), C.c_char_p],
+        "rt_ipc_open": [C.c_char_p, C.POINTER(vp)],
+        "rt_ipc_close": [vp],
+        "rt_ipc_free": [vp],
         "rt_scene_parse": [C.c_char_p, i64],
         "rt_scene_load": [C.c_char_p],
         "rt_write_ppm": [vp, i32, i32, C.c_float, C.c_float, C.c_char_p],
@@ -236,6 +242,44 @@ def shard_layout(width, height, world):
 def render_shard(width, height, max_depth, spp, rank, world, slab):
     _check("rt_render_shard", lib().rt_render_shard(width, height, max_depth, spp, rank, world, _ptr(slab)))
     return slab
+
+
+def render_shard_direct(width, height, max_depth, spp, rank, world, frame_ptr: int, records_ptr: int):
+    """Fused render + gather: this rank's pixels go straight into the (peer) frame (rt.h)."""
+    _check("rt_render_shard_direct", lib().rt_render_shard_direct(width, height, max_depth, spp, rank, world,
+                                                                  frame_ptr, records_ptr))
+
+
+def sum_shard_stats(records_ptr: int, world: int):
+    _check("rt_sum_shard_stats", lib().rt_sum_shard_stats(records_ptr, world))
+
+
+def ipc_alloc(nbytes: int) -> tuple[int, bytes]:
+    ptr, h = C.c_void_p(), C.create_string_buffer(64)
+    _check("rt_ipc_alloc", lib().rt_ipc_alloc(nbytes, C.byref(ptr), h))
+    return ptr.value, h.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    _check("rt_ipc_open", lib().rt_ipc_open(C.create_string_buffer(bytes(handle), 64), C.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int):
+    _check("rt_ipc_close", lib().rt_ipc_close(ptr))
+
+
+def ipc_free(ptr: int):
+    _check("rt_ipc_free", lib().rt_ipc_free(ptr))
+
+
+class DeviceArray:
+    """A raw device allocation seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
 
 
 def assemble_tiles(gathered, width, height, world, out):
