@@ -164,6 +164,10 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
 #ifndef RT_ISECT_MIN_BLOCKS
 #define RT_ISECT_MIN_BLOCKS 3
 #endif
+#ifndef RT_SCAN_UNROLL
+#define RT_SCAN_UNROLL 1
+#endif
+constexpr int kScanUnroll = RT_SCAN_UNROLL;  // batches of the scan loop unrolled together
 template <int kSrc, bool kShadow>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -217,6 +221,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     const float tl_f = (float)tl;
     float tub = 3.0e38f;  // closest: certain upper bound of the nearest accepted root
     int nc = 0;
+#pragma unroll(kScanUnroll)
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
       const float dmax = F.template batch<kSrc>(gp, base, disc);
