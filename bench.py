@@ -182,14 +182,21 @@ def cpu_baseline(name: str, target_core_s: float = 20.0, seed: int = 7, okw: dic
     n = int(min(sc.width * sc.height, max(len(probe), target_core_s / max(per_px_core, 1e-9))))
     pix = rng.choice(sc.width * sc.height, n, replace=False)
     dt, cnt = tm.run(pix)
+    # the same oracle single-threaded, on 1/cores of the sample
+    sub = pix[: max(1, n // tm.cores)]
+    t1 = time.perf_counter()
+    c1 = _oracle_chunk((name, sub.tolist(), dict(okw or {})))
+    dt1 = time.perf_counter() - t1
     tm.close()
     rays = cnt["primary"] + cnt["shadow"] + cnt["secondary"]
+    rays1 = c1["primary"] + c1["shadow"] + c1["secondary"]
     frac = n / (sc.width * sc.height)
     what = f"all {sc.spp} spp" if not okw else f"{sc.spp} progressive passes, global integrator + area lights"
     return {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": tm.cores, "kind": "oracle",
             "sample": f"{n} random pixels of {name} ({what}, depth {sc.max_depth}) = {frac:.2%} of the frame, "
-                      f"{dt:.1f} s wall on {tm.cores} processes",
-            "fps_extrapolated": 1.0 / (dt / frac)}
+                      f"{dt:.2f} s wall on {tm.cores} processes",
+            "fps_extrapolated": 1.0 / (dt / frac),
+            "value_1thread": rays1 / dt1 / 1e6, "sample_1thread": f"{len(sub)} of those pixels in this process"}
 
 
 # ---------------------------------------------------------------------------------------------
