@@ -81,7 +81,9 @@ struct Context {
   float cmax = 0.f, rmax = 0.f, cmax_abs = 0.f;
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
-  DevBuf<float4> pairs, sph_cr, stage;
+  DevBuf<float4> pairs, sph_cr, stage, pairs_eye;
+  std::vector<float4> pairs_host, pairs_eye_host;  // expanded-form pairs; their camera-ray copy
+  bool eye_ready = false;
   DevBuf<int> sph_prim, sph_mat, emit_sph;
   int n_emitters = 0;  // emissive spheres (prim order)
   // integrator settings (rt_set_integrator)
@@ -173,6 +175,28 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   return p;
 }
 
+// Camera rays share the origin `eye`: s1 = K + 2 c'.o' (o' = eye - centre) per sphere, computed
+// in FP64 and rounded once, replaces K in a copy of the pair layout (RayFilterT::batch_eye)
+int build_eye_pairs() {
+  Context& c = g_ctx;
+  c.eye_ready = false;
+  if (!RT_FILTER_EXPANDED || !c.has_scene || !c.has_camera || c.pairs_host.empty()) return RT_OK;
+  const double ox = c.eye[0] - c.centre[0], oy = c.eye[1] - c.centre[1], oz = c.eye[2] - c.centre[2];
+  c.pairs_eye_host = c.pairs_host;
+  for (size_t q = 0; q + 1 < c.pairs_eye_host.size(); q += 2) {
+    const float4 a = c.pairs_host[q], b = c.pairs_host[q + 1];
+    float4& be = c.pairs_eye_host[q + 1];
+    be.z = (float)((double)b.z + 2.0 * ((double)a.x * ox + (double)a.z * oy + (double)b.x * oz));
+    be.w = (float)((double)b.w + 2.0 * ((double)a.y * ox + (double)a.w * oy + (double)b.y * oz));
+  }
+  CU(c.pairs_eye.reserve(c.pairs_eye_host.size()), "cudaMalloc(eye pairs)");
+  CU(cudaMemcpyAsync(c.pairs_eye.p, c.pairs_eye_host.data(), sizeof(float4) * c.pairs_eye_host.size(),
+                     cudaMemcpyHostToDevice, c.stream), "H2D");
+  CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // the host copy may change next call
+  c.eye_ready = true;
+  return RT_OK;
+}
+
 int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
   if (W < 1 || H < 1) return fail(RT_ERR_INVALID_ARG, "width/height must be >= 1 (got %d x %d)", W, H);
   if ((long long)W * H > 2147483647LL) return fail(RT_ERR_INVALID_ARG, "width*height exceeds 2^31-1");
@@ -192,7 +216,8 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   Context& c = g_ctx;
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
-  rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p};
+  rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p,
+                  c.eye_ready ? c.pairs_eye.p : nullptr};
   rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces, accum};
   // AUTO: the wavefront kernels for large scenes, and for the NEXT-1 / NEXT-2 modes, whose long
   // divergent paths (every diffuse hit continues; one lane per pixel walks all its passes) leave
@@ -662,7 +687,8 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     c.amb[k] = env ? env->ambient[k] : 0.f;
   }
   c.has_scene = true;
-  return RT_OK;
+  c.pairs_host = pairs;
+  return build_eye_pairs();
 }
 
 int rt_camera_set(const float eye[3], const float look_at[3], const float up[3], float vfov_deg) {
@@ -688,7 +714,7 @@ int rt_camera_set(const float eye[3], const float look_at[3], const float up[3],
   for (int k = 0; k < 3; ++k) { c.eye[k] = eye[k]; c.f[k] = f[k]; c.r[k] = r[k]; c.u[k] = u[k]; }
   c.h = std::tan(0.5 * (double)vfov_deg * 3.14159265358979323846 / 180.0);
   c.has_camera = true;
-  return RT_OK;
+  return build_eye_pairs();
 }
 
 int rt_render(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba) {

@@ -277,6 +277,38 @@ struct RayFilterT {
     for (int i = 1; i < kPairsPerBatch; ++i) vmax = fmaxf(vmax, fmaxf(v[i].x, v[i].y));
     return vmax;
   }
+  // Camera rays share their origin: s1 = K + 2 c'.o' is then the same for every ray and comes
+  // precomputed per sphere (pairs_eye: {c'x, c'y, c'z, s1} in the pair layout, rt_api.cu), so a
+  // sphere costs tc (3 FMA) + v = tc^2 + s1 (1 FMA) instead of 7 FMA. Same v, same cut; the
+  // precomputed s1 (FP64, rounded once) is more accurate than the FMA chain the slack covers.
+  template <int kSrc>
+  __device__ __forceinline__ float batch_eye(const float4* __restrict__ gp, int base, float2 (&v)[kPairsPerBatch]) const {
+    static_assert(kExp, "shared-origin filter exists in the expanded form");
+    const float2 D1 = make_float2(dx, dx), D2 = make_float2(dy, dy), D3 = make_float2(dz, dz);
+    const float2 B1 = make_float2(b1, b1);
+#pragma unroll
+    for (int i = 0; i < kPairsPerBatch; ++i) {
+      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
+      const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
+      const float2 tc = __ffma2_rn(CX, D1, __ffma2_rn(CY, D2, __ffma2_rn(CZ, D3, B1)));
+      v[i] = __ffma2_rn(tc, tc, S1);
+    }
+    float vmax = fmaxf(v[0].x, v[0].y);
+#pragma unroll
+    for (int i = 1; i < kPairsPerBatch; ++i) vmax = fmaxf(vmax, fmaxf(v[i].x, v[i].y));
+    return vmax;
+  }
+  template <int kSrc>
+  __device__ __forceinline__ void sphere_eye(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
+    const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
+    const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
+    const bool h = k & 1;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, s1 = h ? pb.w : pb.z;
+    tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
+    dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
+  }
   // float discriminant estimate dd (|dd - disc| <= slack) and chord centre tc (|err| <= eta) of
   // one sphere k (rare path). The projected form reads {c, r} of sphere k from `cr` (global):
   // a constant-bank scene is then only ever indexed warp-uniformly (LDCU, not LDC).

@@ -86,6 +86,7 @@ struct DevScene {
   const DevMat* mats;
   const DevLight* lights;
   const int* emit_sph;     // [n_emitters] sphere index of emitter e (prim order), or null
+  const float4* pairs_eye; // pair layout with s1 = K + 2 c'.o'(eye) in place of K (camera rays)
 };
 
 struct DevOutputs {

@@ -635,7 +635,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
   int occ_c = 0, occ_s = 0;
-  for (auto fn : {wf_isect<kSrc, false>, wf_isect<kSrc, true>}) {
+  // camera rays (depth 0) use the shared-origin filter when the eye-specific pairs exist
+  constexpr bool kEyeOk = kSrc != SRC_CONST && RT_FILTER_EXPANDED;
+  using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
+  IsectFn kc0 = wf_isect<kSrc, false>;
+  if (kEyeOk && sc.pairs_eye != nullptr) kc0 = wf_isect<kSrc, false, kEyeOk>;
+  for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
@@ -668,7 +673,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + dd;
       const bool rec = ti < tm.cap;
       if (rec) cudaEventRecord(tm.closest[2 * ti], st);
-      wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+      if (dd == 0) kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+      else wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
       if (rec) cudaEventRecord(tm.closest[2 * ti + 1], st);
     };
     closest_scan(0);
