@@ -639,7 +639,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   constexpr bool kEyeOk = kSrc != SRC_CONST && RT_FILTER_EXPANDED;
   using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
   IsectFn kc0 = wf_isect<kSrc, false>;
-  if (kEyeOk && sc.pairs_eye != nullptr) kc0 = wf_isect<kSrc, false, kEyeOk>;
+#ifndef RT_EYE_TWO_RAYS
+#define RT_EYE_TWO_RAYS 1
+#endif
+  if (kEyeOk && sc.pairs_eye != nullptr) kc0 = RT_EYE_TWO_RAYS ? wf_isect_eye2<kSrc> : wf_isect<kSrc, false, kEyeOk>;
   for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;

@@ -294,6 +294,127 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
 }
 
+// ---- a3 for camera rays, two rays per thread --------------------------------------------------
+// The shared-origin filter needs 4 FMA per sphere, so one ray per thread leaves the kernel
+// co-limited by the shared-memory pipe (2 LDS.128 per 2 spheres). Here every lane carries two
+// camera rays (a warp = 64 rays): each pair of spheres read from shared memory serves both, and
+// the FFMA2 stream is again the only limit. Same filter, same candidate lists as wf_isect.
+#ifndef RT_EYE_PAIRS_PER_BATCH
+#define RT_EYE_PAIRS_PER_BATCH 8
+#endif
+constexpr int kEyePB = RT_EYE_PAIRS_PER_BATCH;
+static_assert(kPairsPerBatch % kEyePB == 0, "n_pairs_pad is padded to kPairsPerBatch");
+
+struct EyeRay {
+  RayFilterT<true> F;
+  float tub;
+  int nc;
+  bool act;
+};
+
+template <int kSrc>
+__device__ __forceinline__ void eye_candidates(const DevParams& P, const float4* __restrict__ gp, unsigned m,
+                                               int kbase, EyeRay& R, int* cand_row) {
+  const float eps_f = (float)kEps;
+  while (m != 0u) {
+    const int i = __ffs(m) - 1;
+    m &= m - 1u;
+    const int k = kbase + i;
+    if (k >= P.n_spheres) break;
+    float dd, tc;
+    R.F.template sphere_eye<kSrc>(gp, k, dd, tc);
+    const float qh = sqrtf(fmaxf(dd - R.F.neg_slack, 0.f));
+    const float ql = sqrtf(fmaxf(dd + R.F.neg_slack, 0.f));
+    const bool sure = dd + R.F.neg_slack > 0.f;
+    if (tc + qh < eps_f - R.F.eta) continue;     // chord certainly behind
+    if (tc - qh - R.F.eta > R.tub) continue;     // certainly farther than a certain hit
+    if (sure) {
+      const float t0lo = tc - qh - R.F.eta, t0hi = tc - ql + R.F.eta;
+      const float t1lo = tc + ql - R.F.eta, t1hi = tc + qh + R.F.eta;
+      if (t0lo >= eps_f) R.tub = fminf(R.tub, t0hi);
+      else if (t0hi < eps_f && t1lo >= eps_f) R.tub = fminf(R.tub, t1hi);
+    }
+    if (R.nc < kCandMax) cand_row[R.nc] = k;
+    ++R.nc;
+  }
+}
+
+template <int kSrc>
+__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  __shared__ uint64_t s_mbar;
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
+  const float4* gp = S.pairs_eye;
+  if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
+  unsigned* work = B.ctr + wf_ctr_wc(d);
+  const WfQueue Q = B.q[d & 1];
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned e0 = 0;
+    if (lane == 0) e0 = atomicAdd(work, 64u);
+    e0 = __shfl_sync(kFull, e0, 0);
+    if (e0 >= n) break;
+    const unsigned ea = e0 + lane, eb = e0 + 32 + lane;
+    EyeRay Ra, Rb;
+    {
+      d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+      Ra.act = ea < n;
+      if (Ra.act) { o = ld3(Q.ray, B.cap, (int)ea, 0); dir = ld3(Q.ray, B.cap, (int)ea, 3); }
+      Ra.F.init(o, dir, P);
+      o = mk(0, 0, 0); dir = mk(0, 0, 1);
+      Rb.act = eb < n;
+      if (Rb.act) { o = ld3(Q.ray, B.cap, (int)eb, 0); dir = ld3(Q.ray, B.cap, (int)eb, 3); }
+      Rb.F.init(o, dir, P);
+    }
+    Ra.tub = Rb.tub = 3.0e38f;
+    Ra.nc = Rb.nc = 0;
+    const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
+    const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+    const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
+    const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
+    for (int base = 0; base < P.n_pairs_pad; base += kEyePB) {
+      float2 va[kEyePB], vb[kEyePB];
+#pragma unroll
+      for (int i = 0; i < kEyePB; ++i) {
+        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
+        const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
+        const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
+        const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
+        va[i] = __ffma2_rn(ta, ta, S1);
+        vb[i] = __ffma2_rn(tb, tb, S1);
+      }
+      float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+#pragma unroll
+      for (int i = 1; i < kEyePB; ++i) {
+        ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
+        mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+      }
+      const bool ca = Ra.act && ma >= Ra.F.cut, cb = Rb.act && mb >= Rb.F.cut;
+      if (__any_sync(kFull, ca || cb)) {
+        if (ca) {
+          unsigned m = 0u;
+#pragma unroll
+          for (int i = 0; i < kEyePB; ++i)
+            m |= ((va[i].x >= Ra.F.cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= Ra.F.cut) ? 1u : 0u) << (2 * i + 1);
+          eye_candidates<kSrc>(P, gp, m, 2 * base, Ra, B.ccand + (size_t)ea * kCandMax);
+        }
+        if (cb) {
+          unsigned m = 0u;
+#pragma unroll
+          for (int i = 0; i < kEyePB; ++i)
+            m |= ((vb[i].x >= Rb.F.cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= Rb.F.cut) ? 1u : 0u) << (2 * i + 1);
+          eye_candidates<kSrc>(P, gp, m, 2 * base, Rb, B.ccand + (size_t)eb * kCandMax);
+        }
+      }
+    }
+    if (ea < n) B.cn[ea] = Ra.nc;
+    if (eb < n) B.cn[eb] = Rb.nc;
+  }
+}
+
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
 // the list overflowed
 __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScene& S, const int* cand, int nc,
