@@ -102,7 +102,7 @@ typedef struct {
  * plane_tests are the algorithmic test counts of SURVEY §8(c).1 step 11 (closest-hit rays
  * test every primitive; shadow rays stop at the first occluder in index order when planes
  * precede spheres in the primitive list). last_render_ms: device time of the render kernel
- * (CUDA events on the library stream; 0 for rt_assemble_tiles). 88 bytes. */
+ * (CUDA events on the library stream; 0 for rt_assemble_tiles). 96 bytes. */
 typedef struct {
   uint64_t primary;
   uint64_t shadow;
@@ -118,6 +118,8 @@ typedef struct {
   int32_t variant;               /* RT_VARIANT_MEGAKERNEL or RT_VARIANT_WAVEFRONT actually used */
   double shade_ms;               /* wavefront: summed device time of the wf_shade launches (a4/a6:
                                     FP64 nearest hit, shading, shadow set-up, bounce) */
+  double isect_eye_ms;           /* wavefront: the part of isect_closest_ms spent on camera rays
+                                    (depth 0, shared-origin filter) */
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane
@@ -159,6 +161,11 @@ int rt_set_stream(void* cuda_stream);
  *   RT_VARIANT_AUTO (default): wavefront for scenes of >= 384 spheres, else megakernel. */
 enum { RT_VARIANT_AUTO = -1, RT_VARIANT_MEGAKERNEL = 0, RT_VARIANT_WAVEFRONT = 1 };
 int rt_set_variant(int32_t variant);
+
+/* Wavefront kernels: 1 (default) runs the shadow-ray scan + accumulation of depth d on a second
+ * stream, concurrently with the closest-hit scan of depth d+1; 0 runs every launch in order on
+ * the library stream (same results bit for bit; used to time each kernel alone). */
+int rt_set_concurrency(int32_t on);
 
 /* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
 int rt_set_seed(uint64_t seed);

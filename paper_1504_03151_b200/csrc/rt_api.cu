@@ -95,13 +95,17 @@ struct Context {
   DevBuf<int> dbg_hits, dbg_bounces;
   // wavefront variant
   int variant = RT_VARIANT_AUTO;
+#ifndef RT_WF_CONCURRENT
+#define RT_WF_CONCURRENT 1
+#endif
+  int concurrent = RT_WF_CONCURRENT;  // shadow scans || next closest scan on a side stream
   DevBuf<unsigned char> wf_mem;
   DevBuf<unsigned> wf_ctr;
   rt::WfBuffers wf{};
   std::vector<cudaEvent_t> ev_c, ev_s, ev_h;  // per-launch scan / shade timing (wavefront)
   cudaStream_t side_stream = nullptr;           // shadow scans || next closest scan
   std::vector<cudaEvent_t> ev_fork, ev_join;
-  int n_timed = 0, last_launches = 0, last_variant = 0;
+  int n_timed = 0, last_launches = 0, last_variant = 0, last_depth = 0;
   // camera (double basis)
   bool has_camera = false;
   double eye[3], f[3], r[3], u[3], h = 0;
@@ -263,10 +267,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     }
     rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
     tm.shade = c.ev_h.data();
-#ifndef RT_WF_CONCURRENT
-#define RT_WF_CONCURRENT 1
-#endif
-    if (RT_WF_CONCURRENT) {
+    if (c.concurrent) {
       tm.side = c.side_stream;
       tm.fork = c.ev_fork.data();
       tm.join = c.ev_join.data();
@@ -308,6 +309,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       if (copied) *copied = rows_done == p.H;
     }
     c.n_timed = tm.n;
+    c.last_depth = p.max_depth;
     c.last_launches = tm.launches;
     c.last_variant = RT_VARIANT_WAVEFRONT;
     return RT_OK;
@@ -343,7 +345,7 @@ int collect_stats(bool timed) {
   c.last.plane_tests = h[4];
   c.last.closest_sphere_tests = h[5];
   c.last.last_render_ms = ms;
-  double tc = 0.0, ts = 0.0, tsh = 0.0;
+  double tc = 0.0, ts = 0.0, tsh = 0.0, te = 0.0;
   if (timed) {
     for (int i = 0; i < c.n_timed; ++i) {
       float a = 0.f, b = 0.f, m = 0.f;
@@ -353,6 +355,7 @@ int collect_stats(bool timed) {
       tc += a;
       ts += b;
       tsh += m;
+      if (i % (c.last_depth + 1) == 0) te += a;  // depth 0: the camera-ray scan
     }
   }
 #ifdef RT_SIMD_PROBE
@@ -367,6 +370,7 @@ int collect_stats(bool timed) {
   c.last.isect_closest_ms = tc;
   c.last.isect_shadow_ms = ts;
   c.last.shade_ms = tsh;
+  c.last.isect_eye_ms = te;
   c.last.launches = timed ? (uint32_t)c.last_launches : 2u;
   c.last.variant = c.last_variant;
   return RT_OK;
@@ -492,6 +496,14 @@ int rt_render_passes_debug(int32_t width, int32_t height, int32_t max_depth, int
   if (!accum_rgb) return fail(RT_ERR_INVALID_ARG, "accum_rgb is NULL");
   if (!out_rgba || !hit_ids || !bounces) return fail(RT_ERR_INVALID_ARG, "out_rgba/hit_ids/bounces must not be NULL");
   return render_common(width, height, max_depth, n_passes, out_rgba, hit_ids, bounces, accum_rgb, pass_begin);
+}
+
+int rt_set_concurrency(int32_t on) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "concurrency must be 0 or 1");
+  g_ctx.concurrent = on;
+  return RT_OK;
 }
 
 int rt_set_seed(uint64_t seed) {

@@ -42,7 +42,7 @@ class RayStats(C.Structure):
                 ("sphere_tests", C.c_uint64), ("plane_tests", C.c_uint64), ("last_render_ms", C.c_double),
                 ("closest_sphere_tests", C.c_uint64), ("isect_closest_ms", C.c_double),
                 ("isect_shadow_ms", C.c_double), ("launches", C.c_uint32), ("variant", C.c_int32),
-                ("shade_ms", C.c_double)]
+                ("shade_ms", C.c_double), ("isect_eye_ms", C.c_double)]
 
 
 _lib = None
@@ -78,6 +78,7 @@ def lib() -> C.CDLL:
         "rt_render_debug": [i32, i32, i32, i32, vp, vp, vp],
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
         "rt_set_integrator": [i32, i32],
+        "rt_set_concurrency": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
         "rt_sum_shard_stats": [vp, i32],
         "rt_ipc_alloc": [i64, C.POINTER(vp), C.c_char_p],
@@ -162,6 +163,11 @@ VARIANTS = {"auto": -1, "megakernel": 0, "wavefront": 1}
 def set_variant(name: str):
     """Kernel organisation: "auto" (default), "wavefront" or "megakernel" (bit-identical results)."""
     _check("rt_set_variant", lib().rt_set_variant(VARIANTS[name]))
+
+
+def set_concurrency(on: bool):
+    """Wavefront: shadow scans concurrent with the next closest scan (default) or all in order."""
+    _check("rt_set_concurrency", lib().rt_set_concurrency(1 if on else 0))
 
 
 def set_stream(stream):

@@ -31,10 +31,10 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_struct_layouts_match_header():
-    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 88 B
+    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 96 B
     assert rt.PRIM_DTYPE.itemsize == 24 and rt.MAT_DTYPE.itemsize == 48
     assert rt.LIGHT_DTYPE.itemsize == 24 and rt.ENV_DTYPE.itemsize == 24
-    assert ctypes.sizeof(rt.RayStats) == 88
+    assert ctypes.sizeof(rt.RayStats) == 96
     hdr = open(os.path.join(ROOT, "include", "rt.h")).read()
     assert re.search(r"RT_TILE_W = 8", hdr) and re.search(r"RT_TILE_H = 4", hdr)
 
