@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
                                                 int* dbg_bounces) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
+  const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int path = Q.path[e];
     const d3 o = ld3(Q.ray, B.cap, (int)e, 0), dir = ld3(Q.ray, B.cap, (int)e, 3);
@@ -476,15 +477,18 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     bool cont = false;
     const int n_src = P.n_lights + P.n_emitters;  // point lights, then emitters (R#41)
     unsigned long long lmask = 0ull;              // sources 0..63 that send a shadow ray
+    // pixel index and global sample index of the path (RNG keys, R#42): 32-bit arithmetic on the
+    // chunk-local path id (path = local item * spp + s), computed only when a draw needs them
     unsigned long long pix = 0;
     unsigned sg = 0;
-    {
-      const long long g = g0 + path;
+    auto pixel_sample = [&]() {
+      const int wl = path / P.spp;
       int px = 0, py = 0;
-      item_pixel(P, (int)(g / P.spp), px, py);
+      item_pixel(P, w0 + wl, px, py);
       pix = (unsigned long long)py * P.W + px;
-      sg = (unsigned)(P.sample_base + (int)(g % P.spp));  // R#42
-    }
+      sg = (unsigned)(P.sample_base + (path - wl * P.spp));
+    };
+    if (P.n_emitters > 0 || P.integrator != 0) pixel_sample();
     unsigned nsh = 0;
     d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
     int mi = 0;
@@ -585,6 +589,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
           r0 *= r0;
           const double mm = 1.0 - c;
           const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
+          if (P.n_emitters == 0 && P.integrator == 0) pixel_sample();
           const double u = rng_u(P.seed, pix, (int)sg, depth);
           refl = u < F;
           if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
