@@ -81,7 +81,8 @@ struct Context {
   float cmax = 0.f, rmax = 0.f, cmax_abs = 0.f;
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
-  DevBuf<float4> pairs, sph_cr, stage, pairs_eye;
+  DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt;
+  int lt_lights = 0;  // point lights with light-origin shadow scans (0 = off)
   std::vector<float4> pairs_host, pairs_eye_host;  // expanded-form pairs; their camera-ray copy
   bool eye_ready = false;
   DevBuf<int> sph_prim, sph_mat, emit_sph;
@@ -173,7 +174,9 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
   p.seed = c.seed;
   p.integrator = c.integrator;
+  // light lists need every source in the 64-bit light mask (point lights + sampled emitters <= 64)
   p.n_emitters = c.area_lights ? c.n_emitters : 0;
+  p.lt_lights = (c.smem_scene && p.n_lights + p.n_emitters <= 64) ? c.lt_lights : 0;
   p.tiles_x = (W + rt::kTileW - 1) / rt::kTileW;
   p.n_tiles = p.tiles_x * ((H + rt::kTileH - 1) / rt::kTileH);
   return p;
@@ -221,7 +224,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
   rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p,
-                  c.eye_ready ? c.pairs_eye.p : nullptr};
+                  c.eye_ready ? c.pairs_eye.p : nullptr, c.lt_lights > 0 ? c.pairs_lt.p : nullptr};
   rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces, accum};
   // AUTO: the wavefront kernels for large scenes, and for the NEXT-1 / NEXT-2 modes, whose long
   // divergent paths (every diffuse hit continues; one lane per pixel walks all its passes) leave
@@ -700,6 +703,33 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   }
   c.has_scene = true;
   c.pairs_host = pairs;
+  // light-origin shadow scans (rt_wavefront.cuh wf_isect_lt): s1 = K + 2 c'.o'(P_l) per point
+  // light, FP64 rounded once, after a copy of the pairs; on while the tables fit 64 KB of smem
+#ifndef RT_LIGHT_ORIGIN
+#define RT_LIGHT_ORIGIN 1
+#endif
+  c.lt_lights = 0;
+  const size_t lt_bytes = (size_t)n_lights * npairs_pad * 8;
+  if (RT_LIGHT_ORIGIN && RT_FILTER_EXPANDED && n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
+      lt_bytes <= 65536 && in_smem) {
+    std::vector<float4> lt(2 * (size_t)npairs_pad + lt_bytes / 16 + 1);
+    std::memcpy(lt.data(), pairs.data(), sizeof(float4) * pairs.size());
+    float2* s1 = reinterpret_cast<float2*>(lt.data() + 2 * (size_t)npairs_pad);
+    for (int l = 0; l < n_lights; ++l) {
+      const double ox = (double)lights[l].position[0] - centre[0], oy = (double)lights[l].position[1] - centre[1],
+                   oz = (double)lights[l].position[2] - centre[2];
+      for (int q = 0; q < npairs_pad; ++q) {
+        const float4 a = pairs[2 * q], b = pairs[2 * q + 1];
+        s1[(size_t)l * npairs_pad + q] =
+            make_float2((float)((double)b.z + 2.0 * ((double)a.x * ox + (double)a.z * oy + (double)b.x * oz)),
+                        (float)((double)b.w + 2.0 * ((double)a.y * ox + (double)a.w * oy + (double)b.y * oz)));
+      }
+    }
+    CU(c.pairs_lt.reserve(lt.size()), "cudaMalloc(light pairs)");
+    CU(cudaMemcpyAsync(c.pairs_lt.p, lt.data(), sizeof(float4) * lt.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+    CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
+    c.lt_lights = n_lights;
+  }
   return build_eye_pairs();
 }
 

@@ -68,6 +68,7 @@ struct DevParams {
   unsigned long long seed;
   // SURVEY §8(f) NEXT-1 / NEXT-2 (all zero = the §8(a) hot path; R#40-R#43)
   int integrator;     // 0 Whitted, 1 global (cosine-weighted diffuse bounce)
+  int lt_lights;      // point lights whose shadow rays are scanned from the light (0 = off)
   int n_emitters;     // emissive spheres sampled as area lights (0 = area lights off)
   int jitter;         // 1: random sub-pixel offsets from RNG streams 1/2 (progressive passes)
   int pad_;
@@ -87,6 +88,9 @@ struct DevScene {
   const DevLight* lights;
   const int* emit_sph;     // [n_emitters] sphere index of emitter e (prim order), or null
   const float4* pairs_eye; // pair layout with s1 = K + 2 c'.o'(eye) in place of K (camera rays)
+  // light-origin shadow scans: the pair layout followed by s1 = K + 2 c'.o'(P_l) per point light,
+  // float2 per sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy stages both)
+  const float4* pairs_lt;
 };
 
 struct DevOutputs {
@@ -128,16 +132,25 @@ struct WfBuffers {
   int* scand;      // [scap * kCandMax]
   int* sn;         // [scap]
   int* srob;       // [scap] robust occluder: sphere index, -1 none, -2-j plane j
+  // when lt_lights > 0: the entries of point light l (< lt_lights) listed in slt[l * cap ..],
+  // every other entry (emitters) in sother; the entries themselves stay path-major
+  int* slt;        // [lt_lights * cap]
+  unsigned long long* lmask;  // [cap] per entry of Q[d]: sources (bit l) with a shadow ray
+  int* sother;     // [scap]
   unsigned* ctr;   // counters, see wf_ctr_*
   int cap, scap;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
-__host__ __device__ constexpr int wf_ctr_q(int d) { return 4 * d; }
-__host__ __device__ constexpr int wf_ctr_s(int d) { return 4 * d + 1; }
-__host__ __device__ constexpr int wf_ctr_wc(int d) { return 4 * d + 2; }
-__host__ __device__ constexpr int wf_ctr_ws(int d) { return 4 * d + 3; }
-constexpr int kWfCtrPerDepth = 4;
+constexpr int kMaxLtLights = 32;  // point lights scanned from the light (RT_MAX_LIGHTS)
+constexpr int kWfCtrPerDepth = 8 + kMaxLtLights;
+__host__ __device__ constexpr int wf_ctr_q(int d) { return kWfCtrPerDepth * d; }       // closest queue
+__host__ __device__ constexpr int wf_ctr_s(int d) { return kWfCtrPerDepth * d + 1; }   // shadow entries
+__host__ __device__ constexpr int wf_ctr_wc(int d) { return kWfCtrPerDepth * d + 2; }  // work heads
+__host__ __device__ constexpr int wf_ctr_ws(int d) { return kWfCtrPerDepth * d + 3; }
+__host__ __device__ constexpr int wf_ctr_so(int d) { return kWfCtrPerDepth * d + 4; }  // "other" list
+__host__ __device__ constexpr int wf_ctr_wlt(int d) { return kWfCtrPerDepth * d + 5; } // light-scan chunks
+__host__ __device__ constexpr int wf_ctr_lt(int d, int l) { return kWfCtrPerDepth * d + 8 + l; }  // light l list
 constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
 // launchers (rt_kernels.cu)

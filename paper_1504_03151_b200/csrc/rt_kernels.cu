@@ -588,8 +588,8 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 // ---- wavefront launcher ---------------------------------------------------------------------
 size_t wf_bytes(int cap, int scap) {
   const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
-  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + kCandMax * 4) +
-         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4) + 32 * 256;
+  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + 8 + kCandMax * 4) +
+         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4 + 4 + 4) + 40 * 256;
 }
 
 void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
@@ -619,6 +619,9 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * scap));
   B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.slt = reinterpret_cast<int*>(take(4 * (size_t)scap));  // lt_lights * cap <= scap
+  B.lmask = reinterpret_cast<unsigned long long*>(take(8 * (size_t)cap));
+  B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.ctr = ctr;
 }
 
@@ -643,6 +646,20 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
 #define RT_EYE_TWO_RAYS 1
 #endif
   if (kEyeOk && sc.pairs_eye != nullptr) kc0 = RT_EYE_TWO_RAYS ? wf_isect_eye2<kSrc> : wf_isect<kSrc, false, kEyeOk>;
+  // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
+  IsectFn klt = nullptr;
+  size_t smem_lt = 0;
+  int grid_lt = 0;
+  if constexpr (kSrc == SRC_SMEM && RT_FILTER_EXPANDED) {
+    if (p.lt_lights > 0) {
+      klt = wf_isect_lt<kSrc>;
+      smem_lt = (size_t)p.n_pairs_pad * 32u + (size_t)p.lt_lights * p.n_pairs_pad * 8u;
+      if ((e = cudaFuncSetAttribute(klt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
+      int occ = 0;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, klt, 256, smem_lt)) != cudaSuccess) return e;
+      grid_lt = num_sms * (occ > 0 ? occ : 1);
+    }
+  }
   for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
@@ -688,6 +705,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
       if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti + 1], st);
+      if (klt) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (tm.side) {
         cudaEventRecord(tm.fork[d], st);
@@ -695,7 +713,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         ss = tm.side;
       }
       if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
-      wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+      if (klt) klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);  // point lights, from the light
+      wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);    // every other shadow ray
       if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
@@ -703,7 +722,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaEventRecord(tm.join[d], tm.side);
         cudaStreamWaitEvent(st, tm.join[d], 0);
       }
-      tm.launches += 4;
+      tm.launches += klt ? 6 : 4;
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

@@ -48,6 +48,16 @@ __device__ __forceinline__ unsigned warp_reserve(unsigned cnt, unsigned* counter
   return __shfl_sync(act, base, leader) + prefix;
 }
 
+// one slot per predicated lane, in lane order, one atomicAdd per warp
+__device__ __forceinline__ unsigned warp_reserve1(bool take, unsigned* counter) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, take);
+  const int leader = __ffs(act) - 1;
+  unsigned base = 0;
+  if ((int)(threadIdx.x & 31) == leader && m) base = atomicAdd(counter, (unsigned)__popc(m));
+  return __shfl_sync(act, base, leader) + (unsigned)__popc(m & lanemask_lt());
+}
+
 __device__ __forceinline__ void warp_stat(unsigned long long* stats, int k, unsigned long long v) {
   const unsigned act = __activemask();
 #pragma unroll
@@ -175,7 +185,9 @@ __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   static_assert(!(kEye && kShadow), "shadow rays start at shading points");
   __shared__ uint64_t s_mbar;
-  const unsigned n = kShadow ? B.ctr[wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
+  const bool listed = kShadow && P.lt_lights > 0;
+  const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
   // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
   // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
   if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
@@ -192,8 +204,10 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     if (lane == 0) e0 = atomicAdd(work, 32u);
     e0 = __shfl_sync(kFull, e0, 0);
     if (e0 >= n) break;
-    const unsigned e = e0 + lane;
+    unsigned e = e0 + lane;
     bool act = e < n;
+    const bool mine = act;
+    if (listed && act) e = (unsigned)B.sother[e];
     d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
     double tl = 0.0;
     int rob = -1, skip = -1, skip2 = -1;  // skip2: the emitter a shadow ray aims at (R#41)
@@ -287,7 +301,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         if (!__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
       }
     }
-    if (e < n) {
+    if (mine) {
       cn[e] = nc;
       if constexpr (kShadow) B.srob[e] = rob;
     }
@@ -412,6 +426,179 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
     }
     if (ea < n) B.cn[ea] = Ra.nc;
     if (eb < n) B.cn[eb] = Rb.nc;
+  }
+}
+
+// ---- a5 for point lights: the shadow scan from the light -------------------------------------
+// The segment [p + EPS_T n, P_l) is the same line whichever end it is traced from, and the scan
+// only filters (FP64 decides on the original ray in wf_accumulate). Traced from the light, every
+// shadow ray of light l shares the origin P_l: s1 = K + 2 c'.o'(P_l) comes precomputed per light
+// (S.pairs_lt), so a sphere costs tc' (3 FMA) + v = tc'^2 + s1 (1 FMA) instead of 7, and a thread
+// carries two rays of the same light (one shared-memory read serves both). Work comes in chunks of
+// 64 entries of one light's list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
+// t = t_l - tc' -/+ q on the original one; the bounds add the error of t_l and of the reversal.
+#ifndef RT_LT_PAIRS_PER_BATCH
+#define RT_LT_PAIRS_PER_BATCH 8
+#endif
+constexpr int kLtPB = RT_LT_PAIRS_PER_BATCH;
+static_assert(kPairsPerBatch % kLtPB == 0, "n_pairs_pad is padded to kPairsPerBatch");
+
+struct LtRay {
+  RayFilterT<true> F;  // filter of the reversed ray (origin P_l, direction -d)
+  float tl_f, tlerr;
+  int nc, rob, skip;
+  bool act;
+};
+
+__device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, const WfBuffers& B, unsigned j, bool valid,
+                                         int l, LtRay& R) {
+  d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+  double tl = 1.0;
+  R.act = valid;
+  R.rob = -1;
+  R.skip = -1;
+  R.nc = 0;
+  if (valid) {
+    o = ld3(B.sray, B.scap, (int)j, 0);
+    dir = ld3(B.sray, B.scap, (int)j, 3);
+    tl = B.sray[6 * (size_t)B.scap + j];
+    R.skip = B.sskip[j];
+    for (int q = 0; q < P.n_planes; ++q) {  // planes first, exactly (FP64), on the original ray
+      const DevPlane pl = c_planes[q];
+      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+      if (fabs(den) >= 1e-12) {
+        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+        if (t >= kEps && t < tl) { R.rob = -2 - q; R.act = false; break; }
+      }
+    }
+  }
+  const DevLight lt = S.lights[l];
+  R.F.init(mk(lt.px, lt.py, lt.pz), mk(-dir.x, -dir.y, -dir.z), P);
+  R.tl_f = (float)tl;
+  R.tlerr = 4.0e-7f * R.tl_f + 1.0e-6f * R.F.eta;  // t_l to float, P_l vs o + t_l d, the subtraction
+}
+
+template <int kSrc>
+__device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ s1p,
+                                              unsigned m, int kbase, LtRay& R, int* cand_row) {
+  const float eps_f = (float)kEps;
+  while (m != 0u) {
+    const int i = __ffs(m) - 1;
+    m &= m - 1u;
+    const int k = kbase + i;
+    if (k >= P.n_spheres) break;
+    if (k == R.skip) continue;
+    const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
+    const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
+    const float2 s1v = s1p[k >> 1];
+    const bool h = k & 1;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, s1 = h ? s1v.y : s1v.x;
+    const float tc = fmaf(cx, R.F.dx, fmaf(cy, R.F.dy, fmaf(cz, R.F.dz, R.F.b1)));  // along -d from P_l
+    const float dd = fmaf(tc, tc, s1) - (R.F.cut - R.F.neg_slack);
+    const float qh = sqrtf(fmaxf(dd - R.F.neg_slack, 0.f));
+    const float ql = sqrtf(fmaxf(dd + R.F.neg_slack, 0.f));
+    const bool sure = dd + R.F.neg_slack > 0.f;
+    const float err = R.F.eta + R.tlerr;
+    // original-ray roots: t0 = t_l - tc - q, t1 = t_l - tc + q
+    const float t0lo = R.tl_f - (tc + qh) - err, t0hi = R.tl_f - (tc + ql) + err;
+    const float t1lo = R.tl_f - (tc - ql) - err, t1hi = R.tl_f - (tc - qh) + err;
+    if (t1hi < eps_f) continue;                        // chord certainly behind the shading point
+    if (t0lo >= R.tl_f * 1.000001f) continue;          // certainly beyond the light
+    if (sure) {
+      const float tlo = R.tl_f * 0.999999f;
+      if ((t0lo >= eps_f && t0hi < tlo) || (t0hi < eps_f && t1lo >= eps_f && t1hi < tlo)) {
+        R.rob = k;  // certain occluder (earlier ambiguous candidates are decided in FP64 later)
+        R.act = false;
+        return;
+      }
+    }
+    if (R.nc < kCandMax) cand_row[R.nc] = k;
+    ++R.nc;
+  }
+}
+
+template <int kSrc>
+__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
+  __shared__ uint64_t s_mbar;
+  __shared__ unsigned s_chunk_end[kMaxLtLights];  // prefix sums of the lights' 64-entry chunk counts
+  if (threadIdx.x == 0) {
+    unsigned acc = 0;
+    for (int l = 0; l < P.lt_lights; ++l) {
+      acc += (B.ctr[wf_ctr_lt(d, l)] + 63u) / 64u;
+      s_chunk_end[l] = acc;
+    }
+  }
+  __syncthreads();
+  const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
+  if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
+  stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
+  const float4* gp = S.pairs_lt;
+  const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(B.ctr + wf_ctr_wlt(d), 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n_chunks) break;
+    int l = 0;
+    while (s_chunk_end[l] <= k) ++l;
+    const unsigned c = k - (l > 0 ? s_chunk_end[l - 1] : 0u);
+    const unsigned cnt = B.ctr[wf_ctr_lt(d, l)];
+    const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
+    const bool va_ = oa < cnt, vb_ = ob < cnt;
+    const unsigned ja = va_ ? (unsigned)B.slt[(size_t)l * B.cap + oa] : 0u;
+    const unsigned jb = vb_ ? (unsigned)B.slt[(size_t)l * B.cap + ob] : 0u;
+    LtRay Ra, Rb;
+    lt_setup(P, S, B, ja, va_, l, Ra);
+    lt_setup(P, S, B, jb, vb_, l, Rb);
+    const float2* s1p = s1_all + (size_t)l * P.n_pairs_pad;
+    const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
+    const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+    const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
+    const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
+    const float cut = Ra.F.cut;  // depends on the origin P_l only: the same for both rays
+    for (int base = 0; base < P.n_pairs_pad; base += kLtPB) {
+      float2 va[kLtPB], vb[kLtPB];
+#pragma unroll
+      for (int i = 0; i < kLtPB; ++i) {
+        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+        const float2 S1 = s1p[base + i];
+        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w), CZ = make_float2(b.x, b.y);
+        const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
+        const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
+        va[i] = __ffma2_rn(ta, ta, S1);
+        vb[i] = __ffma2_rn(tb, tb, S1);
+      }
+      float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+#pragma unroll
+      for (int i = 1; i < kLtPB; ++i) {
+        ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
+        mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+      }
+      const bool ca = Ra.act && ma >= cut, cb = Rb.act && mb >= cut;
+      if (__any_sync(kFull, ca || cb)) {
+        if (ca) {
+          unsigned m = 0u;
+#pragma unroll
+          for (int i = 0; i < kLtPB; ++i)
+            m |= ((va[i].x >= cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
+          lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Ra, B.scand + (size_t)ja * kCandMax);
+        }
+        if (cb) {
+          unsigned m = 0u;
+#pragma unroll
+          for (int i = 0; i < kLtPB; ++i)
+            m |= ((vb[i].x >= cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
+          lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Rb, B.scand + (size_t)jb * kCandMax);
+        }
+      }
+      if (!__any_sync(kFull, Ra.act || Rb.act)) break;  // Alg. 1 `break`, warp-wide
+    }
+    if (va_) { B.sn[ja] = Ra.nc; B.srob[ja] = Ra.rob; }
+    if (vb_) { B.sn[jb] = Rb.nc; B.srob[jb] = Rb.rob; }
   }
 }
 
@@ -556,6 +743,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     B.shoff[e] = (int)off;
+    if (P.lt_lights > 0) B.lmask[e] = lmask;  // wf_bin lists the entries per light
     // part 3: stack-free continuation
     d3 dn = mk(0, 0, 0);
     bool mi_kind_diffuse_global = false;
@@ -625,6 +813,64 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
     warp_stat(stats, 5, (unsigned long long)P.n_spheres);
+  }
+}
+
+// ---- lists of the shadow entries per point light (light-origin scans) and the rest ----------
+// One global atomicAdd per light per CTA iteration (256 entries): warps count with ballots, the
+// CTA reserves, warps place their lanes in lane order.
+__global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
+  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // per warp: entries per light (+ the rest)
+  __shared__ unsigned s_base[kMaxLtLights + 1];
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  const int L = P.lt_lights;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + threadIdx.x;
+    const bool in = e < n;
+    const unsigned long long lmask = in ? B.lmask[e] : 0ull;
+    const unsigned off = in ? (unsigned)B.shoff[e] : 0u;
+    const unsigned long long rest = lmask >> L;
+    const unsigned nrest = (unsigned)__popcll(rest);
+    for (int l = 0; l < L; ++l) {
+      const unsigned m = __ballot_sync(kFull, (lmask >> l) & 1ull);
+      if (lane == 0) s_cnt[warp][l] = (unsigned)__popc(m);
+    }
+    unsigned rsum = nrest;  // the rest: a variable count per lane (warp inclusive scan)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(kFull, rsum, o);
+      if (lane >= o) rsum += v;
+    }
+    if (lane == 31) s_cnt[warp][L] = rsum;
+    __syncthreads();
+    if (threadIdx.x <= (unsigned)L) {  // CTA totals -> one atomic per light, then warp offsets
+      const int l = threadIdx.x;
+      unsigned tot = 0;
+      for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
+      unsigned base = tot ? atomicAdd(B.ctr + (l < L ? wf_ctr_lt(d, l) : wf_ctr_so(d)), tot) : 0u;
+      for (int w = 0; w < 8; ++w) {
+        const unsigned c = s_cnt[w][l];
+        s_cnt[w][l] = base;
+        base += c;
+      }
+    }
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+      const bool has = (lmask >> l) & 1ull;
+      const unsigned m = __ballot_sync(kFull, has);
+      if (has) {
+        const unsigned slot = s_cnt[warp][l] + (unsigned)__popc(m & lt);
+        B.slt[(size_t)l * B.cap + slot] = (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
+      }
+    }
+    if (nrest) {
+      unsigned ob = s_cnt[warp][L] + rsum - nrest;
+      unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
+      for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
+    }
+    __syncthreads();  // s_cnt is rewritten by the next iteration
   }
 }
 
