@@ -714,7 +714,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       }
       if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
       if (klt) klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);  // point lights, from the light
-      wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);    // every other shadow ray
+      if (!klt || p.n_emitters > 0)                                   // every other shadow ray
+        wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
       if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
@@ -722,7 +723,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaEventRecord(tm.join[d], tm.side);
         cudaStreamWaitEvent(st, tm.join[d], 0);
       }
-      tm.launches += klt ? 6 : 4;
+      tm.launches += klt ? (p.n_emitters > 0 ? 6 : 5) : 4;
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
