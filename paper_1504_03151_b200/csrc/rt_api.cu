@@ -100,9 +100,17 @@ struct Context {
 #define RT_WF_CONCURRENT 1
 #endif
   int concurrent = RT_WF_CONCURRENT;  // shadow scans || next closest scan on a side stream
-  DevBuf<unsigned char> wf_mem;
-  DevBuf<unsigned> wf_ctr;
-  rt::WfBuffers wf{};
+  DevBuf<unsigned char> wf_mem, wf_mem2;
+  DevBuf<unsigned> wf_ctr, wf_ctr2;
+  rt::WfBuffers wf{}, wf2{};
+  // chunk pipelining (odd chunks on a second buffer set and stream pair)
+#ifndef RT_WF_PIPELINE
+#define RT_WF_PIPELINE 1
+#endif
+  int pipeline = RT_WF_PIPELINE;
+  cudaStream_t main2 = nullptr, side2 = nullptr;
+  std::vector<cudaEvent_t> ev_fork2, ev_join2;
+  cudaEvent_t ev_start2 = nullptr, ev_done2 = nullptr;
   std::vector<cudaEvent_t> ev_c, ev_s, ev_h;  // per-launch scan / shade timing (wavefront)
   cudaStream_t side_stream = nullptr;           // shadow scans || next closest scan
   std::vector<cudaEvent_t> ev_fork, ev_join;
@@ -250,7 +258,24 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap)), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
     rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
-    const int pairs = rt::wf_timing_pairs(p, cap);
+    const bool pipe = c.pipeline != 0 && c.concurrent != 0;
+    if (pipe) {
+      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap)), "cudaMalloc(wavefront, second chunk slot)");
+      CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
+      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, c.wf_ctr2.p);
+      if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
+      if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");
+      if (!c.ev_start2) CU(cudaEventCreateWithFlags(&c.ev_start2, cudaEventDisableTiming), "cudaEventCreate");
+      if (!c.ev_done2) CU(cudaEventCreateWithFlags(&c.ev_done2, cudaEventDisableTiming), "cudaEventCreate");
+      while ((int)c.ev_fork2.size() < p.max_depth + 1) {
+        cudaEvent_t f, j;
+        CU(cudaEventCreateWithFlags(&f, cudaEventDisableTiming), "cudaEventCreate");
+        CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "cudaEventCreate");
+        c.ev_fork2.push_back(f);
+        c.ev_join2.push_back(j);
+      }
+    }
+    const int pairs = rt::wf_timing_pairs(p, cap, pipe);
     while ((int)c.ev_c.size() < 2 * pairs) {
       cudaEvent_t a, b, h;
       CU(cudaEventCreate(&a), "cudaEventCreate");
@@ -275,9 +300,19 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       tm.fork = c.ev_fork.data();
       tm.join = c.ev_join.data();
     }
+    if (pipe) {
+      tm.B2 = &c.wf2;
+      tm.main2 = c.main2;
+      tm.side2 = c.side2;
+      tm.fork2 = c.ev_fork2.data();
+      tm.join2 = c.ev_join2.data();
+      tm.start_ev = c.ev_start2;
+      tm.done2_ev = c.ev_done2;
+    }
     const bool overlap = host_out != nullptr && p.mode == 0;
     if (overlap) {
-      const int max_chunks = (p.n_items + items - 1) / items;
+      const int ipc = rt::wf_items_per_chunk(p, cap, pipe);
+      const int max_chunks = (p.n_items + ipc - 1) / ipc;
       if (!c.copy_stream) CU(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
       while ((int)c.ev_chunk.size() < max_chunks) {
         cudaEvent_t ev;

@@ -173,6 +173,13 @@ struct WfTiming {
   cudaStream_t side = nullptr;
   cudaEvent_t* fork = nullptr;   // [max_depth + 1]
   cudaEvent_t* join = nullptr;   // [max_depth + 1]
+  // chunk pipelining: odd chunks run on a second buffer set and stream pair, so one chunk's
+  // sparse deep depths overlap the next chunk's dense depth 0 (null = one chunk at a time)
+  WfBuffers* B2 = nullptr;
+  cudaStream_t main2 = nullptr, side2 = nullptr;
+  cudaEvent_t* fork2 = nullptr;
+  cudaEvent_t* join2 = nullptr;
+  cudaEvent_t start_ev = nullptr, done2_ev = nullptr;
   // optional: an event recorded after each chunk's resolve, and the work items resolved so far,
   // so the host can copy finished framebuffer rows while later chunks render
   cudaEvent_t* chunk_done = nullptr;
@@ -183,7 +190,8 @@ struct WfTiming {
 // scene source of the wavefront intersection kernels: 0 global, 1 shared memory, 2 constant bank
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st);
-int wf_timing_pairs(const DevParams& p, int cap_paths);
+int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined);
+int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigned long long* stats, cudaStream_t st);

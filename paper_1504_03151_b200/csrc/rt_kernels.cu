@@ -625,15 +625,24 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.ctr = ctr;
 }
 
-int wf_timing_pairs(const DevParams& p, int cap_paths) {
-  const int items_per_chunk = cap_paths / p.spp;
+// work items (pixels) per chunk: as many as the buffers hold; a pipelined render of a frame that
+// would fit one chunk is cut in two, so the two chunks can overlap
+int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined) {
+  int items = cap_paths / p.spp;
+  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18)) items = (p.n_items + 1) / 2;
+  return items > 0 ? items : 1;
+}
+
+int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined) {
+  const int items_per_chunk = wf_items_per_chunk(p, cap_paths, pipelined);
   const int chunks = (p.n_items + items_per_chunk - 1) / items_per_chunk;
   return chunks * (p.max_depth + 1);
 }
 
 template <int kSrc>
 static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
-                          WfBuffers& B, WfTiming& tm, cudaStream_t st) {
+                          WfBuffers& B0, WfTiming& tm, cudaStream_t st0) {
+  const cudaStream_t st = st0;  // setup launches (debug fill) go on the caller's stream
   const bool dbg = o.dbg_hits != nullptr;
   const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
@@ -667,8 +676,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSrc, false>, 256, smem)) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
-  const int grid_l = num_sms * 8;
-  const int items_per_chunk = B.cap / p.spp;
+#ifndef RT_LOGIC_GRID_PER_SM
+#define RT_LOGIC_GRID_PER_SM 8
+#endif
+  const int grid_l = num_sms * RT_LOGIC_GRID_PER_SM;  // logic kernels: grid-stride loops
+  const bool pipe = tm.B2 != nullptr;
+  const int items_per_chunk = wf_items_per_chunk(p, B0.cap, pipe);
   tm.n = 0;
   tm.launches = 0;
   tm.n_chunks = 0;
@@ -677,7 +690,18 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     fill_int<<<num_sms * 8, 256, 0, st>>>(o.dbg_hits, nh, -2);
     ++tm.launches;
   }
-  for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk) {
+  if (pipe) {  // the second slot's streams start after everything issued on st so far
+    cudaEventRecord(tm.start_ev, st);
+    cudaStreamWaitEvent(tm.main2, tm.start_ev, 0);
+  }
+  int chunk = 0;
+  for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk, ++chunk) {
+    const bool odd = pipe && (chunk & 1);
+    WfBuffers& B = odd ? *tm.B2 : B0;
+    const cudaStream_t st = odd ? tm.main2 : st0;
+    const cudaStream_t side = odd ? tm.side2 : tm.side;
+    cudaEvent_t* fork = odd ? tm.fork2 : tm.fork;
+    cudaEvent_t* join = odd ? tm.join2 : tm.join;
     const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
     const int npaths = nw * p.spp;
     const long long g0 = (long long)w0 * p.spp;
@@ -707,10 +731,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti + 1], st);
       if (klt) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
-      if (tm.side) {
-        cudaEventRecord(tm.fork[d], st);
-        cudaStreamWaitEvent(tm.side, tm.fork[d], 0);
-        ss = tm.side;
+      if (side) {
+        cudaEventRecord(fork[d], st);
+        cudaStreamWaitEvent(side, fork[d], 0);
+        ss = side;
       }
       if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
       if (klt) klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);  // point lights, from the light
@@ -719,9 +743,9 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
-      if (tm.side) {
-        cudaEventRecord(tm.join[d], tm.side);
-        cudaStreamWaitEvent(st, tm.join[d], 0);
+      if (side) {
+        cudaEventRecord(join[d], side);
+        cudaStreamWaitEvent(st, join[d], 0);
       }
       tm.launches += klt ? (p.n_emitters > 0 ? 6 : 5) : 4;
     }
@@ -734,6 +758,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       tm.chunk_items[tm.n_chunks] = w0 + nw;
       ++tm.n_chunks;
     }
+  }
+  if (pipe) {  // the caller's stream resumes after the second slot's last chunk
+    cudaEventRecord(tm.done2_ev, tm.main2);
+    cudaStreamWaitEvent(st0, tm.done2_ev, 0);
   }
   return cudaGetLastError();
 }
