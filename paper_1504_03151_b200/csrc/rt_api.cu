@@ -255,14 +255,14 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
     const int scap = cap * (n_src > 0 ? n_src : 1);
     // (re)carve for this frame's cap
-    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap)), "cudaMalloc(wavefront)");
+    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, c.wf_ctr.p);
+    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, 4 * c.num_sms, c.wf_ctr.p);
     const bool pipe = c.pipeline != 0 && c.concurrent != 0;
     if (pipe) {
-      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap)), "cudaMalloc(wavefront, second chunk slot)");
+      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
       CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, c.wf_ctr2.p);
+      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, 4 * c.num_sms, c.wf_ctr2.p);
       if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.ev_start2) CU(cudaEventCreateWithFlags(&c.ev_start2, cudaEventDisableTiming), "cudaEventCreate");
@@ -403,6 +403,21 @@ int collect_stats(bool timed) {
     fprintf(stderr, "SIMD probe: closest batches %u lanes %u (%.3f) | shadow batches %u lanes %u (%.3f)\n", pr[0], pr[1],
             pr[1] / (32.0 * pr[0] + 1e-9), pr[2], pr[3], pr[3] / (32.0 * pr[2] + 1e-9));
     cudaMemset(c.wf_ctr.p + 70 * rt::kWfCtrPerDepth, 0, sizeof pr);
+  }
+#endif
+#ifdef RT_OVF_PROBE
+  if (c.wf_ctr.p) {
+    unsigned pr[4 * 8] = {}, p2[4 * 8] = {};
+    cudaMemcpy(pr, c.wf_ctr.p + 72 * rt::kWfCtrPerDepth, sizeof pr, cudaMemcpyDeviceToHost);
+    cudaMemset(c.wf_ctr.p + 72 * rt::kWfCtrPerDepth, 0, sizeof pr);
+    if (c.wf_ctr2.p) {
+      cudaMemcpy(p2, c.wf_ctr2.p + 72 * rt::kWfCtrPerDepth, sizeof p2, cudaMemcpyDeviceToHost);
+      cudaMemset(c.wf_ctr2.p + 72 * rt::kWfCtrPerDepth, 0, sizeof p2);
+    }
+    for (int d = 0; d < 8; ++d)
+      fprintf(stderr, "OVF probe d=%d: closest overflows %u (max nc %u) | shadow overflows %u (max nc %u)\n", d,
+              pr[4 * d] + p2[4 * d], pr[4 * d + 2] > p2[4 * d + 2] ? pr[4 * d + 2] : p2[4 * d + 2], pr[4 * d + 1] + p2[4 * d + 1],
+              pr[4 * d + 3] > p2[4 * d + 3] ? pr[4 * d + 3] : p2[4 * d + 3]);
   }
 #endif
   c.last.isect_closest_ms = tc;

@@ -139,6 +139,13 @@ struct WfBuffers {
   int* sother;     // [scap]
   unsigned* ctr;   // counters, see wf_ctr_*
   int cap, scap;
+  // split scans (short queues): per-part candidate lists of the warps of up to xctas CTAs, one
+  // row of kCandMax per ray; closest scans (32 rays per warp) and shadow scans (64 rays per
+  // warp) have their own rows because they run concurrently on two streams
+  int* xcand_c;    // [xctas * 8 * 32 * kCandMax]
+  float* xlo_c;    // [xctas * 8 * 32 * kCandMax] lower bound of each closest candidate's root
+  int* xcand_s;    // [xctas * 8 * 64 * kCandMax]
+  int xctas;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
@@ -158,8 +165,8 @@ cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float
                                cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
-size_t wf_bytes(int cap, int scap);
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr);
+size_t wf_bytes(int cap, int scap, int xctas);
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* ctr);
 // per-launch CUDA events around the intersection kernels (pairs: [2i] before, [2i+1] after)
 struct WfTiming {
   cudaEvent_t* closest;

@@ -586,13 +586,14 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 }
 
 // ---- wavefront launcher ---------------------------------------------------------------------
-size_t wf_bytes(int cap, int scap) {
+size_t wf_bytes(int cap, int scap, int xctas) {
   const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
   return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + 8 + kCandMax * 4) +
-         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4 + 4 + 4) + 40 * 256;
+         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4 + 4 + 4) +
+         (size_t)xctas * 8 * (32 * 2 + 64) * kCandMax * 4 + 40 * 256;
 }
 
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* ctr) {
   char* p = static_cast<char*>(base);
   auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
   B.cap = cap;
@@ -622,6 +623,10 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, unsigned* ctr) {
   B.slt = reinterpret_cast<int*>(take(4 * (size_t)scap));  // lt_lights * cap <= scap
   B.lmask = reinterpret_cast<unsigned long long*>(take(8 * (size_t)cap));
   B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.xctas = xctas;
+  B.xcand_c = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
+  B.xlo_c = reinterpret_cast<float*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
+  B.xcand_s = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 64 * kCandMax));
   B.ctr = ctr;
 }
 
@@ -651,25 +656,34 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   constexpr bool kEyeOk = kSrc != SRC_CONST && RT_FILTER_EXPANDED;
   using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
   IsectFn kc0 = wf_isect<kSrc, false>;
+  // every scan kernel is paired with its split variant (short queues, wf_isect_split): both are
+  // launched with the same grid, read the same queue length and exactly one of them does the work
+  IsectFn kc0s = wf_isect_split<kSrc, false>;
 #ifndef RT_EYE_TWO_RAYS
 #define RT_EYE_TWO_RAYS 1
 #endif
-  if (kEyeOk && sc.pairs_eye != nullptr) kc0 = RT_EYE_TWO_RAYS ? wf_isect_eye2<kSrc> : wf_isect<kSrc, false, kEyeOk>;
+  if (kEyeOk && sc.pairs_eye != nullptr) {
+    kc0 = RT_EYE_TWO_RAYS ? wf_isect_eye2<kSrc> : wf_isect<kSrc, false, kEyeOk>;
+    kc0s = RT_EYE_TWO_RAYS ? nullptr : wf_isect_split<kSrc, false, kEyeOk>;  // camera queues are long
+  }
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
-  IsectFn klt = nullptr;
+  IsectFn klt = nullptr, klts = nullptr;
   size_t smem_lt = 0;
   int grid_lt = 0;
   if constexpr (kSrc == SRC_SMEM && RT_FILTER_EXPANDED) {
     if (p.lt_lights > 0) {
       klt = wf_isect_lt<kSrc>;
+      klts = wf_isect_lt_split<kSrc>;
       smem_lt = (size_t)p.n_pairs_pad * 32u + (size_t)p.lt_lights * p.n_pairs_pad * 8u;
       if ((e = cudaFuncSetAttribute(klt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
+      if ((e = cudaFuncSetAttribute(klts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
       int occ = 0;
       if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, klt, 256, smem_lt)) != cudaSuccess) return e;
       grid_lt = num_sms * (occ > 0 ? occ : 1);
     }
   }
-  for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0}) {
+  for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0, (IsectFn)wf_isect_split<kSrc, false>,
+                  (IsectFn)wf_isect_split<kSrc, true>, (IsectFn)wf_isect_split<kSrc, false, kEyeOk>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
@@ -717,8 +731,15 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + dd;
       const bool rec = ti < tm.cap;
       if (rec) cudaEventRecord(tm.closest[2 * ti], st);
-      if (dd == 0) kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-      else wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+      if (dd == 0) {
+        kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        if (kc0s) kc0s<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        tm.launches += kc0s ? 2 : 1;
+      } else {
+        wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        wf_isect_split<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        tm.launches += 2;
+      }
       if (rec) cudaEventRecord(tm.closest[2 * ti + 1], st);
     };
     closest_scan(0);
@@ -737,9 +758,14 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         ss = side;
       }
       if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
-      if (klt) klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);  // point lights, from the light
-      if (!klt || p.n_emitters > 0)                                   // every other shadow ray
+      if (klt) {  // point lights, from the light
+        klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
+        klts<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
+      }
+      if (!klt || p.n_emitters > 0) {  // every other shadow ray
         wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+        wf_isect_split<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+      }
       if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
@@ -747,7 +773,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaEventRecord(join[d], side);
         cudaStreamWaitEvent(st, join[d], 0);
       }
-      tm.launches += klt ? (p.n_emitters > 0 ? 6 : 5) : 4;
+      // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
+      tm.launches += 2 + (klt ? 3 : 0) + ((!klt || p.n_emitters > 0) ? 2 : 0);
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

@@ -180,6 +180,124 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
 constexpr int kScanUnroll = RT_SCAN_UNROLL;  // batches of the scan loop unrolled together
 // kEye: the closest-hit rays of depth 0 (camera rays, all from the eye) use the shared-origin
 // filter on S.pairs_eye (4 instead of 7 FMA per sphere, RayFilterT::batch_eye)
+// One ray's scan over the sphere pairs [pb, pe): FP32 filter, candidate list in index order
+// (closest: pruned by the certain upper bound tub; shadow: up to the first certain occluder rob).
+// lo_row != nullptr: also store each closest candidate's lower root bound (split scans merge their
+// parts' lists with the smallest tub of all parts).
+template <int kSrc, bool kShadow, bool kEye>
+__device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S, const float4* __restrict__ gp,
+                                           const RayFilterFor<kSrc>& F, int pb, int pe, bool& act, int skip,
+                                           int skip2, float tl_f, float& tub, int& nc, int& rob, int* cand_row,
+                                           float* lo_row) {
+  const float eps_f = (float)kEps;
+#pragma unroll(kScanUnroll)
+  for (int base = pb; base < pe; base += kPairsPerBatch) {
+    float2 disc[kPairsPerBatch];
+    float dmax;
+    if constexpr (kEye) dmax = F.template batch_eye<kSrc>(gp, base, disc);
+    else dmax = F.template batch<kSrc>(gp, base, disc);
+    const bool any = act && dmax >= F.cut;
+    if (__any_sync(kFull, any)) {
+      if (any) {
+        unsigned m = batch_mask(disc, F.cut);
+        while (m != 0u) {
+          const int i = __ffs(m) - 1;
+          m &= m - 1u;
+          const int k = 2 * base + i;
+          if (k >= P.n_spheres) break;
+          if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
+          if (kShadow && k == skip2) continue;
+          float dd, tc;
+          if constexpr (kEye) F.template sphere_eye<kSrc>(gp, k, dd, tc);
+          else F.template sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
+          const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
+          const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
+          const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
+          if (tc + qh < eps_f - F.eta) continue;                  // chord certainly behind
+          if constexpr (kShadow) {
+            if (tc - qh - F.eta >= tl_f * 1.000001f) continue;   // certainly beyond the light
+            if (sure) {
+              const float t0lo = tc - qh - F.eta, t0hi = tc - ql + F.eta;
+              const float t1lo = tc + ql - F.eta, t1hi = tc + qh + F.eta;
+              const float tlo = tl_f * 0.999999f;
+              if ((t0lo >= eps_f && t0hi < tlo) || (t0hi < eps_f && t1lo >= eps_f && t1hi < tlo)) {
+                rob = k;  // certain occluder: earlier ambiguous candidates are decided in FP64 later
+                act = false;
+                break;
+              }
+            }
+          } else {
+            if (tc - qh - F.eta > tub) continue;  // certainly farther than a certain hit
+            if (sure) {
+              const float t0lo = tc - qh - F.eta, t0hi = tc - ql + F.eta;
+              const float t1lo = tc + ql - F.eta, t1hi = tc + qh + F.eta;
+              if (t0lo >= eps_f) tub = fminf(tub, t0hi);
+              else if (t0hi < eps_f && t1lo >= eps_f) tub = fminf(tub, t1hi);
+            }
+          }
+          if (nc < kCandMax) {
+            cand_row[nc] = k;
+            if (!kShadow && lo_row != nullptr) lo_row[nc] = tc - qh - F.eta;
+          }
+          ++nc;
+        }
+      }
+    }
+    if constexpr (kShadow) {
+      if (!__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
+    }
+  }
+}
+
+// Split scans for short queues. A queue of a few hundred 32-ray tasks leaves most of the GPU
+// idle while each warp scans all spheres serially (the deep depths of a small shard: 30-40 us per
+// launch for a few thousand rays). Then `parts` (2, 4 or 8) warps of one CTA scan disjoint,
+// batch-aligned sphere ranges of the same rays; after a CTA barrier the part-0 warp merges the
+// per-part lists in part (= sphere index) order:
+//  * closest: every part's candidates whose lower root bound does not exceed the smallest
+//    certain upper bound tub of all parts (a candidate beyond a certain hit cannot be nearest;
+//    every sphere attaining the minimum root survives, so wf_shade's FP64 decision is unchanged);
+//  * shadow: the parts' candidates up to and including the first part that found a certain
+//    occluder, which becomes the ray's rob: exactly the list of the unsplit index-order scan.
+// A merged list longer than kCandMax overflows into the FP64 full scan, as an unsplit one does.
+#ifndef RT_SPLIT_MAX
+#define RT_SPLIT_MAX 8
+#endif
+#ifndef RT_SPLIT_SLACK
+#define RT_SPLIT_SLACK 2  // split while tasks x parts x SLACK <= resident warps
+#endif
+__device__ __forceinline__ int split_parts(unsigned tasks, const WfBuffers& B) {
+  if ((int)gridDim.x > B.xctas || blockDim.x != 256) return 1;
+  const unsigned warps = gridDim.x * 8u;
+  int p = 1;
+  while (p < RT_SPLIT_MAX && tasks * (unsigned)p * RT_SPLIT_SLACK <= warps) p <<= 1;
+  return p;
+}
+// batch-aligned pair range of part `part` of `parts`
+__device__ __forceinline__ void split_range(const DevParams& P, int part, int parts, int& pb, int& pe) {
+  const int per = ((P.n_pairs_pad + parts - 1) / parts + kPairsPerBatch - 1) / kPairsPerBatch * kPairsPerBatch;
+  pb = part * per < P.n_pairs_pad ? part * per : P.n_pairs_pad;
+  pe = pb + per < P.n_pairs_pad ? pb + per : P.n_pairs_pad;
+}
+// merged shadow list of one ray from the parts' lists (rows of the CTA's warps w0 .. w0+parts-1)
+__device__ __forceinline__ void split_merge_shadow(int parts, const int* s_nc, const int* s_rob, int stride,
+                                                   const int* xrow0, size_t xstride, int* cand_row, int& nc_out,
+                                                   int& rob_out) {
+  int tot = 0, rob = -1;
+  for (int q = 0; q < parts; ++q) {
+    const int nq = s_nc[q * stride];
+    const int* xr = xrow0 + q * xstride;
+    for (int i = 0; i < nq && i < kCandMax; ++i) {
+      if (tot + i < kCandMax) cand_row[tot + i] = xr[i];
+    }
+    tot += nq;
+    const int rq = s_rob[q * stride];
+    if (rq != -1) { rob = rq; break; }
+  }
+  nc_out = tot;
+  rob_out = rob;
+}
+
 template <int kSrc, bool kShadow, bool kEye = false>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -188,6 +306,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
   const bool listed = kShadow && P.lt_lights > 0;
   const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  if (split_parts((n + 31u) / 32u, B) > 1) return;  // a short queue: wf_isect_split scans it
   // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
   // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
   if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
@@ -305,6 +424,101 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
       cn[e] = nc;
       if constexpr (kShadow) B.srob[e] = rob;
     }
+  }
+}
+
+template <int kSrc, bool kShadow, bool kEye = false>
+__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  __shared__ uint64_t s_mbar;
+  __shared__ int s_nc[8][32];
+  __shared__ int s_x[8][32];  // closest: tub (float bits); shadow: rob
+  __shared__ unsigned s_unit;
+  const bool listed = kShadow && P.lt_lights > 0;
+  const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  const unsigned tasks = (n + 31u) / 32u;  // 32 rays each
+  const int parts = split_parts(tasks, B);
+  if (parts == 1) return;  // a long queue: wf_isect scans it
+  const float4* gp = kEye ? S.pairs_eye : S.pairs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tpc = 8 / parts;  // tasks per CTA unit
+  const unsigned units = (tasks + tpc - 1) / tpc;
+  if (blockIdx.x >= units) return;  // CTAs without work leave before staging the scene
+  if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
+  const int slot = warp / parts, part = warp % parts;
+  int pb, pe;
+  split_range(P, part, parts, pb, pe);
+  const size_t xs = (size_t)32 * kCandMax;  // between the scratch rows of consecutive warps
+  const size_t row = ((size_t)(blockIdx.x * 8 + warp) * 32 + lane) * kCandMax;
+  int* xc = (kShadow ? B.xcand_s : B.xcand_c) + row;
+  float* xl = B.xlo_c + row;
+  unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
+  const WfQueue Q = B.q[d & 1];
+  while (true) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(work, 1u);
+    __syncthreads();
+    const unsigned u = s_unit;
+    if (u >= units) break;  // CTA-uniform
+    unsigned e = (u * tpc + slot) * 32u + lane;
+    bool act = e < n;
+    const bool mine = act;
+    if (listed && act) e = (unsigned)B.sother[e];
+    d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+    double tl = 0.0;
+    int rob = -1, skip = -1, skip2 = -1;
+    if (act) {
+      if constexpr (kShadow) {
+        o = ld3(B.sray, B.scap, (int)e, 0);
+        dir = ld3(B.sray, B.scap, (int)e, 3);
+        tl = B.sray[6 * (size_t)B.scap + e];
+        skip = B.sskip[e];
+        skip2 = B.sskip2[e];
+        for (int j = 0; j < P.n_planes; ++j) {  // planes first, exactly (every part alike)
+          const DevPlane pl = c_planes[j];
+          const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+          if (fabs(den) >= 1e-12) {
+            const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+            if (t >= kEps && t < tl) { rob = -2 - j; act = false; break; }
+          }
+        }
+      } else {
+        o = ld3(Q.ray, B.cap, (int)e, 0);
+        dir = ld3(Q.ray, B.cap, (int)e, 3);
+        skip = Q.skip[e];
+      }
+    }
+    RayFilterFor<kSrc> F;
+    F.init(o, dir, P);
+    float tub = 3.0e38f;
+    int nc = 0;
+    isect_scan<kSrc, kShadow, kEye>(P, S, gp, F, pb, pe, act, skip, skip2, (float)tl, tub, nc, rob, xc, xl);
+    s_nc[warp][lane] = nc;
+    s_x[warp][lane] = kShadow ? rob : __float_as_int(tub);
+    __syncthreads();
+    if (part == 0 && mine) {
+      if constexpr (kShadow) {
+        int nco, robo;
+        split_merge_shadow(parts, &s_nc[warp][lane], &s_x[warp][lane], 32, xc, xs, B.scand + (size_t)e * kCandMax, nco, robo);
+        B.sn[e] = nco;
+        B.srob[e] = robo;
+      } else {
+        float tm = __int_as_float(s_x[warp][lane]);
+        for (int q = 1; q < parts; ++q) tm = fminf(tm, __int_as_float(s_x[warp + q][lane]));
+        int* crow = B.ccand + (size_t)e * kCandMax;
+        int tot = 0;
+        for (int q = 0; q < parts; ++q) {
+          const int nq = s_nc[warp + q][lane];
+          if (nq > kCandMax) { tot = kCandMax + 1; break; }  // a part overflowed: FP64 full scan
+          for (int i = 0; i < nq; ++i) {
+            if (xl[q * xs + i] > tm) continue;  // certainly farther than a certain hit
+            if (tot < kCandMax) crow[tot] = xc[q * xs + i];
+            ++tot;
+          }
+        }
+        B.cn[e] = tot;
+      }
+    }
+    __syncthreads();  // s_unit / s_nc / s_x / scratch rows are rewritten by the next unit
   }
 }
 
@@ -517,6 +731,55 @@ __device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* 
   }
 }
 
+// the light-origin scan of two rays of light l (one thread) over the sphere pairs [pb, pe)
+template <int kSrc>
+__device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ s1p,
+                                        int pb, int pe, LtRay& Ra, LtRay& Rb, int* rowa, int* rowb) {
+  const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
+  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+  const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
+  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
+  const float cut = Ra.F.cut;  // depends on the origin P_l only: the same for both rays
+  for (int base = pb; base < pe; base += kLtPB) {
+    float2 va[kLtPB], vb[kLtPB];
+#pragma unroll
+    for (int i = 0; i < kLtPB; ++i) {
+      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+      const float2 S1 = s1p[base + i];
+      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w), CZ = make_float2(b.x, b.y);
+      const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
+      const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
+      va[i] = __ffma2_rn(ta, ta, S1);
+      vb[i] = __ffma2_rn(tb, tb, S1);
+    }
+    float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+#pragma unroll
+    for (int i = 1; i < kLtPB; ++i) {
+      ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
+      mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+    }
+    const bool ca = Ra.act && ma >= cut, cb = Rb.act && mb >= cut;
+    if (__any_sync(kFull, ca || cb)) {
+      if (ca) {
+        unsigned m = 0u;
+#pragma unroll
+        for (int i = 0; i < kLtPB; ++i)
+          m |= ((va[i].x >= cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
+        lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Ra, rowa);
+      }
+      if (cb) {
+        unsigned m = 0u;
+#pragma unroll
+        for (int i = 0; i < kLtPB; ++i)
+          m |= ((vb[i].x >= cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
+        lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Rb, rowb);
+      }
+    }
+    if (!__any_sync(kFull, Ra.act || Rb.act)) break;  // Alg. 1 `break`, warp-wide
+  }
+}
+
 template <int kSrc>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -532,6 +795,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
   __syncthreads();
   const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
+  if (split_parts(n_chunks, B) > 1) return;  // a short list: wf_isect_lt_split scans it
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
@@ -602,6 +866,83 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
 }
 
+// the light-origin scan of a short list: parts warps of a CTA share a 64-entry chunk (sphere
+// ranges), merged in part order as in wf_isect_split
+template <int kSrc>
+__global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
+wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
+  __shared__ uint64_t s_mbar;
+  __shared__ unsigned s_chunk_end[kMaxLtLights];
+  __shared__ int s_nc[8][64];
+  __shared__ int s_rob[8][64];
+  __shared__ unsigned s_unit;
+  if (threadIdx.x == 0) {
+    unsigned acc = 0;
+    for (int l = 0; l < P.lt_lights; ++l) {
+      acc += (B.ctr[wf_ctr_lt(d, l)] + 63u) / 64u;
+      s_chunk_end[l] = acc;
+    }
+  }
+  __syncthreads();
+  const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
+  const int parts = split_parts(n_chunks, B);
+  if (parts == 1) return;  // a long list: wf_isect_lt scans it
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tpc = 8 / parts;  // chunks per CTA unit
+  const unsigned units = (n_chunks + tpc - 1) / tpc;
+  if (blockIdx.x >= units) return;  // CTAs without work leave before staging the scene
+  stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
+  const float4* gp = S.pairs_lt;
+  const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
+  const int slot = warp / parts, part = warp % parts;
+  int pb, pe;
+  split_range(P, part, parts, pb, pe);
+  const size_t xs = (size_t)64 * kCandMax;
+  int* xa = B.xcand_s + ((size_t)(blockIdx.x * 8 + warp) * 64 + lane) * kCandMax;
+  int* xb = xa + 32 * kCandMax;
+  while (true) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(B.ctr + wf_ctr_wlt(d), 1u);
+    __syncthreads();
+    const unsigned u = s_unit;
+    if (u >= units) break;  // CTA-uniform
+    const unsigned k = u * tpc + slot;
+    const bool valid_chunk = k < n_chunks;
+    int l = 0;
+    while (l < P.lt_lights - 1 && s_chunk_end[l] <= k) ++l;
+    const unsigned c = k - (l > 0 ? s_chunk_end[l - 1] : 0u);
+    const unsigned cnt = valid_chunk ? B.ctr[wf_ctr_lt(d, l)] : 0u;
+    const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
+    const bool va_ = oa < cnt, vb_ = ob < cnt;
+    const unsigned ja = va_ ? (unsigned)B.slt[(size_t)l * B.cap + oa] : 0u;
+    const unsigned jb = vb_ ? (unsigned)B.slt[(size_t)l * B.cap + ob] : 0u;
+    LtRay Ra, Rb;
+    lt_setup(P, S, B, ja, va_, l, Ra);
+    lt_setup(P, S, B, jb, vb_, l, Rb);
+    lt_scan<kSrc>(P, gp, s1_all + (size_t)l * P.n_pairs_pad, pb, pe, Ra, Rb, xa, xb);
+    s_nc[warp][lane] = Ra.nc;
+    s_nc[warp][lane + 32] = Rb.nc;
+    s_rob[warp][lane] = Ra.rob;
+    s_rob[warp][lane + 32] = Rb.rob;
+    __syncthreads();
+    if (part == 0) {
+      int nco, robo;
+      if (va_) {
+        split_merge_shadow(parts, &s_nc[warp][lane], &s_rob[warp][lane], 64, xa, xs, B.scand + (size_t)ja * kCandMax, nco, robo);
+        B.sn[ja] = nco;
+        B.srob[ja] = robo;
+      }
+      if (vb_) {
+        split_merge_shadow(parts, &s_nc[warp][lane + 32], &s_rob[warp][lane + 32], 64, xb, xs, B.scand + (size_t)jb * kCandMax,
+                           nco, robo);
+        B.sn[jb] = nco;
+        B.srob[jb] = robo;
+      }
+    }
+    __syncthreads();  // s_unit / s_nc / s_rob / scratch rows are rewritten by the next unit
+  }
+}
+
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
 // the list overflowed
 __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScene& S, const int* cand, int nc,
@@ -646,6 +987,10 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], Q.skip[e], o, dir, tbest, hs, hp);
+#ifdef RT_OVF_PROBE
+    if (B.cn[e] > kCandMax) atomicAdd(B.ctr + 72 * kWfCtrPerDepth + 4 * d, 1u);
+    atomicMax(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 2, (unsigned)B.cn[e]);
+#endif
     const int dword = Q.depth[e];
     const int depth = dword & 0xff;
     int prim = -1;
@@ -899,6 +1244,10 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
           const int skip2 = B.sskip2[j];
           const int nc = B.sn[j];
           int first = -1;
+#ifdef RT_OVF_PROBE
+          if (nc > kCandMax) atomicAdd(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 1, 1u);
+          atomicMax(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 3, (unsigned)nc);
+#endif
           if (nc > 0 || rob >= 0) {
             const d3 os = ld3(B.sray, B.scap, j, 0), ds = ld3(B.sray, B.scap, j, 3);
             const double tl = B.sray[6 * (size_t)B.scap + j];
