@@ -112,7 +112,9 @@ typedef struct {
   double last_render_ms;
   uint64_t closest_sphere_tests; /* part of sphere_tests done by closest-hit (primary/secondary) rays */
   double isect_closest_ms;       /* wavefront: summed device time of the closest-hit intersection
-                                    kernels (CUDA events around each launch); 0 for the megakernel */
+                                    kernels (CUDA events around each launch); 0 for the megakernel
+                                    and for graph replays with concurrency on (rt_set_graphs), whose
+                                    launches overlap: time them with rt_set_concurrency(0) */
   double isect_shadow_ms;        /* wavefront: same for the shadow-ray intersection kernels */
   uint32_t launches;             /* kernels of this library launched by the call */
   int32_t variant;               /* RT_VARIANT_MEGAKERNEL or RT_VARIANT_WAVEFRONT actually used */
@@ -166,6 +168,14 @@ int rt_set_variant(int32_t variant);
  * stream, concurrently with the closest-hit scan of depth d+1; 0 runs every launch in order on
  * the library stream (same results bit for bit; used to time each kernel alone). */
 int rt_set_concurrency(int32_t on);
+
+/* Wavefront kernels: 1 (default) replays a CUDA graph of the launch sequence. The sequence of a
+ * render (frame or shard size, max_depth, spp, output pointers, buffers, concurrency) is captured
+ * the second time the same sequence is requested in a row and replayed while it stays the same,
+ * so a frame loop pays one graph launch per frame instead of ~10 kernel launches per depth; scene
+ * and camera contents may change between replays (the kernels read them at run time). 0 launches
+ * every kernel from the host. Same results bit for bit either way. RT_ERR_INVALID_ARG unless 0/1. */
+int rt_set_graphs(int32_t on);
 
 /* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
 int rt_set_seed(uint64_t seed);

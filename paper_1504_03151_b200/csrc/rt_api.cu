@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -126,6 +127,18 @@ struct Context {
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> ev_chunk;
   std::vector<int> chunk_items;
+  // CUDA graph of the wavefront launch sequence (rt_set_graphs): captured on the second of two
+  // consecutive renders with the same launch key, replayed while the key stays the same
+#ifndef RT_WF_GRAPHS
+#define RT_WF_GRAPHS 1
+#endif
+  int graphs = RT_WF_GRAPHS;
+  cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
+  cudaEvent_t ev_cap = nullptr;
+  std::string last_key, graph_key;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_n = 0, graph_launches = 0, graph_chunks = 0;
+  std::vector<int> graph_chunk_items;
 };
 
 Context g_ctx;
@@ -219,6 +232,94 @@ int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
   if (spp < 1 || spp > 4096) return fail(RT_ERR_INVALID_ARG, "spp must be in [1, 4096] (got %d)", spp);
   if (!g_ctx.has_scene) return fail(RT_ERR_NO_SCENE, "no scene: call rt_scene_upload first");
   if (!g_ctx.has_camera) return fail(RT_ERR_NO_CAMERA, "no camera: call rt_camera_set first");
+  return RT_OK;
+}
+
+// Everything the wavefront launch sequence depends on: the kernel arguments (parameters, scene
+// and output pointers, buffer layout), the scene source, the timing/stream configuration. Scene
+// and camera CONTENTS are read by the kernels at run time and do not enter the key.
+template <class T>
+void key_add(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+std::string wf_launch_key(const rt::DevParams& p, const rt::DevScene& sc, const rt::DevOutputs& o, int src,
+                          const rt::WfTiming& tm, const Context& c) {
+  std::string k;
+  key_add(k, p);
+  key_add(k, sc);
+  key_add(k, o);
+  key_add(k, src);
+  key_add(k, c.num_sms);
+  key_add(k, c.wf);
+  key_add(k, c.wf2);
+  const void* ptrs[] = {tm.closest, tm.shadow, tm.shade, tm.side, tm.fork, tm.join, tm.B2, tm.main2, tm.side2, tm.fork2,
+                        tm.join2, tm.start_ev, tm.done2_ev, tm.chunk_done, tm.chunk_items};
+  key_add(k, ptrs);
+  key_add(k, tm.cap);
+  key_add(k, tm.chunk_cap);
+  return k;
+}
+
+void drop_graph(Context& c) {
+  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
+  c.graph_exec = nullptr;
+  c.graph_key.clear();
+}
+
+// Launch the wavefront sequence: replay the cached graph when the key matches, capture it when
+// the same key comes twice in a row (a frame loop), else launch stream by stream (one-off
+// renders, progressive passes whose pass index changes every call).
+int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc, const rt::DevOutputs& o, int src,
+                     rt::WfTiming& tm) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(c.stream, &cs), "cudaStreamIsCapturing");
+  if (!c.graphs || cs != cudaStreamCaptureStatusNone) {  // the caller captures: plain launches into it
+    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    return RT_OK;
+  }
+  std::string key = wf_launch_key(p, sc, o, src, tm, c);
+  if (c.graph_exec && key == c.graph_key) {
+    CU(cudaGraphLaunch(c.graph_exec, c.stream), "cudaGraphLaunch");
+    tm.n = c.graph_n;
+    tm.launches = c.graph_launches;
+    tm.n_chunks = c.graph_chunks;
+    if (tm.chunk_items) std::copy(c.graph_chunk_items.begin(), c.graph_chunk_items.end(), tm.chunk_items);
+    c.last_key.swap(key);
+    return RT_OK;
+  }
+  if (key != c.last_key) {  // first render with this key: plain launches
+    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    c.last_key.swap(key);
+    return RT_OK;
+  }
+  // second consecutive render with this key: capture on cap_stream (forked from c.stream so the
+  // capture sees the same order), instantiate, launch on c.stream
+  drop_graph(c);
+  if (!c.cap_stream) CU(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  // per-launch timing events become event-record nodes, which serialise the graph around every
+  // scan and shade launch: kept for the in-order timing mode (rt_set_concurrency(0)), dropped
+  // when the launches overlap (their per-launch times would share the GPU anyway)
+  if (c.concurrent) tm.cap = 0;
+  tm.ext_events = true;
+  CU(cudaStreamBeginCapture(c.cap_stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+  const cudaError_t le = rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.cap_stream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(c.cap_stream, &g);
+  tm.ext_events = false;
+  CU(le, "wavefront launch (capture)");
+  CU(ce, "cudaStreamEndCapture");
+  cudaGraphExec_t x = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  CU(ie, "cudaGraphInstantiate");
+  c.graph_exec = x;
+  c.graph_key = key;
+  c.graph_n = tm.n;
+  c.graph_launches = tm.launches;
+  c.graph_chunks = tm.n_chunks;
+  c.graph_chunk_items.assign(tm.chunk_items ? tm.chunk_items : nullptr, tm.chunk_items ? tm.chunk_items + tm.n_chunks : nullptr);
+  CU(cudaGraphLaunch(c.graph_exec, c.stream), "cudaGraphLaunch");
+  c.last_key.swap(key);
   return RT_OK;
 }
 
@@ -329,7 +430,10 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
 #define RT_WF_PREFER_CONST 0
 #endif
     const int src = (RT_WF_PREFER_CONST && c.const_scene) ? 2 : (c.smem_scene ? 1 : 0);
-    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    {
+      const int lrc = launch_wavefront(c, p, sc, o, src, tm);
+      if (lrc) return lrc;
+    }
     CU(cudaEventRecord(c.ev1, c.stream), "cudaEventRecord");
     if (overlap) {  // rows of complete tile rows, in order, each after its chunk's resolve
       const long long row_items = (long long)p.tiles_x * rt::kTilePx;
@@ -556,6 +660,16 @@ int rt_set_concurrency(int32_t on) {
   if (rc) return rc;
   if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "concurrency must be 0 or 1");
   g_ctx.concurrent = on;
+  return RT_OK;
+}
+
+int rt_set_graphs(int32_t on) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "graphs must be 0 or 1");
+  g_ctx.graphs = on;
+  if (!on) drop_graph(g_ctx);
+  g_ctx.last_key.clear();
   return RT_OK;
 }
 

@@ -193,6 +193,12 @@ struct WfTiming {
   int* chunk_items = nullptr;
   int chunk_cap = 0;
   int n_chunks = 0;  // output
+  // while the launch sequence is captured into a CUDA graph, the timing and chunk events become
+  // event-record nodes (cudaEventRecordExternal), so every replay records them
+  bool ext_events = false;
+  void record(cudaEvent_t ev, cudaStream_t s) const {
+    cudaEventRecordWithFlags(ev, s, ext_events ? cudaEventRecordExternal : cudaEventRecordDefault);
+  }
 };
 // scene source of the wavefront intersection kernels: 0 global, 1 shared memory, 2 constant bank
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,

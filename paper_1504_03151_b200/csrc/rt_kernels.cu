@@ -730,7 +730,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     auto closest_scan = [&](int dd) {
       const int ti = t0 + dd;
       const bool rec = ti < tm.cap;
-      if (rec) cudaEventRecord(tm.closest[2 * ti], st);
+      if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
         kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
         if (kc0s) kc0s<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
@@ -740,16 +740,16 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         wf_isect_split<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
         tm.launches += 2;
       }
-      if (rec) cudaEventRecord(tm.closest[2 * ti + 1], st);
+      if (rec) tm.record(tm.closest[2 * ti + 1], st);
     };
     closest_scan(0);
     for (int d = 0; d <= p.max_depth; ++d) {
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
-      if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti], st);
+      if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
-      if (rec && tm.shade) cudaEventRecord(tm.shade[2 * ti + 1], st);
+      if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       if (klt) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (side) {
@@ -757,7 +757,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaStreamWaitEvent(side, fork[d], 0);
         ss = side;
       }
-      if (rec) cudaEventRecord(tm.shadow[2 * ti], ss);
+      if (rec) tm.record(tm.shadow[2 * ti], ss);
       if (klt) {  // point lights, from the light
         klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
         klts<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
@@ -766,7 +766,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
         wf_isect_split<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
       }
-      if (rec) cudaEventRecord(tm.shadow[2 * ti + 1], ss);
+      if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
@@ -781,7 +781,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out, o.accum);
     tm.launches += 2;
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
-      cudaEventRecord(tm.chunk_done[tm.n_chunks], st);
+      tm.record(tm.chunk_done[tm.n_chunks], st);
       tm.chunk_items[tm.n_chunks] = w0 + nw;
       ++tm.n_chunks;
     }

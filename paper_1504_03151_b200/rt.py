@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
         "rt_set_integrator": [i32, i32],
         "rt_set_concurrency": [i32],
+        "rt_set_graphs": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
         "rt_sum_shard_stats": [vp, i32],
         "rt_ipc_alloc": [i64, C.POINTER(vp), C.c_char_p],
@@ -168,6 +169,11 @@ def set_variant(name: str):
 def set_concurrency(on: bool):
     """Wavefront: shadow scans concurrent with the next closest scan (default) or all in order."""
     _check("rt_set_concurrency", lib().rt_set_concurrency(1 if on else 0))
+
+
+def set_graphs(on: bool):
+    """Wavefront: replay a CUDA graph of the launch sequence for repeated identical renders (default)."""
+    _check("rt_set_graphs", lib().rt_set_graphs(1 if on else 0))
 
 
 def set_stream(stream):

@@ -1,6 +1,9 @@
-"""Per-rank work of an N-GPU frame measured on one GPU: rank 0's shard of C4 for world = 1, 2,
-4, 8 (rt_render_shard), timed with CUDA events. Predicts the strong-scaling efficiency before any
-collective: eff(N) = T(1) / (N * T_rank0(N)). Tool only."""
+"""Per-rank work of an N-GPU frame measured on one GPU: every rank's shard of a config for world =
+1, 2, 4, 8 (rt_render_shard), each rank rendered repeatedly as its own process would (the first
+renders launch stream by stream, later ones replay the captured CUDA graph), timed with CUDA
+events (median of the timed repeats). Predicts the strong-scaling efficiency before any
+collective: eff(N) = T(1) / (N * max_rank T_rank(N)). Tool only.
+Usage: python tools/shard_scaling.py [C4] [--no-graphs]"""
 import os
 import sys
 
@@ -10,7 +13,9 @@ import torch  # noqa: E402
 import scenegen  # noqa: E402
 from paper_1504_03151_b200 import rt  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "C4"
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+name = args[0] if args else "C4"
+rt.set_graphs("--no-graphs" not in sys.argv)
 sc = scenegen.get(name)
 rt.load_scene(sc)
 W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
@@ -19,15 +24,18 @@ for world in (1, 2, 4, 8):
     tpr, sb = rt.shard_layout(W, H, world)
     slab = torch.empty(sb // 4, dtype=torch.float32, device="cuda")
     ts = []
-    for r in range(3):
-        for rank in ([0] if r < 2 else range(world)):
+    for rank in range(world):
+        for _ in range(3):  # warm-up: plain launches, capture, first replay
+            rt.render_shard(W, H, D, S, rank, world, slab)
+        reps = []
+        for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             rt.render_shard(W, H, D, S, rank, world, slab)
             e1.record()
             torch.cuda.synchronize()
-            if r == 2:
-                ts.append(e0.elapsed_time(e1))
+            reps.append(e0.elapsed_time(e1))
+        ts.append(sorted(reps)[2])
     worst = max(ts)
     base = base or worst
     print(f"{name} world={world}: rank times ms min {min(ts):.3f} max {worst:.3f} -> predicted efficiency "
