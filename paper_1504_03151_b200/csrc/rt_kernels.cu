@@ -656,8 +656,9 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   constexpr bool kEyeOk = kSrc != SRC_CONST && RT_FILTER_EXPANDED;
   using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
   IsectFn kc0 = wf_isect<kSrc, false>;
-  // every scan kernel is paired with its split variant (short queues, wf_isect_split): both are
-  // launched with the same grid, read the same queue length and exactly one of them does the work
+  // short queues are scanned by the split path (wf_isect_split_body), called from the scan kernel
+  // itself (RT_SPLIT_FUSED) or, otherwise, launched as a second kernel with the same grid: both
+  // read the same queue length and exactly one of them does the work
   IsectFn kc0s = wf_isect_split<kSrc, false>;
 #ifndef RT_EYE_TWO_RAYS
 #define RT_EYE_TWO_RAYS 1
@@ -733,12 +734,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
         kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        if (kc0s) kc0s<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        tm.launches += kc0s ? 2 : 1;
+        if (kc0s && !RT_SPLIT_FUSED) kc0s<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        tm.launches += (kc0s && !RT_SPLIT_FUSED) ? 2 : 1;
       } else {
         wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        wf_isect_split<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        tm.launches += 2;
+        if (!RT_SPLIT_FUSED) wf_isect_split<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        tm.launches += RT_SPLIT_FUSED ? 1 : 2;
       }
       if (rec) tm.record(tm.closest[2 * ti + 1], st);
     };
@@ -760,11 +761,11 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) tm.record(tm.shadow[2 * ti], ss);
       if (klt) {  // point lights, from the light
         klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
-        klts<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
+        if (!RT_SPLIT_FUSED) klts<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
         wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
-        wf_isect_split<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+        if (!RT_SPLIT_FUSED) wf_isect_split<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
       wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
@@ -774,7 +775,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaStreamWaitEvent(st, join[d], 0);
       }
       // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
-      tm.launches += 2 + (klt ? 3 : 0) + ((!klt || p.n_emitters > 0) ? 2 : 0);
+      tm.launches += 2 + (klt ? (RT_SPLIT_FUSED ? 2 : 3) : 0) + ((!klt || p.n_emitters > 0) ? (RT_SPLIT_FUSED ? 1 : 2) : 0);
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

@@ -298,6 +298,19 @@ __device__ __forceinline__ void split_merge_shadow(int parts, const int* s_nc, c
   rob_out = rob;
 }
 
+// RT_SPLIT_FUSED=1: the scan kernel calls the split path itself (a non-inlined function,
+// measured slower: 80 registers and a 528-byte stack frame in the long-queue kernel); 0 (default):
+// a separate wf_isect_split launch
+#ifndef RT_SPLIT_FUSED
+#define RT_SPLIT_FUSED 0
+#endif
+#if RT_SPLIT_FUSED
+#define RT_SPLIT_INL __noinline__
+#else
+#define RT_SPLIT_INL __forceinline__  // inlined into its own kernel: parameters stay in the constant bank
+#endif
+template <int kSrc, bool kShadow, bool kEye>
+__device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d);
 template <int kSrc, bool kShadow, bool kEye = false>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -306,7 +319,10 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
   const bool listed = kShadow && P.lt_lights > 0;
   const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
-  if (split_parts((n + 31u) / 32u, B) > 1) return;  // a short queue: wf_isect_split scans it
+  if (split_parts((n + 31u) / 32u, B) > 1) {  // a short queue: the split scan
+    if (RT_SPLIT_FUSED) wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
+    return;
+  }
   // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
   // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
   if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
@@ -427,9 +443,8 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
 }
 
-template <int kSrc, bool kShadow, bool kEye = false>
-__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
-wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+template <int kSrc, bool kShadow, bool kEye>
+__device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
   __shared__ uint64_t s_mbar;
   __shared__ int s_nc[8][32];
   __shared__ int s_x[8][32];  // closest: tub (float bits); shadow: rob
@@ -520,6 +535,12 @@ wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
     }
     __syncthreads();  // s_unit / s_nc / s_x / scratch rows are rewritten by the next unit
   }
+}
+
+template <int kSrc, bool kShadow, bool kEye = false>
+__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
 }
 
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
@@ -781,6 +802,8 @@ __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __rest
 }
 
 template <int kSrc>
+__device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d);
+template <int kSrc>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
@@ -795,7 +818,10 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
   __syncthreads();
   const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
-  if (split_parts(n_chunks, B) > 1) return;  // a short list: wf_isect_lt_split scans it
+  if (split_parts(n_chunks, B) > 1) {  // a short list: the split scan
+    if (RT_SPLIT_FUSED) wf_isect_lt_split_body<kSrc>(P, S, B, d);
+    return;
+  }
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
@@ -869,8 +895,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // the light-origin scan of a short list: parts warps of a CTA share a 64-entry chunk (sphere
 // ranges), merged in part order as in wf_isect_split
 template <int kSrc>
-__global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
-wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+__device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
   static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights];
@@ -941,6 +966,12 @@ wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
     }
     __syncthreads();  // s_unit / s_nc / s_rob / scratch rows are rewritten by the next unit
   }
+}
+
+template <int kSrc>
+__global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
+wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  wf_isect_lt_split_body<kSrc>(P, S, B, d);
 }
 
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
