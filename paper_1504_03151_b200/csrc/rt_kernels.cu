@@ -751,7 +751,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
       else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
-      if (klt) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
+      if (klt && !RT_BIN_FUSED) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (side) {
         cudaEventRecord(fork[d], st);
@@ -775,7 +775,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaStreamWaitEvent(st, join[d], 0);
       }
       // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
-      tm.launches += 2 + (klt ? (RT_SPLIT_FUSED ? 2 : 3) : 0) + ((!klt || p.n_emitters > 0) ? (RT_SPLIT_FUSED ? 1 : 2) : 0);
+      tm.launches += 2 + (klt ? (RT_SPLIT_FUSED ? 1 : 2) + (RT_BIN_FUSED ? 0 : 1) : 0) +
+                     ((!klt || p.n_emitters > 0) ? (RT_SPLIT_FUSED ? 1 : 2) : 0);
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

@@ -993,7 +993,72 @@ __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScen
   }
 }
 
+// ---- lists of the shadow entries per point light (light-origin scans) and the rest ----------
+// One global atomicAdd per light per CTA iteration (256 entries): warps count with ballots, the
+// CTA reserves, warps place their lanes in lane order. Called by every thread of the CTA (lmask
+// = 0 for threads without an entry); contains CTA barriers.
+__device__ __forceinline__ void bin_entries(const DevParams& P, const WfBuffers& B, int d, unsigned long long lmask,
+                                            unsigned off, unsigned (*s_cnt)[kMaxLtLights + 1]) {
+  const int L = P.lt_lights;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const unsigned long long rest = lmask >> L;
+  const unsigned nrest = (unsigned)__popcll(rest);
+  for (int l = 0; l < L; ++l) {
+    const unsigned m = __ballot_sync(kFull, (lmask >> l) & 1ull);
+    if (lane == 0) s_cnt[warp][l] = (unsigned)__popc(m);
+  }
+  unsigned rsum = nrest;  // the rest: a variable count per lane (warp inclusive scan)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(kFull, rsum, o);
+    if (lane >= o) rsum += v;
+  }
+  if (lane == 31) s_cnt[warp][L] = rsum;
+  __syncthreads();
+  if (threadIdx.x <= (unsigned)L) {  // CTA totals -> one atomic per light, then warp offsets
+    const int l = threadIdx.x;
+    unsigned tot = 0;
+    for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
+    unsigned base = tot ? atomicAdd(B.ctr + (l < L ? wf_ctr_lt(d, l) : wf_ctr_so(d)), tot) : 0u;
+    for (int w = 0; w < 8; ++w) {
+      const unsigned c = s_cnt[w][l];
+      s_cnt[w][l] = base;
+      base += c;
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < L; ++l) {
+    const bool has = (lmask >> l) & 1ull;
+    const unsigned m = __ballot_sync(kFull, has);
+    if (has) {
+      const unsigned slot = s_cnt[warp][l] + (unsigned)__popc(m & lt);
+      B.slt[(size_t)l * B.cap + slot] = (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
+    }
+  }
+  if (nrest) {
+    unsigned ob = s_cnt[warp][L] + rsum - nrest;
+    unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
+    for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
+  }
+  __syncthreads();  // s_cnt is rewritten by the next iteration
+}
+
+// the lists as a kernel of their own (RT_BIN_FUSED=0; by default wf_shade builds them)
+__global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
+  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // per warp: entries per light (+ the rest)
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + threadIdx.x;
+    const bool in = e < n;
+    bin_entries(P, B, d, in ? B.lmask[e] : 0ull, in ? (unsigned)B.shoff[e] : 0u, s_cnt);
+  }
+}
+
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
+#ifndef RT_BIN_FUSED
+#define RT_BIN_FUSED 1  // wf_shade builds the per-light lists of its shadow entries (no wf_bin launch)
+#endif
 #ifndef RT_LOGIC_MIN_BLOCKS
 #define RT_LOGIC_MIN_BLOCKS 4
 #endif
@@ -1004,7 +1069,14 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // fused wf_bin (per-light entry lists)
+  const bool bin = RT_BIN_FUSED && P.lt_lights > 0;
+  // CTA-uniform iterations (the fused list building has CTA barriers)
+  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + threadIdx.x;
+    unsigned long long lm = 0ull;  // sources with a shadow ray, and the first entry, for the lists
+    unsigned of = 0u;
+    if (e < n) {
     const int path = Q.path[e];
     const d3 o = ld3(Q.ray, B.cap, (int)e, 0), dir = ld3(Q.ray, B.cap, (int)e, 3);
     double tbest = kInf;
@@ -1119,7 +1191,9 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     B.shoff[e] = (int)off;
-    if (P.lt_lights > 0) B.lmask[e] = lmask;  // wf_bin lists the entries per light
+    lm = lmask;
+    of = off;
+    if (!RT_BIN_FUSED && P.lt_lights > 0) B.lmask[e] = lmask;  // wf_bin lists the entries per light
     // part 3: stack-free continuation
     d3 dn = mk(0, 0, 0);
     bool mi_kind_diffuse_global = false;
@@ -1189,64 +1263,8 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
     warp_stat(stats, 5, (unsigned long long)P.n_spheres);
-  }
-}
-
-// ---- lists of the shadow entries per point light (light-origin scans) and the rest ----------
-// One global atomicAdd per light per CTA iteration (256 entries): warps count with ballots, the
-// CTA reserves, warps place their lanes in lane order.
-__global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
-  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // per warp: entries per light (+ the rest)
-  __shared__ unsigned s_base[kMaxLtLights + 1];
-  const unsigned n = B.ctr[wf_ctr_q(d)];
-  const int L = P.lt_lights;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
-    const unsigned e = e0 + threadIdx.x;
-    const bool in = e < n;
-    const unsigned long long lmask = in ? B.lmask[e] : 0ull;
-    const unsigned off = in ? (unsigned)B.shoff[e] : 0u;
-    const unsigned long long rest = lmask >> L;
-    const unsigned nrest = (unsigned)__popcll(rest);
-    for (int l = 0; l < L; ++l) {
-      const unsigned m = __ballot_sync(kFull, (lmask >> l) & 1ull);
-      if (lane == 0) s_cnt[warp][l] = (unsigned)__popc(m);
     }
-    unsigned rsum = nrest;  // the rest: a variable count per lane (warp inclusive scan)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(kFull, rsum, o);
-      if (lane >= o) rsum += v;
-    }
-    if (lane == 31) s_cnt[warp][L] = rsum;
-    __syncthreads();
-    if (threadIdx.x <= (unsigned)L) {  // CTA totals -> one atomic per light, then warp offsets
-      const int l = threadIdx.x;
-      unsigned tot = 0;
-      for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
-      unsigned base = tot ? atomicAdd(B.ctr + (l < L ? wf_ctr_lt(d, l) : wf_ctr_so(d)), tot) : 0u;
-      for (int w = 0; w < 8; ++w) {
-        const unsigned c = s_cnt[w][l];
-        s_cnt[w][l] = base;
-        base += c;
-      }
-    }
-    __syncthreads();
-    for (int l = 0; l < L; ++l) {
-      const bool has = (lmask >> l) & 1ull;
-      const unsigned m = __ballot_sync(kFull, has);
-      if (has) {
-        const unsigned slot = s_cnt[warp][l] + (unsigned)__popc(m & lt);
-        B.slt[(size_t)l * B.cap + slot] = (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
-      }
-    }
-    if (nrest) {
-      unsigned ob = s_cnt[warp][L] + rsum - nrest;
-      unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
-      for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
-    }
-    __syncthreads();  // s_cnt is rewritten by the next iteration
+    if (bin) bin_entries(P, B, d, lm, of, s_cnt);
   }
 }
 
