@@ -633,8 +633,12 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
 // work items (pixels) per chunk: as many as the buffers hold; a pipelined render of a frame that
 // would fit one chunk is cut in two, so the two chunks can overlap
 int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined) {
+#ifndef RT_PIPE_SPLIT
+#define RT_PIPE_SPLIT 2
+#endif
   int items = cap_paths / p.spp;
-  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18)) items = (p.n_items + 1) / 2;
+  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18))
+    items = (p.n_items + RT_PIPE_SPLIT - 1) / RT_PIPE_SPLIT;
   return items > 0 ? items : 1;
 }
 
@@ -642,6 +646,26 @@ int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined) {
   const int items_per_chunk = wf_items_per_chunk(p, cap_paths, pipelined);
   const int chunks = (p.n_items + items_per_chunk - 1) / items_per_chunk;
   return chunks * (p.max_depth + 1);
+}
+
+#ifndef RT_PDL
+#define RT_PDL 0  // measured: early trigger +4.5 % (waiting CTAs squat on SMs), late trigger +-0
+#endif
+// launch with programmatic stream serialisation (see pdl_enter): the kernel may start while the
+// previous kernel of the stream finishes; its griddepcontrol.wait keeps the data dependency
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), int grid, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = RT_PDL ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 template <int kSrc>
@@ -702,7 +726,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   tm.n_chunks = 0;
   if (dbg) {
     const long long nh = (long long)p.W * p.H * p.spp * (p.max_depth + 1);
-    fill_int<<<num_sms * 8, 256, 0, st>>>(o.dbg_hits, nh, -2);
+    launch_pdl(fill_int, num_sms * 8, 0, st, o.dbg_hits, nh, -2);
     ++tm.launches;
   }
   if (pipe) {  // the second slot's streams start after everything issued on st so far
@@ -722,7 +746,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const long long g0 = (long long)w0 * p.spp;
     if ((e = cudaMemsetAsync(B.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
     const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
-    wf_raygen<<<grid_r, 256, 0, st>>>(p, B, g0, npaths, o.stats);
+    launch_pdl(wf_raygen, grid_r, 0, st, p, B, g0, npaths, o.stats);
     // per depth d: closest scan (d) -> shade (d) -> { shadow scan (d) -> accumulate (d) on the side
     // stream  ||  closest scan (d + 1) on the main stream } -> join -> shade (d + 1) ...
     // (independent: the shadow side reads the shadow entries and writes L into Q[d+1]; the closest
@@ -733,12 +757,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const bool rec = ti < tm.cap;
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
-        kc0<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        if (kc0s && !RT_SPLIT_FUSED) kc0s<<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        launch_pdl(kc0, grid_c, smem, st, p, sc, B, dd);
+        if (kc0s && !RT_SPLIT_FUSED) launch_pdl(kc0s, grid_c, smem, st, p, sc, B, dd);
         tm.launches += (kc0s && !RT_SPLIT_FUSED) ? 2 : 1;
       } else {
-        wf_isect<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
-        if (!RT_SPLIT_FUSED) wf_isect_split<kSrc, false><<<grid_c, 256, smem, st>>>(p, sc, B, dd);
+        launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
+        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
         tm.launches += RT_SPLIT_FUSED ? 1 : 2;
       }
       if (rec) tm.record(tm.closest[2 * ti + 1], st);
@@ -748,10 +772,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      if (dbg) wf_shade<true><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
-      else wf_shade<false><<<grid_l, 256, 0, st>>>(p, sc, B, d, g0, o.stats, nullptr, nullptr);
+      if (dbg) launch_pdl(wf_shade<true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
+      else launch_pdl(wf_shade<false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
-      if (klt && !RT_BIN_FUSED) wf_bin<<<grid_l, 256, 0, st>>>(p, B, d);  // per-light lists of the shadow entries
+      if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (side) {
         cudaEventRecord(fork[d], st);
@@ -760,15 +784,15 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       }
       if (rec) tm.record(tm.shadow[2 * ti], ss);
       if (klt) {  // point lights, from the light
-        klt<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
-        if (!RT_SPLIT_FUSED) klts<<<grid_lt, 256, smem_lt, ss>>>(p, sc, B, d);
+        launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, B, d);
+        if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, B, d);
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
-        wf_isect<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
-        if (!RT_SPLIT_FUSED) wf_isect_split<kSrc, true><<<grid_s, 256, smem, ss>>>(p, sc, B, d);
+        launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
+        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
-      wf_accumulate<<<grid_l, 256, 0, ss>>>(p, sc, B, d, o.stats);
+      launch_pdl(wf_accumulate, grid_l, 0, ss, p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
         cudaEventRecord(join[d], side);
@@ -780,7 +804,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
-    wf_resolve<<<grid_w, 256, 0, st>>>(p, B, w0, nw, o.out, o.accum);
+    launch_pdl(wf_resolve, grid_w, 0, st, p, B, w0, nw, o.out, o.accum);
     tm.launches += 2;
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
       tm.record(tm.chunk_done[tm.n_chunks], st);

@@ -30,6 +30,18 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Programmatic dependent launch (RT_PDL): every wavefront kernel first waits for the grid it
+// depends on (griddepcontrol.wait: that grid has completed and its memory is visible; a no-op
+// without a programmatic dependency), then lets the next kernel of its stream launch, so the
+// next launch and its CTA rasterisation overlap this kernel instead of following it.
+#ifndef RT_PDL_EARLY
+#define RT_PDL_EARLY 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (RT_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // warp-aggregated reservation of `cnt` (< 64) slots on a global counter: exclusive prefix of
 // the counts by bit-plane ballots (valid for any set of active lanes), one atomicAdd per warp
 __device__ __forceinline__ unsigned warp_reserve(unsigned cnt, unsigned* counter) {
@@ -150,6 +162,7 @@ __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene&
 // ---- a2: ray generation -> Q[0] ------------------------------------------------------------
 __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
                                                  unsigned long long* stats) {
+  pdl_enter();
   const WfQueue Q = B.q[0];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long g = g0 + i;
@@ -314,6 +327,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
 template <int kSrc, bool kShadow, bool kEye = false>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  pdl_enter();
   static_assert(!(kEye && kShadow), "shadow rays start at shading points");
   __shared__ uint64_t s_mbar;
   // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
@@ -540,6 +554,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
 template <int kSrc, bool kShadow, bool kEye = false>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  pdl_enter();
   wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
 }
 
@@ -591,6 +606,7 @@ __device__ __forceinline__ void eye_candidates(const DevParams& P, const float4*
 template <int kSrc>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  pdl_enter();
   __shared__ uint64_t s_mbar;
   const unsigned n = B.ctr[wf_ctr_q(d)];
   if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
@@ -806,6 +822,7 @@ __device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const De
 template <int kSrc>
 __global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  pdl_enter();
   static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights];  // prefix sums of the lights' 64-entry chunk counts
@@ -971,6 +988,7 @@ __device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const De
 template <int kSrc>
 __global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
 wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  pdl_enter();
   wf_isect_lt_split_body<kSrc>(P, S, B, d);
 }
 
@@ -1046,6 +1064,7 @@ __device__ __forceinline__ void bin_entries(const DevParams& P, const WfBuffers&
 
 // the lists as a kernel of their own (RT_BIN_FUSED=0; by default wf_shade builds them)
 __global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
+  pdl_enter();
   __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // per warp: entries per light (+ the rest)
   const unsigned n = B.ctr[wf_ctr_q(d)];
   for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
@@ -1066,6 +1085,7 @@ template <bool kDebug>
 __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
+  pdl_enter();
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
@@ -1271,6 +1291,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
 // ---- a5 decision + accumulation of the visible lights, in light order ----------------------
 __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
+  pdl_enter();
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Qn = B.q[(d + 1) & 1];
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -1333,6 +1354,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
 // ---- a7: mean over samples in order, 16-byte store ------------------------------------------
 __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out,
                                                   double* accum) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
     const int w = w0 + i;
     int px = 0, py = 0;
@@ -1367,6 +1389,7 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
 }
 
 __global__ void fill_int(int* p, long long n, int v) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
 }
