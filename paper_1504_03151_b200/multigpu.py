@@ -45,72 +45,101 @@ def rank_tiles(width: int, height: int, rank: int, world: int) -> list[int]:
 
 class P2PRenderer:
     """Fused render + gather over NVLink peer memory (SURVEY §8(e) ablation; include/rt.h
-    rt_render_shard_direct). Rank 0 owns the frame and a world x 8 uint64 stats-record array,
+    rt_render_shard_direct). Rank 0 owns the frames and world x 8 uint64 stats-record arrays,
     allocated for CUDA IPC; the handles travel once over the process group and every other rank
     maps them (peer access over NVLink / NVSwitch). Each frame, every rank's resolve kernel
-    stores its pixels straight into rank 0's frame — no slab, no all-gather, no assembly kernel —
-    then one barrier orders the frame before rank 0 uses it, and a second (`release`) before the
-    next frame may overwrite it."""
+    stores its pixels straight into rank 0's frame — no slab, no all-gather, no assembly kernel.
 
-    def __init__(self, width: int, height: int, max_depth: int, spp: int, group=None):
+    Ordering. With NCCL, one stream-ordered all-reduce of a 4-byte token per frame is the barrier:
+    it completes on every rank only after every rank's render kernels have completed (their peer
+    stores included), and the host never waits. With other backends (gloo, the CPU tests) the
+    host synchronises its stream and calls dist.barrier(). Frames alternate between two buffers,
+    so rank r may start frame i+1 while rank 0 still uses frame i: frame i's buffer is written
+    again only by frame i+2, after the barrier of frame i+1, which rank 0 reaches after it has
+    issued its work on frame i (image valid until the next-but-one render call)."""
+
+    def __init__(self, width: int, height: int, max_depth: int, spp: int, group=None, buffers: int = 2):
         self.W, self.H, self.D, self.spp = width, height, max_depth, spp
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.frame_ptr = self.rec_ptr = None
-        handles = [None, None]
+        self.nbuf = max(1, int(buffers))
+        self.frame_ptrs: list = []
+        self.rec_ptrs: list = []
+        handles = [None] * (2 * self.nbuf)
         if self.rank == 0:
             try:
-                self.frame_ptr, hf = rt.ipc_alloc(width * height * 16)
-                self.rec_ptr, hr = rt.ipc_alloc(self.world * 64)
-                handles = [hf, hr]
+                for b in range(self.nbuf):
+                    fp, hf = rt.ipc_alloc(width * height * 16)
+                    self.frame_ptrs.append(fp)
+                    rp, hr = rt.ipc_alloc(self.world * 64)
+                    self.rec_ptrs.append(rp)
+                    handles[2 * b], handles[2 * b + 1] = hf, hr
             except rt.RtError:
-                handles = [None, None]
+                handles = [None] * (2 * self.nbuf)
         if self.world > 1:
             dist.broadcast_object_list(handles, src=0, group=self.group)
-        ok = handles[0] is not None
+        ok = all(h is not None for h in handles)
         if ok and self.rank != 0:
             try:
-                self.frame_ptr = rt.ipc_open(handles[0])
-                self.rec_ptr = rt.ipc_open(handles[1])
+                for b in range(self.nbuf):
+                    self.frame_ptrs.append(rt.ipc_open(handles[2 * b]))
+                    self.rec_ptrs.append(rt.ipc_open(handles[2 * b + 1]))
             except rt.RtError:
                 ok = False
+        self.nccl = self.world > 1 and dist.get_backend(group) == "nccl"
         if self.world > 1:  # every rank agrees, so a failure raises everywhere (no one waits forever)
-            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
-                                device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda" if self.nccl else "cpu")
             dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
             ok = bool(flag.item())
         if not ok:
             self.close()
             raise RuntimeError("peer-memory frame unavailable (CUDA IPC / peer access failed on some rank)")
-        self.image = None
+        self.token = torch.zeros(1, dtype=torch.int32, device="cuda") if self.nccl else None
+        self.images = []
         if self.rank == 0:
-            self.image = torch.as_tensor(rt.DeviceArray(self.frame_ptr, (height, width, 4), "<f4"), device="cuda")
+            self.images = [torch.as_tensor(rt.DeviceArray(fp, (height, width, 4), "<f4"), device="cuda")
+                           for fp in self.frame_ptrs]
+        self.image = None
+        self.frames = 0
 
     def _barrier(self):
-        torch.cuda.current_stream().synchronize()  # this rank's stores (and stats record) issued and done
-        if self.world > 1:
+        if self.world == 1:
+            return
+        if self.nccl:  # stream-ordered: no host wait
+            dist.all_reduce(self.token, group=self.group)
+        else:
+            torch.cuda.current_stream().synchronize()  # this rank's stores (and stats record) done
             dist.barrier(group=self.group)
 
-    def render(self) -> Frame:
-        rt.render_shard_direct(self.W, self.H, self.D, self.spp, self.rank, self.world, self.frame_ptr, self.rec_ptr)
+    def render(self, want_stats: bool = True) -> Frame:
+        """Render this rank's tiles of the next frame into rank 0's buffer. Rank 0 gets the image
+        (stream-ordered after every rank's stores) and, with want_stats, the summed statistics
+        (a host sync); the image stays valid until the next-but-one call."""
+        b = self.frames % self.nbuf
+        self.frames += 1
+        rt.render_shard_direct(self.W, self.H, self.D, self.spp, self.rank, self.world, self.frame_ptrs[b],
+                               self.rec_ptrs[b])
         self._barrier()
         if self.rank == 0:
-            rt.sum_shard_stats(self.rec_ptr, self.world)
-            return Frame(self.image, rt.stats())
+            rt.sum_shard_stats(self.rec_ptrs[b], self.world)
+            self.image = self.images[b]
+            return Frame(self.image, rt.stats() if want_stats else None)
         return Frame(None, None)
 
     def release(self):
-        """Rank 0 is done with the frame: the next render may overwrite it."""
-        if self.world > 1:
+        """Kept for callers of the single-buffered version: with two buffers, rank 0 releases a
+        frame by calling render() again, so there is nothing to wait for."""
+        if self.nbuf == 1 and self.world > 1:
             dist.barrier(group=self.group)
 
     def close(self):
         self.image = None
-        for ptr in (self.frame_ptr, self.rec_ptr):
+        self.images = []
+        for ptr in self.frame_ptrs + self.rec_ptrs:
             if ptr:
                 (rt.ipc_free if self.rank == 0 else rt.ipc_close)(ptr)
-        self.frame_ptr = self.rec_ptr = None
+        self.frame_ptrs, self.rec_ptrs = [], []
 
 
 class CudaBackend:
