@@ -139,6 +139,7 @@ struct Context {
   cudaGraphExec_t graph_exec = nullptr;
   int graph_n = 0, graph_launches = 0, graph_chunks = 0;
   std::vector<int> graph_chunk_items;
+  std::vector<unsigned> hint0, hint1;  // queue counters of the render before the capture
 };
 
 Context g_ctx;
@@ -293,8 +294,25 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
     return RT_OK;
   }
   // second consecutive render with this key: capture on cap_stream (forked from c.stream so the
-  // capture sees the same order), instantiate, launch on c.stream
+  // capture sees the same order), instantiate, launch on c.stream. The previous render (same
+  // sequence) left its queue lengths in the counters of each buffer set: with them, each scan is
+  // captured as one kernel (long-queue scan or split variant) instead of the self-selecting pair.
   drop_graph(c);
+#ifndef RT_SCAN_HINTS
+#define RT_SCAN_HINTS 1
+#endif
+  if (RT_SCAN_HINTS) {
+    const size_t nctr = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
+    CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
+    c.hint0.assign(nctr, 0u);
+    CU(cudaMemcpy(c.hint0.data(), c.wf_ctr.p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
+    tm.hint[0] = c.hint0.data();
+    if (tm.B2 && c.wf_ctr2.p) {
+      c.hint1.assign(nctr, 0u);
+      CU(cudaMemcpy(c.hint1.data(), c.wf_ctr2.p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
+      tm.hint[1] = c.hint1.data();
+    }
+  }
   if (!c.cap_stream) CU(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   // per-launch timing events become event-record nodes, which serialise the graph around every
   // scan and shade launch: kept for the in-order timing mode (rt_set_concurrency(0)), dropped

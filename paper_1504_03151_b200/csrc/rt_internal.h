@@ -146,6 +146,10 @@ struct WfBuffers {
   float* xlo_c;    // [xctas * 8 * 32 * kCandMax] lower bound of each closest candidate's root
   int* xcand_s;    // [xctas * 8 * 64 * kCandMax]
   int xctas;
+  // 0: a scan kernel and its split variant are launched as a pair and exactly one works;
+  // 1 (set on the copy passed to a launch): the kernel is the only one launched and works
+  // whatever the queue length (the host chose it from the previous frame's queue lengths)
+  int solo;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
@@ -189,6 +193,10 @@ struct WfTiming {
   cudaEvent_t start_ev = nullptr, done2_ev = nullptr;
   // optional: an event recorded after each chunk's resolve, and the work items resolved so far,
   // so the host can copy finished framebuffer rows while later chunks render
+  // queue counters of the previous render with the same launch sequence, per buffer set (host
+  // copies; null = unknown): each scan is then launched as one kernel, the long-queue scan or
+  // its split variant, instead of the pair
+  const unsigned* hint[2] = {nullptr, nullptr};
   cudaEvent_t* chunk_done = nullptr;
   int* chunk_items = nullptr;
   int chunk_cap = 0;

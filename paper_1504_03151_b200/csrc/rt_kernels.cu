@@ -624,6 +624,7 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
   B.lmask = reinterpret_cast<unsigned long long*>(take(8 * (size_t)cap));
   B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.xctas = xctas;
+  B.solo = 0;
   B.xcand_c = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xlo_c = reinterpret_cast<float*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xcand_s = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 64 * kCandMax));
@@ -719,6 +720,14 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
 #define RT_LOGIC_GRID_PER_SM 8
 #endif
   const int grid_l = num_sms * RT_LOGIC_GRID_PER_SM;  // logic kernels: grid-stride loops
+  // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length
+  auto host_parts = [&](unsigned tasks, int grid) -> int {
+    if (grid > B0.xctas) return 1;
+    const unsigned warps = (unsigned)grid * 8u;
+    int pp = 1;
+    while (pp < RT_SPLIT_MAX && tasks * (unsigned)pp * RT_SPLIT_SLACK <= warps) pp <<= 1;
+    return pp;
+  };
   const bool pipe = tm.B2 != nullptr;
   const int items_per_chunk = wf_items_per_chunk(p, B0.cap, pipe);
   tm.n = 0;
@@ -741,6 +750,9 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const cudaStream_t side = odd ? tm.side2 : tm.side;
     cudaEvent_t* fork = odd ? tm.fork2 : tm.fork;
     cudaEvent_t* join = odd ? tm.join2 : tm.join;
+    const unsigned* hint = tm.hint[odd ? 1 : 0];
+    WfBuffers Bs = B;  // the copy passed to a single (solo) scan launch
+    Bs.solo = 1;
     const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
     const int npaths = nw * p.spp;
     const long long g0 = (long long)w0 * p.spp;
@@ -760,6 +772,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         launch_pdl(kc0, grid_c, smem, st, p, sc, B, dd);
         if (kc0s && !RT_SPLIT_FUSED) launch_pdl(kc0s, grid_c, smem, st, p, sc, B, dd);
         tm.launches += (kc0s && !RT_SPLIT_FUSED) ? 2 : 1;
+      } else if (hint && !RT_SPLIT_FUSED) {  // one kernel, chosen from the previous frame's queue
+        if (host_parts((hint[wf_ctr_q(dd)] + 31u) / 32u, grid_c) > 1)
+          launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+        else
+          launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+        tm.launches += 1;
       } else {
         launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
         if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
@@ -783,13 +801,32 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         ss = side;
       }
       if (rec) tm.record(tm.shadow[2 * ti], ss);
+      int scan_launches = 0;
       if (klt) {  // point lights, from the light
-        launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, B, d);
-        if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, B, d);
+        if (hint && !RT_SPLIT_FUSED) {
+          unsigned chunks = 0;
+          for (int l = 0; l < p.lt_lights; ++l) chunks += (hint[wf_ctr_lt(d, l)] + 63u) / 64u;
+          launch_pdl(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
+          scan_launches += 1;
+        } else {
+          launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, B, d);
+          if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, B, d);
+          scan_launches += RT_SPLIT_FUSED ? 1 : 2;
+        }
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
-        launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
-        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
+        if (hint && !RT_SPLIT_FUSED) {
+          const unsigned ns = hint[p.lt_lights > 0 ? wf_ctr_so(d) : wf_ctr_s(d)];
+          if (host_parts((ns + 31u) / 32u, grid_s) > 1)
+            launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
+          else
+            launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
+          scan_launches += 1;
+        } else {
+          launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
+          if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
+          scan_launches += RT_SPLIT_FUSED ? 1 : 2;
+        }
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
       launch_pdl(wf_accumulate, grid_l, 0, ss, p, sc, B, d, o.stats);
@@ -799,8 +836,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaStreamWaitEvent(st, join[d], 0);
       }
       // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
-      tm.launches += 2 + (klt ? (RT_SPLIT_FUSED ? 1 : 2) + (RT_BIN_FUSED ? 0 : 1) : 0) +
-                     ((!klt || p.n_emitters > 0) ? (RT_SPLIT_FUSED ? 1 : 2) : 0);
+      // shade, accumulate, (wf_bin), the shadow scans (closest scans are counted above)
+      tm.launches += 2 + ((klt && !RT_BIN_FUSED) ? 1 : 0) + scan_launches;
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

@@ -333,7 +333,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
   const bool listed = kShadow && P.lt_lights > 0;
   const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
-  if (split_parts((n + 31u) / 32u, B) > 1) {  // a short queue: the split scan
+  if (!B.solo && split_parts((n + 31u) / 32u, B) > 1) {  // a short queue: the split scan
     if (RT_SPLIT_FUSED) wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
     return;
   }
@@ -467,7 +467,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
   const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
   const unsigned tasks = (n + 31u) / 32u;  // 32 rays each
   const int parts = split_parts(tasks, B);
-  if (parts == 1) return;  // a long queue: wf_isect scans it
+  if (parts == 1 && !B.solo) return;  // a long queue: wf_isect scans it (solo: one part here)
   const float4* gp = kEye ? S.pairs_eye : S.pairs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tpc = 8 / parts;  // tasks per CTA unit
@@ -835,7 +835,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
   __syncthreads();
   const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
-  if (split_parts(n_chunks, B) > 1) {  // a short list: the split scan
+  if (!B.solo && split_parts(n_chunks, B) > 1) {  // a short list: the split scan
     if (RT_SPLIT_FUSED) wf_isect_lt_split_body<kSrc>(P, S, B, d);
     return;
   }
@@ -929,7 +929,7 @@ __device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const De
   __syncthreads();
   const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
   const int parts = split_parts(n_chunks, B);
-  if (parts == 1) return;  // a long list: wf_isect_lt scans it
+  if (parts == 1 && !B.solo) return;  // a long list: wf_isect_lt scans it (solo: one part here)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tpc = 8 / parts;  // chunks per CTA unit
   const unsigned units = (n_chunks + tpc - 1) / tpc;
