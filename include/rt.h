@@ -183,8 +183,10 @@ int rt_set_seed(uint64_t seed);
 /* Message of the last failing call on this thread ("" if none). Owned by the library. */
 const char* rt_last_error(void);
 
-/* Shard layout for `world` ranks: the image is cut into RT_TILE_W x RT_TILE_H tiles; tile t
- * belongs to rank t % world (cyclic). tiles_per_rank = ceil(n_tiles / world); slab_bytes =
+/* Shard layout for `world` ranks: the image is cut into RT_TILE_W x RT_TILE_H tiles; rank r owns
+ * one tile of every group of `world` consecutive tiles, its local tile j being the global tile
+ * j * world + (r + j) % world (cyclic, the slot rotating per group so a rank's tiles do not line
+ * up in image columns). tiles_per_rank = ceil(n_tiles / world); slab_bytes =
  * tiles_per_rank * 32 * 16 + 64 (pixel slab, tile-major, then a 64-byte stats record of 8
  * uint64: primary, shadow, secondary, sphere_tests, plane_tests, closest_sphere_tests, 0, 0). */
 int rt_shard_layout(int32_t width, int32_t height, int32_t world, int32_t* tiles_per_rank,
@@ -204,7 +206,7 @@ int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, 
                       float* out_rgba_dev);
 
 /* ---- fused render + gather over NVLink peer memory (SURVEY §8(e) ablation) -------------------
- * Direct shard: render this rank's tiles (the cyclic assignment of rt_shard_layout) and store
+ * Direct shard: render this rank's tiles (the rotated cyclic assignment of rt_shard_layout) and store
  * each finished pixel straight into the row-major frame `frame_dev` — rank 0's framebuffer, a
  * peer pointer (rt_ipc_open) on the other ranks, so the pixels cross NVLink inside the resolve
  * kernel instead of through a slab and an all-gather. The rank's 8-uint64 stats record goes to

@@ -111,13 +111,17 @@ __device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int
                       P.F[2] + a * P.R[2] + b * P.U[2]));
 }
 
-// work item w (tile-major, 8x4 tiles; shard mode maps local tile j to global tile j*world+rank)
+// global tile of a rank's local tile j: one tile of every group of `world` consecutive tiles,
+// the slot rotating with the group (rank_tile_slot), so a rank's tiles do not line up in tile
+// columns (tiles_x is often a multiple of world) and every rank sees the same mix of the image
+__host__ __device__ __forceinline__ int rank_tile(int j, int rank, int world) { return j * world + (rank + j) % world; }
+// work item w (tile-major, 8x4 tiles; shard mode maps local tile j to global tile rank_tile(j))
 // -> pixel; returns false for pixels outside the image / tiles past the end
 __device__ __forceinline__ bool item_pixel(const DevParams& P, int w, int& px, int& py) {
   int t = w / kTilePx;
   const int i = w % kTilePx;
-  if (P.mode >= 1) {  // shard (1) or direct shard (2): local tile j is global tile j*world + rank
-    t = t * P.world + P.rank;
+  if (P.mode >= 1) {  // shard (1) or direct shard (2): local tile j is global tile rank_tile(j)
+    t = rank_tile(t, P.rank, P.world);
     if (t >= P.n_tiles) return false;
   }
   px = (t % P.tiles_x) * kTileW + (i % kTileW);

@@ -65,7 +65,7 @@ __device__ __forceinline__ bool start_item(Lane& L, const DevParams& P, int w, f
   int t = w / kTilePx;
   const int i = w % kTilePx;
   if (P.mode >= 1) {
-    t = t * P.world + P.rank;
+    t = rank_tile(t, P.rank, P.world);
     if (t >= P.n_tiles) {
       if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
       return false;
@@ -468,7 +468,7 @@ __global__ void assemble_kernel(const float4* __restrict__ g, int W, int H, int 
        pix += (long long)gridDim.x * blockDim.x) {
     const int px = (int)(pix % W), py = (int)(pix / W);
     const int t = (py / kTileH) * tiles_x + px / kTileW;
-    const int r = t % world, j = t / world;
+    const int j = t / world, r = ((t % world) - j % world + world) % world;  // inverse of rank_tile
     const int i = (py % kTileH) * kTileW + (px % kTileW);
     out[pix] = g[r * slab_f4 + (long long)j * kTilePx + i];
   }

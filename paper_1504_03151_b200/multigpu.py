@@ -1,6 +1,7 @@
 """Multi-GPU frame driver: image tiles sharded across ranks, one collective per frame.
 
-SURVEY.md §8(e): the image is cut into 8x4-pixel tiles; tile t belongs to rank t % world
+SURVEY.md §8(e): the image is cut into 8x4-pixel tiles; group j of `world` consecutive tiles gives
+rank r its tile j * world + (r + j) % world
 (cyclic, spatially interleaved, statistically balanced); inside a rank, persistent CTAs take the
 rank's tiles dynamically. Each rank renders its tiles into a dense slab (plus a 64-byte stats
 record); ONE all-gather over NCCL (NVLink 5 / NVSwitch) brings the slabs to every rank and rank 0
@@ -40,7 +41,8 @@ def rank_tiles(width: int, height: int, rank: int, world: int) -> list[int]:
     """Global tile ids owned by `rank`, in slab order (cyclic assignment)."""
     tpr, _ = shard_layout(width, height, world)
     _, nt = n_tiles(width, height)
-    return [j * world + rank for j in range(tpr) if j * world + rank < nt]
+    tiles = [j * world + (rank + j) % world for j in range(tpr)]  # rank_tile (rt_device.cuh)
+    return [t for t in tiles if t < nt]
 
 
 class P2PRenderer:
