@@ -159,6 +159,31 @@ __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene&
   return true;
 }
 
+// Does light l send a shadow ray from p (light_sample returns true)? The same decision without
+// normalising w when its sign is certain: light_sample tests cos_s = n.(w * (1/|w|)), whose
+// rounding error is below 8u |w|_1 / |w| (u = 2^-53: the reciprocal, the products and the sum),
+// while the unnormalised t = n.w is within 3u |w|_1 of the exact value. Outside the band
+// |t| <= 1e-14 |w|_1 (~90u) both therefore have the sign of the exact n.w; inside it (and for
+// emitters) light_sample itself decides. Bit-identical decisions, no FP64 sqrt or division
+// in the count pass for almost every light.
+__device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevScene& S, int l, d3 p, d3 nrm,
+                                                 unsigned long long pix, unsigned sg, int depth) {
+#ifndef RT_COUNT_SIGN
+#define RT_COUNT_SIGN 1
+#endif
+  if (RT_COUNT_SIGN && l < P.n_lights) {
+    const DevLight lt = S.lights[l];
+    const d3 w = mk(lt.px, lt.py, lt.pz) - p;
+    if (dot(w, w) < 1e-12) return false;  // the same d^2 test as light_sample
+    const double t = dot(nrm, w);
+    const double band = 1e-14 * (fabs(w.x) + fabs(w.y) + fabs(w.z));
+    if (t > band) return true;
+    if (t < -band) return false;
+  }
+  LightSample ls;
+  return light_sample(P, S, l, p, nrm, pix, sg, depth, ls);
+}
+
 // ---- a2: ray generation -> Q[0] ------------------------------------------------------------
 __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
                                                  unsigned long long* stats) {
@@ -1171,8 +1196,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       if (m.kind == 0) {
         L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
         for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
-          LightSample ls;
-          if (light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) {
+          if (sends_shadow_ray(P, S, l, p, nrm, pix, sg, depth)) {
             ++nsh;
             if (l < 64) lmask |= 1ull << l;
           }
