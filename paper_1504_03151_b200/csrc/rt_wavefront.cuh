@@ -85,6 +85,11 @@ __device__ __forceinline__ void st3(double* a, int cap, int i, int c0, d3 v) {
   a[(c0 + 1) * (size_t)cap + i] = v.y;
   a[(c0 + 2) * (size_t)cap + i] = v.z;
 }
+// origin / skipped sphere of closest-hit entry e of Q[d] (depth 0: the eye, none)
+__device__ __forceinline__ d3 q_origin(const DevParams& P, const WfQueue& Q, int cap, unsigned e, int d) {
+  return d == 0 ? mk(P.eye[0], P.eye[1], P.eye[2]) : ld3(Q.ray, cap, (int)e, 0);
+}
+__device__ __forceinline__ int q_skip(const WfQueue& Q, unsigned e, int d) { return d == 0 ? -1 : Q.skip[e]; }
 __device__ __forceinline__ float3 lf3(const float* a, int cap, int i) {
   return f3(a[i], a[(size_t)cap + i], a[2 * (size_t)cap + i]);
 }
@@ -196,13 +201,11 @@ __global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B,
     const bool valid = item_pixel(P, w, px, py);
     const unsigned slot = warp_reserve(valid ? 1u : 0u, B.ctr + wf_ctr_q(0));
     if (valid) {
+      // camera rays: only the path id and the direction are stored; origin (the eye), throughput
+      // (1), radiance (0), depth (0) and skip (-1) are the same for every entry of Q[0] and are
+      // supplied by the kernels of depth 0 (q_origin / q_skip / wf_shade)
       Q.path[slot] = i;
-      st3(Q.ray, B.cap, slot, 0, mk(P.eye[0], P.eye[1], P.eye[2]));
       st3(Q.ray, B.cap, slot, 3, camera_dir(P, px, py, s));
-      sf3(Q.T, B.cap, slot, f3(1.f, 1.f, 1.f));
-      sf3(Q.L, B.cap, slot, f3(0.f, 0.f, 0.f));
-      Q.depth[slot] = 0;
-      Q.skip[slot] = -1;
     }
     warp_stat(stats, 0, valid ? 1ull : 0ull);
   }
@@ -402,9 +405,9 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
           }
         }
       } else {
-        o = ld3(Q.ray, B.cap, (int)e, 0);
+        o = q_origin(P, Q, B.cap, e, d);
         dir = ld3(Q.ray, B.cap, (int)e, 3);
-        skip = Q.skip[e];
+        skip = q_skip(Q, e, d);
       }
     }
     RayFilterFor<kSrc> F;
@@ -536,9 +539,9 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
           }
         }
       } else {
-        o = ld3(Q.ray, B.cap, (int)e, 0);
+        o = q_origin(P, Q, B.cap, e, d);
         dir = ld3(Q.ray, B.cap, (int)e, 3);
-        skip = Q.skip[e];
+        skip = q_skip(Q, e, d);
       }
     }
     RayFilterFor<kSrc> F;
@@ -650,11 +653,11 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
     {
       d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
       Ra.act = ea < n;
-      if (Ra.act) { o = ld3(Q.ray, B.cap, (int)ea, 0); dir = ld3(Q.ray, B.cap, (int)ea, 3); }
+      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); dir = ld3(Q.ray, B.cap, (int)ea, 3); }
       Ra.F.init(o, dir, P);
       o = mk(0, 0, 0); dir = mk(0, 0, 1);
       Rb.act = eb < n;
-      if (Rb.act) { o = ld3(Q.ray, B.cap, (int)eb, 0); dir = ld3(Q.ray, B.cap, (int)eb, 3); }
+      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); dir = ld3(Q.ray, B.cap, (int)eb, 3); }
       Rb.F.init(o, dir, P);
     }
     Ra.tub = Rb.tub = 3.0e38f;
@@ -1087,6 +1090,34 @@ __device__ __forceinline__ void bin_entries(const DevParams& P, const WfBuffers&
   __syncthreads();  // s_cnt is rewritten by the next iteration
 }
 
+// The same lists built by one warp (all 32 lanes, converged; lmask = 0 for lanes without an
+// entry): one atomicAdd per light per warp instead of per CTA, but no CTA barrier, so the warps
+// of a wf_shade CTA do not wait for its slowest warp (the barrier version spent 44 % of the
+// kernel's warp samples at the first __syncthreads).
+__device__ __forceinline__ void bin_entries_warp(const DevParams& P, const WfBuffers& B, int d, unsigned long long lmask,
+                                                 unsigned off) {
+  const int L = P.lt_lights;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  for (int l = 0; l < L; ++l) {
+    const bool has = (lmask >> l) & 1ull;
+    const unsigned m = __ballot_sync(kFull, has);
+    if (m == 0u) continue;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(B.ctr + wf_ctr_lt(d, l), (unsigned)__popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    if (has) B.slt[(size_t)l * B.cap + base + (unsigned)__popc(m & lt)] =
+        (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
+  }
+  const unsigned long long rest = lmask >> L;
+  const unsigned nrest = (unsigned)__popcll(rest);
+  if (__any_sync(kFull, nrest != 0u)) {
+    unsigned ob = warp_reserve(nrest, B.ctr + wf_ctr_so(d));
+    unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
+    for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
+  }
+}
+
 // the lists as a kernel of their own (RT_BIN_FUSED=0; by default wf_shade builds them)
 __global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
   pdl_enter();
@@ -1123,7 +1154,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     unsigned of = 0u;
     if (e < n) {
     const int path = Q.path[e];
-    const d3 o = ld3(Q.ray, B.cap, (int)e, 0), dir = ld3(Q.ray, B.cap, (int)e, 3);
+    const d3 o = q_origin(P, Q, B.cap, e, d), dir = ld3(Q.ray, B.cap, (int)e, 3);
     double tbest = kInf;
     int hs = -1, hp = -1;
     for (int j = 0; j < P.n_planes; ++j) {
@@ -1134,12 +1165,12 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         if (t >= kEps && t < tbest) { tbest = t; hp = j; }
       }
     }
-    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], Q.skip[e], o, dir, tbest, hs, hp);
+    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
 #ifdef RT_OVF_PROBE
     if (B.cn[e] > kCandMax) atomicAdd(B.ctr + 72 * kWfCtrPerDepth + 4 * d, 1u);
     atomicMax(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 2, (unsigned)B.cn[e]);
 #endif
-    const int dword = Q.depth[e];
+    const int dword = d == 0 ? 0 : Q.depth[e];
     const int depth = dword & 0xff;
     int prim = -1;
     if (hp >= 0) prim = c_planes[hp].prim;
@@ -1152,8 +1183,8 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
       dbg_hits[si * (P.max_depth + 1) + depth] = prim;
     }
-    float3 T = lf3(Q.T, B.cap, (int)e);
-    float3 L = lf3(Q.L, B.cap, (int)e);
+    float3 T = d == 0 ? f3(1.f, 1.f, 1.f) : lf3(Q.T, B.cap, (int)e);
+    float3 L = d == 0 ? f3(0.f, 0.f, 0.f) : lf3(Q.L, B.cap, (int)e);
     bool cont = false;
     const int n_src = P.n_lights + P.n_emitters;  // point lights, then emitters (R#41)
     unsigned long long lmask = 0ull;              // sources 0..63 that send a shadow ray
@@ -1308,7 +1339,13 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
     warp_stat(stats, 5, (unsigned long long)P.n_spheres);
     }
-    if (bin) bin_entries(P, B, d, lm, of, s_cnt);
+#ifndef RT_BIN_WARP
+#define RT_BIN_WARP 0  // measured: C4 +1.6 % (atomic contention outweighs the barrier wait)
+#endif
+    if (bin) {
+      if (RT_BIN_WARP) bin_entries_warp(P, B, d, lm, of);
+      else bin_entries(P, B, d, lm, of, s_cnt);
+    }
   }
 }
 
