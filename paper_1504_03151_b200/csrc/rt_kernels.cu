@@ -717,7 +717,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
 #ifndef RT_LOGIC_GRID_PER_SM
-#define RT_LOGIC_GRID_PER_SM 8
+#define RT_LOGIC_GRID_PER_SM 6  // measured C4 world 1 / 8: 4 -> 7.00 / 1.10 ms, 6 -> 7.03 / 1.084, 8 -> 7.04 / 1.082, 16 -> 7.11 / 1.11
 #endif
   const int grid_l = num_sms * RT_LOGIC_GRID_PER_SM;  // logic kernels: grid-stride loops
   // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length

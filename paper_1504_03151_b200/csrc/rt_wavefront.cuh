@@ -305,7 +305,7 @@ __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S
 #define RT_SPLIT_MAX 8
 #endif
 #ifndef RT_SPLIT_SLACK
-#define RT_SPLIT_SLACK 2  // split while tasks x parts x SLACK <= resident warps
+#define RT_SPLIT_SLACK 4  // split while tasks x parts x SLACK <= resident warps (measured: 2, 4, 8, 16 -> world-8 rank 1.105, 1.082, 1.082, 1.095 ms)
 #endif
 __device__ __forceinline__ int split_parts(unsigned tasks, const WfBuffers& B) {
   if ((int)gridDim.x > B.xctas || blockDim.x != 256) return 1;

@@ -1,6 +1,7 @@
 # Round evidence with the current code (one GPU): bench line, launch list, ncu full capture of
 # the depth-0 kernels, shard scaling, report rows, progressive bench. Writes gpurun_out/ev_*.
 set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ev_pytest.log 2>&1
 python bench.py > gpurun_out/ev_bench_c4.json 2> gpurun_out/ev_bench_c4.err
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/ev_launches_c4.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_list.log 2>&1
