@@ -177,6 +177,12 @@ int rt_set_concurrency(int32_t on);
  * every kernel from the host. Same results bit for bit either way. RT_ERR_INVALID_ARG unless 0/1. */
 int rt_set_graphs(int32_t on);
 
+/* Wavefront kernels, test and tuning knob: -1 (default) splits a scan over 2-8 warps per ray
+ * group only when its queue is short (split scans); 1, 2, 4 or 8 forces that many
+ * parts on every intersection scan (1: never split). Results are bit-identical for every value.
+ * RT_ERR_INVALID_ARG otherwise. */
+int rt_set_scan_split(int32_t parts);
+
 /* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
 int rt_set_seed(uint64_t seed);
 

@@ -150,6 +150,9 @@ struct WfBuffers {
   // 1 (set on the copy passed to a launch): the kernel is the only one launched and works
   // whatever the queue length (the host chose it from the previous frame's queue lengths)
   int solo;
+  // rt_set_scan_split: -1 = by queue length (split_parts); 1, 2, 4 or 8 = that many parts for
+  // every scan (a test and tuning knob)
+  int force_parts;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth

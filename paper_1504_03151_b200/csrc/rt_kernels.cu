@@ -625,6 +625,7 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
   B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.xctas = xctas;
   B.solo = 0;
+  B.force_parts = -1;
   B.xcand_c = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xlo_c = reinterpret_cast<float*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xcand_s = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 64 * kCandMax));
@@ -723,6 +724,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length
   auto host_parts = [&](unsigned tasks, int grid) -> int {
     if (grid > B0.xctas) return 1;
+    if (B0.force_parts > 0) return B0.force_parts;
     const unsigned warps = (unsigned)grid * 8u;
     int pp = 1;
     while (pp < RT_SPLIT_MAX && tasks * (unsigned)pp * RT_SPLIT_SLACK <= warps) pp <<= 1;

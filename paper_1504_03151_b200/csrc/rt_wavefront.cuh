@@ -309,6 +309,7 @@ __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S
 #endif
 __device__ __forceinline__ int split_parts(unsigned tasks, const WfBuffers& B) {
   if ((int)gridDim.x > B.xctas || blockDim.x != 256) return 1;
+  if (B.force_parts > 0) return B.force_parts;
   const unsigned warps = gridDim.x * 8u;
   int p = 1;
   while (p < RT_SPLIT_MAX && tasks * (unsigned)p * RT_SPLIT_SLACK <= warps) p <<= 1;

@@ -80,6 +80,7 @@ def lib() -> C.CDLL:
         "rt_set_integrator": [i32, i32],
         "rt_set_concurrency": [i32],
         "rt_set_graphs": [i32],
+        "rt_set_scan_split": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
         "rt_sum_shard_stats": [vp, i32],
         "rt_ipc_alloc": [i64, C.POINTER(vp), C.c_char_p],
@@ -174,6 +175,11 @@ def set_concurrency(on: bool):
 def set_graphs(on: bool):
     """Wavefront: replay a CUDA graph of the launch sequence for repeated identical renders (default)."""
     _check("rt_set_graphs", lib().rt_set_graphs(1 if on else 0))
+
+
+def set_scan_split(parts: int = -1):
+    """Wavefront scans: -1 split short queues only (default); 1/2/4/8 force that many parts."""
+    _check("rt_set_scan_split", lib().rt_set_scan_split(int(parts)))
 
 
 def set_stream(stream):
