@@ -246,10 +246,18 @@ def run_b200(args):
     local = _env_int("LOCAL_RANK", 0)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # B200RT_DIST_BACKEND=gloo + B200RT_SHARE_GPU=1: every rank on cuda:0 with host barriers — a
+    # smoke test of the multi-rank flow on a one-GPU box (the ranks' kernels never wait on each
+    # other there); the benchmark itself is NCCL, one GPU per rank
+    backend = os.environ.get("B200RT_DIST_BACKEND", "nccl")
+    gpu = 0 if os.environ.get("B200RT_SHARE_GPU") == "1" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     rtbuild.build()  # no-op when the in-tree library is current
     stream = torch.cuda.current_stream()
     rt.set_stream(stream)
@@ -284,7 +292,11 @@ def run_b200(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[gpu])
+            else:
+                torch.cuda.synchronize()
+                dist.barrier()
         torch.cuda.synchronize()
 
     if world > 1:  # kernels per frame on this rank: the shard render (+ assembly or stats sum on rank 0)
@@ -298,7 +310,7 @@ def run_b200(args):
         flush.zero_()
         step()
     barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     clocks.start()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
@@ -378,7 +390,9 @@ def run_b200(args):
            "d2h_bytes_per_step": int(d2h), "steps": ke, "ms_per_step": 1e3 * dt / ke,
            "timing": "host wall clock (max over ranks) around rt_scene_upload + rt_camera_set + "
                      + ("rt_render(pinned host buffer)" if world == 1 else
-                        "rt_render_shard + NCCL all-gather + rt_assemble_tiles + D2H to pinned host")}
+                        ("rt_render_shard_direct (pixels stored into rank 0's frame over peer memory) + per-frame "
+                         "barrier + D2H to pinned host" if isinstance(rend, P2PRenderer) else
+                         "rt_render_shard + NCCL all-gather + rt_assemble_tiles + D2H to pinned host"))}
 
     if rank == 0:
         rays = st["primary"] + st["shadow"] + st["secondary"]
@@ -454,7 +468,7 @@ def run_b200(args):
             line["cpu_baseline"] = cpu_baseline(args.config, target_core_s=args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
     return 0
 
