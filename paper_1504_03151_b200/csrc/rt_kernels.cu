@@ -537,6 +537,7 @@ template <bool kExt>
 static cudaError_t launch_x(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene, int num_sms,
                             cudaStream_t st) {
   const bool dbg = o.dbg_hits != nullptr;
+  const bool ext = p.n_emitters > 0 || p.integrator != 0;  // wf_shade with the NEXT-1/NEXT-2 paths
   if (smem_scene) return dbg ? launch_t<true, true, kExt>(p, sc, o, num_sms, st, nullptr)
                              : launch_t<true, false, kExt>(p, sc, o, num_sms, st, nullptr);
   return dbg ? launch_t<false, true, kExt>(p, sc, o, num_sms, st, nullptr)
@@ -675,6 +676,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
                           WfBuffers& B0, WfTiming& tm, cudaStream_t st0) {
   const cudaStream_t st = st0;  // setup launches (debug fill) go on the caller's stream
   const bool dbg = o.dbg_hits != nullptr;
+  const bool ext = p.n_emitters > 0 || p.integrator != 0;  // wf_shade with the NEXT-1/NEXT-2 paths
   const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
   int occ_c = 0, occ_s = 0;
@@ -792,8 +794,13 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      if (dbg) launch_pdl(wf_shade<true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
-      else launch_pdl(wf_shade<false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
+      if (ext) {
+        if (dbg) launch_pdl(wf_shade<true, true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
+        else launch_pdl(wf_shade<false, true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
+      } else {
+        if (dbg) launch_pdl(wf_shade<true, false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
+        else launch_pdl(wf_shade<false, false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
+      }
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, B, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;

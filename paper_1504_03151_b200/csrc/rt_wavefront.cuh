@@ -129,11 +129,12 @@ struct LightSample {
   float ir, ig, ib;
 };
 constexpr double kPiD = 3.14159265358979323846;
+template <bool kExt = true>  // kExt = false: point lights only (no emitters sampled)
 __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene& S, int l, d3 p, d3 nrm,
                                              unsigned long long pix, unsigned sg, int depth, LightSample& ls) {
   d3 nl = mk(0, 0, 0);
   double r = 0.0;
-  const bool emitter = l >= P.n_lights;
+  const bool emitter = kExt && l >= P.n_lights;
   if (!emitter) {
     const DevLight lt = S.lights[l];
     ls.x = mk(lt.px, lt.py, lt.pz);
@@ -171,6 +172,7 @@ __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene&
 // |t| <= 1e-14 |w|_1 (~90u) both therefore have the sign of the exact n.w; inside it (and for
 // emitters) light_sample itself decides. Bit-identical decisions, no FP64 sqrt or division
 // in the count pass for almost every light.
+template <bool kExt>
 __device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevScene& S, int l, d3 p, d3 nrm,
                                                  unsigned long long pix, unsigned sg, int depth) {
 #ifndef RT_COUNT_SIGN
@@ -186,7 +188,7 @@ __device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevSc
     if (t < -band) return false;
   }
   LightSample ls;
-  return light_sample(P, S, l, p, nrm, pix, sg, depth, ls);
+  return light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);
 }
 
 // ---- a2: ray generation -> Q[0] ------------------------------------------------------------
@@ -1138,7 +1140,9 @@ __global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, in
 #ifndef RT_LOGIC_MIN_BLOCKS
 #define RT_LOGIC_MIN_BLOCKS 4
 #endif
-template <bool kDebug>
+// kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
+// are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance
+template <bool kDebug, bool kExt>
 __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
@@ -1187,7 +1191,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     float3 T = d == 0 ? f3(1.f, 1.f, 1.f) : lf3(Q.T, B.cap, (int)e);
     float3 L = d == 0 ? f3(0.f, 0.f, 0.f) : lf3(Q.L, B.cap, (int)e);
     bool cont = false;
-    const int n_src = P.n_lights + P.n_emitters;  // point lights, then emitters (R#41)
+    const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);  // point lights, then emitters (R#41)
     unsigned long long lmask = 0ull;              // sources 0..63 that send a shadow ray
     // pixel index and global sample index of the path (RNG keys, R#42): 32-bit arithmetic on the
     // chunk-local path id (path = local item * spp + s), computed only when a draw needs them
@@ -1200,7 +1204,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       pix = (unsigned long long)py * P.W + px;
       sg = (unsigned)(P.sample_base + (path - wl * P.spp));
     };
-    if (P.n_emitters > 0 || P.integrator != 0) pixel_sample();
+    if (kExt && (P.n_emitters > 0 || P.integrator != 0)) pixel_sample();
     unsigned nsh = 0;
     d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
     int mi = 0;
@@ -1223,12 +1227,12 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       nrm = entering ? ng : ng * -1.0;
       const DevMat m = S.mats[mi];
       // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
-      const bool sampled = (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
+      const bool sampled = kExt && (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
       if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
       if (m.kind == 0) {
         L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
         for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
-          if (sends_shadow_ray(P, S, l, p, nrm, pix, sg, depth)) {
+          if (sends_shadow_ray<kExt>(P, S, l, p, nrm, pix, sg, depth)) {
             ++nsh;
             if (l < 64) lmask |= 1ull << l;
           }
@@ -1245,7 +1249,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       for (int l = 0; l < n_src; ++l) {
         if (l < 64 && !((lmask >> l) & 1ull)) continue;  // no shadow ray (decided in the count pass)
         LightSample ls;
-        if (!light_sample(P, S, l, p, nrm, pix, sg, depth, ls)) continue;
+        if (!light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls)) continue;
         // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3),
         // or L_e cos_s cos_l / (d^2 pdf) for an emitter sample (Eq. 8, R#41)
         const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
@@ -1254,13 +1258,13 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         const float g = (float)ls.g;
         d3 os, ds;
         double tl;
-        if (l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
+        if (!kExt || l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
         else shadow_ray_to(p, nrm, ls.x, os, ds, tl);
         st3(B.sray, B.scap, (int)k, 0, os);
         st3(B.sray, B.scap, (int)k, 3, ds);
         B.sray[6 * (size_t)B.scap + k] = tl;
         B.sskip[k] = shadow_skip(out_sph, nrm, ds);
-        B.sskip2[k] = l >= P.n_lights ? S.emit_sph[l - P.n_lights] : -1;
+        B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
         sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
                                        fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
         ++k;
@@ -1275,12 +1279,12 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     bool mi_kind_diffuse_global = false;
     if (prim >= 0 && depth < P.max_depth) {
       const DevMat m = S.mats[mi];
-      mi_kind_diffuse_global = m.kind == 0 && P.integrator == 1;
+      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
       if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
         dn = reflect(dir, nrm);
         T = mul(T, f3(m.ar, m.ag, m.ab));
         cont = true;
-      } else if (m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
+      } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
         dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
         T = mul(T, f3(m.ar, m.ag, m.ab));
         cont = true;
@@ -1303,7 +1307,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
           r0 *= r0;
           const double mm = 1.0 - c;
           const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-          if (P.n_emitters == 0 && P.integrator == 0) pixel_sample();
+          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
           const double u = rng_u(P.seed, pix, (int)sg, depth);
           refl = u < F;
           if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
