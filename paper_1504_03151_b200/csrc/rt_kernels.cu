@@ -838,7 +838,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         }
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
-      launch_pdl(wf_accumulate, grid_l, 0, ss, p, sc, B, d, o.stats);
+      // wf_accumulate<false> when no entry aims at an emitter and wf_shade skips the skip2
+      // column (the same condition as there: no extensions, light-origin scans on)
+      if (ext || p.lt_lights == 0) launch_pdl(wf_accumulate<true>, grid_l, 0, ss, p, sc, B, d, o.stats);
+      else launch_pdl(wf_accumulate<false>, grid_l, 0, ss, p, sc, B, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
         cudaEventRecord(join[d], side);

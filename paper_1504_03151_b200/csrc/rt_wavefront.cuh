@@ -397,7 +397,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         dir = ld3(B.sray, B.scap, (int)e, 3);
         tl = B.sray[6 * (size_t)B.scap + e];
         skip = B.sskip[e];
-        skip2 = B.sskip2[e];
+        skip2 = P.n_emitters > 0 ? B.sskip2[e] : -1;  // written only when an entry may aim at an emitter
         // planes first, exactly (FP64): the first plane in index order that occludes decides
         for (int j = 0; j < P.n_planes; ++j) {
           const DevPlane pl = c_planes[j];
@@ -532,7 +532,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
         dir = ld3(B.sray, B.scap, (int)e, 3);
         tl = B.sray[6 * (size_t)B.scap + e];
         skip = B.sskip[e];
-        skip2 = B.sskip2[e];
+        skip2 = P.n_emitters > 0 ? B.sskip2[e] : -1;  // written only when an entry may aim at an emitter
         for (int j = 0; j < P.n_planes; ++j) {  // planes first, exactly (every part alike)
           const DevPlane pl = c_planes[j];
           const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
@@ -1264,7 +1264,8 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
         st3(B.sray, B.scap, (int)k, 3, ds);
         B.sray[6 * (size_t)B.scap + k] = tl;
         B.sskip[k] = shadow_skip(out_sph, nrm, ds);
-        B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
+        // the aimed-at emitter: read by wf_accumulate<true> and by the generic shadow scan only
+        if (kExt || P.lt_lights == 0) B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
         sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
                                        fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
         ++k;
@@ -1355,6 +1356,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
 }
 
 // ---- a5 decision + accumulation of the visible lights, in light order ----------------------
+template <bool kExt>  // false: no emitters, every skip2 is -1 (not read)
 __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
   pdl_enter();
@@ -1377,7 +1379,7 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
           st_pl += (unsigned long long)(-2 - rob + 1);
         } else {
           st_pl += (unsigned long long)P.n_planes;
-          const int skip2 = B.sskip2[j];
+          const int skip2 = kExt ? B.sskip2[j] : -1;
           const int nc = B.sn[j];
           int first = -1;
 #ifdef RT_OVF_PROBE
