@@ -1240,7 +1240,73 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     const unsigned off = warp_reserve(nsh, B.ctr + wf_ctr_s(d));  // converged: ballot/scan/atomic
-    // part 2: shadow entries — the shadow ray itself and the contribution T f_r I cos / d^2
+    // part 3 (before the entries, so the continuation's temporaries are dead during the light
+    // loop): stack-free continuation; Tn = the throughput after the bounce
+    float3 Tn = T;
+    d3 dn = mk(0, 0, 0);
+    bool mi_kind_diffuse_global = false;
+    if (prim >= 0 && depth < P.max_depth) {
+      const DevMat m = S.mats[mi];
+      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
+      if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
+        dn = reflect(dir, nrm);
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
+        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
+        if (m.kr > 0.f) {
+          dn = reflect(dir, nrm);
+          Tn = f3(Tn.x * m.kr, Tn.y * m.kr, Tn.z * m.kr);
+          cont = true;
+        }
+      } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
+        const double ior = m.ior;
+        const double eta = entering ? 1.0 / ior : ior;
+        const double ci = -dot(dir, nrm);
+        const double sin2t = eta * eta * (1.0 - ci * ci);
+        bool refl = sin2t > 1.0;
+        if (!refl) {
+          const double cosT = sqrt(1.0 - sin2t);
+          const double c = entering ? ci : cosT;
+          double r0 = (1.0 - ior) / (1.0 + ior);
+          r0 *= r0;
+          const double mm = 1.0 - c;
+          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
+          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
+          const double u = rng_u(P.seed, pix, (int)sg, depth);
+          refl = u < F;
+          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
+        }
+        if (refl) dn = reflect(dir, nrm);
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      }
+      if (cont) dn = normalize(dn);
+    }
+    B.shcnt[e] = (int)nsh;
+    if constexpr (kDebug) {
+      if (!cont) dbg_bounces[si] = depth;
+    }
+    const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
+    if (cont) {  // the path moves to slot `slot` of Q[d+1] with its whole state
+      Qn.path[slot] = path;
+      st3(Qn.ray, B.cap, (int)slot, 0, p);
+      st3(Qn.ray, B.cap, (int)slot, 3, dn);
+      sf3(Qn.T, B.cap, (int)slot, Tn);
+      sf3(Qn.L, B.cap, (int)slot, L);
+      Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
+      // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
+      // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
+      Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
+      B.nxt[e] = (int)slot;
+    } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
+      sf3(B.Lr, B.cap, path, L);
+      B.nxt[e] = -1 - path;
+    }
+    // part 2 (after the continuation): shadow entries — the shadow ray itself and the contribution T f_r I cos / d^2
     // (Eq. 3, 5, 6); a shadow ray leaving a sphere hit from outside skips it exactly (convexity)
     if (nsh) {
       const DevMat m = S.mats[mi];
@@ -1275,70 +1341,6 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevPa
     lm = lmask;
     of = off;
     if (!RT_BIN_FUSED && P.lt_lights > 0) B.lmask[e] = lmask;  // wf_bin lists the entries per light
-    // part 3: stack-free continuation
-    d3 dn = mk(0, 0, 0);
-    bool mi_kind_diffuse_global = false;
-    if (prim >= 0 && depth < P.max_depth) {
-      const DevMat m = S.mats[mi];
-      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
-      if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
-        dn = reflect(dir, nrm);
-        T = mul(T, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
-        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
-        T = mul(T, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
-        if (m.kr > 0.f) {
-          dn = reflect(dir, nrm);
-          T = f3(T.x * m.kr, T.y * m.kr, T.z * m.kr);
-          cont = true;
-        }
-      } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
-        const double ior = m.ior;
-        const double eta = entering ? 1.0 / ior : ior;
-        const double ci = -dot(dir, nrm);
-        const double sin2t = eta * eta * (1.0 - ci * ci);
-        bool refl = sin2t > 1.0;
-        if (!refl) {
-          const double cosT = sqrt(1.0 - sin2t);
-          const double c = entering ? ci : cosT;
-          double r0 = (1.0 - ior) / (1.0 + ior);
-          r0 *= r0;
-          const double mm = 1.0 - c;
-          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
-          const double u = rng_u(P.seed, pix, (int)sg, depth);
-          refl = u < F;
-          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
-        }
-        if (refl) dn = reflect(dir, nrm);
-        T = mul(T, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      }
-      if (cont) dn = normalize(dn);
-    }
-    B.shcnt[e] = (int)nsh;
-    if constexpr (kDebug) {
-      if (!cont) dbg_bounces[si] = depth;
-    }
-    const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
-    if (cont) {  // the path moves to slot `slot` of Q[d+1] with its whole state
-      Qn.path[slot] = path;
-      st3(Qn.ray, B.cap, (int)slot, 0, p);
-      st3(Qn.ray, B.cap, (int)slot, 3, dn);
-      sf3(Qn.T, B.cap, (int)slot, T);
-      sf3(Qn.L, B.cap, (int)slot, L);
-      Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
-      // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
-      // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
-      Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
-      B.nxt[e] = (int)slot;
-    } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
-      sf3(B.Lr, B.cap, path, L);
-      B.nxt[e] = -1 - path;
-    }
     warp_stat(stats, 1, nsh);
     warp_stat(stats, 2, cont ? 1ull : 0ull);
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
