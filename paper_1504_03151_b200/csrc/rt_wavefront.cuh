@@ -1142,8 +1142,11 @@ __global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, in
 #endif
 // kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
 // are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance
+#ifndef RT_SHADE_MIN_BLOCKS
+#define RT_SHADE_MIN_BLOCKS RT_LOGIC_MIN_BLOCKS
+#endif
 template <bool kDebug, bool kExt>
-__global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
+__global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
   pdl_enter();
