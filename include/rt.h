@@ -183,6 +183,12 @@ int rt_set_graphs(int32_t on);
  * RT_ERR_INVALID_ARG otherwise. */
 int rt_set_scan_split(int32_t parts);
 
+/* Wavefront kernels, test and tuning knob: 1 shades every depth with one warp per path (lane l
+ * evaluates light l); -1 (default) and 0 use one thread per path (the warp-per-path form for
+ * short queues only when the library is built with RT_SHADE_WIDE=1; measured neutral on C4).
+ * Results are bit-identical for every value. RT_ERR_INVALID_ARG unless -1, 0 or 1. */
+int rt_set_shade_wide(int32_t mode);
+
 /* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
 int rt_set_seed(uint64_t seed);
 

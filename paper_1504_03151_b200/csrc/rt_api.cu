@@ -134,6 +134,7 @@ struct Context {
 #endif
   int graphs = RT_WF_GRAPHS;
   int scan_split = -1;  // rt_set_scan_split
+  int shade_wide = -1;  // rt_set_shade_wide
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
   cudaEvent_t ev_cap = nullptr;
   std::string last_key, graph_key;
@@ -379,12 +380,14 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
     rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, 4 * c.num_sms, c.wf_ctr.p);
     c.wf.force_parts = c.scan_split;
+    c.wf.force_wide = c.shade_wide;
     const bool pipe = c.pipeline != 0 && c.concurrent != 0;
     if (pipe) {
       CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
       CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
       rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, 4 * c.num_sms, c.wf_ctr2.p);
       c.wf2.force_parts = c.scan_split;
+      c.wf2.force_wide = c.shade_wide;
       if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.ev_start2) CU(cudaEventCreateWithFlags(&c.ev_start2, cudaEventDisableTiming), "cudaEventCreate");
@@ -690,6 +693,14 @@ int rt_set_scan_split(int32_t parts) {
   if (parts != -1 && parts != 1 && parts != 2 && parts != 4 && parts != 8)
     return fail(RT_ERR_INVALID_ARG, "scan split must be -1, 1, 2, 4 or 8 (got %d)", parts);
   g_ctx.scan_split = parts;
+  return RT_OK;
+}
+
+int rt_set_shade_wide(int32_t mode) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (mode < -1 || mode > 1) return fail(RT_ERR_INVALID_ARG, "shade wide must be -1, 0 or 1 (got %d)", mode);
+  g_ctx.shade_wide = mode;
   return RT_OK;
 }
 

@@ -153,6 +153,8 @@ struct WfBuffers {
   // rt_set_scan_split: -1 = by queue length (split_parts); 1, 2, 4 or 8 = that many parts for
   // every scan (a test and tuning knob)
   int force_parts;
+  // rt_set_shade_wide: -1 = by queue length (shade_wide); 0 = never, 1 = always one warp per path
+  int force_wide;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth

@@ -627,6 +627,7 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
   B.xctas = xctas;
   B.solo = 0;
   B.force_parts = -1;
+  B.force_wide = -1;
   B.xcand_c = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xlo_c = reinterpret_cast<float*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xcand_s = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 64 * kCandMax));
@@ -794,12 +795,26 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      if (ext) {
-        if (dbg) launch_pdl(wf_shade<true, true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
-        else launch_pdl(wf_shade<false, true>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
-      } else {
-        if (dbg) launch_pdl(wf_shade<true, false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, o.dbg_hits, o.dbg_bounces);
-        else launch_pdl(wf_shade<false, false>, grid_l, 0, st, p, sc, B, d, g0, o.stats, (int*)nullptr, (int*)nullptr);
+      {
+        // the path-per-thread shade and the warp-per-path shade (short queues): a self-selecting
+        // pair, or with a hint the one the rule picks (solo)
+        using ShadeFn = void (*)(const DevParams, const DevScene, WfBuffers, int, long long, unsigned long long*, int*, int*);
+        const ShadeFn narrow = ext ? (dbg ? wf_shade<true, true> : wf_shade<false, true>)
+                                   : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
+        const ShadeFn wide = ext ? (dbg ? wf_shade_wide<true, true> : wf_shade_wide<false, true>)
+                                 : (dbg ? wf_shade_wide<true, false> : wf_shade_wide<false, false>);
+        int* dh = dbg ? o.dbg_hits : nullptr;
+        int* db = dbg ? o.dbg_bounces : nullptr;
+        const bool wide_ok = (RT_SHADE_WIDE || B.force_wide == 1) && p.n_lights + p.n_emitters <= 64;
+        if (hint && wide_ok) {
+          const bool w = B.force_wide >= 0 ? B.force_wide == 1 : hint[wf_ctr_q(d)] <= (unsigned)grid_l * 8u / RT_SHADE_WIDE_DIV;
+          launch_pdl(w ? wide : narrow, grid_l, 0, st, p, sc, Bs, d, g0, o.stats, dh, db);
+          tm.launches += 1;
+        } else {
+          launch_pdl(narrow, grid_l, 0, st, p, sc, B, d, g0, o.stats, dh, db);
+          if (wide_ok) launch_pdl(wide, grid_l, 0, st, p, sc, B, d, g0, o.stats, dh, db);
+          tm.launches += wide_ok ? 2 : 1;
+        }
       }
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, B, d);  // per-light lists of the shadow entries
@@ -848,8 +863,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaStreamWaitEvent(st, join[d], 0);
       }
       // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
-      // shade, accumulate, (wf_bin), the shadow scans (closest scans are counted above)
-      tm.launches += 2 + ((klt && !RT_BIN_FUSED) ? 1 : 0) + scan_launches;
+      // accumulate, (wf_bin), the shadow scans (shade and the closest scans are counted above)
+      tm.launches += 1 + ((klt && !RT_BIN_FUSED) ? 1 : 0) + scan_launches;
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;

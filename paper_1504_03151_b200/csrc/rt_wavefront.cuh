@@ -1142,6 +1142,20 @@ __global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, in
 #endif
 // kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
 // are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance
+// measured neutral on C4 (world-8 rank 1.048 ms with and without, thresholds warps / 1, 4, 16):
+// off by default; rt_set_shade_wide(1) still selects it (tested bit-identical)
+#ifndef RT_SHADE_WIDE
+#define RT_SHADE_WIDE 0
+#endif
+#ifndef RT_SHADE_WIDE_DIV
+#define RT_SHADE_WIDE_DIV 1  // one warp per path when the queue holds at most warps / DIV paths
+#endif
+__device__ __forceinline__ bool shade_wide(unsigned n, const DevParams& P, const WfBuffers& B) {
+  if (P.n_lights + P.n_emitters > 64 || blockDim.x != 256) return false;
+  if (B.force_wide >= 0) return B.force_wide == 1;
+  return n <= gridDim.x * 8u / RT_SHADE_WIDE_DIV;
+}
+
 #ifndef RT_SHADE_MIN_BLOCKS
 #define RT_SHADE_MIN_BLOCKS RT_LOGIC_MIN_BLOCKS
 #endif
@@ -1151,6 +1165,7 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
                                                 int* dbg_bounces) {
   pdl_enter();
   const unsigned n = B.ctr[wf_ctr_q(d)];
+  if (!B.solo && (RT_SHADE_WIDE || B.force_wide == 1) && shade_wide(n, P, B)) return;  // wf_shade_wide
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
   __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // fused wf_bin (per-light entry lists)
@@ -1357,6 +1372,211 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
       if (RT_BIN_WARP) bin_entries_warp(P, B, d, lm, of);
       else bin_entries(P, B, d, lm, of, s_cnt);
     }
+  }
+}
+
+// ---- a4 + a6 for short queues: one warp per path ----------------------------------------------
+// The deep depths of a chunk hold a few thousand paths; wf_shade then runs one thread per path
+// and its duration is one thread's latency: the nearest-hit decision, then two passes over up to
+// n_src light samples (FP64 square roots and divisions). Here a warp takes one path: every lane
+// evaluates the hit and the continuation identically (broadcast loads, same arithmetic), lane l
+// evaluates light l (and l + 32) in both passes, and lane 0 writes the path's records. The
+// shadow entries, their per-light lists, the next-queue entry and the statistics are the ones
+// wf_shade writes (list order within a light may differ; every consumer is order-free there).
+// Chosen, like the split scans, when the queue fits one warp per path in the grid.
+template <bool kDebug, bool kExt>
+__global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade_wide(const DevParams P, const DevScene S, WfBuffers B, int d,
+                                                     long long g0, unsigned long long* stats, int* dbg_hits,
+                                                     int* dbg_bounces) {
+  pdl_enter();
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  if (!B.solo && !shade_wide(n, P, B)) return;  // a long queue: wf_shade shades it
+  const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
+  const int w0 = (int)(g0 / P.spp);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);
+  for (unsigned e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nwarps) {  // warp-uniform
+    const int path = Q.path[e];
+    const d3 o = q_origin(P, Q, B.cap, e, d), dir = ld3(Q.ray, B.cap, (int)e, 3);
+    double tbest = kInf;
+    int hs = -1, hp = -1;
+    for (int j = 0; j < P.n_planes; ++j) {
+      const DevPlane pl = c_planes[j];
+      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+      if (fabs(den) >= 1e-12) {
+        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+        if (t >= kEps && t < tbest) { tbest = t; hp = j; }
+      }
+    }
+    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
+    const int dword = d == 0 ? 0 : Q.depth[e];
+    const int depth = dword & 0xff;
+    int prim = -1;
+    if (hp >= 0) prim = c_planes[hp].prim;
+    else if (hs >= 0) prim = S.sph_prim[hs];
+    long long si = 0;
+    if constexpr (kDebug) {
+      const long long g = g0 + path;
+      int px = 0, py = 0;
+      item_pixel(P, (int)(g / P.spp), px, py);
+      si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
+      if (lane == 0) dbg_hits[si * (P.max_depth + 1) + depth] = prim;
+    }
+    const float3 T = d == 0 ? f3(1.f, 1.f, 1.f) : lf3(Q.T, B.cap, (int)e);
+    float3 L = d == 0 ? f3(0.f, 0.f, 0.f) : lf3(Q.L, B.cap, (int)e);
+    unsigned long long pix = 0;
+    unsigned sg = 0;
+    auto pixel_sample = [&]() {
+      const int wl = path / P.spp;
+      int px = 0, py = 0;
+      item_pixel(P, w0 + wl, px, py);
+      pix = (unsigned long long)py * P.W + px;
+      sg = (unsigned)(P.sample_base + (path - wl * P.spp));
+    };
+    if (kExt && (P.n_emitters > 0 || P.integrator != 0)) pixel_sample();
+    d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
+    int mi = 0;
+    bool entering = false, diffuse = false;
+    if (prim < 0) {  // miss -> background
+      L = add(L, mul(T, f3(P.bg[0], P.bg[1], P.bg[2])));
+    } else {
+      p = o + dir * tbest;
+      if (hp >= 0) {
+        const DevPlane pl = c_planes[hp];
+        ng = mk(pl.nx, pl.ny, pl.nz);
+        mi = pl.mat;
+      } else {
+        const float4 cr = __ldg(S.sph_cr + hs);
+        ng = (p - mk(cr.x, cr.y, cr.z)) * (1.0 / (double)cr.w);
+        mi = S.sph_mat[hs];
+      }
+      entering = dot(dir, ng) < 0.0;
+      nrm = entering ? ng : ng * -1.0;
+      const DevMat m = S.mats[mi];
+      const bool sampled = kExt && (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
+      if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
+      if (m.kind == 0) {
+        L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
+        diffuse = true;
+      }
+    }
+    // count pass, one light per lane (two for n_src > 32)
+    const bool s0 = diffuse && lane < n_src && sends_shadow_ray<kExt>(P, S, lane, p, nrm, pix, sg, depth);
+    const bool s1 = diffuse && lane + 32 < n_src && sends_shadow_ray<kExt>(P, S, lane + 32, p, nrm, pix, sg, depth);
+    const unsigned long long lmask =
+        (unsigned long long)__ballot_sync(kFull, s0) | ((unsigned long long)__ballot_sync(kFull, s1) << 32);
+    const unsigned nsh = (unsigned)__popcll(lmask);
+    unsigned off = 0;
+    if (lane == 0 && nsh) off = atomicAdd(B.ctr + wf_ctr_s(d), nsh);
+    off = __shfl_sync(kFull, off, 0);
+    // continuation (every lane alike; lane 0 writes)
+    float3 Tn = T;
+    d3 dn = mk(0, 0, 0);
+    bool cont = false, mi_kind_diffuse_global = false;
+    if (prim >= 0 && depth < P.max_depth) {
+      const DevMat m = S.mats[mi];
+      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
+      if (m.kind == 1) {
+        dn = reflect(dir, nrm);
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (kExt && m.kind == 0 && P.integrator == 1) {
+        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      } else if (m.kind == 0) {
+        if (m.kr > 0.f) {
+          dn = reflect(dir, nrm);
+          Tn = f3(Tn.x * m.kr, Tn.y * m.kr, Tn.z * m.kr);
+          cont = true;
+        }
+      } else {
+        const double ior = m.ior;
+        const double eta = entering ? 1.0 / ior : ior;
+        const double ci = -dot(dir, nrm);
+        const double sin2t = eta * eta * (1.0 - ci * ci);
+        bool refl = sin2t > 1.0;
+        if (!refl) {
+          const double cosT = sqrt(1.0 - sin2t);
+          const double c = entering ? ci : cosT;
+          double r0 = (1.0 - ior) / (1.0 + ior);
+          r0 *= r0;
+          const double mm = 1.0 - c;
+          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
+          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
+          const double u = rng_u(P.seed, pix, (int)sg, depth);
+          refl = u < F;
+          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
+        }
+        if (refl) dn = reflect(dir, nrm);
+        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+        cont = true;
+      }
+      if (cont) dn = normalize(dn);
+    }
+    if (lane == 0) {
+      B.shcnt[e] = (int)nsh;
+      B.shoff[e] = (int)off;
+      if (!RT_BIN_FUSED && P.lt_lights > 0) B.lmask[e] = lmask;
+      if constexpr (kDebug) {
+        if (!cont) dbg_bounces[si] = depth;
+      }
+      if (cont) {
+        const unsigned slot = atomicAdd(B.ctr + wf_ctr_q(d + 1), 1u);
+        Qn.path[slot] = path;
+        st3(Qn.ray, B.cap, (int)slot, 0, p);
+        st3(Qn.ray, B.cap, (int)slot, 3, dn);
+        sf3(Qn.T, B.cap, (int)slot, Tn);
+        sf3(Qn.L, B.cap, (int)slot, L);
+        Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
+        Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
+        B.nxt[e] = (int)slot;
+      } else {
+        sf3(B.Lr, B.cap, path, L);
+        B.nxt[e] = -1 - path;
+      }
+      atomicAdd(stats + 1, (unsigned long long)nsh);
+      atomicAdd(stats + 2, cont ? 1ull : 0ull);
+      atomicAdd(stats + 3, (unsigned long long)P.n_spheres);
+      if (P.n_planes) atomicAdd(stats + 4, (unsigned long long)P.n_planes);
+      atomicAdd(stats + 5, (unsigned long long)P.n_spheres);
+    }
+    // shadow entries: lane l writes light l's (and l + 32's) entry
+    if (nsh) {
+      const DevMat m = S.mats[mi];
+      const int out_sph = (hs >= 0 && entering) ? hs : -1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        if (!((lmask >> l) & 1ull)) continue;
+        LightSample ls;
+        light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);  // true: the count pass decided
+        const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
+        const float alpha = (float)fmax(0.0, -dot(rl, dir));
+        const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+        const float g = (float)ls.g;
+        d3 os, ds;
+        double tl;
+        if (!kExt || l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
+        else shadow_ray_to(p, nrm, ls.x, os, ds, tl);
+        const unsigned k = off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull));
+        st3(B.sray, B.scap, (int)k, 0, os);
+        st3(B.sray, B.scap, (int)k, 3, ds);
+        B.sray[6 * (size_t)B.scap + k] = tl;
+        B.sskip[k] = shadow_skip(out_sph, nrm, ds);
+        if (kExt || P.lt_lights == 0) B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
+        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
+                                       fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
+        // the per-light lists of the light-origin scans (fused wf_bin), or the rest
+        if (RT_BIN_FUSED && P.lt_lights > 0) {
+          if (l < P.lt_lights) B.slt[(size_t)l * B.cap + atomicAdd(B.ctr + wf_ctr_lt(d, l), 1u)] = (int)k;
+          else B.sother[atomicAdd(B.ctr + wf_ctr_so(d), 1u)] = (int)k;
+        }
+      }
+    }
+    (void)lt;
   }
 }
 
