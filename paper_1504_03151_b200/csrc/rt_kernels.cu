@@ -731,6 +731,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const unsigned warps = (unsigned)grid * 8u;
     int pp = 1;
     while (pp < RT_SPLIT_MAX && tasks * (unsigned)pp * RT_SPLIT_SLACK <= warps) pp <<= 1;
+    if (pp == 1 && RT_SPLIT_MID > 0 && tasks * 2u <= warps * (unsigned)RT_SPLIT_MID) pp = 2;
     return pp;
   };
   const bool pipe = tm.B2 != nullptr;

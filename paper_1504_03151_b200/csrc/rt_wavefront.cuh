@@ -306,6 +306,9 @@ __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S
 #ifndef RT_SPLIT_MAX
 #define RT_SPLIT_MAX 8
 #endif
+#ifndef RT_SPLIT_MID
+#define RT_SPLIT_MID 0  // > 0: two parts also while tasks <= warps * MID / 2 (the last-task tail)
+#endif
 #ifndef RT_SPLIT_SLACK
 #define RT_SPLIT_SLACK 4  // split while tasks x parts x SLACK <= resident warps (measured: 2, 4, 8, 16 -> world-8 rank 1.105, 1.082, 1.082, 1.095 ms)
 #endif
@@ -315,6 +318,7 @@ __device__ __forceinline__ int split_parts(unsigned tasks, const WfBuffers& B) {
   const unsigned warps = gridDim.x * 8u;
   int p = 1;
   while (p < RT_SPLIT_MAX && tasks * (unsigned)p * RT_SPLIT_SLACK <= warps) p <<= 1;
+  if (p == 1 && RT_SPLIT_MID > 0 && tasks * 2u <= warps * (unsigned)RT_SPLIT_MID) p = 2;  // halve the last task
   return p;
 }
 // batch-aligned pair range of part `part` of `parts`
