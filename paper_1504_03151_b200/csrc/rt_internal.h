@@ -155,6 +155,9 @@ struct WfBuffers {
   int force_parts;
   // rt_set_shade_wide: -1 = by queue length (shade_wide); 0 = never, 1 = always one warp per path
   int force_wide;
+  // set per chunk on the copies passed to its launches: global sample index of the chunk's path 0
+  // (the camera rays of depth 0 are implicit: entry e of Q[0] is path e, its ray computed on use)
+  long long g0;
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth

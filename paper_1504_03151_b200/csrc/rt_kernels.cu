@@ -537,7 +537,6 @@ template <bool kExt>
 static cudaError_t launch_x(const DevParams& p, const DevScene& sc, const DevOutputs& o, bool smem_scene, int num_sms,
                             cudaStream_t st) {
   const bool dbg = o.dbg_hits != nullptr;
-  const bool ext = p.n_emitters > 0 || p.integrator != 0;  // wf_shade with the NEXT-1/NEXT-2 paths
   if (smem_scene) return dbg ? launch_t<true, true, kExt>(p, sc, o, num_sms, st, nullptr)
                              : launch_t<true, false, kExt>(p, sc, o, num_sms, st, nullptr);
   return dbg ? launch_t<false, true, kExt>(p, sc, o, num_sms, st, nullptr)
@@ -751,20 +750,23 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   int chunk = 0;
   for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk, ++chunk) {
     const bool odd = pipe && (chunk & 1);
-    WfBuffers& B = odd ? *tm.B2 : B0;
+    WfBuffers& Bset = odd ? *tm.B2 : B0;
     const cudaStream_t st = odd ? tm.main2 : st0;
     const cudaStream_t side = odd ? tm.side2 : tm.side;
     cudaEvent_t* fork = odd ? tm.fork2 : tm.fork;
     cudaEvent_t* join = odd ? tm.join2 : tm.join;
     const unsigned* hint = tm.hint[odd ? 1 : 0];
-    WfBuffers Bs = B;  // the copy passed to a single (solo) scan launch
+    WfBuffers Bc = Bset;  // this chunk's launches: the buffer set with the chunk's first sample
+    Bc.g0 = (long long)w0 * p.spp;
+    WfBuffers Bs = Bc;  // the copy passed to a single (solo) kernel launch
     Bs.solo = 1;
     const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
     const int npaths = nw * p.spp;
     const long long g0 = (long long)w0 * p.spp;
-    if ((e = cudaMemsetAsync(B.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(Bc.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
     const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
-    launch_pdl(wf_raygen, grid_r, 0, st, p, B, g0, npaths, o.stats);
+    if (RT_Q0_IMPLICIT) launch_pdl(wf_q0_len, 1, 0, st, Bc, npaths);  // camera rays computed on use
+    else launch_pdl(wf_raygen, grid_r, 0, st, p, Bc, g0, npaths, o.stats);
     // per depth d: closest scan (d) -> shade (d) -> { shadow scan (d) -> accumulate (d) on the side
     // stream  ||  closest scan (d + 1) on the main stream } -> join -> shade (d + 1) ...
     // (independent: the shadow side reads the shadow entries and writes L into Q[d+1]; the closest
@@ -775,8 +777,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const bool rec = ti < tm.cap;
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
-        launch_pdl(kc0, grid_c, smem, st, p, sc, B, dd);
-        if (kc0s && !RT_SPLIT_FUSED) launch_pdl(kc0s, grid_c, smem, st, p, sc, B, dd);
+        launch_pdl(kc0, grid_c, smem, st, p, sc, Bc, dd);
+        if (kc0s && !RT_SPLIT_FUSED) launch_pdl(kc0s, grid_c, smem, st, p, sc, Bc, dd);
         tm.launches += (kc0s && !RT_SPLIT_FUSED) ? 2 : 1;
       } else if (hint && !RT_SPLIT_FUSED) {  // one kernel, chosen from the previous frame's queue
         if (host_parts((hint[wf_ctr_q(dd)] + 31u) / 32u, grid_c) > 1)
@@ -785,8 +787,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
           launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
         tm.launches += 1;
       } else {
-        launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
-        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, B, dd);
+        launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
+        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
         tm.launches += RT_SPLIT_FUSED ? 1 : 2;
       }
       if (rec) tm.record(tm.closest[2 * ti + 1], st);
@@ -806,19 +808,19 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
                                  : (dbg ? wf_shade_wide<true, false> : wf_shade_wide<false, false>);
         int* dh = dbg ? o.dbg_hits : nullptr;
         int* db = dbg ? o.dbg_bounces : nullptr;
-        const bool wide_ok = (RT_SHADE_WIDE || B.force_wide == 1) && p.n_lights + p.n_emitters <= 64;
+        const bool wide_ok = (RT_SHADE_WIDE || Bc.force_wide == 1) && p.n_lights + p.n_emitters <= 64;
         if (hint && wide_ok) {
-          const bool w = B.force_wide >= 0 ? B.force_wide == 1 : hint[wf_ctr_q(d)] <= (unsigned)grid_l * 8u / RT_SHADE_WIDE_DIV;
+          const bool w = Bc.force_wide >= 0 ? Bc.force_wide == 1 : hint[wf_ctr_q(d)] <= (unsigned)grid_l * 8u / RT_SHADE_WIDE_DIV;
           launch_pdl(w ? wide : narrow, grid_l, 0, st, p, sc, Bs, d, g0, o.stats, dh, db);
           tm.launches += 1;
         } else {
-          launch_pdl(narrow, grid_l, 0, st, p, sc, B, d, g0, o.stats, dh, db);
-          if (wide_ok) launch_pdl(wide, grid_l, 0, st, p, sc, B, d, g0, o.stats, dh, db);
+          launch_pdl(narrow, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
+          if (wide_ok) launch_pdl(wide, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
           tm.launches += wide_ok ? 2 : 1;
         }
       }
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
-      if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, B, d);  // per-light lists of the shadow entries
+      if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, Bc, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (side) {
         cudaEventRecord(fork[d], st);
@@ -834,8 +836,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
           launch_pdl(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, B, d);
-          if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, B, d);
+          launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
+          if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, Bc, d);
           scan_launches += RT_SPLIT_FUSED ? 1 : 2;
         }
       }
@@ -848,16 +850,16 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
             launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
-          if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, B, d);
+          launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
+          if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
           scan_launches += RT_SPLIT_FUSED ? 1 : 2;
         }
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
       // wf_accumulate<false> when no entry aims at an emitter and wf_shade skips the skip2
       // column (the same condition as there: no extensions, light-origin scans on)
-      if (ext || p.lt_lights == 0) launch_pdl(wf_accumulate<true>, grid_l, 0, ss, p, sc, B, d, o.stats);
-      else launch_pdl(wf_accumulate<false>, grid_l, 0, ss, p, sc, B, d, o.stats);
+      if (ext || p.lt_lights == 0) launch_pdl(wf_accumulate<true>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
+      else launch_pdl(wf_accumulate<false>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
         cudaEventRecord(join[d], side);
@@ -869,7 +871,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
-    launch_pdl(wf_resolve, grid_w, 0, st, p, B, w0, nw, o.out, o.accum);
+    launch_pdl(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum);
     tm.launches += 2;
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
       tm.record(tm.chunk_done[tm.n_chunks], st);

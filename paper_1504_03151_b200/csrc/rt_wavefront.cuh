@@ -70,11 +70,15 @@ __device__ __forceinline__ unsigned warp_reserve1(bool take, unsigned* counter) 
   return __shfl_sync(act, base, leader) + (unsigned)__popc(m & lanemask_lt());
 }
 
+// warp-aggregated statistics for ANY set of active lanes (a butterfly of shuffles would read
+// inactive lanes, e.g. the work items outside the image between valid ones): two 32-bit
+// reductions over the active mask (low 20 bits and the rest; per-lane values < 2^52)
 __device__ __forceinline__ void warp_stat(unsigned long long* stats, int k, unsigned long long v) {
   const unsigned act = __activemask();
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(act, v, off);
-  if ((threadIdx.x & 31) == (__ffs(act) - 1) && v) atomicAdd(stats + k, v);
+  const unsigned lo = __reduce_add_sync(act, (unsigned)(v & 0xFFFFFull));
+  const unsigned hi = __reduce_add_sync(act, (unsigned)(v >> 20));
+  const unsigned long long sum = ((unsigned long long)hi << 20) + lo;
+  if ((threadIdx.x & 31) == (__ffs(act) - 1) && sum) atomicAdd(stats + k, sum);
 }
 
 __device__ __forceinline__ d3 ld3(const double* a, int cap, int i, int c0) {
@@ -90,6 +94,27 @@ __device__ __forceinline__ d3 q_origin(const DevParams& P, const WfQueue& Q, int
   return d == 0 ? mk(P.eye[0], P.eye[1], P.eye[2]) : ld3(Q.ray, cap, (int)e, 0);
 }
 __device__ __forceinline__ int q_skip(const WfQueue& Q, unsigned e, int d) { return d == 0 ? -1 : Q.skip[e]; }
+#ifndef RT_Q0_IMPLICIT
+#define RT_Q0_IMPLICIT 1
+#endif
+// direction of closest-hit entry e of Q[d]. Depth 0 (RT_Q0_IMPLICIT): entry e is the chunk's
+// path e, whose camera ray is computed here exactly as wf_raygen would store it; false for a
+// work item outside the image (partial edge tiles, shard tiles past the end)
+__device__ __forceinline__ bool q_dir(const DevParams& P, const WfBuffers& B, const WfQueue& Q, unsigned e, int d,
+                                      d3& dir) {
+  if (RT_Q0_IMPLICIT && d == 0) {
+    const long long g = B.g0 + e;
+    int px = 0, py = 0;
+    if (!item_pixel(P, (int)(g / P.spp), px, py)) return false;
+    dir = camera_dir(P, px, py, (int)(g % P.spp));
+    return true;
+  }
+  dir = ld3(Q.ray, B.cap, (int)e, 3);
+  return true;
+}
+__device__ __forceinline__ int q_path(const WfQueue& Q, unsigned e, int d) {
+  return (RT_Q0_IMPLICIT && d == 0) ? (int)e : Q.path[e];
+}
 __device__ __forceinline__ float3 lf3(const float* a, int cap, int i) {
   return f3(a[i], a[(size_t)cap + i], a[2 * (size_t)cap + i]);
 }
@@ -189,6 +214,12 @@ __device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevSc
   }
   LightSample ls;
   return light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);
+}
+
+// ---- a2 with the implicit camera queue: only its length (the rays are computed on use) ---------
+__global__ void wf_q0_len(WfBuffers B, int n) {
+  pdl_enter();
+  if (threadIdx.x == 0) B.ctr[wf_ctr_q(0)] = (unsigned)n;
 }
 
 // ---- a2: ray generation -> Q[0] ------------------------------------------------------------
@@ -413,7 +444,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         }
       } else {
         o = q_origin(P, Q, B.cap, e, d);
-        dir = ld3(Q.ray, B.cap, (int)e, 3);
+        if (!q_dir(P, B, Q, e, d, dir)) act = false;  // outside the image: no candidates
         skip = q_skip(Q, e, d);
       }
     }
@@ -547,7 +578,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
         }
       } else {
         o = q_origin(P, Q, B.cap, e, d);
-        dir = ld3(Q.ray, B.cap, (int)e, 3);
+        if (!q_dir(P, B, Q, e, d, dir)) act = false;  // outside the image: no candidates
         skip = q_skip(Q, e, d);
       }
     }
@@ -660,11 +691,11 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
     {
       d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
       Ra.act = ea < n;
-      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); dir = ld3(Q.ray, B.cap, (int)ea, 3); }
+      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); Ra.act = q_dir(P, B, Q, ea, d, dir); }
       Ra.F.init(o, dir, P);
       o = mk(0, 0, 0); dir = mk(0, 0, 1);
       Rb.act = eb < n;
-      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); dir = ld3(Q.ray, B.cap, (int)eb, 3); }
+      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
       Rb.F.init(o, dir, P);
     }
     Ra.tub = Rb.tub = 3.0e38f;
@@ -1179,9 +1210,12 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
     const unsigned e = e0 + threadIdx.x;
     unsigned long long lm = 0ull;  // sources with a shadow ray, and the first entry, for the lists
     unsigned of = 0u;
-    if (e < n) {
-    const int path = Q.path[e];
-    const d3 o = q_origin(P, Q, B.cap, e, d), dir = ld3(Q.ray, B.cap, (int)e, 3);
+    d3 dir = mk(0, 0, 1);
+    const bool valid = e < n && q_dir(P, B, Q, e, d, dir);
+    if (e < n && !valid) B.shcnt[e] = 0;  // a work item outside the image (depth 0): nothing to shade
+    if (valid) {
+    const int path = q_path(Q, e, d);
+    const d3 o = q_origin(P, Q, B.cap, e, d);
     double tbest = kInf;
     int hs = -1, hp = -1;
     for (int j = 0; j < P.n_planes; ++j) {
@@ -1368,6 +1402,7 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
     warp_stat(stats, 5, (unsigned long long)P.n_spheres);
+    if (RT_Q0_IMPLICIT && d == 0) warp_stat(stats, 0, 1ull);  // primary rays (wf_raygen otherwise)
     }
 #ifndef RT_BIN_WARP
 #define RT_BIN_WARP 0  // measured: C4 +1.6 % (atomic contention outweighs the barrier wait)
@@ -1402,8 +1437,13 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade_wide(const 
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);
   for (unsigned e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nwarps) {  // warp-uniform
-    const int path = Q.path[e];
-    const d3 o = q_origin(P, Q, B.cap, e, d), dir = ld3(Q.ray, B.cap, (int)e, 3);
+    d3 dir = mk(0, 0, 1);
+    if (!q_dir(P, B, Q, e, d, dir)) {  // a work item outside the image (depth 0)
+      if (lane == 0) B.shcnt[e] = 0;
+      continue;
+    }
+    const int path = q_path(Q, e, d);
+    const d3 o = q_origin(P, Q, B.cap, e, d);
     double tbest = kInf;
     int hs = -1, hp = -1;
     for (int j = 0; j < P.n_planes; ++j) {
@@ -1546,6 +1586,7 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade_wide(const 
       atomicAdd(stats + 3, (unsigned long long)P.n_spheres);
       if (P.n_planes) atomicAdd(stats + 4, (unsigned long long)P.n_planes);
       atomicAdd(stats + 5, (unsigned long long)P.n_spheres);
+      if (RT_Q0_IMPLICIT && d == 0) atomicAdd(stats + 0, 1ull);
     }
     // shadow entries: lane l writes light l's (and l + 32's) entry
     if (nsh) {
