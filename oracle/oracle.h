@@ -18,6 +18,13 @@
  * brute-force bisection of Eq. 9 along the ray, BRDF/Phong hemisphere normalisation
  * quadrature, splitmix64 reference vector, invariants (miss -> background bit-exact,
  * linearity, depth monotonicity, partition invariance).
+ * Continuation and shadow arithmetic (tests/test_oracle_continuation.py): Schlick closed forms
+ * and the exit-side cosine, DIFFUSE-kr and coloured-glass weights,
+ * the p + EPS_T n shadow origin, the [EPS_T, t_max) interval, ambient at DIFFUSE hits
+ * only (R#4), ties to the lowest index, the inclusive EPS_T threshold, the RNG
+ * composition against an independent splitmix64 stream, hand-counted test counts in
+ * index order (§8(c).1 step 11). tools/oracle_mutations.py applies 16 plausible mistakes to this
+ * file; each one fails at least one of these tests (profiles/r02_oracle_mutations.txt).
  * NEXT-1 / NEXT-2 extensions (tests/test_oracle_next.py): sphere-irradiance closed form and an
  * independent quadrature for the area-light estimator, cosine-lobe moments, furnace and
  * constant-sky closed forms for the global bounce, SPEC S:148-150 / S:166-168 / S:302-303

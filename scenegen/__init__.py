@@ -17,7 +17,8 @@ these are sphere/plane scenes shaped like the paper's workload (spheres only, PA
 Primitive convention (shared input contract, not method arithmetic):
   type 0 = sphere, p = (cx, cy, cz, radius)
   type 1 = plane,  p = (nx, ny, nz, d) with unit n and n.x = d
-Planes are emitted before spheres so that index order == "planes first" order.
+Planes are emitted before spheres so that index order == "planes first" order (except
+``build(keep_order=True)`` / ``random_tiny(interleave=True)``: interleaved-order parity cases).
 Material kinds: 0 DIFFUSE, 1 SPECULAR, 2 REFRACTIVE.
 """
 from __future__ import annotations
@@ -129,9 +130,14 @@ class _Builder:
         self.lights.append((pos, intensity))
 
     def build(self, name, eye, look_at, up, vfov, width, height, max_depth, spp,
-              background=(0, 0, 0), ambient=(0, 0, 0), seed=0, notes="") -> Scene:
-        # planes first (stable), so index order equals the "planes, then spheres" test order
-        prims = [p for p in self.prims if p[0] == PLANE] + [p for p in self.prims if p[0] == SPHERE]
+              background=(0, 0, 0), ambient=(0, 0, 0), seed=0, notes="", keep_order=False) -> Scene:
+        # planes first (stable) by default, so index order equals the "planes, then spheres" order
+        # of the generated configs; keep_order=True keeps the insertion order (interleaved
+        # sphere/plane indices: tie-break and test-count parity cases)
+        if keep_order:
+            prims = list(self.prims)
+        else:
+            prims = [p for p in self.prims if p[0] == PLANE] + [p for p in self.prims if p[0] == SPHERE]
         f32 = np.float32
         m = self.mats
         L = self.lights
@@ -338,19 +344,37 @@ def get(name: str) -> Scene:
 
 def random_tiny(seed: int, n_spheres: int = 6, n_planes: int = 1, n_lights: int = 2,
                 width: int = 12, height: int = 9, max_depth: int = 3, spp: int = 1,
-                n_emitters: int = 0) -> Scene:
-    """Tiny random scenes for brute-force and randomized parity tests (all material kinds)."""
+                n_emitters: int = 0, glass_tint: bool = False, interleave: bool = False) -> Scene:
+    """Tiny random scenes for brute-force and randomized parity tests (all material kinds).
+    glass_tint: REFRACTIVE materials get a random albedo in [0.3, 1]^3 instead of (1, 1, 1) (the
+    glass weight T *= rho, is then visible). interleave: the planes are inserted between
+    the spheres and the primitive order is kept (plane indices interleaved with sphere indices)."""
     g = SplitMix64(0xC0FFEE ^ seed)
     b = _Builder()
-    for i in range(n_planes):
-        if i == 0:
-            b.plane((0, 1, 0), 0.0, _mixed_material(b, g, 0.5))
-        else:
-            b.plane((0, 0, -1), -12.0, _mixed_material(b, g, 0.5))
-    for _ in range(n_spheres):
+
+    def material():
+        m = _mixed_material(b, g, 0.5)
+        if glass_tint and b.mats[m]["kind"] == REFRACTIVE:
+            b.mats[m]["albedo"] = (_f32(g.uniform(0.3, 1)), _f32(g.uniform(0.3, 1)), _f32(g.uniform(0.3, 1)))
+        return m
+
+    def add_planes():
+        for i in range(n_planes):
+            if i == 0:
+                b.plane((0, 1, 0), 0.0, material())
+            else:
+                b.plane((0, 0, -1), -12.0, material())
+
+    if not interleave:
+        add_planes()
+    for k in range(n_spheres):
+        if interleave and k == n_spheres // 2:
+            add_planes()
         r = _f32(g.uniform(0.3, 1.5))
         c = (_f32(g.uniform(-4, 4)), _f32(g.uniform(0.2, 3)), _f32(g.uniform(2, 9)))
-        b.sphere(c, r, _mixed_material(b, g, 0.5))
+        b.sphere(c, r, material())
+    if interleave and n_spheres == 0:
+        add_planes()
     for _ in range(n_emitters):  # spherical area lights (NEXT-1): emissive DIFFUSE spheres
         r = _f32(g.uniform(0.2, 0.6))
         c = (_f32(g.uniform(-4, 4)), _f32(g.uniform(3, 6)), _f32(g.uniform(1, 8)))
@@ -361,7 +385,7 @@ def random_tiny(seed: int, n_spheres: int = 6, n_planes: int = 1, n_lights: int 
         b.light((_f32(g.uniform(-5, 5)), _f32(g.uniform(4, 8)), _f32(g.uniform(-2, 6))), (I, I * 0.9, I * 0.8))
     return b.build(f"tiny{seed}", eye=(0, 2, -6), look_at=(0, 1, 5), up=(0, 1, 0), vfov=55,
                    width=width, height=height, max_depth=max_depth, spp=spp,
-                   background=(0.1, 0.2, 0.3), ambient=(0.03, 0.03, 0.03), seed=seed)
+                   background=(0.1, 0.2, 0.3), ambient=(0.03, 0.03, 0.03), seed=seed, keep_order=interleave)
 
 
 _KIND_NAMES = {DIFFUSE: "diffuse", SPECULAR: "specular", REFRACTIVE: "refractive"}
