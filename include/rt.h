@@ -100,9 +100,10 @@ typedef struct {
 /* Ray statistics of the last rt_render / rt_render_shard / rt_assemble_tiles (BJ "rt_stats
  * (rays_cast)"). primary + shadow + secondary = rays cast (BJ metric). sphere_tests and
  * plane_tests are the algorithmic test counts of SURVEY §8(c).1 step 11 (closest-hit rays
- * test every primitive; shadow rays stop at the first occluder in index order when planes
- * precede spheres in the primitive list). last_render_ms: device time of the render kernel
- * (CUDA events on the library stream; 0 for rt_assemble_tiles). 96 bytes. */
+ * test every primitive; shadow rays count the primitives up to and including the first
+ * occluder in primitive index order, for any interleaving of spheres and planes).
+ * last_render_ms: device time of the render kernel (CUDA events on the library stream; 0 for
+ * rt_assemble_tiles). 104 bytes. */
 typedef struct {
   uint64_t primary;
   uint64_t shadow;
@@ -122,6 +123,10 @@ typedef struct {
                                     FP64 nearest hit, shading, shadow set-up, bounce) */
   double isect_eye_ms;           /* wavefront: the part of isect_closest_ms spent on camera rays
                                     (depth 0, shared-origin filter) */
+  int32_t graph;                 /* wavefront launch of the call: 0 kernel by kernel, 1 captured
+                                    into a CUDA graph and launched, 2 replay of a cached graph
+                                    (rt_set_graphs; up to 4 launch keys are cached) */
+  int32_t _pad;
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane

@@ -137,12 +137,23 @@ struct Context {
   int shade_wide = -1;  // rt_set_shade_wide
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
   cudaEvent_t ev_cap = nullptr;
-  std::string last_key, graph_key;
-  cudaGraphExec_t graph_exec = nullptr;
-  int graph_n = 0, graph_launches = 0, graph_chunks = 0;
-  std::vector<int> graph_chunk_items;
+  // a few instantiated graphs, one per launch key (e.g. frames alternating between two output
+  // buffers, as the multi-GPU double-buffered frame does), least recently used evicted; a key is
+  // captured on its second plain render among the last kRecentKeys renders
+  struct Graph {
+    std::string key;
+    cudaGraphExec_t exec = nullptr;
+    int n = 0, launches = 0, chunks = 0;
+    std::vector<int> chunk_items;
+    unsigned long long used = 0;
+  };
+  std::vector<Graph> graph_cache;
+  std::vector<std::string> recent_keys;
+  unsigned long long graph_clock = 0;
+  int last_graph = 0;  // how the last wavefront render was launched: 0 plain, 1 captured, 2 replayed
   std::vector<unsigned> hint0, hint1;  // queue counters of the render before the capture
 };
+constexpr size_t kGraphCache = 4, kRecentKeys = 8;
 
 Context g_ctx;
 // AUTO picks the wavefront kernels for scenes where the sphere scan dominates (measured on B200:
@@ -263,17 +274,20 @@ std::string wf_launch_key(const rt::DevParams& p, const rt::DevScene& sc, const 
   return k;
 }
 
-void drop_graph(Context& c) {
-  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
-  c.graph_exec = nullptr;
-  c.graph_key.clear();
+void drop_graphs(Context& c) {
+  for (auto& g : c.graph_cache)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c.graph_cache.clear();
+  c.recent_keys.clear();
 }
 
-// Launch the wavefront sequence: replay the cached graph when the key matches, capture it when
-// the same key comes twice in a row (a frame loop), else launch stream by stream (one-off
-// renders, progressive passes whose pass index changes every call).
+// Launch the wavefront sequence: replay a cached graph when one matches the key, capture one when
+// the key was launched plainly in one of the last kRecentKeys renders (a frame loop, or frames
+// alternating between a few output buffers), else launch stream by stream (one-off renders,
+// progressive passes whose pass index changes every call).
 int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc, const rt::DevOutputs& o, int src,
                      rt::WfTiming& tm) {
+  c.last_graph = 0;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CU(cudaStreamIsCapturing(c.stream, &cs), "cudaStreamIsCapturing");
   if (!c.graphs || cs != cudaStreamCaptureStatusNone) {  // the caller captures: plain launches into it
@@ -281,25 +295,28 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
     return RT_OK;
   }
   std::string key = wf_launch_key(p, sc, o, src, tm, c);
-  if (c.graph_exec && key == c.graph_key) {
-    CU(cudaGraphLaunch(c.graph_exec, c.stream), "cudaGraphLaunch");
-    tm.n = c.graph_n;
-    tm.launches = c.graph_launches;
-    tm.n_chunks = c.graph_chunks;
-    if (tm.chunk_items) std::copy(c.graph_chunk_items.begin(), c.graph_chunk_items.end(), tm.chunk_items);
-    c.last_key.swap(key);
+  for (auto& g : c.graph_cache) {
+    if (g.key != key) continue;
+    CU(cudaGraphLaunch(g.exec, c.stream), "cudaGraphLaunch");
+    g.used = ++c.graph_clock;
+    tm.n = g.n;
+    tm.launches = g.launches;
+    tm.n_chunks = g.chunks;
+    if (tm.chunk_items) std::copy(g.chunk_items.begin(), g.chunk_items.end(), tm.chunk_items);
+    c.last_graph = 2;
     return RT_OK;
   }
-  if (key != c.last_key) {  // first render with this key: plain launches
+  if (std::find(c.recent_keys.begin(), c.recent_keys.end(), key) == c.recent_keys.end()) {
+    // first render with this key (recently): plain launches
     CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
-    c.last_key.swap(key);
+    c.recent_keys.push_back(key);
+    if (c.recent_keys.size() > kRecentKeys) c.recent_keys.erase(c.recent_keys.begin());
     return RT_OK;
   }
-  // second consecutive render with this key: capture on cap_stream (forked from c.stream so the
-  // capture sees the same order), instantiate, launch on c.stream. The previous render (same
-  // sequence) left its queue lengths in the counters of each buffer set: with them, each scan is
-  // captured as one kernel (long-queue scan or split variant) instead of the self-selecting pair.
-  drop_graph(c);
+  // second render with this key: capture on cap_stream (forked from c.stream so the capture sees
+  // the same order), instantiate, launch on c.stream. The previous render left its queue lengths in
+  // the counters of each buffer set: with them, each scan is captured as one kernel (long-queue scan
+  // or split variant) instead of the self-selecting pair (a stale hint costs speed, never results).
 #ifndef RT_SCAN_HINTS
 #define RT_SCAN_HINTS 1
 #endif
@@ -332,14 +349,23 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
   cudaGraphDestroy(g);
   CU(ie, "cudaGraphInstantiate");
-  c.graph_exec = x;
-  c.graph_key = key;
-  c.graph_n = tm.n;
-  c.graph_launches = tm.launches;
-  c.graph_chunks = tm.n_chunks;
-  c.graph_chunk_items.assign(tm.chunk_items ? tm.chunk_items : nullptr, tm.chunk_items ? tm.chunk_items + tm.n_chunks : nullptr);
-  CU(cudaGraphLaunch(c.graph_exec, c.stream), "cudaGraphLaunch");
-  c.last_key.swap(key);
+  if (c.graph_cache.size() >= kGraphCache) {  // evict the least recently used graph
+    auto lru = std::min_element(c.graph_cache.begin(), c.graph_cache.end(),
+                                [](const Context::Graph& a, const Context::Graph& b) { return a.used < b.used; });
+    cudaGraphExecDestroy(lru->exec);
+    c.graph_cache.erase(lru);
+  }
+  Context::Graph e;
+  e.key = key;
+  e.exec = x;
+  e.n = tm.n;
+  e.launches = tm.launches;
+  e.chunks = tm.n_chunks;
+  if (tm.chunk_items) e.chunk_items.assign(tm.chunk_items, tm.chunk_items + tm.n_chunks);
+  e.used = ++c.graph_clock;
+  c.graph_cache.push_back(std::move(e));
+  CU(cudaGraphLaunch(x, c.stream), "cudaGraphLaunch");
+  c.last_graph = 1;
   return RT_OK;
 }
 
@@ -554,6 +580,7 @@ int collect_stats(bool timed) {
   c.last.isect_eye_ms = te;
   c.last.launches = timed ? (uint32_t)c.last_launches : 2u;
   c.last.variant = c.last_variant;
+  c.last.graph = c.last_variant == RT_VARIANT_WAVEFRONT ? c.last_graph : 0;
   return RT_OK;
 }
 
@@ -709,8 +736,7 @@ int rt_set_graphs(int32_t on) {
   if (rc) return rc;
   if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "graphs must be 0 or 1");
   g_ctx.graphs = on;
-  if (!on) drop_graph(g_ctx);
-  g_ctx.last_key.clear();
+  drop_graphs(g_ctx);
   return RT_OK;
 }
 

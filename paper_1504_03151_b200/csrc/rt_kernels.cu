@@ -137,7 +137,9 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));
       if (tc + qh < (float)kEps - F.eta || tc - qh > tmax_hi) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
-      if (t >= kEps && t < tmax) {
+      // closest hits: a sphere at the same t as the plane found first wins iff its primitive
+      // index is lower; shadow rays stop at any occluder (the counts are fixed below)
+      if (t >= kEps && (t < tmax || (!shadow && t == tmax && hp >= 0 && S.sph_prim[k] < c_planes[hp].prim))) {
         hs = k; hp = -1;
         if (shadow) act = false; else tmax = t;
       }
@@ -190,15 +192,11 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
     L.n_stests += (unsigned)P.n_spheres;
     L.n_ctests += (unsigned)P.n_spheres;
     L.n_ptests += (unsigned)P.n_planes;
-  } else if (L.qkind == Q_SHADOW) {
-    if (hp >= 0) {
-      L.n_ptests += (unsigned)(hp + 1);
-    } else {
-      L.n_ptests += (unsigned)P.n_planes;
-      unsigned nt = (unsigned)(hs >= 0 ? hs + 1 : P.n_spheres);
-      if (kExt && L.qskip >= 0 && (hs < 0 || L.qskip < hs)) --nt;  // the emitter is not tested
-      L.n_stests += nt;
-    }
+  } else if (L.qkind == Q_SHADOW) {  // up to the first occluder in primitive index order
+    unsigned long long ns = 0, np = 0;
+    shadow_counts(P, S, o, d, L.tmax, hp, hs, -1, kExt ? L.qskip : -1, ns, np);
+    L.n_stests += ns;
+    L.n_ptests += np;
   }
   L.tmax = tmax;
   L.qs = hs;

@@ -1059,21 +1059,65 @@ wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
 }
 
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when
-// the list overflowed
+// the list overflowed. The planes were decided first (tbest, hp): a sphere at exactly the same t
+// wins the tie when its primitive index is lower (ties -> lowest index, whatever the
+// interleaving of spheres and planes in the input)
+__device__ __forceinline__ bool beats(const DevScene& S, double t, int k, double tbest, int hp) {
+  return t < tbest || (t == tbest && hp >= 0 && S.sph_prim[k] < c_planes[hp].prim);
+}
 __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScene& S, const int* cand, int nc,
                                                int skip, d3 o, d3 d, double& tbest, int& hs, int& hp) {
   if (nc <= kCandMax) {
     for (int c = 0; c < nc; ++c) {
       const int k = cand[c];
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
-      if (t >= kEps && t < tbest) { tbest = t; hs = k; hp = -1; }
+      if (t >= kEps && beats(S, t, k, tbest, hp)) { tbest = t; hs = k; hp = -1; }
     }
   } else {
     for (int k = 0; k < P.n_spheres; ++k) {
       if (k == skip) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
-      if (t >= kEps && t < tbest) { tbest = t; hs = k; hp = -1; }
+      if (t >= kEps && beats(S, t, k, tbest, hp)) { tbest = t; hs = k; hp = -1; }
     }
+  }
+}
+
+// Test counts of one shadow ray in primitive index order (§8(c).1 step 11; Alg. 1 `break`). The
+// scans test planes first: hp = the first occluding plane (or -1); otherwise hs = the first
+// occluding sphere in sphere order (or -1). Spheres precede a plane in index order when the input
+// interleaves them (sph_prim / DevPlane::prim): if plane hp occludes, a sphere listed before it may
+// be the first occluder in index order, decided here in FP64 (a loop over those spheres only; the
+// generated scenes list planes first, where it is empty). skip: the sphere the ray leaves (tested,
+// never an occluder); skip2: the aimed-at emitter (not tested, R#41).
+// the first occluder among spheres 0..n-1 (FP64), or -1: a rare path (interleaved inputs only),
+// kept out of line so the callers' register budgets stay those of the planes-first case
+__device__ __noinline__ int first_occluder_before(const DevScene& S, d3 o, d3 d, double tl, int n, int skip, int skip2) {
+  for (int k = 0; k < n; ++k) {
+    if (k == skip || k == skip2) continue;
+    const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
+    if (t >= kEps && t < tl) return k;
+  }
+  return -1;
+}
+__device__ __forceinline__ void shadow_counts(const DevParams& P, const DevScene& S, d3 o, d3 d, double tl, int hp,
+                                              int hs, int skip, int skip2, unsigned long long& nsph,
+                                              unsigned long long& npl) {
+  int first = hs;
+  if (hp >= 0) {
+    const int before = c_planes[hp].prim - hp;  // spheres listed before plane hp
+    if (before > 0) first = first_occluder_before(S, o, d, tl, before, skip, skip2);
+    if (first < 0) {
+      npl = (unsigned long long)(hp + 1);
+      nsph = (unsigned long long)before - ((skip2 >= 0 && skip2 < before) ? 1ull : 0ull);
+      return;
+    }
+  }
+  if (first >= 0) {
+    nsph = (unsigned long long)(first + 1) - ((skip2 >= 0 && skip2 < first) ? 1ull : 0ull);
+    npl = (unsigned long long)(S.sph_prim[first] - first);  // planes listed before sphere `first`
+  } else {
+    nsph = (unsigned long long)P.n_spheres - (skip2 >= 0 ? 1ull : 0ull);
+    npl = (unsigned long long)P.n_planes;
   }
 }
 
@@ -1643,19 +1687,12 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
       float3 L = lf3(Ls, B.cap, li);
       for (int j = off; j < off + cnt; ++j) {
         const int rob = B.srob[j];
-        bool occluded = false;
+        const int skip2 = kExt ? B.sskip2[j] : -1;
+        int hp = -1, first = -1;
         if (rob <= -2) {  // plane -2-rob occludes (planes are tested first, in index order)
-          occluded = true;
-          st_pl += (unsigned long long)(-2 - rob + 1);
+          hp = -2 - rob;
         } else {
-          st_pl += (unsigned long long)P.n_planes;
-          const int skip2 = kExt ? B.sskip2[j] : -1;
           const int nc = B.sn[j];
-          int first = -1;
-#ifdef RT_OVF_PROBE
-          if (nc > kCandMax) atomicAdd(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 1, 1u);
-          atomicMax(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 3, (unsigned)nc);
-#endif
           if (nc > 0 || rob >= 0) {
             const d3 os = ld3(B.sray, B.scap, j, 0), ds = ld3(B.sray, B.scap, j, 3);
             const double tl = B.sray[6 * (size_t)B.scap + j];
@@ -1675,11 +1712,18 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
               }
             }
           }
-          occluded = first >= 0;
-          // tests up to the first occluder in index order; the aimed-at emitter is not tested
-          const unsigned long long nsk = (skip2 >= 0 && (!occluded || skip2 < first)) ? 1ull : 0ull;
-          st_sph += (occluded ? (unsigned long long)(first + 1) : (unsigned long long)P.n_spheres) - nsk;
         }
+        const bool occluded = hp >= 0 || first >= 0;
+        // tests up to the first occluder in index order; the aimed-at emitter is not tested
+        unsigned long long ns = 0, np = 0;
+        if (hp >= 0 && c_planes[hp].prim != hp) {  // spheres listed before the occluding plane
+          shadow_counts(P, S, ld3(B.sray, B.scap, j, 0), ld3(B.sray, B.scap, j, 3), B.sray[6 * (size_t)B.scap + j], hp,
+                        -1, B.sskip[j], skip2, ns, np);
+        } else {
+          shadow_counts(P, S, mk(0, 0, 0), mk(0, 0, 1), 0.0, hp < 0 ? -1 : hp, first, -1, skip2, ns, np);
+        }
+        st_sph += ns;
+        st_pl += np;
         if (!occluded) L = add(L, lf3(B.sq_c, B.scap, j));
       }
       sf3(Ls, B.cap, li, L);

@@ -42,7 +42,7 @@ class RayStats(C.Structure):
                 ("sphere_tests", C.c_uint64), ("plane_tests", C.c_uint64), ("last_render_ms", C.c_double),
                 ("closest_sphere_tests", C.c_uint64), ("isect_closest_ms", C.c_double),
                 ("isect_shadow_ms", C.c_double), ("launches", C.c_uint32), ("variant", C.c_int32),
-                ("shade_ms", C.c_double), ("isect_eye_ms", C.c_double)]
+                ("shade_ms", C.c_double), ("isect_eye_ms", C.c_double), ("graph", C.c_int32), ("_pad", C.c_int32)]
 
 
 _lib = None

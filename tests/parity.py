@@ -30,6 +30,8 @@ COND_REL_THR = 1e-4
 REL_TOL = 1e-4
 ABS_TOL = 1e-6
 MAX_DIFF_FRAC = 1e-3
+MIN_EXACT_ID_FRAC = 0.999  # hit ids + bounce counts bit-exact on >= 99.9 % of all pixels
+COUNT_KEYS = ("primary", "shadow", "secondary", "sphere_tests", "plane_tests")
 
 
 def tonemap8(v):
@@ -115,3 +117,17 @@ def ray_budget_ok(g_stats: dict, ref_counts: dict, ref, cls: Classified, n_light
     dsec = g_stats["secondary"] - ref_counts["secondary"]
     ok = dp == 0 and abs(ds) <= budget_sh and abs(dsec) <= budget_sec
     return ok, f"d_primary={dp} d_shadow={ds} (budget {budget_sh}) d_secondary={dsec} (budget {budget_sec})"
+
+
+def exact_id_fraction(g_ids, g_bounces, ref) -> float:
+    """Fraction of ALL compared pixels (exact- and edge-class) whose hit ids and bounce counts
+    equal the oracle's bit for bit (both sides decide in FP64)."""
+    ok = (np.asarray(g_ids) == ref.hit_ids).all(axis=(1, 2)) & (np.asarray(g_bounces) == ref.bounces).all(axis=1)
+    return float(ok.mean()) if len(ok) else 1.0
+
+
+def counts_equal(g_stats: dict, ref_counts: dict) -> tuple[bool, str]:
+    """Full frames: the algorithmic counts (rays and sphere/plane tests, §8(c).1 step 11; the
+    roofline's numerator) equal the oracle's exactly."""
+    diff = {k: int(g_stats[k]) - int(ref_counts[k]) for k in COUNT_KEYS}
+    return all(v == 0 for v in diff.values()), " ".join(f"d_{k}={v}" for k, v in diff.items())

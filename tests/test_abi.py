@@ -30,11 +30,25 @@ def test_library_exports_every_declared_symbol(lib):
     assert not missing, missing
 
 
-def test_struct_layouts_match_header():
-    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 96 B
+def test_struct_layouts_match_header(tmp_path):
+    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 104 B
     assert rt.PRIM_DTYPE.itemsize == 24 and rt.MAT_DTYPE.itemsize == 48
     assert rt.LIGHT_DTYPE.itemsize == 24 and rt.ENV_DTYPE.itemsize == 24
-    assert ctypes.sizeof(rt.RayStats) == 96
+    assert ctypes.sizeof(rt.RayStats) == 104
+    # every rt_ray_stats field of the binding sits at the offset the C compiler gives the header's
+    fields = [f for f, _ in rt.RayStats._fields_]
+    src = "#include <stddef.h>\n#include <stdio.h>\n#include \"rt.h\"\nint main(void) {\n"
+    src += f'  printf("%zu\\n", sizeof(rt_ray_stats));\n'
+    for f in fields:
+        src += f'  printf("%zu\\n", offsetof(rt_ray_stats, {f}));\n'
+    src += "  return 0;\n}\n"
+    (tmp_path / "t.c").write_text(src)
+    import subprocess
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), "-o", str(tmp_path / "t"),
+                           str(tmp_path / "t.c")])
+    out = [int(x) for x in subprocess.check_output([str(tmp_path / "t")]).split()]
+    assert out[0] == ctypes.sizeof(rt.RayStats)
+    assert out[1:] == [getattr(rt.RayStats, f).offset for f in fields]
     hdr = open(os.path.join(ROOT, "include", "rt.h")).read()
     assert re.search(r"RT_TILE_W = 8", hdr) and re.search(r"RT_TILE_H = 4", hdr)
 

@@ -34,9 +34,17 @@ def _check(oracle_lib, sc, pixels=None, label="", variant="wavefront"):
     rep = parity.compare(g["rgb"][pix], g["ids"][pix], g["bounces"][pix], ref, cls)
     print(f"[{label or sc.name}] {rep}")
     assert rep.ok, f"{label or sc.name}: {rep}"
+    # every discrete decision is taken in FP64 on both sides: hit ids and bounce counts match on
+    # (almost) every pixel, edge-class ones included
+    frac = parity.exact_id_fraction(g["ids"][pix], g["bounces"][pix], ref)
+    print(f"[{label or sc.name}] bit-exact hit ids + bounces: {frac:.5%} of {len(pix)} pixels")
+    assert frac >= parity.MIN_EXACT_ID_FRAC, frac
     if pixels is None:
         ok, msg = parity.ray_budget_ok(g["stats"], ref.counts, ref, cls, sc.n_lights)
         print(f"[{label or sc.name}] rays: {msg}")
+        assert ok, msg
+        ok, msg = parity.counts_equal(g["stats"], ref.counts)
+        print(f"[{label or sc.name}] counts: {msg}")
         assert ok, msg
     return g, ref, rep
 
@@ -80,6 +88,27 @@ def test_c2_ragged_deeper_supersampled(oracle_lib):
 def test_tiny_random_scenes(oracle_lib, seed, W, H, D, spp, variant):
     sc = scenegen.random_tiny(seed, n_spheres=7, n_planes=2, n_lights=3, width=W, height=H, max_depth=D, spp=spp)
     _check(oracle_lib, sc, label=f"tiny{seed}/{variant}", variant=variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("seed,W,H,D,spp", [(20, 13, 7, 4, 1), (21, 9, 9, 6, 4), (22, 17, 5, 3, 2), (23, 11, 10, 5, 1)])
+def test_interleaved_order_and_tinted_glass(oracle_lib, seed, W, H, D, spp, variant):
+    """Primitive orders other than planes-first (two planes inserted between the spheres: ties
+    and test counts follow primitive indices, §8(c).1 step 11) and coloured glass (the
+    REFRACTIVE weight T *= rho); exact counts against the oracle."""
+    sc = scenegen.random_tiny(seed, n_spheres=8, n_planes=2, n_lights=3, width=W, height=H, max_depth=D, spp=spp,
+                              glass_tint=True, interleave=True)
+    assert list(sc.prim_type[:5]) == [0, 0, 0, 0, 1]  # spheres before the planes
+    assert (sc.mat_albedo[sc.mat_kind == scenegen.REFRACTIVE] < 1).any()
+    _check(oracle_lib, sc, label=f"interleaved{seed}/{variant}", variant=variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_tinted_glass_c2_shaped(oracle_lib, variant):
+    """C2-sized frame of a scene with many coloured-glass spheres (every third material glass)."""
+    sc = scenegen.random_tiny(31, n_spheres=12, n_planes=1, n_lights=2, width=96, height=64, max_depth=5, spp=1,
+                              glass_tint=True)
+    _check(oracle_lib, sc, label=f"tinted/{variant}", variant=variant)
 
 
 def test_c3_full_size_sampled(oracle_lib):

@@ -286,3 +286,25 @@ def test_occluder_beyond_the_light_does_not_shadow(oracle_lib):
     sc = bb.build("before", eye=(0, 0, 0), look_at=(0, 0, 1), up=(0, 1, 0), vfov=30, width=1, height=1,
                   max_depth=0, spp=1, ambient=(0.1, 0.1, 0.1))
     assert oracle_lib.render(sc).rgb[0].tolist() == [0.5 * _f32(0.1)] * 3
+
+
+@pytest.mark.parametrize("order,sph,pl", [("S0 S1 Pocc", 4, 1), ("S1 S0 Pocc", 3, 1), ("Pocc S0 S1", 2, 2),
+                                          ("S0 Pocc S1", 3, 2)])
+def test_counts_with_an_occluding_plane(oracle_lib, order, sph, pl):
+    # as above with a plane y = 2 that also blocks the shadow ray (between the shading point and the
+    # light, parallel to the camera ray): the first occluder in index order stops the count
+    b = scenegen.builder()
+    mt = b.material(DIFFUSE, (0.5, 0.5, 0.5))
+    for tok in order.split():
+        if tok == "S0":
+            b.sphere((0, 0, 5), 1.0, mt)
+        elif tok == "S1":
+            b.sphere((0, 1.5, 2.5), 0.5, mt)
+        else:
+            b.plane((0, 1, 0), 2.0, mt)
+    b.light((0, 3, 1), (36 * math.pi,) * 3)
+    sc = b.build("counts2", eye=(0, 0, 0), look_at=(0, 0, 1), up=(0, 1, 0), vfov=60, width=1, height=1,
+                 max_depth=0, spp=1, ambient=(0.1, 0.1, 0.1), keep_order=True)
+    r = oracle_lib.render(sc)
+    assert r.rgb[0, 0] == 0.5 * _f32(0.1)
+    assert (r.counts["sphere_tests"], r.counts["plane_tests"]) == (sph, pl)
