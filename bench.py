@@ -112,6 +112,24 @@ def _measured_peak(key: str, fallback: float) -> float:
         return fallback
 
 
+def measure_fp32_peak(gpu: int) -> dict:
+    """The FFMA2 chain microbenchmark (tools/micro/ffma2_peak.cu) on this box right before the
+    timed frames, with nvidia-smi sampling the SM clock under that FP32 load."""
+    from paper_1504_03151_b200 import build as rtbuild
+    try:
+        exe = rtbuild.build_peak_tool()
+        clk = ClockSampler(gpu, period_ms=20)
+        clk.start()
+        out = subprocess.run([exe, "40"], capture_output=True, text=True, timeout=120,
+                             env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(gpu))))
+        c = clk.stop()
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+        res.update(sm_mhz_under_load=c.get("sm_mhz"), clock_reasons=c.get("reasons"))
+        return res
+    except Exception as ex:  # noqa: BLE001 - reported, the derived figure is used instead
+        return {"error": f"{type(ex).__name__}: {ex}"}
+
+
 def _load_profile_traffic(workload: str):
     """dram bytes per launch of the render kernel from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "ncu_render_kernel.json")
@@ -305,6 +323,7 @@ def run_b200(args):
         extra = (2 if isinstance(rend, ShardedRenderer) else 1) if rank == 0 else 0
         launches_per_step = rt.stats()["launches"] + extra
         del probe
+    fp32 = measure_fp32_peak(gpu) if rank == 0 else None
     # warm-up (after the probe, so the frame's launch sequence is captured as a CUDA graph here)
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -341,15 +360,16 @@ def run_b200(args):
     if world == 1 and st["variant"] == 1:
         rt.set_concurrency(False)
         ks = max(3, min(args.steps, 20))
-        acc = {"closest": 0.0, "shadow": 0.0, "eye": 0.0, "shade": 0.0, "frame": 0.0}
+        keys = (("closest", "isect_closest_ms"), ("shadow", "isect_shadow_ms"), ("eye", "isect_eye_ms"),
+                ("shade", "shade_ms"), ("accumulate", "accumulate_ms"), ("frame", "last_render_ms"))
+        acc = {k: 0.0 for k, _ in keys}
         for it in range(3 + ks):  # 3 warm-up frames: the in-order sequence is captured as a graph
             flush.zero_()
             step()
             f = rt.stats()
             if it < 3:
                 continue
-            for k, key in (("closest", "isect_closest_ms"), ("shadow", "isect_shadow_ms"), ("eye", "isect_eye_ms"),
-                           ("shade", "shade_ms"), ("frame", "last_render_ms")):
+            for k, key in keys:
                 acc[k] += f[key]
         rt.set_concurrency(True)
         kt = {k: v / ks for k, v in acc.items()}
@@ -398,53 +418,88 @@ def run_b200(args):
         rays = st["primary"] + st["shadow"] + st["secondary"]
         ms_per_step = total_ms / args.steps
         value = rays / (ms_per_step * 1e-3) / 1e6
-        # roofline of the dominant kernel (19 flops per ray-sphere test, 12 per
-        # ray-plane test) = algorithmic flops per launch / its CUDA-event launch time
+        # roofline of the dominant kernel (the largest share of the in-order frame):
+        #  * scans: bound "alu"; achieved = EXECUTED FP32 flops (the FMAs the filter form needs per
+        #    test: 4 FMA for camera rays and light-origin shadow rays, 7 FMA for secondary rays)
+        #    per second of the kernel's own launches; peak = the FFMA2 microbenchmark measured on
+        #    this box in this run; the counted figure (19 flops per test) beside it;
+        #  * wf_shade / wf_accumulate: bound "hbm"; achieved = algorithmic bytes /
+        #    time; peak = MEASURED_PEAKS.json hbm_gbs.
         props = torch.cuda.get_device_properties(dev)
         sms = props.multi_processor_count
         sm_max = clk.get("sm_max_mhz") or PEAK_FALLBACK_MHZ
-        peak = sms * 128 * 2 * sm_max * 1e6 / 1e12
+        derived = sms * 128 * 2 * sm_max * 1e6 / 1e12
+        peak, peak_basis = derived, f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (derived; measurement failed)"
+        if fp32 and fp32.get("tflops"):
+            peak = fp32["tflops"]
+            peak_basis = (f"measured in this run: FFMA2 dependent chains on all SMs (tools/micro/ffma2_peak.cu), "
+                          f"best of {fp32.get('reps')}, SM clock {fp32.get('sm_mhz_under_load')} MHz under that load "
+                          f"(derived {derived:.2f} at {sm_max:.0f} MHz)")
+        hbm_peak = _measured_peak("hbm_gbs", 6549.1)
         traffic = _load_profile_traffic(args.config) if world == 1 else None
+        extra = {}
         if kt is not None:
-            # algorithmic work per unit: 19 flops per ray-sphere test. Executed:
-            # 7 FMA (14 flops) per test in the general scans, 4 FMA (8 flops) for camera rays
             n_closest = st["closest_sphere_tests"]
             n_eye = st["primary"] * sc.n_spheres
             n_shadow = st["sphere_tests"] - n_closest
-            # executed: 4 FMA per test in the camera-ray scan and in the light-origin shadow scan
-            # (point lights, no sampled emitters here), 7 FMA in the secondary closest-hit scans
-            sh_flops = 8 if sc.n_lights > 0 else 14
-            scans = {
+            sh_fma = 4 if sc.n_lights > 0 else 7
+            prim, sec, shd = st["primary"], st["secondary"], st["shadow"]
+            cands = {
                 "shadow": {"kernel": "wf_isect_lt (shadow rays to point lights, scanned from the light; FP32 FFMA2, "
-                                     "early exit at a certain occluder)",
-                           "ms": kt["shadow"], "tests": n_shadow, "executed_flops": sh_flops * n_shadow},
-                "camera": {"kernel": "wf_isect_eye2 (camera rays, shared-origin FP32 FFMA2 scan)",
-                           "ms": kt["eye"], "tests": n_eye, "executed_flops": 8 * n_eye},
-                "secondary": {"kernel": "wf_isect<closest> (secondary closest-hit rays, FP32 FFMA2 scan)",
-                              "ms": kt["closest"] - kt["eye"], "tests": n_closest - n_eye,
-                              "executed_flops": 14 * (n_closest - n_eye)},
+                                     "early exit at a certain occluder)", "bound": "alu",
+                           "ms": kt["shadow"], "tests": n_shadow, "fma_per_test": sh_fma},
+                "camera": {"kernel": "wf_isect_eye2 (camera rays, shared-origin FP32 FFMA2 scan)", "bound": "alu",
+                           "ms": kt["eye"], "tests": n_eye, "fma_per_test": 4},
+                "secondary": {"kernel": "wf_isect<closest> (secondary closest-hit rays, FP32 FFMA2 scan)", "bound": "alu",
+                              "ms": kt["closest"] - kt["eye"], "tests": n_closest - n_eye, "fma_per_test": 7},
+                # algorithmic bytes: per shaded path the ray state in (84 B at depth >= 1;
+                # camera rays are implicit) + its candidate count (4 B); per continuation the next state
+                # out (84 B); per ended path its radiance (12 B); per shadow ray the FP64 shadow ray and
+                # its contribution out (68 B)
+                "shade": {"kernel": "wf_shade (FP64 nearest hit, shading, shadow-ray set-up, bounce)", "bound": "hbm",
+                          "ms": kt["shade"], "bytes": 84 * sec + 4 * (prim + sec) + 84 * sec + 12 * prim + 68 * shd},
+                # per shadow ray its decision inputs (status 8 B) and contribution (12 B); per shading
+                # path the entry range (8 B) and the radiance read and written (24 B)
+                "accumulate": {"kernel": "wf_accumulate (FP64 occlusion decisions, radiance sums)", "bound": "hbm",
+                               "ms": kt["accumulate"], "bytes": 20 * shd + 32 * (prim + sec)},
             }
-            dom = max(scans, key=lambda k: scans[k]["ms"])
-            for k, v in scans.items():
-                v["achieved"] = FLOP_SPHERE * v["tests"] / (v["ms"] * 1e-3) / 1e12
-                v["achieved_executed"] = v["executed_flops"] / (v["ms"] * 1e-3) / 1e12
+            for k, v in cands.items():
                 v["share_of_frame"] = v["ms"] / kt["frame"]
-            achieved = scans[dom]["achieved"]
-            kernel = scans[dom]["kernel"] + ", CUDA events per launch, launches in order on one stream"
+                if v["bound"] == "alu":
+                    v["achieved"] = 2 * v["fma_per_test"] * v["tests"] / (v["ms"] * 1e-3) / 1e12
+                    v["achieved_counted"] = FLOP_SPHERE * v["tests"] / (v["ms"] * 1e-3) / 1e12
+                    v["frac"] = v["achieved"] / peak
+                    v["unit"] = "TFLOP/s"
+                else:
+                    v["achieved"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+                    v["frac"] = v["achieved"] / hbm_peak
+                    v["unit"] = "GB/s"
+            dom = max(cands, key=lambda k: cands[k]["ms"])
+            d = cands[dom]
+            achieved, bound, unit = d["achieved"], d["bound"], d["unit"]
+            rpeak = peak if bound == "alu" else hbm_peak
+            kernel = d["kernel"] + ", CUDA events per launch, launches in order on one stream"
             traffic = _load_profile_traffic(f"{args.config}:{dom}") or traffic
-            extra = {"share_of_frame": scans[dom]["share_of_frame"],
-                     "achieved_executed": scans[dom]["achieved_executed"],
-                     "other_scan": {k: {kk: vv for kk, vv in v.items() if kk not in ("kernel",)} | {"kernel": v["kernel"]}
-                                    for k, v in scans.items() if k != dom},
+            extra = {"share_of_frame": d["share_of_frame"],
+                     "kernels": {k: {kk: vv for kk, vv in v.items() if kk != "kernel"} for k, v in cands.items()},
                      "kernel_timing_pass": f"{kt['frames']} frames, frame {kt['frame']:.3f} ms in order vs "
                                            f"{ms_per_step:.3f} ms in the timed (concurrent) frames",
-                     "whole_frame_achieved": (FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"])
+                     "whole_frame_counted_tflops": (FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"])
                      / (ms_per_step * 1e-3) / 1e12}
+            if bound == "alu":
+                extra["achieved_counted"] = d["achieved_counted"]
         else:
             flops = FLOP_SPHERE * st["sphere_tests"] + FLOP_PLANE * st["plane_tests"]
             achieved = flops / world / (total_ms / args.steps * 1e-3) / 1e12
-            kernel = "render_kernel (megakernel)" if world == 1 else "whole shard frame incl. all-gather"
-            extra = {}
+            bound, unit, rpeak = "alu", "TFLOP/s", peak
+            kernel = ("render_kernel (megakernel), counted flops" if world == 1
+                      else "whole shard frame incl. the gather, counted flops")
+        roofline = {"bound": bound, "achieved": achieved, "peak": rpeak, "unit": unit, "frac": achieved / rpeak,
+                    "traffic": traffic, "kernel": kernel, **extra,
+                    "peak_basis": peak_basis if bound == "alu" else "MEASURED_PEAKS.json hbm_gbs (burst copy bandwidth)",
+                    "fp32_peak_measured": fp32,
+                    "flops_basis": "executed: 4 FMA per camera-ray / light-origin shadow test, 7 per secondary test; "
+                                   "counted: 19 flops/sphere test + 12/plane test (SURVEY 8(d).3)"}
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -456,10 +511,7 @@ def run_b200(args):
                            rays_per_frame=int(rays), primary=int(st["primary"]), shadow=int(st["shadow"]),
                            secondary=int(st["secondary"]), sphere_tests=int(st["sphere_tests"]),
                            plane_tests=int(st["plane_tests"]), wall_s=t_wall),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel, **extra,
-                         "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (derived, DESIGN.md)",
-                         "flops_basis": "19 flops/sphere test + 12/plane test (SURVEY 8(d).3) x algorithmic test counts"},
+            "roofline": roofline,
             "clocks": clk,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
@@ -613,9 +665,9 @@ def main():
     ap.add_argument("--mode", choices=["hot", "progressive"], default="hot",
                     help="hot: the §8(a) path on C4 (default); progressive: NEXT-1/2 passes on C0")
     ap.add_argument("--passes", type=int, default=16, help="--mode progressive: passes per step")
-    ap.add_argument("--collective", choices=["p2p", "allgather"], default="p2p",
-                    help="N>1: fused render+gather into rank 0's frame over peer memory (default, falls back to "
-                         "allgather if CUDA IPC / peer access is unavailable) or the NCCL all-gather of slabs")
+    ap.add_argument("--collective", choices=["allgather", "p2p"], default="allgather",
+                    help="N>1: the NCCL all-gather of the tile slabs + rank-0 assembly (default, north_star's one "
+                         "collective) or the ablation: render+gather fused into rank 0's frame over peer memory")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

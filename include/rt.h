@@ -103,7 +103,7 @@ typedef struct {
  * test every primitive; shadow rays count the primitives up to and including the first
  * occluder in primitive index order, for any interleaving of spheres and planes).
  * last_render_ms: device time of the render kernel (CUDA events on the library stream; 0 for
- * rt_assemble_tiles). 104 bytes. */
+ * rt_assemble_tiles). 112 bytes. */
 typedef struct {
   uint64_t primary;
   uint64_t shadow;
@@ -127,6 +127,8 @@ typedef struct {
                                     into a CUDA graph and launched, 2 replay of a cached graph
                                     (rt_set_graphs; up to 4 launch keys are cached) */
   int32_t _pad;
+  double accumulate_ms;          /* wavefront: summed device time of the wf_accumulate launches
+                                    (a5 FP64 occlusion decisions, a4 light sums) */
 } rt_ray_stats;
 
 /* Upload the scene: validates every element, normalises plane
@@ -176,10 +178,12 @@ int rt_set_concurrency(int32_t on);
 
 /* Wavefront kernels: 1 (default) replays a CUDA graph of the launch sequence. The sequence of a
  * render (frame or shard size, max_depth, spp, output pointers, buffers, concurrency) is captured
- * the second time the same sequence is requested in a row and replayed while it stays the same,
- * so a frame loop pays one graph launch per frame instead of ~10 kernel launches per depth; scene
- * and camera contents may change between replays (the kernels read them at run time). 0 launches
- * every kernel from the host. Same results bit for bit either way. RT_ERR_INVALID_ARG unless 0/1. */
+ * the second time it is requested within the last 8 renders and replayed whenever it comes again
+ * (up to 4 sequences cached, least recently used evicted: e.g. frames alternating between two
+ * output buffers), so a frame loop pays one graph launch per frame instead of ~6 kernel launches
+ * per depth; scene and camera contents may change between replays (the kernels read them at run
+ * time). 0 launches every kernel from the host and empties the cache (calling it with 1 empties
+ * it too). Same results bit for bit either way. RT_ERR_INVALID_ARG unless 0/1. */
 int rt_set_graphs(int32_t on);
 
 /* Wavefront kernels, test and tuning knob: -1 (default) splits a scan over 2-8 warps per ray
@@ -187,12 +191,6 @@ int rt_set_graphs(int32_t on);
  * parts on every intersection scan (1: never split). Results are bit-identical for every value.
  * RT_ERR_INVALID_ARG otherwise. */
 int rt_set_scan_split(int32_t parts);
-
-/* Wavefront kernels, test and tuning knob: 1 shades every depth with one warp per path (lane l
- * evaluates light l); -1 (default) and 0 use one thread per path (the warp-per-path form for
- * short queues only when the library is built with RT_SHADE_WIDE=1; measured neutral on C4).
- * Results are bit-identical for every value. RT_ERR_INVALID_ARG unless -1, 0 or 1. */
-int rt_set_shade_wide(int32_t mode);
 
 /* Seed of the counter-based RNG that picks reflection vs refraction (R#9). */
 int rt_set_seed(uint64_t seed);

@@ -42,6 +42,21 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+FFMA2_PEAK_SRC = os.path.join(ROOT, "tools", "micro", "ffma2_peak.cu")
+FFMA2_PEAK_BIN = os.path.join(ROOT, "tools", "micro", "ffma2_peak")
+
+
+def build_peak_tool(force: bool = False) -> str:
+    """The FFMA2 peak microbenchmark bench.py runs before timing (a measurement tool, not part of
+    the library)."""
+    if not force and os.path.exists(FFMA2_PEAK_BIN) and os.path.getmtime(FFMA2_PEAK_BIN) >= os.path.getmtime(FFMA2_PEAK_SRC):
+        return FFMA2_PEAK_BIN
+    tmp = FFMA2_PEAK_BIN + f".tmp{os.getpid()}"
+    subprocess.check_call([nvcc(), *ARCH, "-O3", "-lineinfo", "-o", tmp, FFMA2_PEAK_SRC])
+    os.replace(tmp, FFMA2_PEAK_BIN)
+    return FFMA2_PEAK_BIN
+
+
 if __name__ == "__main__":
     import argparse
     ap = argparse.ArgumentParser()

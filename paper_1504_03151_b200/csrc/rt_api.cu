@@ -77,9 +77,8 @@ struct Context {
   // scene
   bool has_scene = false;
   bool smem_scene = true;
-  bool const_scene = true;
   int n_spheres = 0, n_pairs_pad = 0, n_planes = 0, n_lights = 0, n_mats = 0;
-  float cmax = 0.f, rmax = 0.f, cmax_abs = 0.f;
+  float cmax = 0.f, rmax = 0.f;
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt;
@@ -97,22 +96,16 @@ struct Context {
   DevBuf<int> dbg_hits, dbg_bounces;
   // wavefront variant
   int variant = RT_VARIANT_AUTO;
-#ifndef RT_WF_CONCURRENT
-#define RT_WF_CONCURRENT 1
-#endif
-  int concurrent = RT_WF_CONCURRENT;  // shadow scans || next closest scan on a side stream
+  int concurrent = 1;  // shadow scans || next closest scan on a side stream (rt_set_concurrency)
   DevBuf<unsigned char> wf_mem, wf_mem2;
   DevBuf<unsigned> wf_ctr, wf_ctr2;
   rt::WfBuffers wf{}, wf2{};
   // chunk pipelining (odd chunks on a second buffer set and stream pair)
-#ifndef RT_WF_PIPELINE
-#define RT_WF_PIPELINE 1
-#endif
-  int pipeline = RT_WF_PIPELINE;
+  int pipeline = 1;
   cudaStream_t main2 = nullptr, side2 = nullptr;
   std::vector<cudaEvent_t> ev_fork2, ev_join2;
   cudaEvent_t ev_start2 = nullptr, ev_done2 = nullptr;
-  std::vector<cudaEvent_t> ev_c, ev_s, ev_h;  // per-launch scan / shade timing (wavefront)
+  std::vector<cudaEvent_t> ev_c, ev_s, ev_h, ev_a;  // per-launch scan / shade / accumulate timing
   cudaStream_t side_stream = nullptr;           // shadow scans || next closest scan
   std::vector<cudaEvent_t> ev_fork, ev_join;
   int n_timed = 0, last_launches = 0, last_variant = 0, last_depth = 0;
@@ -129,12 +122,8 @@ struct Context {
   std::vector<int> chunk_items;
   // CUDA graph of the wavefront launch sequence (rt_set_graphs): captured on the second of two
   // consecutive renders with the same launch key, replayed while the key stays the same
-#ifndef RT_WF_GRAPHS
-#define RT_WF_GRAPHS 1
-#endif
-  int graphs = RT_WF_GRAPHS;
+  int graphs = 1;
   int scan_split = -1;  // rt_set_scan_split
-  int shade_wide = -1;  // rt_set_shade_wide
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
   cudaEvent_t ev_cap = nullptr;
   // a few instantiated graphs, one per launch key (e.g. frames alternating between two output
@@ -203,7 +192,6 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   }
   p.cmax = c.cmax;
   p.rmax = c.rmax;
-  p.cmax_abs = c.cmax_abs;
   for (int i = 0; i < 3; ++i) p.centre[i] = c.centre[i];
   p.W = W; p.H = H; p.max_depth = max_depth; p.spp = spp;
   p.n_spheres = c.n_spheres; p.n_pairs_pad = c.n_pairs_pad; p.n_planes = c.n_planes; p.n_lights = c.n_lights;
@@ -218,11 +206,11 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
 }
 
 // Camera rays share the origin `eye`: s1 = K + 2 c'.o' (o' = eye - centre) per sphere, computed
-// in FP64 and rounded once, replaces K in a copy of the pair layout (RayFilterT::batch_eye)
+// in FP64 and rounded once, replaces K in a copy of the pair layout (wf_isect_eye2)
 int build_eye_pairs() {
   Context& c = g_ctx;
   c.eye_ready = false;
-  if (!RT_FILTER_EXPANDED || !c.has_scene || !c.has_camera || c.pairs_host.empty()) return RT_OK;
+  if (!c.has_scene || !c.has_camera || c.pairs_host.empty()) return RT_OK;
   const double ox = c.eye[0] - c.centre[0], oy = c.eye[1] - c.centre[1], oz = c.eye[2] - c.centre[2];
   c.pairs_eye_host = c.pairs_host;
   for (size_t q = 0; q + 1 < c.pairs_eye_host.size(); q += 2) {
@@ -317,10 +305,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   // the same order), instantiate, launch on c.stream. The previous render left its queue lengths in
   // the counters of each buffer set: with them, each scan is captured as one kernel (long-queue scan
   // or split variant) instead of the self-selecting pair (a stale hint costs speed, never results).
-#ifndef RT_SCAN_HINTS
-#define RT_SCAN_HINTS 1
-#endif
-  if (RT_SCAN_HINTS) {
+  {
     const size_t nctr = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
     CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
     c.hint0.assign(nctr, 0u);
@@ -390,12 +375,9 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   if (wavefront) {
     // chunk of whole pixels: at most 2^22 paths; shadow entries: paths x lights
     const long long want = (long long)p.n_items * p.spp;
-    // chunks of at most 2^22 paths (host framebuffers: 2^RT_HOST_CHUNK_LOG2; smaller chunks hide
-    // more of the row copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21)
-#ifndef RT_HOST_CHUNK_LOG2
-#define RT_HOST_CHUNK_LOG2 22
-#endif
-    const long long chunk = (host_out != nullptr && p.mode == 0) ? (1ll << RT_HOST_CHUNK_LOG2) : (1ll << 22);
+    // chunks of at most 2^22 paths (smaller chunks for host framebuffers hide more of the row
+    // copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21)
+    const long long chunk = 1ll << 22;
     int items = (int)((want < chunk ? want : chunk) / p.spp);
     if (items < 1) items = 1;
     const int cap = items * p.spp;
@@ -406,14 +388,12 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
     rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, 4 * c.num_sms, c.wf_ctr.p);
     c.wf.force_parts = c.scan_split;
-    c.wf.force_wide = c.shade_wide;
     const bool pipe = c.pipeline != 0 && c.concurrent != 0;
     if (pipe) {
       CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
       CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
       rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, 4 * c.num_sms, c.wf_ctr2.p);
       c.wf2.force_parts = c.scan_split;
-      c.wf2.force_wide = c.shade_wide;
       if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.ev_start2) CU(cudaEventCreateWithFlags(&c.ev_start2, cudaEventDisableTiming), "cudaEventCreate");
@@ -428,13 +408,15 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     }
     const int pairs = rt::wf_timing_pairs(p, cap, pipe);
     while ((int)c.ev_c.size() < 2 * pairs) {
-      cudaEvent_t a, b, h;
+      cudaEvent_t a, b, h, m;
       CU(cudaEventCreate(&a), "cudaEventCreate");
       CU(cudaEventCreate(&b), "cudaEventCreate");
       CU(cudaEventCreate(&h), "cudaEventCreate");
+      CU(cudaEventCreate(&m), "cudaEventCreate");
       c.ev_c.push_back(a);
       c.ev_s.push_back(b);
       c.ev_h.push_back(h);
+      c.ev_a.push_back(m);
     }
     if (!c.side_stream) CU(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     while ((int)c.ev_fork.size() < p.max_depth + 1) {
@@ -446,6 +428,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     }
     rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
     tm.shade = c.ev_h.data();
+    tm.accum = c.ev_a.data();
     if (c.concurrent) {
       tm.side = c.side_stream;
       tm.fork = c.ev_fork.data();
@@ -476,10 +459,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       tm.chunk_cap = max_chunks;
     }
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
-    #ifndef RT_WF_PREFER_CONST
-#define RT_WF_PREFER_CONST 0
-#endif
-    const int src = (RT_WF_PREFER_CONST && c.const_scene) ? 2 : (c.smem_scene ? 1 : 0);
+    const int src = c.smem_scene ? 1 : 0;
     {
       const int lrc = launch_wavefront(c, p, sc, o, src, tm);
       if (lrc) return lrc;
@@ -537,47 +517,26 @@ int collect_stats(bool timed) {
   c.last.plane_tests = h[4];
   c.last.closest_sphere_tests = h[5];
   c.last.last_render_ms = ms;
-  double tc = 0.0, ts = 0.0, tsh = 0.0, te = 0.0;
+  double tc = 0.0, ts = 0.0, tsh = 0.0, te = 0.0, tac = 0.0;
   if (timed) {
     for (int i = 0; i < c.n_timed; ++i) {
-      float a = 0.f, b = 0.f, m = 0.f;
+      float a = 0.f, b = 0.f, m = 0.f, ac = 0.f;
       CU(cudaEventElapsedTime(&a, c.ev_c[2 * i], c.ev_c[2 * i + 1]), "cudaEventElapsedTime");
       CU(cudaEventElapsedTime(&b, c.ev_s[2 * i], c.ev_s[2 * i + 1]), "cudaEventElapsedTime");
       CU(cudaEventElapsedTime(&m, c.ev_h[2 * i], c.ev_h[2 * i + 1]), "cudaEventElapsedTime");
+      CU(cudaEventElapsedTime(&ac, c.ev_a[2 * i], c.ev_a[2 * i + 1]), "cudaEventElapsedTime");
       tc += a;
       ts += b;
       tsh += m;
+      tac += ac;
       if (i % (c.last_depth + 1) == 0) te += a;  // depth 0: the camera-ray scan
     }
   }
-#ifdef RT_SIMD_PROBE
-  if (c.wf_ctr.p) {
-    unsigned pr[4];
-    cudaMemcpy(pr, c.wf_ctr.p + 70 * rt::kWfCtrPerDepth, sizeof pr, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "SIMD probe: closest batches %u lanes %u (%.3f) | shadow batches %u lanes %u (%.3f)\n", pr[0], pr[1],
-            pr[1] / (32.0 * pr[0] + 1e-9), pr[2], pr[3], pr[3] / (32.0 * pr[2] + 1e-9));
-    cudaMemset(c.wf_ctr.p + 70 * rt::kWfCtrPerDepth, 0, sizeof pr);
-  }
-#endif
-#ifdef RT_OVF_PROBE
-  if (c.wf_ctr.p) {
-    unsigned pr[4 * 8] = {}, p2[4 * 8] = {};
-    cudaMemcpy(pr, c.wf_ctr.p + 72 * rt::kWfCtrPerDepth, sizeof pr, cudaMemcpyDeviceToHost);
-    cudaMemset(c.wf_ctr.p + 72 * rt::kWfCtrPerDepth, 0, sizeof pr);
-    if (c.wf_ctr2.p) {
-      cudaMemcpy(p2, c.wf_ctr2.p + 72 * rt::kWfCtrPerDepth, sizeof p2, cudaMemcpyDeviceToHost);
-      cudaMemset(c.wf_ctr2.p + 72 * rt::kWfCtrPerDepth, 0, sizeof p2);
-    }
-    for (int d = 0; d < 8; ++d)
-      fprintf(stderr, "OVF probe d=%d: closest overflows %u (max nc %u) | shadow overflows %u (max nc %u)\n", d,
-              pr[4 * d] + p2[4 * d], pr[4 * d + 2] > p2[4 * d + 2] ? pr[4 * d + 2] : p2[4 * d + 2], pr[4 * d + 1] + p2[4 * d + 1],
-              pr[4 * d + 3] > p2[4 * d + 3] ? pr[4 * d + 3] : p2[4 * d + 3]);
-  }
-#endif
   c.last.isect_closest_ms = tc;
   c.last.isect_shadow_ms = ts;
   c.last.shade_ms = tsh;
   c.last.isect_eye_ms = te;
+  c.last.accumulate_ms = tac;
   c.last.launches = timed ? (uint32_t)c.last_launches : 2u;
   c.last.variant = c.last_variant;
   c.last.graph = c.last_variant == RT_VARIANT_WAVEFRONT ? c.last_graph : 0;
@@ -723,14 +682,6 @@ int rt_set_scan_split(int32_t parts) {
   return RT_OK;
 }
 
-int rt_set_shade_wide(int32_t mode) {
-  int rc = ensure_device();
-  if (rc) return rc;
-  if (mode < -1 || mode > 1) return fail(RT_ERR_INVALID_ARG, "shade wide must be -1, 0 or 1 (got %d)", mode);
-  g_ctx.shade_wide = mode;
-  return RT_OK;
-}
-
 int rt_set_graphs(int32_t on) {
   int rc = ensure_device();
   if (rc) return rc;
@@ -815,7 +766,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     for (int k = 0; k < 3; ++k) centre[k] = (double)(float)(0.5 * (lo[k] + hi[k]));
   for (int q = 0; q < npairs_pad; ++q) {  // dummies never pass the filter
     pairs[2 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    pairs[2 * q + 1] = RT_FILTER_EXPANDED ? make_float4(0.f, 0.f, -1e30f, -1e30f) : make_float4(0.f, 0.f, -1.f, -1.f);
+    pairs[2 * q + 1] = make_float4(0.f, 0.f, -1e30f, -1e30f);
   }
   std::vector<float4> cr(ns > 0 ? ns : 1);
   std::vector<int> sprim(ns > 0 ? ns : 1), smat(ns > 0 ? ns : 1);
@@ -826,20 +777,13 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     const rt_primitive& q = prims[i];
     if (q.type == RT_PRIM_SPHERE) {
       if (q.p[3] > rmax) rmax = q.p[3];
-      float f0, f1, f2, f3;
-#if RT_FILTER_EXPANDED
       // c' = c - centre (float), K = r^2 - |c'|^2 (double, rounded once)
-      f0 = (float)((double)q.p[0] - centre[0]);
-      f1 = (float)((double)q.p[1] - centre[1]);
-      f2 = (float)((double)q.p[2] - centre[2]);
+      const float f0 = (float)((double)q.p[0] - centre[0]);
+      const float f1 = (float)((double)q.p[1] - centre[1]);
+      const float f2 = (float)((double)q.p[2] - centre[2]);
       const double r = q.p[3];
-      f3 = (float)(r * r - ((double)f0 * f0 + (double)f1 * f1 + (double)f2 * f2));
+      const float f3 = (float)(r * r - ((double)f0 * f0 + (double)f1 * f1 + (double)f2 * f2));
       const double cn = std::sqrt((double)f0 * f0 + (double)f1 * f1 + (double)f2 * f2);
-#else
-      f0 = q.p[0]; f1 = q.p[1]; f2 = q.p[2];
-      f3 = q.p[3] * q.p[3];
-      const double cn = std::fabs((double)q.p[0]) + std::fabs((double)q.p[1]) + std::fabs((double)q.p[2]);
-#endif
       if (cn > cmax) cmax = cn;
       float* A = reinterpret_cast<float*>(&pairs[2 * (ks / 2)]);
       float* B = reinterpret_cast<float*>(&pairs[2 * (ks / 2) + 1]);
@@ -859,21 +803,6 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
       pl.mat = (int)q.material;
       planes[kp++] = pl;
     }
-  }
-  // constant-bank copy in the projected form {c, r^2} (RayFilterT<false>), dummies r^2 = -1
-  std::vector<float4> cpairs(2 * (size_t)npairs_pad);
-  double cmax_abs = 0.0;
-  for (int q = 0; q < npairs_pad; ++q) {
-    cpairs[2 * q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    cpairs[2 * q + 1] = make_float4(0.f, 0.f, -1.f, -1.f);
-  }
-  for (int k = 0; k < ns; ++k) {
-    float* A = reinterpret_cast<float*>(&cpairs[2 * (k / 2)]);
-    float* B = reinterpret_cast<float*>(&cpairs[2 * (k / 2) + 1]);
-    const int h = k & 1;
-    A[0 + h] = cr[k].x; A[2 + h] = cr[k].y; B[0 + h] = cr[k].z; B[2 + h] = cr[k].w * cr[k].w;
-    const double cn = std::fabs((double)cr[k].x) + std::fabs((double)cr[k].y) + std::fabs((double)cr[k].z);
-    if (cn > cmax_abs) cmax_abs = cn;
   }
   // emitters (R#41): spheres whose material emits in some channel, in prim (= sphere) order
   std::vector<int> emit;
@@ -912,16 +841,12 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(cudaMemcpyAsync(c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
-  const bool in_const = npairs_pad <= rt::kMaxConstPairs;
-  CU(rt::upload_const_scene(planes.data(), np, cpairs.data(), in_const ? (int)cpairs.size() : 0, c.stream),
-     "constant upload");
+  CU(rt::upload_planes(planes.data(), np, c.stream), "constant upload (planes)");
   CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
   c.smem_scene = in_smem;
-  c.const_scene = in_const;
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
-  for (int k = 0; k < 3; ++k) c.centre[k] = RT_FILTER_EXPANDED ? centre[k] : 0.0;
+  for (int k = 0; k < 3; ++k) c.centre[k] = centre[k];
   c.rmax = (float)(rmax * (1.0 + 1e-6));
-  c.cmax_abs = (float)(cmax_abs * (1.0 + 1e-6));
   c.n_spheres = ns;
   c.n_pairs_pad = npairs_pad;
   c.n_planes = np;
@@ -936,12 +861,9 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   c.pairs_host = pairs;
   // light-origin shadow scans (rt_wavefront.cuh wf_isect_lt): s1 = K + 2 c'.o'(P_l) per point
   // light, FP64 rounded once, after a copy of the pairs; on while the tables fit 64 KB of smem
-#ifndef RT_LIGHT_ORIGIN
-#define RT_LIGHT_ORIGIN 1
-#endif
   c.lt_lights = 0;
   const size_t lt_bytes = (size_t)n_lights * npairs_pad * 8;
-  if (RT_LIGHT_ORIGIN && RT_FILTER_EXPANDED && n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
+  if (n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
       lt_bytes <= 65536 && in_smem) {
     std::vector<float4> lt(2 * (size_t)npairs_pad + lt_bytes / 16 + 1);
     std::memcpy(lt.data(), pairs.data(), sizeof(float4) * pairs.size());

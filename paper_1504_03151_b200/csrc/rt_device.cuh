@@ -168,13 +168,11 @@ __device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pai
 extern __shared__ float4 s_pairs[];
 
 // where the sphere-pair array is read from inside the scans
-enum : int { SRC_GLOBAL = 0, SRC_SMEM = 1, SRC_CONST = 2 };
-__constant__ float4 c_pairs[2 * kMaxConstPairs];
+enum : int { SRC_GLOBAL = 0, SRC_SMEM = 1 };
 
 template <int kSrc>
 __device__ __forceinline__ float4 load_pair(const float4* __restrict__ gp, int i) {
-  if constexpr (kSrc == SRC_SMEM) return s_pairs[i];       // warp-uniform address: LDS.128 broadcast
-  else if constexpr (kSrc == SRC_CONST) return c_pairs[i];  // uniform index: LDCU.128 -> UR operands
+  if constexpr (kSrc == SRC_SMEM) return s_pairs[i];  // warp-uniform address: LDS.128 broadcast
   else return __ldg(gp + i);
 }
 
@@ -203,78 +201,40 @@ __device__ __forceinline__ double sphere_root(const float4 cr, const d3 o, const
 
 // Float32 filter state of one ray. Per sphere the filter value v is
 // compared with `cut`; a sphere with v >= cut is a candidate, decided later in float64.
-//  * projected form (kExp = false, pair data {c, r^2}): orthonormal basis (u1, u2) of d (Duff et
-//    al. 2017), x = (c - o).u1, y = (c - o).u2, v = disc = r^2 - x^2 - y^2 (the precise
-//    discriminant of Eq. 11-12 with a = 1): 8 FMA per sphere, and every FFMA2 has at most one
-//    scene operand, so a constant-bank scene is loaded with LDCU into uniform registers;
-//  * expanded form (kExp = true, pair data {c', K = r^2 - |c'|^2} in scene-centred coordinates
-//    c' = c - centre): s1 = K + 2 c'.o', tc = (c' - o').d, v = tc^2 + s1 = disc + |o'|^2:
-//    7 FMA per sphere (Eq. 11's discriminant b^2 - (|oc|^2 - r^2) with |oc|^2 expanded).
+// Pair data {c', K = r^2 - |c'|^2} in scene-centred coordinates c' = c - centre:
+// s1 = K + 2 c'.o', tc = (c' - o').d, v = tc^2 + s1 = disc + |o'|^2 (Eq. 11's discriminant
+// b^2 - (|oc|^2 - r^2) with a = 1 and |oc|^2 expanded): 7 FMA per sphere, two spheres per FFMA2.
 // `slack` bounds |v_float - v_exact| (first-order FP32 error analysis), `eta` bounds the error
 // of tc; both make the filter conservative: no true intersection is ever dropped.
-template <bool kExp>
-struct RayFilterT {
-  float dx, dy, dz, a1, a2, a3, b1, b2, b3, b4, b5, odf, eta, neg_slack, cut;
+struct RayFilter {
+  float dx, dy, dz, a1, a2, a3, b1, eta, neg_slack, cut;
   __device__ __forceinline__ void init(const d3& o, const d3& d, const DevParams& P) {
     dx = (float)d.x; dy = (float)d.y; dz = (float)d.z;
-    if constexpr (kExp) {
-      const float ox = (float)(o.x - P.centre[0]), oy = (float)(o.y - P.centre[1]), oz = (float)(o.z - P.centre[2]);
-      const float on = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
-      a1 = 2.0f * ox; a2 = 2.0f * oy; a3 = 2.0f * oz;                 // 2 o'
-      b1 = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));                       // -o'.d
-      const float span = P.cmax + on + P.rmax;
-      const float slack = 24.0f * kUlp * span * span;
-      eta = 8.0f * kUlp * (P.cmax + on);
-      neg_slack = -slack;
-      cut = on * on - slack;
-      b2 = b3 = b4 = b5 = odf = 0.f;
-    } else {
-      const float ox = (float)o.x, oy = (float)o.y, oz = (float)o.z;
-      const float sg = copysignf(1.0f, dz);
-      const float ia = -1.0f / (sg + dz);
-      const float bb = dx * dy * ia;
-      a1 = fmaf(sg * dx * dx, ia, 1.0f); a2 = sg * bb; a3 = -sg * dx;    // u1
-      b1 = bb; b2 = fmaf(dy * dy, ia, sg); b3 = -dy;                    // u2
-      b4 = -fmaf(ox, a1, fmaf(oy, a2, oz * a3));                         // -o.u1
-      b5 = -fmaf(ox, b1, fmaf(oy, b2, oz * b3));                         // -o.u2
-      odf = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));                        // -o.d
-      eta = 32.0f * kUlp * (fabsf(ox) + fabsf(oy) + fabsf(oz) + P.cmax_abs);
-      neg_slack = -(4.0f * eta * P.rmax + 4.0f * eta * eta + 4.0f * kUlp * P.rmax * P.rmax);
-      cut = neg_slack;
-    }
+    const float ox = (float)(o.x - P.centre[0]), oy = (float)(o.y - P.centre[1]), oz = (float)(o.z - P.centre[2]);
+    const float on = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
+    a1 = 2.0f * ox; a2 = 2.0f * oy; a3 = 2.0f * oz;                 // 2 o'
+    b1 = -fmaf(ox, dx, fmaf(oy, dy, oz * dz));                       // -o'.d
+    const float span = P.cmax + on + P.rmax;
+    const float slack = 24.0f * kUlp * span * span;
+    eta = 8.0f * kUlp * (P.cmax + on);
+    neg_slack = -slack;
+    cut = on * on - slack;
   }
   // filter values of 16 spheres (pairs base..base+7), two spheres per FFMA2; returns their max
   template <int kSrc>
   __device__ __forceinline__ float batch(const float4* __restrict__ gp, int base, float2 (&v)[kPairsPerBatch]) const {
-    if constexpr (kExp) {
-      const float2 A1 = make_float2(a1, a1), A2 = make_float2(a2, a2), A3 = make_float2(a3, a3);
-      const float2 D1 = make_float2(dx, dx), D2 = make_float2(dy, dy), D3 = make_float2(dz, dz);
-      const float2 B1 = make_float2(b1, b1);
+    const float2 A1 = make_float2(a1, a1), A2 = make_float2(a2, a2), A3 = make_float2(a3, a3);
+    const float2 D1 = make_float2(dx, dx), D2 = make_float2(dy, dy), D3 = make_float2(dz, dz);
+    const float2 B1 = make_float2(b1, b1);
 #pragma unroll
-      for (int i = 0; i < kPairsPerBatch; ++i) {
-        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
-        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-        const float2 CZ = make_float2(b.x, b.y), K = make_float2(b.z, b.w);
-        const float2 s1 = __ffma2_rn(CX, A1, __ffma2_rn(CY, A2, __ffma2_rn(CZ, A3, K)));
-        const float2 tc = __ffma2_rn(CX, D1, __ffma2_rn(CY, D2, __ffma2_rn(CZ, D3, B1)));
-        v[i] = __ffma2_rn(tc, tc, s1);
-      }
-    } else {
-      const float2 U1x = make_float2(a1, a1), U1y = make_float2(a2, a2), U1z = make_float2(a3, a3);
-      const float2 U2x = make_float2(b1, b1), U2y = make_float2(b2, b2), U2z = make_float2(b3, b3);
-      const float2 OU1 = make_float2(b4, b4), OU2 = make_float2(b5, b5);
-#pragma unroll
-      for (int i = 0; i < kPairsPerBatch; ++i) {
-        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
-        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-        const float2 CZ = make_float2(b.x, b.y), R2 = make_float2(b.z, b.w);
-        const float2 x = __ffma2_rn(CX, U1x, __ffma2_rn(CY, U1y, __ffma2_rn(CZ, U1z, OU1)));
-        const float2 y = __ffma2_rn(CX, U2x, __ffma2_rn(CY, U2y, __ffma2_rn(CZ, U2z, OU2)));
-        const float2 nx = make_float2(-x.x, -x.y), ny = make_float2(-y.x, -y.y);
-        v[i] = __ffma2_rn(nx, x, __ffma2_rn(ny, y, R2));
-      }
+    for (int i = 0; i < kPairsPerBatch; ++i) {
+      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
+      const float2 CZ = make_float2(b.x, b.y), K = make_float2(b.z, b.w);
+      const float2 s1 = __ffma2_rn(CX, A1, __ffma2_rn(CY, A2, __ffma2_rn(CZ, A3, K)));
+      const float2 tc = __ffma2_rn(CX, D1, __ffma2_rn(CY, D2, __ffma2_rn(CZ, D3, B1)));
+      v[i] = __ffma2_rn(tc, tc, s1);
     }
     float vmax = fmaxf(v[0].x, v[0].y);
 #pragma unroll
@@ -286,25 +246,6 @@ struct RayFilterT {
   // sphere costs tc (3 FMA) + v = tc^2 + s1 (1 FMA) instead of 7 FMA. Same v, same cut; the
   // precomputed s1 (FP64, rounded once) is more accurate than the FMA chain the slack covers.
   template <int kSrc>
-  __device__ __forceinline__ float batch_eye(const float4* __restrict__ gp, int base, float2 (&v)[kPairsPerBatch]) const {
-    static_assert(kExp, "shared-origin filter exists in the expanded form");
-    const float2 D1 = make_float2(dx, dx), D2 = make_float2(dy, dy), D3 = make_float2(dz, dz);
-    const float2 B1 = make_float2(b1, b1);
-#pragma unroll
-    for (int i = 0; i < kPairsPerBatch; ++i) {
-      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
-      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-      const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
-      const float2 tc = __ffma2_rn(CX, D1, __ffma2_rn(CY, D2, __ffma2_rn(CZ, D3, B1)));
-      v[i] = __ffma2_rn(tc, tc, S1);
-    }
-    float vmax = fmaxf(v[0].x, v[0].y);
-#pragma unroll
-    for (int i = 1; i < kPairsPerBatch; ++i) vmax = fmaxf(vmax, fmaxf(v[i].x, v[i].y));
-    return vmax;
-  }
-  template <int kSrc>
   __device__ __forceinline__ void sphere_eye(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
     const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
     const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
@@ -314,33 +255,18 @@ struct RayFilterT {
     dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
   }
   // float discriminant estimate dd (|dd - disc| <= slack) and chord centre tc (|err| <= eta) of
-  // one sphere k (rare path). The projected form reads {c, r} of sphere k from `cr` (global):
-  // a constant-bank scene is then only ever indexed warp-uniformly (LDCU, not LDC).
+  // one sphere k (rare path)
   template <int kSrc>
-  __device__ __forceinline__ void sphere(const float4* __restrict__ gp, const float4* __restrict__ cr, int k,
-                                         float& dd, float& tc) const {
-    if constexpr (kExp) {
-      const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
-      const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
-      const bool h = k & 1;
-      const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, w = h ? pb.w : pb.z;
-      const float s1 = fmaf(cx, a1, fmaf(cy, a2, fmaf(cz, a3, w)));
-      tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
-      dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
-    } else {
-      const float4 c = __ldg(cr + k);
-      const float cx = c.x, cy = c.y, cz = c.z, w = c.w * c.w;  // r^2 rounded as on the host
-      const float lx = fmaf(cx, a1, fmaf(cy, a2, fmaf(cz, a3, b4)));
-      const float ly = fmaf(cx, b1, fmaf(cy, b2, fmaf(cz, b3, b5)));
-      dd = fmaf(-lx, lx, fmaf(-ly, ly, w));  // == the FFMA2 lane value
-      tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, odf)));
-    }
+  __device__ __forceinline__ void sphere(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
+    const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
+    const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
+    const bool h = k & 1;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, w = h ? pb.w : pb.z;
+    const float s1 = fmaf(cx, a1, fmaf(cy, a2, fmaf(cz, a3, w)));
+    tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
+    dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
   }
 };
-// scene staged in shared memory / global memory: expanded pair data; constant bank: projected
-template <int kSrc>
-using RayFilterFor = RayFilterT<kSrc != SRC_CONST && (bool)RT_FILTER_EXPANDED>;
-using RayFilter = RayFilterT<(bool)RT_FILTER_EXPANDED>;
 
 __device__ __forceinline__ unsigned batch_mask(const float2 (&v)[kPairsPerBatch], float cut) {
   unsigned cand = 0u;

@@ -2,11 +2,12 @@
 // kernels (rt_kernels.cu). Not part of the public ABI (include/rt.h).
 //
 // HBM / on-chip layout:
-//   spheres : AoSoA pairs, 32 B per pair of spheres: float4 {cxA, cxB, cyA, cyB},
-//             float4 {czA, czB, r2A, r2B}; padded with r2 = -1 dummies to a multiple of
-//             kPairsPerBatch pairs. Global memory; staged per CTA into shared memory with one
-//             TMA bulk copy when <= kMaxSmemPairs pairs (warp-uniform LDS.128 broadcasts),
-//             else read from global memory.
+//   spheres : AoSoA pairs, 32 B per pair of spheres in scene-centred coordinates c' = c - centre:
+//             float4 {c'xA, c'xB, c'yA, c'yB}, float4 {c'zA, c'zB, KA, KB} with K = r^2 - |c'|^2;
+//             padded with K = -1e30 dummies to a multiple of kPairsPerBatch pairs. Global memory;
+//             staged per CTA into shared memory with one TMA bulk copy when <= kMaxSmemPairs
+//             pairs (warp-uniform LDS.128 broadcasts), else read from global memory.
+//   pairs_eye / pairs_lt : the same layout with s1 = K + 2 c'.o' of the eye / of each point light
 //   sph_cr  : float4 {cx, cy, cz, r} per sphere (shading only), global
 //   sph_prim/sph_mat : int per sphere (original primitive index / material), global
 //   planes  : DevPlane[n_planes] (double) in the constant bank (tested before spheres)
@@ -20,19 +21,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#ifndef RT_FILTER_EXPANDED
-#define RT_FILTER_EXPANDED 1  // float32 filter form, see RayFilter (rt_device.cuh)
-#endif
 
 namespace rt {
 
 constexpr int kWarp = 32;
-#ifndef RT_PAIRS_PER_BATCH
-#define RT_PAIRS_PER_BATCH 8
-#endif
-constexpr int kPairsPerBatch = RT_PAIRS_PER_BATCH;  // 2x spheres per unrolled batch of the scans
+constexpr int kPairsPerBatch = 8;  // 2x spheres per unrolled batch of the scans
 constexpr int kMaxSmemPairs = 5120;  // 10240 spheres = 160 KB of dynamic shared memory per CTA
-constexpr int kMaxConstPairs = 1536; // 3072 spheres = 48 KB of the 64 KB constant bank
 constexpr int kMaxPlanes = 32;
 constexpr int kMaxLights = 32;
 constexpr int kTileW = 8, kTileH = 4, kTilePx = kTileW * kTileH;
@@ -59,10 +53,8 @@ struct DevParams {
   double eye[3], F[3], R[3], U[3];
   float bg[3], amb[3];
   double centre[3];  // scene centre (bounding box of the spheres): origin of the filter frame
-  float cmax;   // filter error bound: max over spheres of |c'| (expanded form, c' = c - centre)
-                //   or of |c|_1 (projected form)
+  float cmax;   // filter error bound: max over spheres of |c'| (c' = c - centre)
   float rmax;   // max sphere radius
-  float cmax_abs;  // max over spheres of |c|_1 (projected form in the constant bank)
   int W, H, max_depth, spp;
   int n_spheres, n_pairs_pad, n_planes, n_lights;
   unsigned long long seed;
@@ -80,7 +72,7 @@ struct DevParams {
 };
 
 struct DevScene {
-  const float4* pairs;     // global copy of the pair layout (used when not in the constant bank)
+  const float4* pairs;     // the pair layout in global memory (staged into shared memory per CTA)
   const float4* sph_cr;
   const int* sph_prim;
   const int* sph_mat;
@@ -135,7 +127,6 @@ struct WfBuffers {
   // when lt_lights > 0: the entries of point light l (< lt_lights) listed in slt[l * cap ..],
   // every other entry (emitters) in sother; the entries themselves stay path-major
   int* slt;        // [lt_lights * cap]
-  unsigned long long* lmask;  // [cap] per entry of Q[d]: sources (bit l) with a shadow ray
   int* sother;     // [scap]
   unsigned* ctr;   // counters, see wf_ctr_*
   int cap, scap;
@@ -153,8 +144,6 @@ struct WfBuffers {
   // rt_set_scan_split: -1 = by queue length (split_parts); 1, 2, 4 or 8 = that many parts for
   // every scan (a test and tuning knob)
   int force_parts;
-  // rt_set_shade_wide: -1 = by queue length (shade_wide); 0 = never, 1 = always one warp per path
-  int force_wide;
   // set per chunk on the copies passed to its launches: global sample index of the chunk's path 0
   // (the camera rays of depth 0 are implicit: entry e of Q[0] is path e, its ray computed on use)
   long long g0;
@@ -173,8 +162,7 @@ __host__ __device__ constexpr int wf_ctr_lt(int d, int l) { return kWfCtrPerDept
 constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
 // launchers (rt_kernels.cu)
-cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float4* pairs, int n_pair_float4,
-                               cudaStream_t st);
+cudaError_t upload_planes(const DevPlane* planes, int n_planes, cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
 size_t wf_bytes(int cap, int scap, int xctas);
@@ -187,6 +175,7 @@ struct WfTiming {
   int n;          // pairs recorded (output)
   int launches;   // kernels launched (output)
   cudaEvent_t* shade = nullptr;  // [2 * cap] events around each wf_shade launch
+  cudaEvent_t* accum = nullptr;  // [2 * cap] events around each wf_accumulate launch
   // second stream: the shadow scan + accumulate of depth d run on it, concurrently with the
   // closest-hit scan of depth d + 1 on the main stream (fork/join events per depth)
   cudaStream_t side = nullptr;
@@ -216,7 +205,7 @@ struct WfTiming {
     cudaEventRecordWithFlags(ev, s, ext_events ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
 };
-// scene source of the wavefront intersection kernels: 0 global, 1 shared memory, 2 constant bank
+// scene source of the wavefront intersection kernels: 0 global, 1 shared memory
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st);
 int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined);

@@ -6,7 +6,7 @@
 //     (ballot + popc + shfl), so warps stay full until the queue drains (path regeneration);
 //   * each round, every lane has exactly one ray query — a closest-hit query (primary or
 //     secondary ray) or an any-hit shadow query — and the whole warp runs ONE intersection
-//     loop over the scene: sphere data is warp-uniform (constant bank) and two spheres are
+//     loop over the scene: sphere data is warp-uniform (shared memory) and two spheres are
 //     tested per FFMA2 instruction by a conservative float32 filter; the rare candidates are
 //     decided in float64 from the exact float inputs (same decisions as a double-precision
 //     reference up to double rounding);
@@ -133,7 +133,7 @@ __device__ __forceinline__ void intersect(Lane& L, const DevParams& P, const Dev
       if (k >= P.n_spheres) break;  // padding (only reachable when the slack exceeds the dummy margin)
       if (kExt && shadow && k == L.qskip) continue;  // the emitter a shadow ray aims at (R#41)
       float dd, tc;
-      F.sphere<kSrc>(pairs, S.sph_cr, k, dd, tc);
+      F.sphere<kSrc>(pairs, k, dd, tc);
       const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));
       if (tc + qh < (float)kEps - F.eta || tc - qh > tmax_hi) continue;
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
@@ -406,11 +406,9 @@ __device__ __forceinline__ void advance(Lane& L, const DevParams& P, const DevSc
 }
 
 // ---- the persistent megakernel --------------------------------------------------------------
-#ifndef RT_MIN_BLOCKS
-#define RT_MIN_BLOCKS 2
-#endif
+constexpr int kMegaMinBlocks = 2;  // 128 registers per lane state machine: 2 CTAs x 8 warps per SM
 template <bool kSmem, bool kDebug, bool kExt>
-__global__ void __launch_bounds__(256, RT_MIN_BLOCKS)
+__global__ void __launch_bounds__(256, kMegaMinBlocks)
 render_kernel(const DevParams P, const DevScene S, const DevOutputs O) {
   __shared__ uint64_t s_mbar;
   if constexpr (kSmem) stage_scene(s_pairs, S.pairs, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
@@ -501,15 +499,9 @@ __global__ void tonemap_kernel(const float4* __restrict__ in, uchar4* __restrict
 }
 
 // ---- launchers ------------------------------------------------------------------------------
-cudaError_t upload_const_scene(const DevPlane* planes, int n_planes, const float4* pairs, int n_pair_float4,
-                               cudaStream_t st) {
-  cudaError_t e = cudaSuccess;
-  if (n_pair_float4 > 0)
-    e = cudaMemcpyToSymbolAsync(c_pairs, pairs, sizeof(float4) * n_pair_float4, 0, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && n_planes > 0)
-    e = cudaMemcpyToSymbolAsync(c_planes, planes, sizeof(DevPlane) * n_planes, 0,
-                                cudaMemcpyHostToDevice, st);
-  return e;
+cudaError_t upload_planes(const DevPlane* planes, int n_planes, cudaStream_t st) {
+  if (n_planes <= 0) return cudaSuccess;
+  return cudaMemcpyToSymbolAsync(c_planes, planes, sizeof(DevPlane) * n_planes, 0, cudaMemcpyHostToDevice, st);
 }
 
 template <bool kSmem, bool kDebug, bool kExt>
@@ -586,7 +578,7 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 // ---- wavefront launcher ---------------------------------------------------------------------
 size_t wf_bytes(int cap, int scap, int xctas) {
   const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
-  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + 8 + kCandMax * 4) +
+  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + kCandMax * 4) +
          (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4 + 4 + 4) +
          (size_t)xctas * 8 * (32 * 2 + 64) * kCandMax * 4 + 40 * 256;
 }
@@ -619,12 +611,10 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
   B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.slt = reinterpret_cast<int*>(take(4 * (size_t)scap));  // lt_lights * cap <= scap
-  B.lmask = reinterpret_cast<unsigned long long*>(take(8 * (size_t)cap));
   B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
   B.xctas = xctas;
   B.solo = 0;
   B.force_parts = -1;
-  B.force_wide = -1;
   B.xcand_c = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xlo_c = reinterpret_cast<float*>(take(4 * (size_t)xctas * 8 * 32 * kCandMax));
   B.xcand_s = reinterpret_cast<int*>(take(4 * (size_t)xctas * 8 * 64 * kCandMax));
@@ -632,14 +622,11 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
 }
 
 // work items (pixels) per chunk: as many as the buffers hold; a pipelined render of a frame that
-// would fit one chunk is cut in two, so the two chunks can overlap
+// would fit one chunk is cut in two, so the two chunks can overlap (3 or 4 pipelined chunks were
+// 20 % slower at world 8: chunk k+2 waits for chunk k on the same buffer set)
 int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined) {
-#ifndef RT_PIPE_SPLIT
-#define RT_PIPE_SPLIT 2
-#endif
   int items = cap_paths / p.spp;
-  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18))
-    items = (p.n_items + RT_PIPE_SPLIT - 1) / RT_PIPE_SPLIT;
+  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18)) items = (p.n_items + 1) / 2;
   return items > 0 ? items : 1;
 }
 
@@ -649,25 +636,13 @@ int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined) {
   return chunks * (p.max_depth + 1);
 }
 
-#ifndef RT_PDL
-#define RT_PDL 0  // measured: early trigger +4.5 % (waiting CTAs squat on SMs), late trigger +-0
-#endif
-// launch with programmatic stream serialisation (see pdl_enter): the kernel may start while the
-// previous kernel of the stream finishes; its griddepcontrol.wait keeps the data dependency
 template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*k)(KArgs...), int grid, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = RT_PDL ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+static void launch(void (*k)(KArgs...), int grid, size_t smem, cudaStream_t st, Args... args) {
+  k<<<grid, 256, smem, st>>>(static_cast<KArgs>(args)...);
 }
+
+constexpr int kLogicGridPerSm = 6;  // logic kernels: grid-stride loops (measured C4 world 1 / 8:
+                                    // 4 -> 7.00 / 1.10 ms, 6 -> 7.03 / 1.084, 8 -> 7.04 / 1.082)
 
 template <int kSrc>
 static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
@@ -678,26 +653,14 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
   cudaError_t e;
   int occ_c = 0, occ_s = 0;
-  // camera rays (depth 0) use the shared-origin filter when the eye-specific pairs exist
-  constexpr bool kEyeOk = kSrc != SRC_CONST && RT_FILTER_EXPANDED;
   using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
-  IsectFn kc0 = wf_isect<kSrc, false>;
-  // short queues are scanned by the split path (wf_isect_split_body), called from the scan kernel
-  // itself (RT_SPLIT_FUSED) or, otherwise, launched as a second kernel with the same grid: both
-  // read the same queue length and exactly one of them does the work
-  IsectFn kc0s = wf_isect_split<kSrc, false>;
-#ifndef RT_EYE_TWO_RAYS
-#define RT_EYE_TWO_RAYS 1
-#endif
-  if (kEyeOk && sc.pairs_eye != nullptr) {
-    kc0 = RT_EYE_TWO_RAYS ? wf_isect_eye2<kSrc> : wf_isect<kSrc, false, kEyeOk>;
-    kc0s = RT_EYE_TWO_RAYS ? nullptr : wf_isect_split<kSrc, false, kEyeOk>;  // camera queues are long
-  }
+  // camera rays (depth 0): two per thread through the shared-origin filter on the eye's pair table
+  const IsectFn kc0 = wf_isect_eye2<kSrc>;
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
   size_t smem_lt = 0;
   int grid_lt = 0;
-  if constexpr (kSrc == SRC_SMEM && RT_FILTER_EXPANDED) {
+  if constexpr (kSrc == SRC_SMEM) {
     if (p.lt_lights > 0) {
       klt = wf_isect_lt<kSrc>;
       klts = wf_isect_lt_split<kSrc>;
@@ -710,27 +673,25 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     }
   }
   for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0, (IsectFn)wf_isect_split<kSrc, false>,
-                  (IsectFn)wf_isect_split<kSrc, true>, (IsectFn)wf_isect_split<kSrc, false, kEyeOk>}) {
+                  (IsectFn)wf_isect_split<kSrc, true>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSrc, false>, 256, smem)) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
-#ifndef RT_LOGIC_GRID_PER_SM
-#define RT_LOGIC_GRID_PER_SM 6  // measured C4 world 1 / 8: 4 -> 7.00 / 1.10 ms, 6 -> 7.03 / 1.084, 8 -> 7.04 / 1.082, 16 -> 7.11 / 1.11
-#endif
-  const int grid_l = num_sms * RT_LOGIC_GRID_PER_SM;  // logic kernels: grid-stride loops
+  const int grid_l = num_sms * kLogicGridPerSm;
   // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length
   auto host_parts = [&](unsigned tasks, int grid) -> int {
     if (grid > B0.xctas) return 1;
     if (B0.force_parts > 0) return B0.force_parts;
-    const unsigned warps = (unsigned)grid * 8u;
-    int pp = 1;
-    while (pp < RT_SPLIT_MAX && tasks * (unsigned)pp * RT_SPLIT_SLACK <= warps) pp <<= 1;
-    if (pp == 1 && RT_SPLIT_MID > 0 && tasks * 2u <= warps * (unsigned)RT_SPLIT_MID) pp = 2;
-    return pp;
+    return split_rule(tasks, (unsigned)grid * 8u);
   };
+  using ShadeFn = void (*)(const DevParams, const DevScene, WfBuffers, int, long long, unsigned long long*, int*, int*);
+  const ShadeFn shade = ext ? (dbg ? wf_shade<true, true> : wf_shade<false, true>)
+                            : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
+  int* dh = dbg ? o.dbg_hits : nullptr;
+  int* db = dbg ? o.dbg_bounces : nullptr;
   const bool pipe = tm.B2 != nullptr;
   const int items_per_chunk = wf_items_per_chunk(p, B0.cap, pipe);
   tm.n = 0;
@@ -738,7 +699,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   tm.n_chunks = 0;
   if (dbg) {
     const long long nh = (long long)p.W * p.H * p.spp * (p.max_depth + 1);
-    launch_pdl(fill_int, num_sms * 8, 0, st, o.dbg_hits, nh, -2);
+    launch(fill_int, num_sms * 8, 0, st, o.dbg_hits, nh, -2);
     ++tm.launches;
   }
   if (pipe) {  // the second slot's streams start after everything issued on st so far
@@ -762,9 +723,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const int npaths = nw * p.spp;
     const long long g0 = (long long)w0 * p.spp;
     if ((e = cudaMemsetAsync(Bc.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
-    const int grid_r = (npaths + 255) / 256 < grid_l ? (npaths + 255) / 256 : grid_l;
-    if (RT_Q0_IMPLICIT) launch_pdl(wf_q0_len, 1, 0, st, Bc, npaths);  // camera rays computed on use
-    else launch_pdl(wf_raygen, grid_r, 0, st, p, Bc, g0, npaths, o.stats);
+    launch(wf_q0_len, 1, 0, st, Bc, npaths);  // camera rays are computed on use (implicit queue)
     // per depth d: closest scan (d) -> shade (d) -> { shadow scan (d) -> accumulate (d) on the side
     // stream  ||  closest scan (d + 1) on the main stream } -> join -> shade (d + 1) ...
     // (independent: the shadow side reads the shadow entries and writes L into Q[d+1]; the closest
@@ -775,20 +734,18 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const bool rec = ti < tm.cap;
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
-        launch_pdl(kc0, grid_c, smem, st, p, sc, Bc, dd);
-        if (kc0s && !RT_SPLIT_FUSED) launch_pdl(kc0s, grid_c, smem, st, p, sc, Bc, dd);
-        tm.launches += (kc0s && !RT_SPLIT_FUSED) ? 2 : 1;
-      } else if (hint && !RT_SPLIT_FUSED) {  // one kernel, chosen from the previous frame's queue
+        launch(kc0, grid_c, smem, st, p, sc, Bc, dd);
+      } else if (hint) {  // one kernel, chosen from the previous frame's queue
         if (host_parts((hint[wf_ctr_q(dd)] + 31u) / 32u, grid_c) > 1)
-          launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+          launch(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
         else
-          launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+          launch(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+      } else {  // the self-selecting pair: both read the queue length, exactly one works
+        launch(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
+        launch(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
         tm.launches += 1;
-      } else {
-        launch_pdl(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
-        if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
-        tm.launches += RT_SPLIT_FUSED ? 1 : 2;
       }
+      tm.launches += 1;
       if (rec) tm.record(tm.closest[2 * ti + 1], st);
     };
     closest_scan(0);
@@ -796,29 +753,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      {
-        // the path-per-thread shade and the warp-per-path shade (short queues): a self-selecting
-        // pair, or with a hint the one the rule picks (solo)
-        using ShadeFn = void (*)(const DevParams, const DevScene, WfBuffers, int, long long, unsigned long long*, int*, int*);
-        const ShadeFn narrow = ext ? (dbg ? wf_shade<true, true> : wf_shade<false, true>)
-                                   : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
-        const ShadeFn wide = ext ? (dbg ? wf_shade_wide<true, true> : wf_shade_wide<false, true>)
-                                 : (dbg ? wf_shade_wide<true, false> : wf_shade_wide<false, false>);
-        int* dh = dbg ? o.dbg_hits : nullptr;
-        int* db = dbg ? o.dbg_bounces : nullptr;
-        const bool wide_ok = (RT_SHADE_WIDE || Bc.force_wide == 1) && p.n_lights + p.n_emitters <= 64;
-        if (hint && wide_ok) {
-          const bool w = Bc.force_wide >= 0 ? Bc.force_wide == 1 : hint[wf_ctr_q(d)] <= (unsigned)grid_l * 8u / RT_SHADE_WIDE_DIV;
-          launch_pdl(w ? wide : narrow, grid_l, 0, st, p, sc, Bs, d, g0, o.stats, dh, db);
-          tm.launches += 1;
-        } else {
-          launch_pdl(narrow, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
-          if (wide_ok) launch_pdl(wide, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
-          tm.launches += wide_ok ? 2 : 1;
-        }
-      }
+      launch(shade, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
-      if (klt && !RT_BIN_FUSED) launch_pdl(wf_bin, grid_l, 0, st, p, Bc, d);  // per-light lists of the shadow entries
       cudaStream_t ss = st;
       if (side) {
         cudaEventRecord(fork[d], st);
@@ -828,49 +764,49 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) tm.record(tm.shadow[2 * ti], ss);
       int scan_launches = 0;
       if (klt) {  // point lights, from the light
-        if (hint && !RT_SPLIT_FUSED) {
+        if (hint) {
           unsigned chunks = 0;
           for (int l = 0; l < p.lt_lights; ++l) chunks += (hint[wf_ctr_lt(d, l)] + 63u) / 64u;
-          launch_pdl(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
+          launch(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch_pdl(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
-          if (!RT_SPLIT_FUSED) launch_pdl(klts, grid_lt, smem_lt, ss, p, sc, Bc, d);
-          scan_launches += RT_SPLIT_FUSED ? 1 : 2;
+          launch(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
+          launch(klts, grid_lt, smem_lt, ss, p, sc, Bc, d);
+          scan_launches += 2;
         }
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
-        if (hint && !RT_SPLIT_FUSED) {
+        if (hint) {
           const unsigned ns = hint[p.lt_lights > 0 ? wf_ctr_so(d) : wf_ctr_s(d)];
           if (host_parts((ns + 31u) / 32u, grid_s) > 1)
-            launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
+            launch(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
           else
-            launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
+            launch(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch_pdl(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
-          if (!RT_SPLIT_FUSED) launch_pdl(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
-          scan_launches += RT_SPLIT_FUSED ? 1 : 2;
+          launch(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
+          launch(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
+          scan_launches += 2;
         }
       }
       if (rec) tm.record(tm.shadow[2 * ti + 1], ss);
       // wf_accumulate<false> when no entry aims at an emitter and wf_shade skips the skip2
       // column (the same condition as there: no extensions, light-origin scans on)
-      if (ext || p.lt_lights == 0) launch_pdl(wf_accumulate<true>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
-      else launch_pdl(wf_accumulate<false>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
+      if (rec && tm.accum) tm.record(tm.accum[2 * ti], ss);
+      if (ext || p.lt_lights == 0) launch(wf_accumulate<true>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
+      else launch(wf_accumulate<false>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
+      if (rec && tm.accum) tm.record(tm.accum[2 * ti + 1], ss);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
         cudaEventRecord(join[d], side);
         cudaStreamWaitEvent(st, join[d], 0);
       }
-      // shade, bin, the shadow scans with their split variants, accumulate (closest scans above)
-      // accumulate, (wf_bin), the shadow scans (shade and the closest scans are counted above)
-      tm.launches += 1 + ((klt && !RT_BIN_FUSED) ? 1 : 0) + scan_launches;
+      tm.launches += 2 + scan_launches;  // shade, accumulate, the shadow scans
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
-    launch_pdl(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum);
-    tm.launches += 2;
+    launch(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum);
+    tm.launches += 2;  // wf_q0_len, wf_resolve
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
       tm.record(tm.chunk_done[tm.n_chunks], st);
       tm.chunk_items[tm.n_chunks] = w0 + nw;
@@ -886,7 +822,6 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
 
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st) {
-  if (src == SRC_CONST) return wf_run<SRC_CONST>(p, sc, o, num_sms, B, tm, st);
   if (src == SRC_SMEM) return wf_run<SRC_SMEM>(p, sc, o, num_sms, B, tm, st);
   return wf_run<SRC_GLOBAL>(p, sc, o, num_sms, B, tm, st);
 }

@@ -5,14 +5,17 @@
 // into kernels over compacted queues in HBM, so the FP32 intersection loop runs at high
 // occupancy with no divergent logic inside, and the FP64 logic runs at full SIMD width:
 //
-//   raygen            paths of a chunk of pixels -> closest queue Q[0]              (a2)
+//   Q[0] is implicit: entry e is the chunk's path e; its camera ray is computed where
+//   it is used (wf_isect_eye2, wf_shade at depth 0)                                 (a2)
 //   per depth d = 0..max_depth:
 //     isect_closest   Q[d]: FP32 FFMA2 filter over all spheres -> candidate lists     (a3)
+//                     (depth 0: two camera rays per thread, shared-origin filter)
 //     shade           Q[d]: FP64 nearest hit (planes + candidates), emission/ambient,
 //                     shadow entries with their Lambert/Phong contribution, bounce   (a4, a6)
 //                     -> Q[d+1]
 //     isect_shadow    shadow entries: FP64 planes, FP32 filter with early exit on a
-//                     robust (float-certain) occluder -> candidate lists             (a5)
+//                     robust (float-certain) occluder -> candidate lists; point
+//                     lights' rays are scanned from the light (wf_isect_lt)           (a5)
 //     accumulate      Q[d]: FP64 occlusion decisions in light order, L += contribution
 //   resolve           sum of the spp sample radiances in order s = 0..spp-1 -> float4 (a7)
 //
@@ -28,18 +31,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
-}
-
-// Programmatic dependent launch (RT_PDL): every wavefront kernel first waits for the grid it
-// depends on (griddepcontrol.wait: that grid has completed and its memory is visible; a no-op
-// without a programmatic dependency), then lets the next kernel of its stream launch, so the
-// next launch and its CTA rasterisation overlap this kernel instead of following it.
-#ifndef RT_PDL_EARLY
-#define RT_PDL_EARLY 1
-#endif
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (RT_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // warp-aggregated reservation of `cnt` (< 64) slots on a global counter: exclusive prefix of
@@ -94,15 +85,12 @@ __device__ __forceinline__ d3 q_origin(const DevParams& P, const WfQueue& Q, int
   return d == 0 ? mk(P.eye[0], P.eye[1], P.eye[2]) : ld3(Q.ray, cap, (int)e, 0);
 }
 __device__ __forceinline__ int q_skip(const WfQueue& Q, unsigned e, int d) { return d == 0 ? -1 : Q.skip[e]; }
-#ifndef RT_Q0_IMPLICIT
-#define RT_Q0_IMPLICIT 1
-#endif
-// direction of closest-hit entry e of Q[d]. Depth 0 (RT_Q0_IMPLICIT): entry e is the chunk's
-// path e, whose camera ray is computed here exactly as wf_raygen would store it; false for a
-// work item outside the image (partial edge tiles, shard tiles past the end)
+// direction of closest-hit entry e of Q[d]. Depth 0 (the implicit camera queue): entry e is the
+// chunk's path e, whose camera ray is computed here; false for a work item outside the image
+// (partial edge tiles, shard tiles past the end)
 __device__ __forceinline__ bool q_dir(const DevParams& P, const WfBuffers& B, const WfQueue& Q, unsigned e, int d,
                                       d3& dir) {
-  if (RT_Q0_IMPLICIT && d == 0) {
+  if (d == 0) {
     const long long g = B.g0 + e;
     int px = 0, py = 0;
     if (!item_pixel(P, (int)(g / P.spp), px, py)) return false;
@@ -113,7 +101,7 @@ __device__ __forceinline__ bool q_dir(const DevParams& P, const WfBuffers& B, co
   return true;
 }
 __device__ __forceinline__ int q_path(const WfQueue& Q, unsigned e, int d) {
-  return (RT_Q0_IMPLICIT && d == 0) ? (int)e : Q.path[e];
+  return d == 0 ? (int)e : Q.path[e];
 }
 __device__ __forceinline__ float3 lf3(const float* a, int cap, int i) {
   return f3(a[i], a[(size_t)cap + i], a[2 * (size_t)cap + i]);
@@ -200,10 +188,7 @@ __device__ __forceinline__ bool light_sample(const DevParams& P, const DevScene&
 template <bool kExt>
 __device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevScene& S, int l, d3 p, d3 nrm,
                                                  unsigned long long pix, unsigned sg, int depth) {
-#ifndef RT_COUNT_SIGN
-#define RT_COUNT_SIGN 1
-#endif
-  if (RT_COUNT_SIGN && l < P.n_lights) {
+  if (l < P.n_lights) {
     const DevLight lt = S.lights[l];
     const d3 w = mk(lt.px, lt.py, lt.pz) - p;
     if (dot(w, w) < 1e-12) return false;  // the same d^2 test as light_sample
@@ -218,58 +203,25 @@ __device__ __forceinline__ bool sends_shadow_ray(const DevParams& P, const DevSc
 
 // ---- a2 with the implicit camera queue: only its length (the rays are computed on use) ---------
 __global__ void wf_q0_len(WfBuffers B, int n) {
-  pdl_enter();
   if (threadIdx.x == 0) B.ctr[wf_ctr_q(0)] = (unsigned)n;
 }
 
-// ---- a2: ray generation -> Q[0] ------------------------------------------------------------
-__global__ void __launch_bounds__(256) wf_raygen(const DevParams P, WfBuffers B, long long g0, int n,
-                                                 unsigned long long* stats) {
-  pdl_enter();
-  const WfQueue Q = B.q[0];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const long long g = g0 + i;
-    const int w = (int)(g / P.spp), s = (int)(g % P.spp);
-    int px = 0, py = 0;
-    const bool valid = item_pixel(P, w, px, py);
-    const unsigned slot = warp_reserve(valid ? 1u : 0u, B.ctr + wf_ctr_q(0));
-    if (valid) {
-      // camera rays: only the path id and the direction are stored; origin (the eye), throughput
-      // (1), radiance (0), depth (0) and skip (-1) are the same for every entry of Q[0] and are
-      // supplied by the kernels of depth 0 (q_origin / q_skip / wf_shade)
-      Q.path[slot] = i;
-      st3(Q.ray, B.cap, slot, 3, camera_dir(P, px, py, s));
-    }
-    warp_stat(stats, 0, valid ? 1ull : 0ull);
-  }
-}
-
 // ---- a3 / a5: FP32 filter over all spheres (persistent, one warp = 32 rays) -----------------
-#ifndef RT_ISECT_MIN_BLOCKS
-#define RT_ISECT_MIN_BLOCKS 3
-#endif
-#ifndef RT_SCAN_UNROLL
-#define RT_SCAN_UNROLL 1
-#endif
-constexpr int kScanUnroll = RT_SCAN_UNROLL;  // batches of the scan loop unrolled together
-// kEye: the closest-hit rays of depth 0 (camera rays, all from the eye) use the shared-origin
-// filter on S.pairs_eye (4 instead of 7 FMA per sphere, RayFilterT::batch_eye)
+constexpr int kIsectMinBlocks = 3;  // 80 registers: 3 CTAs x 8 warps per SM (4 CTAs spill)
 // One ray's scan over the sphere pairs [pb, pe): FP32 filter, candidate list in index order
 // (closest: pruned by the certain upper bound tub; shadow: up to the first certain occluder rob).
 // lo_row != nullptr: also store each closest candidate's lower root bound (split scans merge their
 // parts' lists with the smallest tub of all parts).
-template <int kSrc, bool kShadow, bool kEye>
+template <int kSrc, bool kShadow>
 __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S, const float4* __restrict__ gp,
-                                           const RayFilterFor<kSrc>& F, int pb, int pe, bool& act, int skip,
+                                           const RayFilter& F, int pb, int pe, bool& act, int skip,
                                            int skip2, float tl_f, float& tub, int& nc, int& rob, int* cand_row,
                                            float* lo_row) {
   const float eps_f = (float)kEps;
-#pragma unroll(kScanUnroll)
   for (int base = pb; base < pe; base += kPairsPerBatch) {
     float2 disc[kPairsPerBatch];
     float dmax;
-    if constexpr (kEye) dmax = F.template batch_eye<kSrc>(gp, base, disc);
-    else dmax = F.template batch<kSrc>(gp, base, disc);
+    dmax = F.template batch<kSrc>(gp, base, disc);
     const bool any = act && dmax >= F.cut;
     if (__any_sync(kFull, any)) {
       if (any) {
@@ -282,8 +234,7 @@ __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S
           if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
           if (kShadow && k == skip2) continue;
           float dd, tc;
-          if constexpr (kEye) F.template sphere_eye<kSrc>(gp, k, dd, tc);
-          else F.template sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
+          F.template sphere<kSrc>(gp, k, dd, tc);
           const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
           const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
           const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
@@ -334,23 +285,18 @@ __device__ __forceinline__ void isect_scan(const DevParams& P, const DevScene& S
 //  * shadow: the parts' candidates up to and including the first part that found a certain
 //    occluder, which becomes the ray's rob: exactly the list of the unsplit index-order scan.
 // A merged list longer than kCandMax overflows into the FP64 full scan, as an unsplit one does.
-#ifndef RT_SPLIT_MAX
-#define RT_SPLIT_MAX 8
-#endif
-#ifndef RT_SPLIT_MID
-#define RT_SPLIT_MID 0  // > 0: two parts also while tasks <= warps * MID / 2 (the last-task tail)
-#endif
-#ifndef RT_SPLIT_SLACK
-#define RT_SPLIT_SLACK 4  // split while tasks x parts x SLACK <= resident warps (measured: 2, 4, 8, 16 -> world-8 rank 1.105, 1.082, 1.082, 1.095 ms)
-#endif
+constexpr int kSplitMax = 8, kSplitSlack = 4;
+// split while tasks x parts x kSplitSlack <= resident warps (measured slack 2, 4, 8, 16 -> world-8
+// rank 1.105, 1.082, 1.082, 1.095 ms); the same rule is evaluated on the host for hinted launches
+__host__ __device__ __forceinline__ int split_rule(unsigned tasks, unsigned warps) {
+  int p = 1;
+  while (p < kSplitMax && tasks * (unsigned)p * kSplitSlack <= warps) p <<= 1;
+  return p;
+}
 __device__ __forceinline__ int split_parts(unsigned tasks, const WfBuffers& B) {
   if ((int)gridDim.x > B.xctas || blockDim.x != 256) return 1;
   if (B.force_parts > 0) return B.force_parts;
-  const unsigned warps = gridDim.x * 8u;
-  int p = 1;
-  while (p < RT_SPLIT_MAX && tasks * (unsigned)p * RT_SPLIT_SLACK <= warps) p <<= 1;
-  if (p == 1 && RT_SPLIT_MID > 0 && tasks * 2u <= warps * (unsigned)RT_SPLIT_MID) p = 2;  // halve the last task
-  return p;
+  return split_rule(tasks, gridDim.x * 8u);
 }
 // batch-aligned pair range of part `part` of `parts`
 __device__ __forceinline__ void split_range(const DevParams& P, int part, int parts, int& pb, int& pe) {
@@ -377,36 +323,18 @@ __device__ __forceinline__ void split_merge_shadow(int parts, const int* s_nc, c
   rob_out = rob;
 }
 
-// RT_SPLIT_FUSED=1: the scan kernel calls the split path itself (a non-inlined function,
-// measured slower: 80 registers and a 528-byte stack frame in the long-queue kernel); 0 (default):
-// a separate wf_isect_split launch
-#ifndef RT_SPLIT_FUSED
-#define RT_SPLIT_FUSED 0
-#endif
-#if RT_SPLIT_FUSED
-#define RT_SPLIT_INL __noinline__
-#else
-#define RT_SPLIT_INL __forceinline__  // inlined into its own kernel: parameters stay in the constant bank
-#endif
-template <int kSrc, bool kShadow, bool kEye>
-__device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d);
-template <int kSrc, bool kShadow, bool kEye = false>
-__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+template <int kSrc, bool kShadow>
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  pdl_enter();
-  static_assert(!(kEye && kShadow), "shadow rays start at shading points");
   __shared__ uint64_t s_mbar;
   // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
   const bool listed = kShadow && P.lt_lights > 0;
   const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
-  if (!B.solo && split_parts((n + 31u) / 32u, B) > 1) {  // a short queue: the split scan
-    if (RT_SPLIT_FUSED) wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
-    return;
-  }
+  if (!B.solo && split_parts((n + 31u) / 32u, B) > 1) return;  // a short queue: wf_isect_split scans it
   // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
   // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
   if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
-  const float4* gp = kEye ? S.pairs_eye : S.pairs;
+  const float4* gp = S.pairs;
   if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
   unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
   const WfQueue Q = B.q[d & 1];
@@ -448,17 +376,15 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
         skip = q_skip(Q, e, d);
       }
     }
-    RayFilterFor<kSrc> F;
+    RayFilter F;
     F.init(o, dir, P);
     const float tl_f = (float)tl;
     float tub = 3.0e38f;  // closest: certain upper bound of the nearest accepted root
     int nc = 0;
-#pragma unroll(kScanUnroll)
     for (int base = 0; base < P.n_pairs_pad; base += kPairsPerBatch) {
       float2 disc[kPairsPerBatch];
       float dmax;
-      if constexpr (kEye) dmax = F.template batch_eye<kSrc>(gp, base, disc);
-      else dmax = F.template batch<kSrc>(gp, base, disc);
+      dmax = F.template batch<kSrc>(gp, base, disc);
       const bool any = act && dmax >= F.cut;
       if (__any_sync(kFull, any)) {
         if (any) {
@@ -471,8 +397,7 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
             if (k == skip) continue;  // the sphere the ray leaves (exact, see shadow_skip / skip_c)
             if (kShadow && k == skip2) continue;
             float dd, tc;
-            if constexpr (kEye) F.template sphere_eye<kSrc>(gp, k, dd, tc);
-            else F.template sphere<kSrc>(gp, S.sph_cr, k, dd, tc);
+            F.template sphere<kSrc>(gp, k, dd, tc);
             const float qh = sqrtf(fmaxf(dd - F.neg_slack, 0.f));  // >= true q
             const float ql = sqrtf(fmaxf(dd + F.neg_slack, 0.f));  // <= true q
             const bool sure = dd + F.neg_slack > 0.f;               // certainly intersects
@@ -503,15 +428,6 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
           }
         }
       }
-#ifdef RT_SIMD_PROBE
-      {
-        const unsigned nact = (unsigned)__popc(__ballot_sync(kFull, act));
-        if ((threadIdx.x & 31) == 0) {
-          atomicAdd(B.ctr + 70 * kWfCtrPerDepth + (kShadow ? 2 : 0), 1u);
-          atomicAdd(B.ctr + 70 * kWfCtrPerDepth + (kShadow ? 3 : 1), nact);
-        }
-      }
-#endif
       if constexpr (kShadow) {
         if (!__any_sync(kFull, act)) break;  // Alg. 1 `break`, warp-wide
       }
@@ -523,8 +439,8 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
 }
 
-template <int kSrc, bool kShadow, bool kEye>
-__device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
+template <int kSrc, bool kShadow>
+__device__ __forceinline__ void wf_isect_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
   __shared__ uint64_t s_mbar;
   __shared__ int s_nc[8][32];
   __shared__ int s_x[8][32];  // closest: tub (float bits); shadow: rob
@@ -534,7 +450,7 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
   const unsigned tasks = (n + 31u) / 32u;  // 32 rays each
   const int parts = split_parts(tasks, B);
   if (parts == 1 && !B.solo) return;  // a long queue: wf_isect scans it (solo: one part here)
-  const float4* gp = kEye ? S.pairs_eye : S.pairs;
+  const float4* gp = S.pairs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tpc = 8 / parts;  // tasks per CTA unit
   const unsigned units = (tasks + tpc - 1) / tpc;
@@ -582,11 +498,11 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
         skip = q_skip(Q, e, d);
       }
     }
-    RayFilterFor<kSrc> F;
+    RayFilter F;
     F.init(o, dir, P);
     float tub = 3.0e38f;
     int nc = 0;
-    isect_scan<kSrc, kShadow, kEye>(P, S, gp, F, pb, pe, act, skip, skip2, (float)tl, tub, nc, rob, xc, xl);
+    isect_scan<kSrc, kShadow>(P, S, gp, F, pb, pe, act, skip, skip2, (float)tl, tub, nc, rob, xc, xl);
     s_nc[warp][lane] = nc;
     s_x[warp][lane] = kShadow ? rob : __float_as_int(tub);
     __syncthreads();
@@ -617,11 +533,10 @@ __device__ RT_SPLIT_INL void wf_isect_split_body(const DevParams& P, const DevSc
   }
 }
 
-template <int kSrc, bool kShadow, bool kEye = false>
-__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+template <int kSrc, bool kShadow>
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  pdl_enter();
-  wf_isect_split_body<kSrc, kShadow, kEye>(P, S, B, d);
+  wf_isect_split_body<kSrc, kShadow>(P, S, B, d);
 }
 
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
@@ -629,14 +544,11 @@ wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // co-limited by the shared-memory pipe (2 LDS.128 per 2 spheres). Here every lane carries two
 // camera rays (a warp = 64 rays): each pair of spheres read from shared memory serves both, and
 // the FFMA2 stream is again the only limit. Same filter, same candidate lists as wf_isect.
-#ifndef RT_EYE_PAIRS_PER_BATCH
-#define RT_EYE_PAIRS_PER_BATCH 8
-#endif
-constexpr int kEyePB = RT_EYE_PAIRS_PER_BATCH;
+constexpr int kEyePB = 8;
 static_assert(kPairsPerBatch % kEyePB == 0, "n_pairs_pad is padded to kPairsPerBatch");
 
 struct EyeRay {
-  RayFilterT<true> F;
+  RayFilter F;
   float tub;
   int nc;
   bool act;
@@ -670,9 +582,8 @@ __device__ __forceinline__ void eye_candidates(const DevParams& P, const float4*
 }
 
 template <int kSrc>
-__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  pdl_enter();
   __shared__ uint64_t s_mbar;
   const unsigned n = B.ctr[wf_ctr_q(d)];
   if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
@@ -754,14 +665,11 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // carries two rays of the same light (one shared-memory read serves both). Work comes in chunks of
 // 64 entries of one light's list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
 // t = t_l - tc' -/+ q on the original one; the bounds add the error of t_l and of the reversal.
-#ifndef RT_LT_PAIRS_PER_BATCH
-#define RT_LT_PAIRS_PER_BATCH 8
-#endif
-constexpr int kLtPB = RT_LT_PAIRS_PER_BATCH;
+constexpr int kLtPB = 8;
 static_assert(kPairsPerBatch % kLtPB == 0, "n_pairs_pad is padded to kPairsPerBatch");
 
 struct LtRay {
-  RayFilterT<true> F;  // filter of the reversed ray (origin P_l, direction -d)
+  RayFilter F;  // filter of the reversed ray (origin P_l, direction -d)
   float tl_f, tlerr;
   int nc, rob, skip;
   bool act;
@@ -884,12 +792,9 @@ __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __rest
 }
 
 template <int kSrc>
-__device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d);
-template <int kSrc>
-__global__ void __launch_bounds__(256, RT_ISECT_MIN_BLOCKS)
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  pdl_enter();
-  static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
+  static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights];  // prefix sums of the lights' 64-entry chunk counts
   if (threadIdx.x == 0) {
@@ -901,10 +806,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
   __syncthreads();
   const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
-  if (!B.solo && split_parts(n_chunks, B) > 1) {  // a short list: the split scan
-    if (RT_SPLIT_FUSED) wf_isect_lt_split_body<kSrc>(P, S, B, d);
-    return;
-  }
+  if (!B.solo && split_parts(n_chunks, B) > 1) return;  // a short list: wf_isect_lt_split scans it
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
@@ -978,8 +880,8 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // the light-origin scan of a short list: parts warps of a CTA share a 64-entry chunk (sphere
 // ranges), merged in part order as in wf_isect_split
 template <int kSrc>
-__device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
-  static_assert(kSrc == SRC_SMEM && RT_FILTER_EXPANDED, "light-origin scan stages the light tables in smem");
+__device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
+  static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights];
   __shared__ int s_nc[8][64];
@@ -1054,7 +956,6 @@ __device__ RT_SPLIT_INL void wf_isect_lt_split_body(const DevParams& P, const De
 template <int kSrc>
 __global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
 wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  pdl_enter();
   wf_isect_lt_split_body<kSrc>(P, S, B, d);
 }
 
@@ -1172,83 +1073,19 @@ __device__ __forceinline__ void bin_entries(const DevParams& P, const WfBuffers&
   __syncthreads();  // s_cnt is rewritten by the next iteration
 }
 
-// The same lists built by one warp (all 32 lanes, converged; lmask = 0 for lanes without an
-// entry): one atomicAdd per light per warp instead of per CTA, but no CTA barrier, so the warps
-// of a wf_shade CTA do not wait for its slowest warp (the barrier version spent 44 % of the
-// kernel's warp samples at the first __syncthreads).
-__device__ __forceinline__ void bin_entries_warp(const DevParams& P, const WfBuffers& B, int d, unsigned long long lmask,
-                                                 unsigned off) {
-  const int L = P.lt_lights;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  for (int l = 0; l < L; ++l) {
-    const bool has = (lmask >> l) & 1ull;
-    const unsigned m = __ballot_sync(kFull, has);
-    if (m == 0u) continue;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(B.ctr + wf_ctr_lt(d, l), (unsigned)__popc(m));
-    base = __shfl_sync(kFull, base, 0);
-    if (has) B.slt[(size_t)l * B.cap + base + (unsigned)__popc(m & lt)] =
-        (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
-  }
-  const unsigned long long rest = lmask >> L;
-  const unsigned nrest = (unsigned)__popcll(rest);
-  if (__any_sync(kFull, nrest != 0u)) {
-    unsigned ob = warp_reserve(nrest, B.ctr + wf_ctr_so(d));
-    unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
-    for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
-  }
-}
-
-// the lists as a kernel of their own (RT_BIN_FUSED=0; by default wf_shade builds them)
-__global__ void __launch_bounds__(256) wf_bin(const DevParams P, WfBuffers B, int d) {
-  pdl_enter();
-  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // per warp: entries per light (+ the rest)
-  const unsigned n = B.ctr[wf_ctr_q(d)];
-  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
-    const unsigned e = e0 + threadIdx.x;
-    const bool in = e < n;
-    bin_entries(P, B, d, in ? B.lmask[e] : 0ull, in ? (unsigned)B.shoff[e] : 0u, s_cnt);
-  }
-}
-
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
-#ifndef RT_BIN_FUSED
-#define RT_BIN_FUSED 1  // wf_shade builds the per-light lists of its shadow entries (no wf_bin launch)
-#endif
-#ifndef RT_LOGIC_MIN_BLOCKS
-#define RT_LOGIC_MIN_BLOCKS 4
-#endif
+constexpr int kLogicMinBlocks = 4;  // wf_shade / wf_accumulate: 64 registers, 4 CTAs per SM
 // kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
 // are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance
-// measured neutral on C4 (world-8 rank 1.048 ms with and without, thresholds warps / 1, 4, 16):
-// off by default; rt_set_shade_wide(1) still selects it (tested bit-identical)
-#ifndef RT_SHADE_WIDE
-#define RT_SHADE_WIDE 0
-#endif
-#ifndef RT_SHADE_WIDE_DIV
-#define RT_SHADE_WIDE_DIV 1  // one warp per path when the queue holds at most warps / DIV paths
-#endif
-__device__ __forceinline__ bool shade_wide(unsigned n, const DevParams& P, const WfBuffers& B) {
-  if (P.n_lights + P.n_emitters > 64 || blockDim.x != 256) return false;
-  if (B.force_wide >= 0) return B.force_wide == 1;
-  return n <= gridDim.x * 8u / RT_SHADE_WIDE_DIV;
-}
-
-#ifndef RT_SHADE_MIN_BLOCKS
-#define RT_SHADE_MIN_BLOCKS RT_LOGIC_MIN_BLOCKS
-#endif
 template <bool kDebug, bool kExt>
-__global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
+__global__ void __launch_bounds__(256, kLogicMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, unsigned long long* stats, int* dbg_hits,
                                                 int* dbg_bounces) {
-  pdl_enter();
   const unsigned n = B.ctr[wf_ctr_q(d)];
-  if (!B.solo && (RT_SHADE_WIDE || B.force_wide == 1) && shade_wide(n, P, B)) return;  // wf_shade_wide
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
-  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // fused wf_bin (per-light entry lists)
-  const bool bin = RT_BIN_FUSED && P.lt_lights > 0;
+  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // bin_entries (per-light entry lists)
+  const bool bin = P.lt_lights > 0;
   // CTA-uniform iterations (the fused list building has CTA barriers)
   for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
     const unsigned e = e0 + threadIdx.x;
@@ -1271,10 +1108,6 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
       }
     }
     nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
-#ifdef RT_OVF_PROBE
-    if (B.cn[e] > kCandMax) atomicAdd(B.ctr + 72 * kWfCtrPerDepth + 4 * d, 1u);
-    atomicMax(B.ctr + 72 * kWfCtrPerDepth + 4 * d + 2, (unsigned)B.cn[e]);
-#endif
     const int dword = d == 0 ? 0 : Q.depth[e];
     const int depth = dword & 0xff;
     int prim = -1;
@@ -1440,240 +1273,21 @@ __global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade(const DevPa
     B.shoff[e] = (int)off;
     lm = lmask;
     of = off;
-    if (!RT_BIN_FUSED && P.lt_lights > 0) B.lmask[e] = lmask;  // wf_bin lists the entries per light
     warp_stat(stats, 1, nsh);
     warp_stat(stats, 2, cont ? 1ull : 0ull);
     warp_stat(stats, 3, (unsigned long long)P.n_spheres);
     warp_stat(stats, 4, (unsigned long long)P.n_planes);
     warp_stat(stats, 5, (unsigned long long)P.n_spheres);
-    if (RT_Q0_IMPLICIT && d == 0) warp_stat(stats, 0, 1ull);  // primary rays (wf_raygen otherwise)
+    if (d == 0) warp_stat(stats, 0, 1ull);  // primary rays (the camera queue is implicit)
     }
-#ifndef RT_BIN_WARP
-#define RT_BIN_WARP 0  // measured: C4 +1.6 % (atomic contention outweighs the barrier wait)
-#endif
-    if (bin) {
-      if (RT_BIN_WARP) bin_entries_warp(P, B, d, lm, of);
-      else bin_entries(P, B, d, lm, of, s_cnt);
-    }
-  }
-}
-
-// ---- a4 + a6 for short queues: one warp per path ----------------------------------------------
-// The deep depths of a chunk hold a few thousand paths; wf_shade then runs one thread per path
-// and its duration is one thread's latency: the nearest-hit decision, then two passes over up to
-// n_src light samples (FP64 square roots and divisions). Here a warp takes one path: every lane
-// evaluates the hit and the continuation identically (broadcast loads, same arithmetic), lane l
-// evaluates light l (and l + 32) in both passes, and lane 0 writes the path's records. The
-// shadow entries, their per-light lists, the next-queue entry and the statistics are the ones
-// wf_shade writes (list order within a light may differ; every consumer is order-free there).
-// Chosen, like the split scans, when the queue fits one warp per path in the grid.
-template <bool kDebug, bool kExt>
-__global__ void __launch_bounds__(256, RT_SHADE_MIN_BLOCKS) wf_shade_wide(const DevParams P, const DevScene S, WfBuffers B, int d,
-                                                     long long g0, unsigned long long* stats, int* dbg_hits,
-                                                     int* dbg_bounces) {
-  pdl_enter();
-  const unsigned n = B.ctr[wf_ctr_q(d)];
-  if (!B.solo && !shade_wide(n, P, B)) return;  // a long queue: wf_shade shades it
-  const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
-  const int w0 = (int)(g0 / P.spp);
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-  const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);
-  for (unsigned e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nwarps) {  // warp-uniform
-    d3 dir = mk(0, 0, 1);
-    if (!q_dir(P, B, Q, e, d, dir)) {  // a work item outside the image (depth 0)
-      if (lane == 0) B.shcnt[e] = 0;
-      continue;
-    }
-    const int path = q_path(Q, e, d);
-    const d3 o = q_origin(P, Q, B.cap, e, d);
-    double tbest = kInf;
-    int hs = -1, hp = -1;
-    for (int j = 0; j < P.n_planes; ++j) {
-      const DevPlane pl = c_planes[j];
-      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
-      if (fabs(den) >= 1e-12) {
-        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
-        if (t >= kEps && t < tbest) { tbest = t; hp = j; }
-      }
-    }
-    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
-    const int dword = d == 0 ? 0 : Q.depth[e];
-    const int depth = dword & 0xff;
-    int prim = -1;
-    if (hp >= 0) prim = c_planes[hp].prim;
-    else if (hs >= 0) prim = S.sph_prim[hs];
-    long long si = 0;
-    if constexpr (kDebug) {
-      const long long g = g0 + path;
-      int px = 0, py = 0;
-      item_pixel(P, (int)(g / P.spp), px, py);
-      si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
-      if (lane == 0) dbg_hits[si * (P.max_depth + 1) + depth] = prim;
-    }
-    const float3 T = d == 0 ? f3(1.f, 1.f, 1.f) : lf3(Q.T, B.cap, (int)e);
-    float3 L = d == 0 ? f3(0.f, 0.f, 0.f) : lf3(Q.L, B.cap, (int)e);
-    unsigned long long pix = 0;
-    unsigned sg = 0;
-    auto pixel_sample = [&]() {
-      const int wl = path / P.spp;
-      int px = 0, py = 0;
-      item_pixel(P, w0 + wl, px, py);
-      pix = (unsigned long long)py * P.W + px;
-      sg = (unsigned)(P.sample_base + (path - wl * P.spp));
-    };
-    if (kExt && (P.n_emitters > 0 || P.integrator != 0)) pixel_sample();
-    d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
-    int mi = 0;
-    bool entering = false, diffuse = false;
-    if (prim < 0) {  // miss -> background
-      L = add(L, mul(T, f3(P.bg[0], P.bg[1], P.bg[2])));
-    } else {
-      p = o + dir * tbest;
-      if (hp >= 0) {
-        const DevPlane pl = c_planes[hp];
-        ng = mk(pl.nx, pl.ny, pl.nz);
-        mi = pl.mat;
-      } else {
-        const float4 cr = __ldg(S.sph_cr + hs);
-        ng = (p - mk(cr.x, cr.y, cr.z)) * (1.0 / (double)cr.w);
-        mi = S.sph_mat[hs];
-      }
-      entering = dot(dir, ng) < 0.0;
-      nrm = entering ? ng : ng * -1.0;
-      const DevMat m = S.mats[mi];
-      const bool sampled = kExt && (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
-      if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
-      if (m.kind == 0) {
-        L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
-        diffuse = true;
-      }
-    }
-    // count pass, one light per lane (two for n_src > 32)
-    const bool s0 = diffuse && lane < n_src && sends_shadow_ray<kExt>(P, S, lane, p, nrm, pix, sg, depth);
-    const bool s1 = diffuse && lane + 32 < n_src && sends_shadow_ray<kExt>(P, S, lane + 32, p, nrm, pix, sg, depth);
-    const unsigned long long lmask =
-        (unsigned long long)__ballot_sync(kFull, s0) | ((unsigned long long)__ballot_sync(kFull, s1) << 32);
-    const unsigned nsh = (unsigned)__popcll(lmask);
-    unsigned off = 0;
-    if (lane == 0 && nsh) off = atomicAdd(B.ctr + wf_ctr_s(d), nsh);
-    off = __shfl_sync(kFull, off, 0);
-    // continuation (every lane alike; lane 0 writes)
-    float3 Tn = T;
-    d3 dn = mk(0, 0, 0);
-    bool cont = false, mi_kind_diffuse_global = false;
-    if (prim >= 0 && depth < P.max_depth) {
-      const DevMat m = S.mats[mi];
-      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
-      if (m.kind == 1) {
-        dn = reflect(dir, nrm);
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (kExt && m.kind == 0 && P.integrator == 1) {
-        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (m.kind == 0) {
-        if (m.kr > 0.f) {
-          dn = reflect(dir, nrm);
-          Tn = f3(Tn.x * m.kr, Tn.y * m.kr, Tn.z * m.kr);
-          cont = true;
-        }
-      } else {
-        const double ior = m.ior;
-        const double eta = entering ? 1.0 / ior : ior;
-        const double ci = -dot(dir, nrm);
-        const double sin2t = eta * eta * (1.0 - ci * ci);
-        bool refl = sin2t > 1.0;
-        if (!refl) {
-          const double cosT = sqrt(1.0 - sin2t);
-          const double c = entering ? ci : cosT;
-          double r0 = (1.0 - ior) / (1.0 + ior);
-          r0 *= r0;
-          const double mm = 1.0 - c;
-          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
-          const double u = rng_u(P.seed, pix, (int)sg, depth);
-          refl = u < F;
-          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
-        }
-        if (refl) dn = reflect(dir, nrm);
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      }
-      if (cont) dn = normalize(dn);
-    }
-    if (lane == 0) {
-      B.shcnt[e] = (int)nsh;
-      B.shoff[e] = (int)off;
-      if (!RT_BIN_FUSED && P.lt_lights > 0) B.lmask[e] = lmask;
-      if constexpr (kDebug) {
-        if (!cont) dbg_bounces[si] = depth;
-      }
-      if (cont) {
-        const unsigned slot = atomicAdd(B.ctr + wf_ctr_q(d + 1), 1u);
-        Qn.path[slot] = path;
-        st3(Qn.ray, B.cap, (int)slot, 0, p);
-        st3(Qn.ray, B.cap, (int)slot, 3, dn);
-        sf3(Qn.T, B.cap, (int)slot, Tn);
-        sf3(Qn.L, B.cap, (int)slot, L);
-        Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
-        Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
-        B.nxt[e] = (int)slot;
-      } else {
-        sf3(B.Lr, B.cap, path, L);
-        B.nxt[e] = -1 - path;
-      }
-      atomicAdd(stats + 1, (unsigned long long)nsh);
-      atomicAdd(stats + 2, cont ? 1ull : 0ull);
-      atomicAdd(stats + 3, (unsigned long long)P.n_spheres);
-      if (P.n_planes) atomicAdd(stats + 4, (unsigned long long)P.n_planes);
-      atomicAdd(stats + 5, (unsigned long long)P.n_spheres);
-      if (RT_Q0_IMPLICIT && d == 0) atomicAdd(stats + 0, 1ull);
-    }
-    // shadow entries: lane l writes light l's (and l + 32's) entry
-    if (nsh) {
-      const DevMat m = S.mats[mi];
-      const int out_sph = (hs >= 0 && entering) ? hs : -1;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int l = lane + 32 * h;
-        if (!((lmask >> l) & 1ull)) continue;
-        LightSample ls;
-        light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);  // true: the count pass decided
-        const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
-        const float alpha = (float)fmax(0.0, -dot(rl, dir));
-        const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
-        const float g = (float)ls.g;
-        d3 os, ds;
-        double tl;
-        if (!kExt || l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
-        else shadow_ray_to(p, nrm, ls.x, os, ds, tl);
-        const unsigned k = off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull));
-        st3(B.sray, B.scap, (int)k, 0, os);
-        st3(B.sray, B.scap, (int)k, 3, ds);
-        B.sray[6 * (size_t)B.scap + k] = tl;
-        B.sskip[k] = shadow_skip(out_sph, nrm, ds);
-        if (kExt || P.lt_lights == 0) B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
-        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
-                                       fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
-        // the per-light lists of the light-origin scans (fused wf_bin), or the rest
-        if (RT_BIN_FUSED && P.lt_lights > 0) {
-          if (l < P.lt_lights) B.slt[(size_t)l * B.cap + atomicAdd(B.ctr + wf_ctr_lt(d, l), 1u)] = (int)k;
-          else B.sother[atomicAdd(B.ctr + wf_ctr_so(d), 1u)] = (int)k;
-        }
-      }
-    }
-    (void)lt;
+    if (bin) bin_entries(P, B, d, lm, of, s_cnt);
   }
 }
 
 // ---- a5 decision + accumulation of the visible lights, in light order ----------------------
 template <bool kExt>  // false: no emitters, every skip2 is -1 (not read)
-__global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
+__global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
-  pdl_enter();
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Qn = B.q[(d + 1) & 1];
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -1736,7 +1350,6 @@ __global__ void __launch_bounds__(256, RT_LOGIC_MIN_BLOCKS) wf_accumulate(const 
 // ---- a7: mean over samples in order, 16-byte store ------------------------------------------
 __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out,
                                                   double* accum) {
-  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
     const int w = w0 + i;
     int px = 0, py = 0;
@@ -1771,7 +1384,6 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
 }
 
 __global__ void fill_int(int* p, long long n, int v) {
-  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
 }

@@ -42,7 +42,8 @@ class RayStats(C.Structure):
                 ("sphere_tests", C.c_uint64), ("plane_tests", C.c_uint64), ("last_render_ms", C.c_double),
                 ("closest_sphere_tests", C.c_uint64), ("isect_closest_ms", C.c_double),
                 ("isect_shadow_ms", C.c_double), ("launches", C.c_uint32), ("variant", C.c_int32),
-                ("shade_ms", C.c_double), ("isect_eye_ms", C.c_double), ("graph", C.c_int32), ("_pad", C.c_int32)]
+                ("shade_ms", C.c_double), ("isect_eye_ms", C.c_double), ("graph", C.c_int32), ("_pad", C.c_int32),
+                ("accumulate_ms", C.c_double)]
 
 
 _lib = None
@@ -81,7 +82,6 @@ def lib() -> C.CDLL:
         "rt_set_concurrency": [i32],
         "rt_set_graphs": [i32],
         "rt_set_scan_split": [i32],
-        "rt_set_shade_wide": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
         "rt_sum_shard_stats": [vp, i32],
         "rt_ipc_alloc": [i64, C.POINTER(vp), C.c_char_p],
@@ -181,11 +181,6 @@ def set_graphs(on: bool):
 def set_scan_split(parts: int = -1):
     """Wavefront scans: -1 split short queues only (default); 1/2/4/8 force that many parts."""
     _check("rt_set_scan_split", lib().rt_set_scan_split(int(parts)))
-
-
-def set_shade_wide(mode: int = -1):
-    """Wavefront shade: -1 one warp per path for short queues (default); 0 never; 1 always."""
-    _check("rt_set_shade_wide", lib().rt_set_shade_wide(int(mode)))
 
 
 def set_stream(stream):

@@ -31,10 +31,10 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_struct_layouts_match_header(tmp_path):
-    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 104 B
+    # rt_primitive 24 B, rt_material 48 B, rt_light 24 B, rt_env 24 B, rt_ray_stats 112 B
     assert rt.PRIM_DTYPE.itemsize == 24 and rt.MAT_DTYPE.itemsize == 48
     assert rt.LIGHT_DTYPE.itemsize == 24 and rt.ENV_DTYPE.itemsize == 24
-    assert ctypes.sizeof(rt.RayStats) == 104
+    assert ctypes.sizeof(rt.RayStats) == 112
     # every rt_ray_stats field of the binding sits at the offset the C compiler gives the header's
     fields = [f for f, _ in rt.RayStats._fields_]
     src = "#include <stddef.h>\n#include <stdio.h>\n#include \"rt.h\"\nint main(void) {\n"

@@ -1,7 +1,6 @@
-"""Split scans and the warp-per-path shade: forcing 1, 2, 4 or 8 warps per ray group
-on every intersection scan (rt_set_scan_split), or the one-warp-per-path shade on or off for every
-depth (rt_set_shade_wide), must reproduce the default frame bit for bit, debug hit records and
-ray statistics included — whatever the queue length, with stream launches and with graph replays
+"""Split scans: forcing 1, 2, 4 or 8 warps per ray group on every intersection scan
+(rt_set_scan_split) must reproduce the default frame bit for bit, debug hit records and ray
+statistics included — whatever the queue length, with stream launches and with graph replays
 (where each kernel pair is captured as the one kernel the previous frame's queue lengths pick)."""
 import numpy as np
 import pytest
@@ -23,18 +22,16 @@ def _cuda():
     from paper_1504_03151_b200 import rt
     yield
     rt.set_scan_split(-1)
-    rt.set_shade_wide(-1)
     rt.set_graphs(True)
     rt.set_variant("auto")
 
 
-def _render(sc, split, graphs, reps, wide=-1):
+def _render(sc, split, graphs, reps):
     import torch
     from paper_1504_03151_b200 import rt
     rt.set_variant("wavefront")
     rt.set_graphs(graphs)
     rt.set_scan_split(split)
-    rt.set_shade_wide(wide)
     rt.load_scene(sc)
     W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
     out = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
@@ -65,25 +62,8 @@ def test_forced_split_is_bit_identical(name, frame):
                 assert st == ref[3], (split, graphs)
 
 
-@pytest.mark.parametrize("name,frame", [("C2", dict(width=256, height=192)),
-                                        ("C4", dict(width=320, height=180, spp=1)),
-                                        ("C5", dict(width=256, height=144, spp=1, max_depth=8))])
-def test_forced_shade_form_is_bit_identical(name, frame):
-    sc = scenegen.get(name).with_frame(**frame)
-    ref = _render(sc, -1, False, 1)[0]
-    for wide in (0, 1):
-        for graphs, reps in ((False, 1), (True, 3)):
-            for out, ids, bn, st in _render(sc, -1, graphs, reps, wide=wide):
-                assert np.array_equal(out, ref[0]), (wide, graphs)
-                assert np.array_equal(ids, ref[1]) and np.array_equal(bn, ref[2]), (wide, graphs)
-                assert st == ref[3], (wide, graphs)
-
-
 def test_invalid_split_rejected():
     from paper_1504_03151_b200 import rt
     for bad in (0, 3, 16, -2):
         with pytest.raises(rt.RtError):
             rt.set_scan_split(bad)
-    for bad in (2, -2):
-        with pytest.raises(rt.RtError):
-            rt.set_shade_wide(bad)
