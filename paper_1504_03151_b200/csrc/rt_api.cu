@@ -383,16 +383,20 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     const int cap = items * p.spp;
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
     const int scap = cap * (n_src > 0 ? n_src : 1);
+    // point lights with light-origin scans get list slots; every other source a generic slot
+    const int n_gen = n_src - p.lt_lights;
+    const int gcap = cap * (n_gen > 0 ? n_gen : 1);
+    const int lt_lists = p.lt_lights * rt::kLtSub;
     // (re)carve for this frame's cap
-    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront)");
+    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, gcap, lt_lists, 4 * c.num_sms)), "cudaMalloc(wavefront)");
     CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, 4 * c.num_sms, c.wf_ctr.p);
+    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, gcap, lt_lists, 4 * c.num_sms, c.wf_ctr.p);
     c.wf.force_parts = c.scan_split;
     const bool pipe = c.pipeline != 0 && c.concurrent != 0;
     if (pipe) {
-      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
+      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, gcap, lt_lists, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
       CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, 4 * c.num_sms, c.wf_ctr2.p);
+      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, gcap, lt_lists, 4 * c.num_sms, c.wf_ctr2.p);
       c.wf2.force_parts = c.scan_split;
       if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");

@@ -209,7 +209,11 @@ __device__ __forceinline__ double sphere_root(const float4 cr, const d3 o, const
 struct RayFilter {
   float dx, dy, dz, a1, a2, a3, b1, eta, neg_slack, cut;
   __device__ __forceinline__ void init(const d3& o, const d3& d, const DevParams& P) {
-    dx = (float)d.x; dy = (float)d.y; dz = (float)d.z;
+    init(o, (float)d.x, (float)d.y, (float)d.z, P);
+  }
+  // direction already rounded to float (the same values as the FP64 overload's conversion)
+  __device__ __forceinline__ void init(const d3& o, float fdx, float fdy, float fdz, const DevParams& P) {
+    dx = fdx; dy = fdy; dz = fdz;
     const float ox = (float)(o.x - P.centre[0]), oy = (float)(o.y - P.centre[1]), oz = (float)(o.z - P.centre[2]);
     const float on = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
     a1 = 2.0f * ox; a2 = 2.0f * oy; a3 = 2.0f * oz;                 // 2 o'

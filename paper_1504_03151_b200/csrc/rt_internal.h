@@ -117,19 +117,27 @@ struct WfBuffers {
   int* shcnt;      // [cap]  per entry of Q[d]: number of shadow entries (lights in order)
   int* ccand;      // [cap * kCandMax] closest-hit candidates per entry of Q[d]
   int* cn;         // [cap]
-  double* sray;    // [7][scap] shadow entry: o_s (3), d_s (3), t_max
-  int* sskip;      // [scap] sphere the shadow ray leaves (exact skip) or -1
-  int* sskip2;     // [scap] emitter sphere the ray aims at (not tested, R#41) or -1
+  // shadow entries j (path-major: entry e of Q[d] owns shoff[e] .. shoff[e] + shcnt[e] - 1)
   float* sq_c;     // [3][scap] contribution T f_r I cos / d^2 (or the emitter estimator)
-  int* scand;      // [scap * kCandMax]
-  int* sn;         // [scap]
-  int* srob;       // [scap] robust occluder: sphere index, -1 none, -2-j plane j
-  // when lt_lights > 0: the entries of point light l (< lt_lights) listed in slt[l * cap ..],
-  // every other entry (emitters) in sother; the entries themselves stay path-major
-  int* slt;        // [lt_lights * cap]
-  int* sother;     // [scap]
+  int* spos;       // [scap] where entry j is scanned: light-origin list slot g >= 0, or -2 - o
+  double* sorg;    // [3][cap] per entry of Q[d] with light-origin entries: o_s = p + EPS_T n
+  // light-origin lists (point light l < lt_lights): kLtSub sub-lists per light, lt_cap slots each;
+  // slot g = (l * kLtSub + sub) * lt_cap + position
+  float4* lt_dir;  // [slots] the shadow ray's direction and t_max, rounded to float
+  int2* lt_rec;    // [slots] {entry e of Q[d], skip: sphere the ray leaves or -1; -2-j plane j occludes}
+  int2* lt_res;    // [slots] {robust occluder rob, candidate count nc}, written by the scan
+  int* lt_cand;    // [slots * kCandMax]
+  int lt_cap;
+  // generic shadow entries (every other source: emitters, or all lights when the scene is not in
+  // shared memory), dense slots o in [0, ctr_so)
+  double* sray;    // [7][gcap] o_s (3), d_s (3), t_max
+  int* sskip;      // [gcap] sphere the shadow ray leaves (exact skip) or -1
+  int* sskip2;     // [gcap] emitter sphere the ray aims at (not tested, R#41) or -1
+  int* scand;      // [gcap * kCandMax]
+  int* sn;         // [gcap]
+  int* srob;       // [gcap] robust occluder: sphere index, -1 none, -2-j plane j
   unsigned* ctr;   // counters, see wf_ctr_*
-  int cap, scap;
+  int cap, scap, gcap;
   // split scans (short queues): per-part candidate lists of the warps of up to xctas CTAs, one
   // row of kCandMax per ray; closest scans (32 rays per warp) and shadow scans (64 rays per
   // warp) have their own rows because they run concurrently on two streams
@@ -151,22 +159,27 @@ struct WfBuffers {
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
 constexpr int kMaxLtLights = 32;  // point lights scanned from the light (RT_MAX_LIGHTS)
-constexpr int kWfCtrPerDepth = 8 + kMaxLtLights;
+constexpr int kLtSub = 8;         // sub-lists per light (slot reservations spread over 8 counters)
+constexpr int kWfCtrPerDepth = 8 + kMaxLtLights * kLtSub;
 __host__ __device__ constexpr int wf_ctr_q(int d) { return kWfCtrPerDepth * d; }       // closest queue
 __host__ __device__ constexpr int wf_ctr_s(int d) { return kWfCtrPerDepth * d + 1; }   // shadow entries
 __host__ __device__ constexpr int wf_ctr_wc(int d) { return kWfCtrPerDepth * d + 2; }  // work heads
 __host__ __device__ constexpr int wf_ctr_ws(int d) { return kWfCtrPerDepth * d + 3; }
-__host__ __device__ constexpr int wf_ctr_so(int d) { return kWfCtrPerDepth * d + 4; }  // "other" list
+__host__ __device__ constexpr int wf_ctr_so(int d) { return kWfCtrPerDepth * d + 4; }  // generic shadow slots
 __host__ __device__ constexpr int wf_ctr_wlt(int d) { return kWfCtrPerDepth * d + 5; } // light-scan chunks
-__host__ __device__ constexpr int wf_ctr_lt(int d, int l) { return kWfCtrPerDepth * d + 8 + l; }  // light l list
+__host__ __device__ constexpr int wf_ctr_lt(int d, int l, int sub) {  // light l's sub-list `sub`
+  return kWfCtrPerDepth * d + 8 + l * kLtSub + sub;
+}
 constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
 // launchers (rt_kernels.cu)
 cudaError_t upload_planes(const DevPlane* planes, int n_planes, cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
-size_t wf_bytes(int cap, int scap, int xctas);
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* ctr);
+// buffer sizes of one chunk: cap paths, scap = cap x sources shadow entries, gcap generic
+// shadow slots, lt_lists = lt_lights x kLtSub light-origin sub-lists
+size_t wf_bytes(int cap, int scap, int gcap, int lt_lists, int xctas);
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, int gcap, int lt_lists, int xctas, unsigned* ctr);
 // per-launch CUDA events around the intersection kernels (pairs: [2i] before, [2i+1] after)
 struct WfTiming {
   cudaEvent_t* closest;

@@ -576,18 +576,26 @@ cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float ex
 }
 
 // ---- wavefront launcher ---------------------------------------------------------------------
-size_t wf_bytes(int cap, int scap, int xctas) {
-  const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
-  return (size_t)cap * (2 * q + 3 * 4 + 4 * 4 + kCandMax * 4) +
-         (size_t)scap * (7 * 8 + 4 + 4 + 3 * 4 + kCandMax * 4 + 4 + 4 + 4 + 4) +
-         (size_t)xctas * 8 * (32 * 2 + 64) * kCandMax * 4 + 40 * 256;
+static int lt_sub_cap(int cap) {  // slots per sub-list: the 256-path blocks of one residue class
+  return ((cap + 256 * kLtSub - 1) / (256 * kLtSub)) * 256;
 }
 
-void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* ctr) {
+size_t wf_bytes(int cap, int scap, int gcap, int lt_lists, int xctas) {
+  const size_t q = 4 + 6 * 8 + 3 * 4 + 3 * 4 + 4 + 4;  // one WfQueue entry
+  const size_t slots = (size_t)lt_lists * lt_sub_cap(cap);
+  return (size_t)cap * (2 * q + 3 * 4 + 3 * 4 + kCandMax * 4 + 4 + 3 * 8) + (size_t)scap * (3 * 4 + 4) +
+         slots * (16 + 8 + 8 + kCandMax * 4) + (size_t)gcap * (7 * 8 + 4 + 4 + kCandMax * 4 + 4 + 4) +
+         (size_t)xctas * 8 * (32 * 2 + 64) * kCandMax * 4 + 64 * 256;
+}
+
+void wf_carve(WfBuffers& B, void* base, int cap, int scap, int gcap, int lt_lists, int xctas, unsigned* ctr) {
   char* p = static_cast<char*>(base);
   auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
   B.cap = cap;
   B.scap = scap;
+  B.gcap = gcap;
+  B.lt_cap = lt_sub_cap(cap);
+  const size_t slots = (size_t)lt_lists * B.lt_cap;
   for (int k = 0; k < 2; ++k) {
     WfQueue& Q = B.q[k];
     Q.path = reinterpret_cast<int*>(take(4 * (size_t)cap));
@@ -603,15 +611,19 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int xctas, unsigned* 
   B.shcnt = reinterpret_cast<int*>(take(4 * (size_t)cap));
   B.ccand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * cap));
   B.cn = reinterpret_cast<int*>(take(4 * (size_t)cap));
-  B.sray = reinterpret_cast<double*>(take(7 * 8 * (size_t)scap));
-  B.sskip = reinterpret_cast<int*>(take(4 * (size_t)scap));
-  B.sskip2 = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.sorg = reinterpret_cast<double*>(take(3 * 8 * (size_t)cap));
   B.sq_c = reinterpret_cast<float*>(take(3 * 4 * (size_t)scap));
-  B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * scap));
-  B.sn = reinterpret_cast<int*>(take(4 * (size_t)scap));
-  B.srob = reinterpret_cast<int*>(take(4 * (size_t)scap));
-  B.slt = reinterpret_cast<int*>(take(4 * (size_t)scap));  // lt_lights * cap <= scap
-  B.sother = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.spos = reinterpret_cast<int*>(take(4 * (size_t)scap));
+  B.lt_dir = reinterpret_cast<float4*>(take(16 * (slots ? slots : 1)));
+  B.lt_rec = reinterpret_cast<int2*>(take(8 * (slots ? slots : 1)));
+  B.lt_res = reinterpret_cast<int2*>(take(8 * (slots ? slots : 1)));
+  B.lt_cand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * (slots ? slots : 1)));
+  B.sray = reinterpret_cast<double*>(take(7 * 8 * (size_t)gcap));
+  B.sskip = reinterpret_cast<int*>(take(4 * (size_t)gcap));
+  B.sskip2 = reinterpret_cast<int*>(take(4 * (size_t)gcap));
+  B.scand = reinterpret_cast<int*>(take(4 * (size_t)kCandMax * gcap));
+  B.sn = reinterpret_cast<int*>(take(4 * (size_t)gcap));
+  B.srob = reinterpret_cast<int*>(take(4 * (size_t)gcap));
   B.xctas = xctas;
   B.solo = 0;
   B.force_parts = -1;
@@ -687,7 +699,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     if (B0.force_parts > 0) return B0.force_parts;
     return split_rule(tasks, (unsigned)grid * 8u);
   };
-  using ShadeFn = void (*)(const DevParams, const DevScene, WfBuffers, int, long long, unsigned long long*, int*, int*);
+  using ShadeFn = void (*)(const DevParams, const DevScene, WfBuffers, int, long long, int*, int*);
   const ShadeFn shade = ext ? (dbg ? wf_shade<true, true> : wf_shade<false, true>)
                             : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
   int* dh = dbg ? o.dbg_hits : nullptr;
@@ -753,7 +765,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      launch(shade, grid_l, 0, st, p, sc, Bc, d, g0, o.stats, dh, db);
+      launch(shade, grid_l, 0, st, p, sc, Bc, d, g0, dh, db);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       cudaStream_t ss = st;
       if (side) {
@@ -766,7 +778,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (klt) {  // point lights, from the light
         if (hint) {
           unsigned chunks = 0;
-          for (int l = 0; l < p.lt_lights; ++l) chunks += (hint[wf_ctr_lt(d, l)] + 63u) / 64u;
+          for (int i = 0; i < p.lt_lights * kLtSub; ++i) chunks += (hint[wf_ctr_lt(d, 0, 0) + i] + 63u) / 64u;
           launch(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
@@ -777,7 +789,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
         if (hint) {
-          const unsigned ns = hint[p.lt_lights > 0 ? wf_ctr_so(d) : wf_ctr_s(d)];
+          const unsigned ns = hint[wf_ctr_so(d)];
           if (host_parts((ns + 31u) / 32u, grid_s) > 1)
             launch(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
           else
@@ -805,7 +817,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     }
     tm.n = t0 + p.max_depth + 1 < tm.cap ? t0 + p.max_depth + 1 : tm.cap;
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
-    launch(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum);
+    launch(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum, o.stats);
     tm.launches += 2;  // wf_q0_len, wf_resolve
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
       tm.record(tm.chunk_done[tm.n_chunks], st);

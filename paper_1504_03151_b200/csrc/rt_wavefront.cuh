@@ -112,13 +112,20 @@ __device__ __forceinline__ void sf3(float* a, int cap, int i, float3 v) {
   a[2 * (size_t)cap + i] = v.z;
 }
 
-// shadow ray of light l from the shading point (S:157): o = p + EPS_T n toward the light
-__device__ __forceinline__ void shadow_ray(const DevScene& S, d3 p, d3 n, int l, d3& os, d3& ds, double& tl) {
-  const DevLight lt = S.lights[l];
-  os = p + n * kEps;
-  const d3 ws = mk(lt.px, lt.py, lt.pz) - os;
+// shadow ray from o_s toward the point x: direction and t_max = |x - o_s|
+__device__ __forceinline__ void shadow_dir(d3 os, d3 x, d3& ds, double& tl) {
+  const d3 ws = x - os;
   tl = sqrt(dot(ws, ws));
   ds = ws * (1.0 / tl);
+}
+__device__ __forceinline__ d3 light_pos(const DevScene& S, int l) {
+  const DevLight lt = S.lights[l];
+  return mk(lt.px, lt.py, lt.pz);
+}
+// shadow ray of light l from the shading point (S:157): o = p + EPS_T n toward the light
+__device__ __forceinline__ void shadow_ray(const DevScene& S, d3 p, d3 n, int l, d3& os, d3& ds, double& tl) {
+  os = p + n * kEps;
+  shadow_dir(os, light_pos(S, l), ds, tl);
 }
 
 // A shadow ray from a point hit on the outside of sphere `out` (origin p + EPS_T n, outside)
@@ -128,9 +135,7 @@ __device__ __forceinline__ int shadow_skip(int out, d3 n, d3 ds) { return (out >
 // shadow ray toward a sampled emitter point x (R#41): o = p + EPS_T n, t_max = |x - o|
 __device__ __forceinline__ void shadow_ray_to(d3 p, d3 n, d3 x, d3& os, d3& ds, double& tl) {
   os = p + n * kEps;
-  const d3 ws = x - os;
-  tl = sqrt(dot(ws, ws));
-  ds = ws * (1.0 / tl);
+  shadow_dir(os, x, ds, tl);
 }
 
 // Light l seen from shading point p: point light l < n_lights (R#2: g = cos / d^2), else
@@ -327,9 +332,9 @@ template <int kSrc, bool kShadow>
 __global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
   __shared__ uint64_t s_mbar;
-  // shadow rays: every entry, or only the "other" list when point lights are scanned from the light
-  const bool listed = kShadow && P.lt_lights > 0;
-  const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  // shadow rays: the generic entries (every shadow ray not scanned from a point light), dense in
+  // [0, ctr_so)
+  const unsigned n = kShadow ? B.ctr[wf_ctr_so(d)] : B.ctr[wf_ctr_q(d)];
   if (!B.solo && split_parts((n + 31u) / 32u, B) > 1) return;  // a short queue: wf_isect_split scans it
   // CTAs beyond ceil(n / blockDim) would find no work: leave before staging the scene (deep
   // depths and small shards have short queues; the remaining warps take every 32-ray chunk)
@@ -347,20 +352,19 @@ wf_isect(const DevParams P, const DevScene S, WfBuffers B, int d) {
     if (lane == 0) e0 = atomicAdd(work, 32u);
     e0 = __shfl_sync(kFull, e0, 0);
     if (e0 >= n) break;
-    unsigned e = e0 + lane;
+    const unsigned e = e0 + lane;
     bool act = e < n;
     const bool mine = act;
-    if (listed && act) e = (unsigned)B.sother[e];
     d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
     double tl = 0.0;
     int rob = -1, skip = -1, skip2 = -1;  // skip2: the emitter a shadow ray aims at (R#41)
     if (act) {
       if constexpr (kShadow) {
-        o = ld3(B.sray, B.scap, (int)e, 0);
-        dir = ld3(B.sray, B.scap, (int)e, 3);
-        tl = B.sray[6 * (size_t)B.scap + e];
+        o = ld3(B.sray, B.gcap, (int)e, 0);
+        dir = ld3(B.sray, B.gcap, (int)e, 3);
+        tl = B.sray[6 * (size_t)B.gcap + e];
         skip = B.sskip[e];
-        skip2 = P.n_emitters > 0 ? B.sskip2[e] : -1;  // written only when an entry may aim at an emitter
+        skip2 = B.sskip2[e];
         // planes first, exactly (FP64): the first plane in index order that occludes decides
         for (int j = 0; j < P.n_planes; ++j) {
           const DevPlane pl = c_planes[j];
@@ -445,8 +449,7 @@ __device__ __forceinline__ void wf_isect_split_body(const DevParams& P, const De
   __shared__ int s_nc[8][32];
   __shared__ int s_x[8][32];  // closest: tub (float bits); shadow: rob
   __shared__ unsigned s_unit;
-  const bool listed = kShadow && P.lt_lights > 0;
-  const unsigned n = kShadow ? B.ctr[listed ? wf_ctr_so(d) : wf_ctr_s(d)] : B.ctr[wf_ctr_q(d)];
+  const unsigned n = kShadow ? B.ctr[wf_ctr_so(d)] : B.ctr[wf_ctr_q(d)];
   const unsigned tasks = (n + 31u) / 32u;  // 32 rays each
   const int parts = split_parts(tasks, B);
   if (parts == 1 && !B.solo) return;  // a long queue: wf_isect scans it (solo: one part here)
@@ -470,20 +473,19 @@ __device__ __forceinline__ void wf_isect_split_body(const DevParams& P, const De
     __syncthreads();
     const unsigned u = s_unit;
     if (u >= units) break;  // CTA-uniform
-    unsigned e = (u * tpc + slot) * 32u + lane;
+    const unsigned e = (u * tpc + slot) * 32u + lane;
     bool act = e < n;
     const bool mine = act;
-    if (listed && act) e = (unsigned)B.sother[e];
     d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
     double tl = 0.0;
     int rob = -1, skip = -1, skip2 = -1;
     if (act) {
       if constexpr (kShadow) {
-        o = ld3(B.sray, B.scap, (int)e, 0);
-        dir = ld3(B.sray, B.scap, (int)e, 3);
-        tl = B.sray[6 * (size_t)B.scap + e];
+        o = ld3(B.sray, B.gcap, (int)e, 0);
+        dir = ld3(B.sray, B.gcap, (int)e, 3);
+        tl = B.sray[6 * (size_t)B.gcap + e];
         skip = B.sskip[e];
-        skip2 = P.n_emitters > 0 ? B.sskip2[e] : -1;  // written only when an entry may aim at an emitter
+        skip2 = B.sskip2[e];
         for (int j = 0; j < P.n_planes; ++j) {  // planes first, exactly (every part alike)
           const DevPlane pl = c_planes[j];
           const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
@@ -663,8 +665,17 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // shadow ray of light l shares the origin P_l: s1 = K + 2 c'.o'(P_l) comes precomputed per light
 // (S.pairs_lt), so a sphere costs tc' (3 FMA) + v = tc'^2 + s1 (1 FMA) instead of 7, and a thread
 // carries two rays of the same light (one shared-memory read serves both). Work comes in chunks of
-// 64 entries of one light's list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
+// 64 entries of one list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
 // t = t_l - tc' -/+ q on the original one; the bounds add the error of t_l and of the reversal.
+//
+// Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per warp, the
+// sub-list chosen by the warp's 256-path block, so no CTA barrier and no single hot counter); a
+// slot holds the ray's direction and t_max rounded to float (what the filter reads; wf_shade
+// computed them in FP64) and {shading entry e of Q[d], skip}: skip = the sphere the ray provably
+// leaves or -1, or -2 - j when wf_shade already found plane j to occlude (planes are decided in
+// FP64 first, in index order). Where an FP64 decision needs the ray, wf_accumulate rebuilds it
+// from the shading point's o_s = p + EPS_T n (B.sorg[e]) with the same arithmetic (shadow_dir).
+// Output per slot: {rob, nc} + candidates.
 constexpr int kLtPB = 8;
 static_assert(kPairsPerBatch % kLtPB == 0, "n_pairs_pad is padded to kPairsPerBatch");
 
@@ -675,31 +686,31 @@ struct LtRay {
   bool act;
 };
 
-__device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, const WfBuffers& B, unsigned j, bool valid,
+// FP64 shadow ray of list slot g of light l (rebuilt from the shading point's o_s)
+__device__ __forceinline__ void lt_ray(const DevScene& S, const WfBuffers& B, int e, int l, d3& os, d3& ds, double& tl) {
+  os = ld3(B.sorg, B.cap, e, 0);
+  shadow_dir(os, light_pos(S, l), ds, tl);
+}
+
+__device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, const WfBuffers& B, unsigned g, bool valid,
                                          int l, LtRay& R) {
-  d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
-  double tl = 1.0;
+  float4 dt = make_float4(0.f, 0.f, 1.f, 1.f);  // direction, t_max (float)
   R.act = valid;
   R.rob = -1;
   R.skip = -1;
   R.nc = 0;
   if (valid) {
-    o = ld3(B.sray, B.scap, (int)j, 0);
-    dir = ld3(B.sray, B.scap, (int)j, 3);
-    tl = B.sray[6 * (size_t)B.scap + j];
-    R.skip = B.sskip[j];
-    for (int q = 0; q < P.n_planes; ++q) {  // planes first, exactly (FP64), on the original ray
-      const DevPlane pl = c_planes[q];
-      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
-      if (fabs(den) >= 1e-12) {
-        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
-        if (t >= kEps && t < tl) { R.rob = -2 - q; R.act = false; break; }
-      }
+    dt = B.lt_dir[g];
+    const int skip = B.lt_rec[g].y;
+    if (skip <= -2) {  // plane -2-skip occludes (decided by wf_shade in FP64)
+      R.rob = skip;
+      R.act = false;
+    } else {
+      R.skip = skip;
     }
   }
-  const DevLight lt = S.lights[l];
-  R.F.init(mk(lt.px, lt.py, lt.pz), mk(-dir.x, -dir.y, -dir.z), P);
-  R.tl_f = (float)tl;
+  R.F.init(light_pos(S, l), -dt.x, -dt.y, -dt.z, P);
+  R.tl_f = dt.w;
   R.tlerr = 4.0e-7f * R.tl_f + 1.0e-6f * R.F.eta;  // t_l to float, P_l vs o + t_l d, the subtraction
 }
 
@@ -791,89 +802,70 @@ __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __rest
   }
 }
 
+// Prefix sums of the lists' 64-entry chunk counts (list i = light i / kLtSub, sub-list i % kLtSub;
+// their counters are contiguous); every thread of the CTA takes part (blockDim = 256 >= lists)
+__device__ __forceinline__ unsigned lt_chunk_prefix(const DevParams& P, const WfBuffers& B, int d, unsigned* s_end,
+                                                    unsigned* s_warp) {
+  const int nl = P.lt_lights * kLtSub;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned v = t < nl ? (B.ctr[wf_ctr_lt(d, 0, 0) + t] + 63u) / 64u : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned u = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) s_warp[warp] = v;
+  __syncthreads();
+  unsigned before = 0;
+  for (int w = 0; w < warp; ++w) before += s_warp[w];
+  if (t < nl) s_end[t] = v + before;
+  __syncthreads();
+  return nl > 0 ? s_end[nl - 1] : 0u;
+}
+// list of chunk k: the first list whose prefix end exceeds k (binary search)
+__device__ __forceinline__ int lt_list_of(const unsigned* s_end, int nl, unsigned k) {
+  int lo = 0, hi = nl - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s_end[mid] > k) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 template <int kSrc>
 __global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
-  __shared__ unsigned s_chunk_end[kMaxLtLights];  // prefix sums of the lights' 64-entry chunk counts
-  if (threadIdx.x == 0) {
-    unsigned acc = 0;
-    for (int l = 0; l < P.lt_lights; ++l) {
-      acc += (B.ctr[wf_ctr_lt(d, l)] + 63u) / 64u;
-      s_chunk_end[l] = acc;
-    }
-  }
-  __syncthreads();
-  const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
+  __shared__ unsigned s_chunk_end[kMaxLtLights * kLtSub];
+  __shared__ unsigned s_warp[8];
+  const unsigned n_chunks = lt_chunk_prefix(P, B, d, s_chunk_end, s_warp);
   if (!B.solo && split_parts(n_chunks, B) > 1) return;  // a short list: wf_isect_lt_split scans it
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
   const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
   const int lane = threadIdx.x & 31;
+  const int nl = P.lt_lights * kLtSub;
   while (true) {
     unsigned k = 0;
     if (lane == 0) k = atomicAdd(B.ctr + wf_ctr_wlt(d), 1u);
     k = __shfl_sync(kFull, k, 0);
     if (k >= n_chunks) break;
-    int l = 0;
-    while (s_chunk_end[l] <= k) ++l;
-    const unsigned c = k - (l > 0 ? s_chunk_end[l - 1] : 0u);
-    const unsigned cnt = B.ctr[wf_ctr_lt(d, l)];
+    const int li = lt_list_of(s_chunk_end, nl, k);
+    const int l = li / kLtSub;
+    const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
+    const unsigned cnt = B.ctr[wf_ctr_lt(d, 0, 0) + li];
     const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
     const bool va_ = oa < cnt, vb_ = ob < cnt;
-    const unsigned ja = va_ ? (unsigned)B.slt[(size_t)l * B.cap + oa] : 0u;
-    const unsigned jb = vb_ ? (unsigned)B.slt[(size_t)l * B.cap + ob] : 0u;
+    const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;  // list slots
     LtRay Ra, Rb;
-    lt_setup(P, S, B, ja, va_, l, Ra);
-    lt_setup(P, S, B, jb, vb_, l, Rb);
-    const float2* s1p = s1_all + (size_t)l * P.n_pairs_pad;
-    const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
-    const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
-    const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
-    const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
-    const float cut = Ra.F.cut;  // depends on the origin P_l only: the same for both rays
-    for (int base = 0; base < P.n_pairs_pad; base += kLtPB) {
-      float2 va[kLtPB], vb[kLtPB];
-#pragma unroll
-      for (int i = 0; i < kLtPB; ++i) {
-        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
-        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-        const float2 S1 = s1p[base + i];
-        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w), CZ = make_float2(b.x, b.y);
-        const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
-        const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
-        va[i] = __ffma2_rn(ta, ta, S1);
-        vb[i] = __ffma2_rn(tb, tb, S1);
-      }
-      float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
-#pragma unroll
-      for (int i = 1; i < kLtPB; ++i) {
-        ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
-        mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
-      }
-      const bool ca = Ra.act && ma >= cut, cb = Rb.act && mb >= cut;
-      if (__any_sync(kFull, ca || cb)) {
-        if (ca) {
-          unsigned m = 0u;
-#pragma unroll
-          for (int i = 0; i < kLtPB; ++i)
-            m |= ((va[i].x >= cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
-          lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Ra, B.scand + (size_t)ja * kCandMax);
-        }
-        if (cb) {
-          unsigned m = 0u;
-#pragma unroll
-          for (int i = 0; i < kLtPB; ++i)
-            m |= ((vb[i].x >= cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
-          lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Rb, B.scand + (size_t)jb * kCandMax);
-        }
-      }
-      if (!__any_sync(kFull, Ra.act || Rb.act)) break;  // Alg. 1 `break`, warp-wide
-    }
-    if (va_) { B.sn[ja] = Ra.nc; B.srob[ja] = Ra.rob; }
-    if (vb_) { B.sn[jb] = Rb.nc; B.srob[jb] = Rb.rob; }
+    lt_setup(P, S, B, ga, va_, l, Ra);
+    lt_setup(P, S, B, gb, vb_, l, Rb);
+    lt_scan<kSrc>(P, gp, s1_all + (size_t)l * P.n_pairs_pad, 0, P.n_pairs_pad, Ra, Rb, B.lt_cand + (size_t)ga * kCandMax,
+                  B.lt_cand + (size_t)gb * kCandMax);
+    if (va_) B.lt_res[ga] = make_int2(Ra.rob, Ra.nc);
+    if (vb_) B.lt_res[gb] = make_int2(Rb.rob, Rb.nc);
   }
 }
 
@@ -883,19 +875,12 @@ template <int kSrc>
 __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
   static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
-  __shared__ unsigned s_chunk_end[kMaxLtLights];
+  __shared__ unsigned s_chunk_end[kMaxLtLights * kLtSub];
+  __shared__ unsigned s_warp[8];
   __shared__ int s_nc[8][64];
   __shared__ int s_rob[8][64];
   __shared__ unsigned s_unit;
-  if (threadIdx.x == 0) {
-    unsigned acc = 0;
-    for (int l = 0; l < P.lt_lights; ++l) {
-      acc += (B.ctr[wf_ctr_lt(d, l)] + 63u) / 64u;
-      s_chunk_end[l] = acc;
-    }
-  }
-  __syncthreads();
-  const unsigned n_chunks = P.lt_lights > 0 ? s_chunk_end[P.lt_lights - 1] : 0u;
+  const unsigned n_chunks = lt_chunk_prefix(P, B, d, s_chunk_end, s_warp);
   const int parts = split_parts(n_chunks, B);
   if (parts == 1 && !B.solo) return;  // a long list: wf_isect_lt scans it (solo: one part here)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -906,6 +891,7 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
   const float4* gp = S.pairs_lt;
   const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
   const int slot = warp / parts, part = warp % parts;
+  const int nl = P.lt_lights * kLtSub;
   int pb, pe;
   split_range(P, part, parts, pb, pe);
   const size_t xs = (size_t)64 * kCandMax;
@@ -918,17 +904,16 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
     if (u >= units) break;  // CTA-uniform
     const unsigned k = u * tpc + slot;
     const bool valid_chunk = k < n_chunks;
-    int l = 0;
-    while (l < P.lt_lights - 1 && s_chunk_end[l] <= k) ++l;
-    const unsigned c = k - (l > 0 ? s_chunk_end[l - 1] : 0u);
-    const unsigned cnt = valid_chunk ? B.ctr[wf_ctr_lt(d, l)] : 0u;
+    const int li = valid_chunk ? lt_list_of(s_chunk_end, nl, k) : 0;
+    const int l = li / kLtSub;
+    const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
+    const unsigned cnt = valid_chunk ? B.ctr[wf_ctr_lt(d, 0, 0) + li] : 0u;
     const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
     const bool va_ = oa < cnt, vb_ = ob < cnt;
-    const unsigned ja = va_ ? (unsigned)B.slt[(size_t)l * B.cap + oa] : 0u;
-    const unsigned jb = vb_ ? (unsigned)B.slt[(size_t)l * B.cap + ob] : 0u;
+    const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;
     LtRay Ra, Rb;
-    lt_setup(P, S, B, ja, va_, l, Ra);
-    lt_setup(P, S, B, jb, vb_, l, Rb);
+    lt_setup(P, S, B, ga, va_, l, Ra);
+    lt_setup(P, S, B, gb, vb_, l, Rb);
     lt_scan<kSrc>(P, gp, s1_all + (size_t)l * P.n_pairs_pad, pb, pe, Ra, Rb, xa, xb);
     s_nc[warp][lane] = Ra.nc;
     s_nc[warp][lane + 32] = Rb.nc;
@@ -938,15 +923,14 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
     if (part == 0) {
       int nco, robo;
       if (va_) {
-        split_merge_shadow(parts, &s_nc[warp][lane], &s_rob[warp][lane], 64, xa, xs, B.scand + (size_t)ja * kCandMax, nco, robo);
-        B.sn[ja] = nco;
-        B.srob[ja] = robo;
+        split_merge_shadow(parts, &s_nc[warp][lane], &s_rob[warp][lane], 64, xa, xs, B.lt_cand + (size_t)ga * kCandMax, nco,
+                           robo);
+        B.lt_res[ga] = make_int2(robo, nco);
       }
       if (vb_) {
-        split_merge_shadow(parts, &s_nc[warp][lane + 32], &s_rob[warp][lane + 32], 64, xb, xs, B.scand + (size_t)jb * kCandMax,
-                           nco, robo);
-        B.sn[jb] = nco;
-        B.srob[jb] = robo;
+        split_merge_shadow(parts, &s_nc[warp][lane + 32], &s_rob[warp][lane + 32], 64, xb, xs,
+                           B.lt_cand + (size_t)gb * kCandMax, nco, robo);
+        B.lt_res[gb] = make_int2(robo, nco);
       }
     }
     __syncthreads();  // s_unit / s_nc / s_rob / scratch rows are rewritten by the next unit
@@ -1022,110 +1006,47 @@ __device__ __forceinline__ void shadow_counts(const DevParams& P, const DevScene
   }
 }
 
-// ---- lists of the shadow entries per point light (light-origin scans) and the rest ----------
-// One global atomicAdd per light per CTA iteration (256 entries): warps count with ballots, the
-// CTA reserves, warps place their lanes in lane order. Called by every thread of the CTA (lmask
-// = 0 for threads without an entry); contains CTA barriers.
-__device__ __forceinline__ void bin_entries(const DevParams& P, const WfBuffers& B, int d, unsigned long long lmask,
-                                            unsigned off, unsigned (*s_cnt)[kMaxLtLights + 1]) {
-  const int L = P.lt_lights;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const unsigned long long rest = lmask >> L;
-  const unsigned nrest = (unsigned)__popcll(rest);
-  for (int l = 0; l < L; ++l) {
-    const unsigned m = __ballot_sync(kFull, (lmask >> l) & 1ull);
-    if (lane == 0) s_cnt[warp][l] = (unsigned)__popc(m);
-  }
-  unsigned rsum = nrest;  // the rest: a variable count per lane (warp inclusive scan)
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(kFull, rsum, o);
-    if (lane >= o) rsum += v;
-  }
-  if (lane == 31) s_cnt[warp][L] = rsum;
-  __syncthreads();
-  if (threadIdx.x <= (unsigned)L) {  // CTA totals -> one atomic per light, then warp offsets
-    const int l = threadIdx.x;
-    unsigned tot = 0;
-    for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
-    unsigned base = tot ? atomicAdd(B.ctr + (l < L ? wf_ctr_lt(d, l) : wf_ctr_so(d)), tot) : 0u;
-    for (int w = 0; w < 8; ++w) {
-      const unsigned c = s_cnt[w][l];
-      s_cnt[w][l] = base;
-      base += c;
-    }
-  }
-  __syncthreads();
-  for (int l = 0; l < L; ++l) {
-    const bool has = (lmask >> l) & 1ull;
-    const unsigned m = __ballot_sync(kFull, has);
-    if (has) {
-      const unsigned slot = s_cnt[warp][l] + (unsigned)__popc(m & lt);
-      B.slt[(size_t)l * B.cap + slot] = (int)(off + (unsigned)__popcll(lmask & ((1ull << l) - 1ull)));
-    }
-  }
-  if (nrest) {
-    unsigned ob = s_cnt[warp][L] + rsum - nrest;
-    unsigned r = (unsigned)__popcll(lmask & ((1ull << L) - 1ull));
-    for (unsigned long long mo = rest; mo != 0ull; mo &= mo - 1ull) B.sother[ob++] = (int)(off + r++);
-  }
-  __syncthreads();  // s_cnt is rewritten by the next iteration
-}
-
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
-constexpr int kLogicMinBlocks = 4;  // wf_shade / wf_accumulate: 64 registers, 4 CTAs per SM
+constexpr int kLogicMinBlocks = 4;  // wf_accumulate: 64 registers, 4 CTAs per SM
+constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~190 B spilled, 10 % slower)
 // kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
-// are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance
+// are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance.
+//
+// Shadow entries: entry j (path-major: the entries of Q[d]'s entry e are shoff[e] .. + shcnt[e],
+// sources in order) carries its contribution sq_c[j] and spos[j], where its scan lives:
+//  * point light l < lt_lights (light-origin scans): a slot g of one of light l's sub-lists,
+//    holding {e, skip}; the ray is rebuilt from B.sorg[e] = p + EPS_T n by the scan and, when an
+//    FP64 decision needs it, by wf_accumulate (spos[j] = g >= 0);
+//  * any other source (emitters, or every light when the scene is not in shared memory): a dense
+//    generic slot o (spos[j] = -2 - o) holding the FP64 shadow ray, its skips and the scan results.
+// Slots are reserved per warp (ballot + one atomic per light and warp on the sub-list of the warp's
+// 256-path block), so no CTA barrier sits between the light loop and the next paths.
 template <bool kDebug, bool kExt>
-__global__ void __launch_bounds__(256, kLogicMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
-                                                long long g0, unsigned long long* stats, int* dbg_hits,
-                                                int* dbg_bounces) {
+__global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
+                                                long long g0, int* dbg_hits, int* dbg_bounces) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
-  __shared__ unsigned s_cnt[8][kMaxLtLights + 1];  // bin_entries (per-light entry lists)
-  const bool bin = P.lt_lights > 0;
-  // CTA-uniform iterations (the fused list building has CTA barriers)
-  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
-    const unsigned e = e0 + threadIdx.x;
-    unsigned long long lm = 0ull;  // sources with a shadow ray, and the first entry, for the lists
-    unsigned of = 0u;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask_lane = lanemask_lt();
+  const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);  // point lights, then emitters (R#41)
+  const int LT = P.lt_lights;                                // point lights 0..LT-1: light-origin lists
+  // warp-uniform iterations: every lane of a warp takes part in the ballots of the slot reservations
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < n; e0 += stride) {
+    const unsigned e = e0 + lane;
+    // this warp's sub-list of every light list: the warps of one 256-path block share one, so a
+    // list keeps neighbouring paths together (coherent early exits in the light-origin scan)
+    const int sub = (int)((e0 >> 8) % kLtSub);
     d3 dir = mk(0, 0, 1);
     const bool valid = e < n && q_dir(P, B, Q, e, d, dir);
     if (e < n && !valid) B.shcnt[e] = 0;  // a work item outside the image (depth 0): nothing to shade
-    if (valid) {
-    const int path = q_path(Q, e, d);
-    const d3 o = q_origin(P, Q, B.cap, e, d);
-    double tbest = kInf;
-    int hs = -1, hp = -1;
-    for (int j = 0; j < P.n_planes; ++j) {
-      const DevPlane pl = c_planes[j];
-      const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
-      if (fabs(den) >= 1e-12) {
-        const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
-        if (t >= kEps && t < tbest) { tbest = t; hp = j; }
-      }
-    }
-    nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
-    const int dword = d == 0 ? 0 : Q.depth[e];
-    const int depth = dword & 0xff;
-    int prim = -1;
-    if (hp >= 0) prim = c_planes[hp].prim;
-    else if (hs >= 0) prim = S.sph_prim[hs];
-    long long si = 0;
-    if constexpr (kDebug) {
-      const long long g = g0 + path;
-      int px = 0, py = 0;
-      item_pixel(P, (int)(g / P.spp), px, py);
-      si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
-      dbg_hits[si * (P.max_depth + 1) + depth] = prim;
-    }
-    float3 T = d == 0 ? f3(1.f, 1.f, 1.f) : lf3(Q.T, B.cap, (int)e);
-    float3 L = d == 0 ? f3(0.f, 0.f, 0.f) : lf3(Q.L, B.cap, (int)e);
-    bool cont = false;
-    const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);  // point lights, then emitters (R#41)
-    unsigned long long lmask = 0ull;              // sources 0..63 that send a shadow ray
+    int path = 0, depth = 0, dword = 0, hs = -1, mi = 0;
+    unsigned long long lmask = 0ull;  // sources 0..63 that send a shadow ray
+    unsigned nsh = 0;
+    d3 p = mk(0, 0, 0), nrm = mk(0, 0, 1);
+    bool entering = false, hit = false;
+    float3 T = f3(1.f, 1.f, 1.f), L = f3(0.f, 0.f, 0.f);
     // pixel index and global sample index of the path (RNG keys, R#42): 32-bit arithmetic on the
     // chunk-local path id (path = local item * spp + s), computed only when a draw needs them
     unsigned long long pix = 0;
@@ -1137,37 +1058,67 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_shade(const DevParams
       pix = (unsigned long long)py * P.W + px;
       sg = (unsigned)(P.sample_base + (path - wl * P.spp));
     };
-    if (kExt && (P.n_emitters > 0 || P.integrator != 0)) pixel_sample();
-    unsigned nsh = 0;
-    d3 p = mk(0, 0, 0), ng = mk(0, 0, 1), nrm = mk(0, 0, 1);
-    int mi = 0;
-    bool entering = false;
-    // part 1: hit geometry, emission/ambient, number of shadow rays
-    if (prim < 0) {  // miss -> background
-      L = add(L, mul(T, f3(P.bg[0], P.bg[1], P.bg[2])));
-    } else {
-      p = o + dir * tbest;
-      if (hp >= 0) {
-        const DevPlane pl = c_planes[hp];
-        ng = mk(pl.nx, pl.ny, pl.nz);
-        mi = pl.mat;
-      } else {
-        const float4 cr = __ldg(S.sph_cr + hs);
-        ng = (p - mk(cr.x, cr.y, cr.z)) * (1.0 / (double)cr.w);
-        mi = S.sph_mat[hs];
+    long long si = 0;
+    // part 1: FP64 nearest hit, hit geometry, emission/ambient, which sources send a shadow ray
+    if (valid) {
+      path = q_path(Q, e, d);
+      const d3 o = q_origin(P, Q, B.cap, e, d);
+      double tbest = kInf;
+      int hp = -1;
+      for (int j = 0; j < P.n_planes; ++j) {
+        const DevPlane pl = c_planes[j];
+        const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+        if (fabs(den) >= 1e-12) {
+          const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+          if (t >= kEps && t < tbest) { tbest = t; hp = j; }
+        }
       }
-      entering = dot(dir, ng) < 0.0;
-      nrm = entering ? ng : ng * -1.0;
-      const DevMat m = S.mats[mi];
-      // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
-      const bool sampled = kExt && (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
-      if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
-      if (m.kind == 0) {
-        L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
-        for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
-          if (sends_shadow_ray<kExt>(P, S, l, p, nrm, pix, sg, depth)) {
-            ++nsh;
-            if (l < 64) lmask |= 1ull << l;
+      nearest_sphere(P, S, B.ccand + (size_t)e * kCandMax, B.cn[e], q_skip(Q, e, d), o, dir, tbest, hs, hp);
+      dword = d == 0 ? 0 : Q.depth[e];
+      depth = dword & 0xff;
+      int prim = -1;
+      if (hp >= 0) prim = c_planes[hp].prim;
+      else if (hs >= 0) prim = S.sph_prim[hs];
+      if constexpr (kDebug) {
+        const long long g = g0 + path;
+        int px = 0, py = 0;
+        item_pixel(P, (int)(g / P.spp), px, py);
+        si = ((long long)py * P.W + px) * P.spp + (int)(g % P.spp);
+        dbg_hits[si * (P.max_depth + 1) + depth] = prim;
+      }
+      if (d > 0) {
+        T = lf3(Q.T, B.cap, (int)e);
+        L = lf3(Q.L, B.cap, (int)e);
+      }
+      if (kExt && (P.n_emitters > 0 || P.integrator != 0)) pixel_sample();
+      if (prim < 0) {  // miss -> background
+        L = add(L, mul(T, f3(P.bg[0], P.bg[1], P.bg[2])));
+      } else {
+        hit = true;
+        p = o + dir * tbest;
+        d3 ng;
+        if (hp >= 0) {
+          const DevPlane pl = c_planes[hp];
+          ng = mk(pl.nx, pl.ny, pl.nz);
+          mi = pl.mat;
+        } else {
+          const float4 cr = __ldg(S.sph_cr + hs);
+          ng = (p - mk(cr.x, cr.y, cr.z)) * (1.0 / (double)cr.w);
+          mi = S.sph_mat[hs];
+        }
+        entering = dot(dir, ng) < 0.0;
+        nrm = entering ? ng : ng * -1.0;
+        const DevMat m = S.mats[mi];
+        // Eq. 7 emission, except an emitter already sampled from the previous diffuse vertex (R#43)
+        const bool sampled = kExt && (dword & kPrevDiffuse) && P.n_emitters > 0 && hs >= 0;
+        if (!sampled) L = add(L, mul(T, f3(m.er, m.eg, m.eb)));
+        if (m.kind == 0) {
+          L = add(L, mul(T, f3(m.ar * P.amb[0], m.ag * P.amb[1], m.ab * P.amb[2])));
+          for (int l = 0; l < n_src; ++l) {  // count shadow rays (none if cos <= 0)
+            if (sends_shadow_ray<kExt>(P, S, l, p, nrm, pix, sg, depth)) {
+              ++nsh;
+              if (l < 64) lmask |= 1ull << l;
+            }
           }
         }
       }
@@ -1175,116 +1126,151 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_shade(const DevParams
     const unsigned off = warp_reserve(nsh, B.ctr + wf_ctr_s(d));  // converged: ballot/scan/atomic
     // part 3 (before the entries, so the continuation's temporaries are dead during the light
     // loop): stack-free continuation; Tn = the throughput after the bounce
-    float3 Tn = T;
-    d3 dn = mk(0, 0, 0);
-    bool mi_kind_diffuse_global = false;
-    if (prim >= 0 && depth < P.max_depth) {
-      const DevMat m = S.mats[mi];
-      mi_kind_diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
-      if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
-        dn = reflect(dir, nrm);
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
-        dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
-      } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
-        if (m.kr > 0.f) {
+    bool cont = false;
+    {
+      float3 Tn = T;
+      d3 dn = mk(0, 0, 0);
+      bool diffuse_global = false;
+      if (hit && depth < P.max_depth) {
+        const DevMat m = S.mats[mi];
+        diffuse_global = kExt && m.kind == 0 && P.integrator == 1;
+        if (m.kind == 1) {  // SPECULAR: mirror, T *= rho
           dn = reflect(dir, nrm);
-          Tn = f3(Tn.x * m.kr, Tn.y * m.kr, Tn.z * m.kr);
+          Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+          cont = true;
+        } else if (kExt && m.kind == 0 && P.integrator == 1) {  // global: cosine-weighted bounce (R#40)
+          dn = cosine_dir(nrm, rng_stream(P.seed, pix, sg, depth, 3u), rng_stream(P.seed, pix, sg, depth, 4u));
+          Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
+          cont = true;
+        } else if (m.kind == 0) {  // DIFFUSE: mirror with weight kr when kr > 0 (R#8)
+          if (m.kr > 0.f) {
+            dn = reflect(dir, nrm);
+            Tn = f3(Tn.x * m.kr, Tn.y * m.kr, Tn.z * m.kr);
+            cont = true;
+          }
+        } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
+          const double ior = m.ior;
+          const double eta = entering ? 1.0 / ior : ior;
+          const double ci = -dot(dir, nrm);
+          const double sin2t = eta * eta * (1.0 - ci * ci);
+          bool refl = sin2t > 1.0;
+          if (!refl) {
+            const double cosT = sqrt(1.0 - sin2t);
+            const double c = entering ? ci : cosT;
+            double r0 = (1.0 - ior) / (1.0 + ior);
+            r0 *= r0;
+            const double mm = 1.0 - c;
+            const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
+            if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
+            const double u = rng_u(P.seed, pix, (int)sg, depth);
+            refl = u < F;
+            if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
+          }
+          if (refl) dn = reflect(dir, nrm);
+          Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
           cont = true;
         }
-      } else {  // REFRACTIVE: Schlick-chosen reflect / refract, TIR -> reflect (R#9-R#11)
-        const double ior = m.ior;
-        const double eta = entering ? 1.0 / ior : ior;
-        const double ci = -dot(dir, nrm);
-        const double sin2t = eta * eta * (1.0 - ci * ci);
-        bool refl = sin2t > 1.0;
-        if (!refl) {
-          const double cosT = sqrt(1.0 - sin2t);
-          const double c = entering ? ci : cosT;
-          double r0 = (1.0 - ior) / (1.0 + ior);
-          r0 *= r0;
-          const double mm = 1.0 - c;
-          const double F = r0 + (1.0 - r0) * (mm * mm * mm * mm * mm);
-          if (!kExt || (P.n_emitters == 0 && P.integrator == 0)) pixel_sample();
-          const double u = rng_u(P.seed, pix, (int)sg, depth);
-          refl = u < F;
-          if (!refl) dn = dir * eta + nrm * (eta * ci - cosT);
-        }
-        if (refl) dn = reflect(dir, nrm);
-        Tn = mul(Tn, f3(m.ar, m.ag, m.ab));
-        cont = true;
+        if (cont) dn = normalize(dn);
       }
-      if (cont) dn = normalize(dn);
+      const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
+      if (valid) {
+        B.shcnt[e] = (int)nsh;
+        B.shoff[e] = (int)off;
+        if constexpr (kDebug) {
+          if (!cont) dbg_bounces[si] = depth;
+        }
+        if (cont) {  // the path moves to slot `slot` of Q[d+1] with its whole state
+          Qn.path[slot] = path;
+          st3(Qn.ray, B.cap, (int)slot, 0, p);
+          st3(Qn.ray, B.cap, (int)slot, 3, dn);
+          sf3(Qn.T, B.cap, (int)slot, Tn);
+          sf3(Qn.L, B.cap, (int)slot, L);
+          Qn.depth[slot] = (depth + 1) | (diffuse_global ? kPrevDiffuse : 0);
+          // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
+          // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
+          // (the outward normal ng = entering ? nrm : -nrm)
+          const double dng = dot(dn, nrm);
+          Qn.skip[slot] = (hs >= 0 && (entering ? dng > 0.0 : dng < 0.0)) ? hs : -1;
+          B.nxt[e] = (int)slot;
+        } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
+          sf3(B.Lr, B.cap, path, L);
+          B.nxt[e] = -1 - path;
+        }
+      }
     }
-    B.shcnt[e] = (int)nsh;
-    if constexpr (kDebug) {
-      if (!cont) dbg_bounces[si] = depth;
-    }
-    const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
-    if (cont) {  // the path moves to slot `slot` of Q[d+1] with its whole state
-      Qn.path[slot] = path;
-      st3(Qn.ray, B.cap, (int)slot, 0, p);
-      st3(Qn.ray, B.cap, (int)slot, 3, dn);
-      sf3(Qn.T, B.cap, (int)slot, Tn);
-      sf3(Qn.L, B.cap, (int)slot, L);
-      Qn.depth[slot] = (depth + 1) | ((mi_kind_diffuse_global) ? kPrevDiffuse : 0);
-      // the new ray starts on sphere hs; heading outward it cannot hit it again (its roots are
-      // 0 and negative), so the scans skip it exactly; inward (refraction, TIR) it may
-      Qn.skip[slot] = (hs >= 0 && dot(dn, ng) > 0.0) ? hs : -1;
-      B.nxt[e] = (int)slot;
-    } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
-      sf3(B.Lr, B.cap, path, L);
-      B.nxt[e] = -1 - path;
-    }
-    // part 2 (after the continuation): shadow entries — the shadow ray itself and the contribution T f_r I cos / d^2
-    // (Eq. 3, 5, 6); a shadow ray leaving a sphere hit from outside skips it exactly (convexity)
-    if (nsh) {
+    // part 2 (after the continuation): shadow entries — the contribution T f_r I cos / d^2
+    // (Eq. 3, 5, 6) or the emitter estimator, and the shadow ray or its list slot. A shadow
+    // ray leaving a sphere hit from outside skips it exactly (convexity): o_s is EPS_T outside and
+    // the ray heads away from the tangent plane, so it cannot meet the sphere again.
+    if (__any_sync(kFull, nsh != 0u)) {
       const DevMat m = S.mats[mi];
       const int out_sph = (hs >= 0 && entering) ? hs : -1;
+      if (nsh != 0u && LT > 0 && (lmask & ((LT >= 64) ? ~0ull : ((1ull << LT) - 1ull))) != 0ull)
+        st3(B.sorg, B.cap, (int)e, 0, p + nrm * kEps);  // the light-origin entries' rays start here
       unsigned k = off;
-      for (int l = 0; l < n_src; ++l) {
-        if (l < 64 && !((lmask >> l) & 1ull)) continue;  // no shadow ray (decided in the count pass)
+      for (int l = 0; l < n_src; ++l) {  // warp-uniform trip count: the slot ballots need every lane
+        const bool has = l < 64 ? ((lmask >> l) & 1ull) != 0ull : false;
+        int g = -1;
+        if (l < LT) {  // a slot in light l's sub-list `sub`
+          const unsigned bal = __ballot_sync(kFull, has);
+          if (bal == 0u) continue;
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(B.ctr + wf_ctr_lt(d, l, sub), (unsigned)__popc(bal));
+          base = __shfl_sync(kFull, base, 0);
+          g = (l * kLtSub + sub) * B.lt_cap + (int)(base + (unsigned)__popc(bal & lt_mask_lane));
+        } else {  // a dense generic slot
+          g = -2 - (int)warp_reserve1(has, B.ctr + wf_ctr_so(d));
+        }
+        if (!has) continue;
         LightSample ls;
-        if (!light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls)) continue;
+        light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);  // true: the count pass decided
         // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3),
         // or L_e cos_s cos_l / (d^2 pdf) for an emitter sample (Eq. 8, R#41)
         const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
         const float alpha = (float)fmax(0.0, -dot(rl, dir));
         const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
-        const float g = (float)ls.g;
-        d3 os, ds;
-        double tl;
-        if (!kExt || l < P.n_lights) shadow_ray(S, p, nrm, l, os, ds, tl);
-        else shadow_ray_to(p, nrm, ls.x, os, ds, tl);
-        st3(B.sray, B.scap, (int)k, 0, os);
-        st3(B.sray, B.scap, (int)k, 3, ds);
-        B.sray[6 * (size_t)B.scap + k] = tl;
-        B.sskip[k] = shadow_skip(out_sph, nrm, ds);
-        // the aimed-at emitter: read by wf_accumulate<true> and by the generic shadow scan only
-        if (kExt || P.lt_lights == 0) B.sskip2[k] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;
-        sf3(B.sq_c, B.scap, k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
-                                       fmaf(m.ab, kInvPi, spec) * ls.ib * g)));
+        const float gg = (float)ls.g;
+        sf3(B.sq_c, B.scap, (int)k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * gg, fmaf(m.ag, kInvPi, spec) * ls.ig * gg,
+                                             fmaf(m.ab, kInvPi, spec) * ls.ib * gg)));
+        B.spos[k] = g;
+        if (g >= 0) {
+          d3 ds;
+          double tl;
+          const d3 os = p + nrm * kEps;
+          shadow_dir(os, ls.x, ds, tl);
+          int skip = shadow_skip(out_sph, nrm, ds);
+          for (int q = 0; q < P.n_planes; ++q) {  // planes first, exactly (FP64), in index order
+            const DevPlane pl = c_planes[q];
+            const double den = pl.nx * ds.x + pl.ny * ds.y + pl.nz * ds.z;
+            if (fabs(den) >= 1e-12) {
+              const double t = (pl.d - (pl.nx * os.x + pl.ny * os.y + pl.nz * os.z)) / den;
+              if (t >= kEps && t < tl) { skip = -2 - q; break; }
+            }
+          }
+          B.lt_dir[g] = make_float4((float)ds.x, (float)ds.y, (float)ds.z, (float)tl);
+          B.lt_rec[g] = make_int2((int)e, skip);
+        } else {
+          const int o = -2 - g;
+          d3 os2, ds;
+          double tl;
+          shadow_ray_to(p, nrm, ls.x, os2, ds, tl);
+          st3(B.sray, B.gcap, o, 0, os2);
+          st3(B.sray, B.gcap, o, 3, ds);
+          B.sray[6 * (size_t)B.gcap + o] = tl;
+          B.sskip[o] = shadow_skip(out_sph, nrm, ds);
+          B.sskip2[o] = (kExt && l >= P.n_lights) ? S.emit_sph[l - P.n_lights] : -1;  // not tested (R#41)
+        }
         ++k;
       }
     }
-    B.shoff[e] = (int)off;
-    lm = lmask;
-    of = off;
-    warp_stat(stats, 1, nsh);
-    warp_stat(stats, 2, cont ? 1ull : 0ull);
-    warp_stat(stats, 3, (unsigned long long)P.n_spheres);
-    warp_stat(stats, 4, (unsigned long long)P.n_planes);
-    warp_stat(stats, 5, (unsigned long long)P.n_spheres);
-    if (d == 0) warp_stat(stats, 0, 1ull);  // primary rays (the camera queue is implicit)
-    }
-    if (bin) bin_entries(P, B, d, lm, of, s_cnt);
   }
 }
 
 // ---- a5 decision + accumulation of the visible lights, in light order ----------------------
+// Per shading entry e of Q[d]: its shadow entries in source order; the scan left each one's
+// certain occluder rob (sphere k >= 0, plane -2-j, or -1) and candidate list; an occlusion that
+// the float filter could not settle is decided here in FP64 on the original ray, exactly as the
+// oracle's step 7 (first accepted root in [EPS_T, t_max) in index order).
 template <bool kExt>  // false: no emitters, every skip2 is -1 (not read)
 __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                      unsigned long long* stats) {
@@ -1300,41 +1286,69 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
       const int li = loc >= 0 ? loc : -1 - loc;
       float3 L = lf3(Ls, B.cap, li);
       for (int j = off; j < off + cnt; ++j) {
-        const int rob = B.srob[j];
-        const int skip2 = kExt ? B.sskip2[j] : -1;
+        const int g = B.spos[j];
+        const bool lt = g >= 0;  // a light-origin list slot, else generic slot o = -2 - g
+        const int o = lt ? 0 : -2 - g;
+        int rob, nc, skip2 = -1;
+        const int* cand;
+        if (lt) {
+          const int2 r = B.lt_res[g];
+          rob = r.x;
+          nc = r.y;
+          cand = B.lt_cand + (size_t)g * kCandMax;
+        } else {
+          rob = B.srob[o];
+          nc = B.sn[o];
+          cand = B.scand + (size_t)o * kCandMax;
+          if (kExt) skip2 = B.sskip2[o];
+        }
+        // the FP64 shadow ray and the sphere it leaves (only when an FP64 decision needs them)
+        auto ray = [&](d3& os, d3& ds, double& tl, int& skip) {
+          if (lt) {
+            skip = max(B.lt_rec[g].y, -1);  // (a plane occluder's code is not a sphere to skip)
+            lt_ray(S, B, (int)e, g / B.lt_cap / kLtSub, os, ds, tl);
+          } else {
+            os = ld3(B.sray, B.gcap, o, 0);
+            ds = ld3(B.sray, B.gcap, o, 3);
+            tl = B.sray[6 * (size_t)B.gcap + o];
+            skip = B.sskip[o];
+          }
+        };
         int hp = -1, first = -1;
         if (rob <= -2) {  // plane -2-rob occludes (planes are tested first, in index order)
           hp = -2 - rob;
-        } else {
-          const int nc = B.sn[j];
-          if (nc > 0 || rob >= 0) {
-            const d3 os = ld3(B.sray, B.scap, j, 0), ds = ld3(B.sray, B.scap, j, 3);
-            const double tl = B.sray[6 * (size_t)B.scap + j];
-            if (nc <= kCandMax) {
-              const int* c = B.scand + (size_t)j * kCandMax;
-              for (int i = 0; i < nc; ++i) {
-                const double t = sphere_root(__ldg(S.sph_cr + c[i]), os, ds);
-                if (t >= kEps && t < tl) { first = c[i]; break; }
-              }
-              if (first < 0) first = rob;
-            } else {
-              const int skip = B.sskip[j];
-              for (int k = 0; k < P.n_spheres; ++k) {
-                if (k == skip || k == skip2) continue;
-                const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
-                if (t >= kEps && t < tl) { first = k; break; }
-              }
+        } else if (nc > 0) {
+          d3 os, ds;
+          double tl;
+          int skip;
+          ray(os, ds, tl, skip);
+          if (nc <= kCandMax) {
+            for (int i = 0; i < nc; ++i) {
+              const double t = sphere_root(__ldg(S.sph_cr + cand[i]), os, ds);
+              if (t >= kEps && t < tl) { first = cand[i]; break; }
+            }
+            if (first < 0) first = rob;
+          } else {
+            for (int k = 0; k < P.n_spheres; ++k) {
+              if (k == skip || k == skip2) continue;
+              const double t = sphere_root(__ldg(S.sph_cr + k), os, ds);
+              if (t >= kEps && t < tl) { first = k; break; }
             }
           }
+        } else {
+          first = rob;  // a certain occluder with no ambiguous candidate before it, or none
         }
         const bool occluded = hp >= 0 || first >= 0;
         // tests up to the first occluder in index order; the aimed-at emitter is not tested
         unsigned long long ns = 0, np = 0;
         if (hp >= 0 && c_planes[hp].prim != hp) {  // spheres listed before the occluding plane
-          shadow_counts(P, S, ld3(B.sray, B.scap, j, 0), ld3(B.sray, B.scap, j, 3), B.sray[6 * (size_t)B.scap + j], hp,
-                        -1, B.sskip[j], skip2, ns, np);
+          d3 os, ds;
+          double tl;
+          int skip;
+          ray(os, ds, tl, skip);
+          shadow_counts(P, S, os, ds, tl, hp, -1, skip, skip2, ns, np);
         } else {
-          shadow_counts(P, S, mk(0, 0, 0), mk(0, 0, 1), 0.0, hp < 0 ? -1 : hp, first, -1, skip2, ns, np);
+          shadow_counts(P, S, mk(0, 0, 0), mk(0, 0, 1), 0.0, hp, first, -1, skip2, ns, np);
         }
         st_sph += ns;
         st_pl += np;
@@ -1348,8 +1362,13 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
 }
 
 // ---- a7: mean over samples in order, 16-byte store ------------------------------------------
+// Also the chunk's ray statistics that need no per-ray work (§8(c).1 step 11): primary rays =
+// the valid samples, secondary = the continuations queued at depths 1..max_depth, shadow = the
+// shadow entries reserved, closest-hit tests = (primary + secondary) x every sphere / plane; the
+// shadow rays' test counts come from wf_accumulate.
 __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B, int w0, int nw, float4* out,
-                                                  double* accum) {
+                                                  double* accum, unsigned long long* stats) {
+  unsigned long long nvalid = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
     const int w = w0 + i;
     int px = 0, py = 0;
@@ -1358,6 +1377,7 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
       if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
       continue;
     }
+    ++nvalid;
     if (accum) {  // progressive passes: double sums in pass order, mean = sum / passes so far
       double* a = accum + 3 * ((long long)py * P.W + px);
       double a0 = a[0], a1 = a[1], a2 = a[2];
@@ -1380,6 +1400,23 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
     const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, 1.0f);
     if (P.mode != 1) out[(long long)py * P.W + px] = v;  // frame (mode 0) or peer frame (mode 2)
     else out[w] = v;
+  }
+  const unsigned long long prim = nvalid * (unsigned long long)P.spp;
+  warp_stat(stats, 0, prim);
+  warp_stat(stats, 3, prim * (unsigned long long)P.n_spheres);
+  warp_stat(stats, 4, prim * (unsigned long long)P.n_planes);
+  warp_stat(stats, 5, prim * (unsigned long long)P.n_spheres);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long sec = 0, sh = 0;
+    for (int dd = 0; dd <= P.max_depth; ++dd) {
+      sh += B.ctr[wf_ctr_s(dd)];
+      if (dd > 0) sec += B.ctr[wf_ctr_q(dd)];
+    }
+    atomicAdd(stats + 1, sh);
+    atomicAdd(stats + 2, sec);
+    atomicAdd(stats + 3, sec * (unsigned long long)P.n_spheres);
+    if (P.n_planes) atomicAdd(stats + 4, sec * (unsigned long long)P.n_planes);
+    atomicAdd(stats + 5, sec * (unsigned long long)P.n_spheres);
   }
 }
 
