@@ -1031,6 +1031,7 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
   const unsigned lt_mask_lane = lanemask_lt();
   const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);  // point lights, then emitters (R#41)
   const int LT = P.lt_lights;                                // point lights 0..LT-1: light-origin lists
+  const int nres = n_src < 30 ? n_src : 30;                  // sources whose slots are reserved together
   // warp-uniform iterations: every lane of a warp takes part in the ballots of the slot reservations
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < n; e0 += stride) {
@@ -1123,10 +1124,10 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         }
       }
     }
-    const unsigned off = warp_reserve(nsh, B.ctr + wf_ctr_s(d));  // converged: ballot/scan/atomic
     // part 3 (before the entries, so the continuation's temporaries are dead during the light
     // loop): stack-free continuation; Tn = the throughput after the bounce
     bool cont = false;
+    unsigned base = 0, off = 0;  // lane l: the first slot of source l's entries (see below); off: lane's first entry
     {
       float3 Tn = T;
       d3 dn = mk(0, 0, 0);
@@ -1172,7 +1173,29 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         }
         if (cont) dn = normalize(dn);
       }
-      const unsigned slot = warp_reserve(cont ? 1u : 0u, B.ctr + wf_ctr_q(d + 1));
+      // every slot the warp needs, reserved in ONE round trip to L2 (the atomics' latency, not their
+      // number, bounded this kernel): lane l < nres takes source l's slots (its light-origin
+      // sub-list, or generic slots), lane 30 the warp's shadow entries, lane 31 its continuations
+      unsigned pre_sh = 0, tot_sh = 0;  // warp-exclusive prefix / total of nsh (< 64) by bit planes
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const unsigned m = __ballot_sync(kFull, (nsh >> b) & 1u);
+        pre_sh += (unsigned)__popc(m & lt_mask_lane) << b;
+        tot_sh += (unsigned)__popc(m) << b;
+      }
+      const unsigned mc = __ballot_sync(kFull, cont);
+      unsigned cnt = 0;
+      for (int l = 0; l < nres; ++l) {
+        const unsigned bl = __ballot_sync(kFull, ((lmask >> l) & 1ull) != 0ull);
+        if (lane == l) cnt = (unsigned)__popc(bl);
+      }
+      unsigned* ctr = nullptr;
+      if (lane < nres) ctr = B.ctr + (lane < LT ? wf_ctr_lt(d, lane, sub) : wf_ctr_so(d));
+      else if (lane == 30) { ctr = B.ctr + wf_ctr_s(d); cnt = tot_sh; }
+      else if (lane == 31) { ctr = B.ctr + wf_ctr_q(d + 1); cnt = (unsigned)__popc(mc); }
+      base = (ctr != nullptr && cnt != 0u) ? atomicAdd(ctr, cnt) : 0u;
+      off = __shfl_sync(kFull, base, 30) + pre_sh;
+      const unsigned slot = __shfl_sync(kFull, base, 31) + (unsigned)__popc(mc & lt_mask_lane);
       if (valid) {
         B.shcnt[e] = (int)nsh;
         B.shoff[e] = (int)off;
@@ -1211,16 +1234,19 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
       for (int l = 0; l < n_src; ++l) {  // warp-uniform trip count: the slot ballots need every lane
         const bool has = l < 64 ? ((lmask >> l) & 1ull) != 0ull : false;
         int g = -1;
-        if (l < LT) {  // a slot in light l's sub-list `sub`
-          const unsigned bal = __ballot_sync(kFull, has);
-          if (bal == 0u) continue;
-          unsigned base = 0;
-          if (lane == 0) base = atomicAdd(B.ctr + wf_ctr_lt(d, l, sub), (unsigned)__popc(bal));
-          base = __shfl_sync(kFull, base, 0);
-          g = (l * kLtSub + sub) * B.lt_cap + (int)(base + (unsigned)__popc(bal & lt_mask_lane));
-        } else {  // a dense generic slot
-          g = -2 - (int)warp_reserve1(has, B.ctr + wf_ctr_so(d));
+        const unsigned bal = __ballot_sync(kFull, has);
+        if (bal == 0u) continue;
+        unsigned first;  // the warp's first slot for source l
+        if (l < nres) {
+          first = __shfl_sync(kFull, base, l);
+        } else {  // sources beyond lane 29 (more than 30 sources): one more round trip each
+          first = 0;
+          if (lane == 0) first = atomicAdd(B.ctr + (l < LT ? wf_ctr_lt(d, l, sub) : wf_ctr_so(d)), (unsigned)__popc(bal));
+          first = __shfl_sync(kFull, first, 0);
         }
+        const unsigned pos = first + (unsigned)__popc(bal & lt_mask_lane);
+        if (l < LT) g = (l * kLtSub + sub) * B.lt_cap + (int)pos;  // a slot in light l's sub-list `sub`
+        else g = -2 - (int)pos;                                     // a dense generic slot
         if (!has) continue;
         LightSample ls;
         light_sample<kExt>(P, S, l, p, nrm, pix, sg, depth, ls);  // true: the count pass decided
