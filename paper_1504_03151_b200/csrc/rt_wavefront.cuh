@@ -668,8 +668,8 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // 64 entries of one list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
 // t = t_l - tc' -/+ q on the original one; the bounds add the error of t_l and of the reversal.
 //
-// Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per warp, the
-// sub-list chosen by the warp's 256-path block, so no CTA barrier and no single hot counter); a
+// Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per CTA iteration,
+// the sub-list chosen by the iteration's 256-path block, so no single hot counter); a
 // slot holds the ray's direction and t_max rounded to float (what the filter reads; wf_shade
 // computed them in FP64) and {shading entry e of Q[d], skip}: skip = the sphere the ray provably
 // leaves or -1, or -2 - j when wf_shade already found plane j to occlude (planes are decided in
@@ -1019,8 +1019,11 @@ constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~1
 //    FP64 decision needs it, by wf_accumulate (spos[j] = g >= 0);
 //  * any other source (emitters, or every light when the scene is not in shared memory): a dense
 //    generic slot o (spos[j] = -2 - o) holding the FP64 shadow ray, its skips and the scan results.
-// Slots are reserved per warp (ballot + one atomic per light and warp on the sub-list of the warp's
-// 256-path block), so no CTA barrier sits between the light loop and the next paths.
+// Every slot a warp needs is reserved in one round trip: lane-parallel atomics for the shadow
+// entries, the continuations and the generic slots; the light-origin lists per CTA (one atomic per
+// light and CTA iteration, warps in order, so a list keeps the CTA's 256 neighbouring paths
+// together: coherent early exits in the scan). The CTA barrier of that reservation sits before the
+// light loop, so warps wait for the slowest warp's hit and bounce, not for its light loop.
 template <bool kDebug, bool kExt>
 __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, int* dbg_hits, int* dbg_bounces) {
@@ -1034,11 +1037,14 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
   const int nres = n_src < 30 ? n_src : 30;                  // sources whose slots are reserved together
   // warp-uniform iterations: every lane of a warp takes part in the ballots of the slot reservations
   const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < n; e0 += stride) {
+  __shared__ unsigned s_cnt[8][kMaxLtLights];  // per warp and light-origin light: entries, then first slot
+  for (unsigned cb = blockIdx.x * blockDim.x; cb < n; cb += stride) {  // CTA-uniform (CTA barriers below)
+    const unsigned e0 = cb + (threadIdx.x & ~31u);
     const unsigned e = e0 + lane;
-    // this warp's sub-list of every light list: the warps of one 256-path block share one, so a
-    // list keeps neighbouring paths together (coherent early exits in the light-origin scan)
-    const int sub = (int)((e0 >> 8) % kLtSub);
+    const int warp = threadIdx.x >> 5;
+    // the CTA's sub-list of every light list: a list keeps the CTA's 256 neighbouring paths
+    // together, in warp order (coherent early exits in the light-origin scan)
+    const int sub = (int)((cb >> 8) % kLtSub);
     d3 dir = mk(0, 0, 1);
     const bool valid = e < n && q_dir(P, B, Q, e, d, dir);
     if (e < n && !valid) B.shcnt[e] = 0;  // a work item outside the image (depth 0): nothing to shade
@@ -1190,10 +1196,25 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         if (lane == l) cnt = (unsigned)__popc(bl);
       }
       unsigned* ctr = nullptr;
-      if (lane < nres) ctr = B.ctr + (lane < LT ? wf_ctr_lt(d, lane, sub) : wf_ctr_so(d));
+      if (lane < LT) s_cnt[warp][lane] = cnt;  // light-origin lists: reserved per CTA below
+      else if (lane < nres) ctr = B.ctr + wf_ctr_so(d);
       else if (lane == 30) { ctr = B.ctr + wf_ctr_s(d); cnt = tot_sh; }
       else if (lane == 31) { ctr = B.ctr + wf_ctr_q(d + 1); cnt = (unsigned)__popc(mc); }
       base = (ctr != nullptr && cnt != 0u) ? atomicAdd(ctr, cnt) : 0u;
+      __syncthreads();
+      if (threadIdx.x < (unsigned)LT) {  // one atomic per light and CTA; warps in order
+        const int l = threadIdx.x;
+        unsigned tot = 0;
+        for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
+        unsigned b0 = tot ? atomicAdd(B.ctr + wf_ctr_lt(d, l, sub), tot) : 0u;
+        for (int w = 0; w < 8; ++w) {
+          const unsigned c = s_cnt[w][l];
+          s_cnt[w][l] = b0;
+          b0 += c;
+        }
+      }
+      __syncthreads();
+      if (lane < LT) base = s_cnt[warp][lane];
       off = __shfl_sync(kFull, base, 30) + pre_sh;
       const unsigned slot = __shfl_sync(kFull, base, 31) + (unsigned)__popc(mc & lt_mask_lane);
       if (valid) {
