@@ -97,17 +97,18 @@ struct Context {
   // wavefront variant
   int variant = RT_VARIANT_AUTO;
   int concurrent = 1;  // shadow scans || next closest scan on a side stream (rt_set_concurrency)
-  DevBuf<unsigned char> wf_mem, wf_mem2;
-  DevBuf<unsigned> wf_ctr, wf_ctr2;
-  rt::WfBuffers wf{}, wf2{};
-  // chunk pipelining (odd chunks on a second buffer set and stream pair)
-  int pipeline = 1;
-  cudaStream_t main2 = nullptr, side2 = nullptr;
-  std::vector<cudaEvent_t> ev_fork2, ev_join2;
-  cudaEvent_t ev_start2 = nullptr, ev_done2 = nullptr;
+  // chunk pipelining over buffer-set slots (rt_set_pipeline): chunk i on slot i % pipeline, each
+  // slot with its own buffers, counters and stream pair (main, side: shadow scans || next closest
+  // scan); slot 0's main stream is the library stream
+  static constexpr int kSlots = rt::WfTiming::kMaxSlots;
+  int pipeline = 2;
+  DevBuf<unsigned char> wf_mem[kSlots];
+  DevBuf<unsigned> wf_ctr[kSlots];
+  rt::WfBuffers wf[kSlots]{};
+  cudaStream_t slot_main[kSlots] = {}, slot_side[kSlots] = {};
+  std::vector<cudaEvent_t> ev_fork[kSlots], ev_join[kSlots];
+  cudaEvent_t ev_start = nullptr, ev_done[kSlots] = {};
   std::vector<cudaEvent_t> ev_c, ev_s, ev_h, ev_a;  // per-launch scan / shade / accumulate timing
-  cudaStream_t side_stream = nullptr;           // shadow scans || next closest scan
-  std::vector<cudaEvent_t> ev_fork, ev_join;
   int n_timed = 0, last_launches = 0, last_variant = 0, last_depth = 0;
   // camera (double basis)
   bool has_camera = false;
@@ -140,7 +141,7 @@ struct Context {
   std::vector<std::string> recent_keys;
   unsigned long long graph_clock = 0;
   int last_graph = 0;  // how the last wavefront render was launched: 0 plain, 1 captured, 2 replayed
-  std::vector<unsigned> hint0, hint1;  // queue counters of the render before the capture
+  std::vector<unsigned> hints[kSlots];  // queue counters of the render before the capture, per slot
 };
 constexpr size_t kGraphCache = 4, kRecentKeys = 8;
 
@@ -253,9 +254,14 @@ std::string wf_launch_key(const rt::DevParams& p, const rt::DevScene& sc, const 
   key_add(k, src);
   key_add(k, c.num_sms);
   key_add(k, c.wf);
-  key_add(k, c.wf2);
-  const void* ptrs[] = {tm.closest, tm.shadow, tm.shade, tm.side, tm.fork, tm.join, tm.B2, tm.main2, tm.side2, tm.fork2,
-                        tm.join2, tm.start_ev, tm.done2_ev, tm.chunk_done, tm.chunk_items};
+  key_add(k, tm.nslots);
+  key_add(k, tm.slot_B);
+  key_add(k, tm.slot_main);
+  key_add(k, tm.slot_side);
+  key_add(k, tm.slot_fork);
+  key_add(k, tm.slot_join);
+  key_add(k, tm.slot_done);
+  const void* ptrs[] = {tm.closest, tm.shadow, tm.shade, tm.accum, tm.start_ev, tm.chunk_done, tm.chunk_items};
   key_add(k, ptrs);
   key_add(k, tm.cap);
   key_add(k, tm.chunk_cap);
@@ -279,7 +285,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CU(cudaStreamIsCapturing(c.stream, &cs), "cudaStreamIsCapturing");
   if (!c.graphs || cs != cudaStreamCaptureStatusNone) {  // the caller captures: plain launches into it
-    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, tm, c.stream), "wavefront launch");
     return RT_OK;
   }
   std::string key = wf_launch_key(p, sc, o, src, tm, c);
@@ -296,7 +302,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   }
   if (std::find(c.recent_keys.begin(), c.recent_keys.end(), key) == c.recent_keys.end()) {
     // first render with this key (recently): plain launches
-    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.stream), "wavefront launch");
+    CU(rt::launch_render_wavefront(p, sc, o, src, c.num_sms, tm, c.stream), "wavefront launch");
     c.recent_keys.push_back(key);
     if (c.recent_keys.size() > kRecentKeys) c.recent_keys.erase(c.recent_keys.begin());
     return RT_OK;
@@ -308,13 +314,10 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   {
     const size_t nctr = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
     CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
-    c.hint0.assign(nctr, 0u);
-    CU(cudaMemcpy(c.hint0.data(), c.wf_ctr.p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
-    tm.hint[0] = c.hint0.data();
-    if (tm.B2 && c.wf_ctr2.p) {
-      c.hint1.assign(nctr, 0u);
-      CU(cudaMemcpy(c.hint1.data(), c.wf_ctr2.p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
-      tm.hint[1] = c.hint1.data();
+    for (int k = 0; k < tm.nslots; ++k) {
+      c.hints[k].assign(nctr, 0u);
+      CU(cudaMemcpy(c.hints[k].data(), c.wf_ctr[k].p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
+      tm.hint[k] = c.hints[k].data();
     }
   }
   if (!c.cap_stream) CU(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -324,7 +327,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   if (c.concurrent) tm.cap = 0;
   tm.ext_events = true;
   CU(cudaStreamBeginCapture(c.cap_stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
-  const cudaError_t le = rt::launch_render_wavefront(p, sc, o, src, c.num_sms, c.wf, tm, c.cap_stream);
+  const cudaError_t le = rt::launch_render_wavefront(p, sc, o, src, c.num_sms, tm, c.cap_stream);
   cudaGraph_t g = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(c.cap_stream, &g);
   tm.ext_events = false;
@@ -373,44 +376,49 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   const bool wavefront = c.variant == RT_VARIANT_WAVEFRONT ||
                          (c.variant == RT_VARIANT_AUTO && (extended || c.n_spheres >= kAutoWavefrontSpheres));
   if (wavefront) {
-    // chunk of whole pixels: at most 2^22 paths; shadow entries: paths x lights
-    const long long want = (long long)p.n_items * p.spp;
-    // chunks of at most 2^22 paths (smaller chunks for host framebuffers hide more of the row
-    // copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21)
-    const long long chunk = 1ll << 22;
-    int items = (int)((want < chunk ? want : chunk) / p.spp);
-    if (items < 1) items = 1;
-    const int cap = items * p.spp;
+    // chunks of whole pixels, at most 2^22 paths each (smaller chunks for host framebuffers hide
+    // more of the row copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21);
+    // a frame that fills fewer chunks than pipeline slots is cut into one chunk per slot
+    const int nslots = c.concurrent ? c.pipeline : 1;
+    const int ipc = rt::wf_items_per_chunk(p, nslots);
+    const int cap = ipc * p.spp;
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
     const int scap = cap * (n_src > 0 ? n_src : 1);
     // point lights with light-origin scans get list slots; every other source a generic slot
     const int n_gen = n_src - p.lt_lights;
     const int gcap = cap * (n_gen > 0 ? n_gen : 1);
     const int lt_lists = p.lt_lights * rt::kLtSub;
-    // (re)carve for this frame's cap
-    CU(c.wf_mem.reserve(rt::wf_bytes(cap, scap, gcap, lt_lists, 4 * c.num_sms)), "cudaMalloc(wavefront)");
-    CU(c.wf_ctr.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-    rt::wf_carve(c.wf, c.wf_mem.p, cap, scap, gcap, lt_lists, 4 * c.num_sms, c.wf_ctr.p);
-    c.wf.force_parts = c.scan_split;
-    const bool pipe = c.pipeline != 0 && c.concurrent != 0;
-    if (pipe) {
-      CU(c.wf_mem2.reserve(rt::wf_bytes(cap, scap, gcap, lt_lists, 4 * c.num_sms)), "cudaMalloc(wavefront, second chunk slot)");
-      CU(c.wf_ctr2.reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
-      rt::wf_carve(c.wf2, c.wf_mem2.p, cap, scap, gcap, lt_lists, 4 * c.num_sms, c.wf_ctr2.p);
-      c.wf2.force_parts = c.scan_split;
-      if (!c.main2) CU(cudaStreamCreateWithFlags(&c.main2, cudaStreamNonBlocking), "cudaStreamCreate");
-      if (!c.side2) CU(cudaStreamCreateWithFlags(&c.side2, cudaStreamNonBlocking), "cudaStreamCreate");
-      if (!c.ev_start2) CU(cudaEventCreateWithFlags(&c.ev_start2, cudaEventDisableTiming), "cudaEventCreate");
-      if (!c.ev_done2) CU(cudaEventCreateWithFlags(&c.ev_done2, cudaEventDisableTiming), "cudaEventCreate");
-      while ((int)c.ev_fork2.size() < p.max_depth + 1) {
+    const int n_chunks = (p.n_items + ipc - 1) / ipc;
+    const int used = n_chunks < nslots ? n_chunks : nslots;  // slots that receive a chunk
+    rt::WfTiming tm{nullptr, nullptr, 0, 0, 0};
+    tm.nslots = used;
+    for (int k = 0; k < used; ++k) {  // (re)carve each slot's buffers for this frame's chunk size
+      CU(c.wf_mem[k].reserve(rt::wf_bytes(cap, scap, gcap, lt_lists, 4 * c.num_sms)), "cudaMalloc(wavefront)");
+      CU(c.wf_ctr[k].reserve(rt::kWfCtrPerDepth * 80), "cudaMalloc(wavefront counters)");
+      rt::wf_carve(c.wf[k], c.wf_mem[k].p, cap, scap, gcap, lt_lists, 4 * c.num_sms, c.wf_ctr[k].p);
+      c.wf[k].force_parts = c.scan_split;
+      tm.slot_B[k] = &c.wf[k];
+      if (k > 0 && !c.slot_main[k]) CU(cudaStreamCreateWithFlags(&c.slot_main[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      if (!c.slot_side[k]) CU(cudaStreamCreateWithFlags(&c.slot_side[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      if (k > 0 && !c.ev_done[k]) CU(cudaEventCreateWithFlags(&c.ev_done[k], cudaEventDisableTiming), "cudaEventCreate");
+      while ((int)c.ev_fork[k].size() < p.max_depth + 1) {
         cudaEvent_t f, j;
         CU(cudaEventCreateWithFlags(&f, cudaEventDisableTiming), "cudaEventCreate");
         CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "cudaEventCreate");
-        c.ev_fork2.push_back(f);
-        c.ev_join2.push_back(j);
+        c.ev_fork[k].push_back(f);
+        c.ev_join[k].push_back(j);
+      }
+      tm.slot_main[k] = c.slot_main[k];
+      tm.slot_done[k] = c.ev_done[k];
+      if (c.concurrent) {
+        tm.slot_side[k] = c.slot_side[k];
+        tm.slot_fork[k] = c.ev_fork[k].data();
+        tm.slot_join[k] = c.ev_join[k].data();
       }
     }
-    const int pairs = rt::wf_timing_pairs(p, cap, pipe);
+    if (used > 1 && !c.ev_start) CU(cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming), "cudaEventCreate");
+    tm.start_ev = c.ev_start;
+    const int pairs = rt::wf_timing_pairs(p, nslots);
     while ((int)c.ev_c.size() < 2 * pairs) {
       cudaEvent_t a, b, h, m;
       CU(cudaEventCreate(&a), "cudaEventCreate");
@@ -422,35 +430,14 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       c.ev_h.push_back(h);
       c.ev_a.push_back(m);
     }
-    if (!c.side_stream) CU(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    while ((int)c.ev_fork.size() < p.max_depth + 1) {
-      cudaEvent_t f, j;
-      CU(cudaEventCreateWithFlags(&f, cudaEventDisableTiming), "cudaEventCreate");
-      CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "cudaEventCreate");
-      c.ev_fork.push_back(f);
-      c.ev_join.push_back(j);
-    }
-    rt::WfTiming tm{c.ev_c.data(), c.ev_s.data(), pairs, 0, 0};
+    tm.closest = c.ev_c.data();
+    tm.shadow = c.ev_s.data();
+    tm.cap = pairs;
     tm.shade = c.ev_h.data();
     tm.accum = c.ev_a.data();
-    if (c.concurrent) {
-      tm.side = c.side_stream;
-      tm.fork = c.ev_fork.data();
-      tm.join = c.ev_join.data();
-    }
-    if (pipe) {
-      tm.B2 = &c.wf2;
-      tm.main2 = c.main2;
-      tm.side2 = c.side2;
-      tm.fork2 = c.ev_fork2.data();
-      tm.join2 = c.ev_join2.data();
-      tm.start_ev = c.ev_start2;
-      tm.done2_ev = c.ev_done2;
-    }
     const bool overlap = host_out != nullptr && p.mode == 0;
     if (overlap) {
-      const int ipc = rt::wf_items_per_chunk(p, cap, pipe);
-      const int max_chunks = (p.n_items + ipc - 1) / ipc;
+      const int max_chunks = n_chunks;
       if (!c.copy_stream) CU(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
       while ((int)c.ev_chunk.size() < max_chunks) {
         cudaEvent_t ev;
@@ -674,6 +661,14 @@ int rt_set_concurrency(int32_t on) {
   if (rc) return rc;
   if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "concurrency must be 0 or 1");
   g_ctx.concurrent = on;
+  return RT_OK;
+}
+
+int rt_set_pipeline(int32_t slots) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (slots < 1 || slots > Context::kSlots) return fail(RT_ERR_INVALID_ARG, "pipeline slots must be in [1, %d]", Context::kSlots);
+  g_ctx.pipeline = slots;
   return RT_OK;
 }
 

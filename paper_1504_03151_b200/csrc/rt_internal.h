@@ -189,24 +189,25 @@ struct WfTiming {
   int launches;   // kernels launched (output)
   cudaEvent_t* shade = nullptr;  // [2 * cap] events around each wf_shade launch
   cudaEvent_t* accum = nullptr;  // [2 * cap] events around each wf_accumulate launch
-  // second stream: the shadow scan + accumulate of depth d run on it, concurrently with the
-  // closest-hit scan of depth d + 1 on the main stream (fork/join events per depth)
-  cudaStream_t side = nullptr;
-  cudaEvent_t* fork = nullptr;   // [max_depth + 1]
-  cudaEvent_t* join = nullptr;   // [max_depth + 1]
-  // chunk pipelining: odd chunks run on a second buffer set and stream pair, so one chunk's
-  // sparse deep depths overlap the next chunk's dense depth 0 (null = one chunk at a time)
-  WfBuffers* B2 = nullptr;
-  cudaStream_t main2 = nullptr, side2 = nullptr;
-  cudaEvent_t* fork2 = nullptr;
-  cudaEvent_t* join2 = nullptr;
-  cudaEvent_t start_ev = nullptr, done2_ev = nullptr;
+  // chunk pipelining: chunk i runs on slot i % nslots, each slot a buffer set with its own stream
+  // pair, so one chunk's sparse deep depths overlap the next chunks' dense depth 0. Within a slot,
+  // the shadow scan + accumulate of depth d run on the side stream, concurrently with the
+  // closest-hit scan of depth d + 1 on the main stream (fork/join events per depth; side = null:
+  // everything in order on the main stream). Slot 0's main stream is the caller's.
+  static constexpr int kMaxSlots = 4;
+  int nslots = 1;
+  WfBuffers* slot_B[kMaxSlots] = {};
+  cudaStream_t slot_main[kMaxSlots] = {}, slot_side[kMaxSlots] = {};
+  cudaEvent_t* slot_fork[kMaxSlots] = {};  // [max_depth + 1] each
+  cudaEvent_t* slot_join[kMaxSlots] = {};
+  cudaEvent_t start_ev = nullptr;           // the other slots start after the caller's prior work
+  cudaEvent_t slot_done[kMaxSlots] = {};    // the caller's stream resumes after every slot
   // optional: an event recorded after each chunk's resolve, and the work items resolved so far,
   // so the host can copy finished framebuffer rows while later chunks render
   // queue counters of the previous render with the same launch sequence, per buffer set (host
   // copies; null = unknown): each scan is then launched as one kernel, the long-queue scan or
   // its split variant, instead of the pair
-  const unsigned* hint[2] = {nullptr, nullptr};
+  const unsigned* hint[kMaxSlots] = {};
   cudaEvent_t* chunk_done = nullptr;
   int* chunk_items = nullptr;
   int chunk_cap = 0;
@@ -220,9 +221,10 @@ struct WfTiming {
 };
 // scene source of the wavefront intersection kernels: 0 global, 1 shared memory
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
-                                    int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st);
-int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined);
-int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined);
+                                    int num_sms, WfTiming& tm, cudaStream_t st);
+// work items (pixels) per chunk of a frame rendered over nslots buffer-set slots
+int wf_items_per_chunk(const DevParams& p, int nslots);
+int wf_timing_pairs(const DevParams& p, int nslots);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigned long long* stats, cudaStream_t st);

@@ -633,17 +633,25 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int gcap, int lt_list
   B.ctr = ctr;
 }
 
-// work items (pixels) per chunk: as many as the buffers hold; a pipelined render of a frame that
-// would fit one chunk is cut in two, so the two chunks can overlap (3 or 4 pipelined chunks were
-// 20 % slower at world 8: chunk k+2 waits for chunk k on the same buffer set)
-int wf_items_per_chunk(const DevParams& p, int cap_paths, bool pipelined) {
-  int items = cap_paths / p.spp;
-  if (pipelined && p.n_items <= items && (long long)p.n_items * p.spp >= (1 << 18)) items = (p.n_items + 1) / 2;
-  return items > 0 ? items : 1;
+// work items (pixels) per chunk: at most 2^22 paths per chunk; with nslots > 1 a frame that
+// would fill fewer chunks than slots is cut into nslots chunks (each >= 2^17 paths), so the chunks
+// overlap (DESIGN.md §7 "chunk pipelining")
+int wf_items_per_chunk(const DevParams& p, int nslots) {
+  const long long paths = (long long)p.n_items * p.spp;
+  const int max_items = (1 << 22) / p.spp > 0 ? (1 << 22) / p.spp : 1;
+  long long chunks = (p.n_items + max_items - 1) / max_items;
+  if (nslots > 1 && chunks < nslots) {
+    long long want = nslots;
+    while (want > 1 && paths / want < (1 << 17)) --want;
+    if (want > chunks) chunks = want;
+  }
+  if (chunks < 1) chunks = 1;
+  const long long items = (p.n_items + chunks - 1) / chunks;
+  return items > 0 ? (int)items : 1;
 }
 
-int wf_timing_pairs(const DevParams& p, int cap_paths, bool pipelined) {
-  const int items_per_chunk = wf_items_per_chunk(p, cap_paths, pipelined);
+int wf_timing_pairs(const DevParams& p, int nslots) {
+  const int items_per_chunk = wf_items_per_chunk(p, nslots);
   const int chunks = (p.n_items + items_per_chunk - 1) / items_per_chunk;
   return chunks * (p.max_depth + 1);
 }
@@ -657,8 +665,9 @@ constexpr int kLogicGridPerSm = 6;  // logic kernels: grid-stride loops (measure
                                     // 4 -> 7.00 / 1.10 ms, 6 -> 7.03 / 1.084, 8 -> 7.04 / 1.082)
 
 template <int kSrc>
-static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms,
-                          WfBuffers& B0, WfTiming& tm, cudaStream_t st0) {
+static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutputs& o, int num_sms, WfTiming& tm,
+                          cudaStream_t st0) {
+  WfBuffers& B0 = *tm.slot_B[0];
   const cudaStream_t st = st0;  // setup launches (debug fill) go on the caller's stream
   const bool dbg = o.dbg_hits != nullptr;
   const bool ext = p.n_emitters > 0 || p.integrator != 0;  // wf_shade with the NEXT-1/NEXT-2 paths
@@ -693,6 +702,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
   const int grid_l = num_sms * kLogicGridPerSm;
+  // grid for a hinted amount of work: twice the CTAs the hint needs (a stale hint costs speed,
+  // never results: every kernel loops over whatever its queue holds), at most the full grid
+  auto hinted_grid = [](unsigned work, unsigned per_cta, int full) -> int {
+    const unsigned long long want = 2ull * ((work + per_cta - 1) / per_cta);
+    return (int)(want < 1ull ? 1ull : (want < (unsigned long long)full ? want : (unsigned long long)full));
+  };
   // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length
   auto host_parts = [&](unsigned tasks, int grid) -> int {
     if (grid > B0.xctas) return 1;
@@ -704,8 +719,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
                             : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
   int* dh = dbg ? o.dbg_hits : nullptr;
   int* db = dbg ? o.dbg_bounces : nullptr;
-  const bool pipe = tm.B2 != nullptr;
-  const int items_per_chunk = wf_items_per_chunk(p, B0.cap, pipe);
+  const int nslots = tm.nslots;
+  const int items_per_chunk = wf_items_per_chunk(p, nslots);
   tm.n = 0;
   tm.launches = 0;
   tm.n_chunks = 0;
@@ -714,19 +729,19 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     launch(fill_int, num_sms * 8, 0, st, o.dbg_hits, nh, -2);
     ++tm.launches;
   }
-  if (pipe) {  // the second slot's streams start after everything issued on st so far
+  if (nslots > 1) {  // the other slots' streams start after everything issued on st so far
     cudaEventRecord(tm.start_ev, st);
-    cudaStreamWaitEvent(tm.main2, tm.start_ev, 0);
+    for (int k = 1; k < nslots; ++k) cudaStreamWaitEvent(tm.slot_main[k], tm.start_ev, 0);
   }
   int chunk = 0;
   for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk, ++chunk) {
-    const bool odd = pipe && (chunk & 1);
-    WfBuffers& Bset = odd ? *tm.B2 : B0;
-    const cudaStream_t st = odd ? tm.main2 : st0;
-    const cudaStream_t side = odd ? tm.side2 : tm.side;
-    cudaEvent_t* fork = odd ? tm.fork2 : tm.fork;
-    cudaEvent_t* join = odd ? tm.join2 : tm.join;
-    const unsigned* hint = tm.hint[odd ? 1 : 0];
+    const int sl = chunk % nslots;
+    WfBuffers& Bset = *tm.slot_B[sl];
+    const cudaStream_t st = sl == 0 ? st0 : tm.slot_main[sl];
+    const cudaStream_t side = tm.slot_side[sl];
+    cudaEvent_t* fork = tm.slot_fork[sl];
+    cudaEvent_t* join = tm.slot_join[sl];
+    const unsigned* hint = tm.hint[sl];
     WfBuffers Bc = Bset;  // this chunk's launches: the buffer set with the chunk's first sample
     Bc.g0 = (long long)w0 * p.spp;
     WfBuffers Bs = Bc;  // the copy passed to a single (solo) kernel launch
@@ -747,11 +762,14 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
         launch(kc0, grid_c, smem, st, p, sc, Bc, dd);
-      } else if (hint) {  // one kernel, chosen from the previous frame's queue
-        if (host_parts((hint[wf_ctr_q(dd)] + 31u) / 32u, grid_c) > 1)
-          launch(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
-        else
-          launch(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bs, dd);
+      } else if (hint) {  // one kernel, chosen from the previous frame's queue, on a grid sized to it
+        const unsigned tasks = (hint[wf_ctr_q(dd)] + 31u) / 32u;
+        const int parts = host_parts(tasks, grid_c);
+        WfBuffers Bp = Bs;
+        Bp.force_parts = parts;  // the device rule on the smaller grid would pick fewer parts
+        const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_c);
+        if (parts > 1) launch(wf_isect_split<kSrc, false>, g, smem, st, p, sc, Bp, dd);
+        else launch(wf_isect<kSrc, false>, g, smem, st, p, sc, Bs, dd);
       } else {  // the self-selecting pair: both read the queue length, exactly one works
         launch(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
         launch(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
@@ -765,7 +783,9 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      launch(shade, grid_l, 0, st, p, sc, Bc, d, g0, dh, db);
+      // logic kernels: grid-stride loops, on a grid sized to the hinted queue (no hint: full grid)
+      const int grid_q = hint ? hinted_grid(hint[wf_ctr_q(d)], 256u, grid_l) : grid_l;
+      launch(shade, grid_q, 0, st, p, sc, Bc, d, g0, dh, db);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       cudaStream_t ss = st;
       if (side) {
@@ -779,7 +799,11 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         if (hint) {
           unsigned chunks = 0;
           for (int i = 0; i < p.lt_lights * kLtSub; ++i) chunks += (hint[wf_ctr_lt(d, 0, 0) + i] + 63u) / 64u;
-          launch(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
+          const int parts = host_parts(chunks, grid_lt);
+          WfBuffers Bp = Bs;
+          Bp.force_parts = parts;
+          launch(parts > 1 ? klts : klt, hinted_grid(chunks * (unsigned)parts, 8u, grid_lt), smem_lt, ss, p, sc,
+                 parts > 1 ? Bp : Bs, d);
           scan_launches += 1;
         } else {
           launch(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
@@ -789,11 +813,13 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       }
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
         if (hint) {
-          const unsigned ns = hint[wf_ctr_so(d)];
-          if (host_parts((ns + 31u) / 32u, grid_s) > 1)
-            launch(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
-          else
-            launch(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bs, d);
+          const unsigned tasks = (hint[wf_ctr_so(d)] + 31u) / 32u;
+          const int parts = host_parts(tasks, grid_s);
+          WfBuffers Bp = Bs;
+          Bp.force_parts = parts;
+          const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_s);
+          if (parts > 1) launch(wf_isect_split<kSrc, true>, g, smem, ss, p, sc, Bp, d);
+          else launch(wf_isect<kSrc, true>, g, smem, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
           launch(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
@@ -805,8 +831,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       // wf_accumulate<false> when no entry aims at an emitter and wf_shade skips the skip2
       // column (the same condition as there: no extensions, light-origin scans on)
       if (rec && tm.accum) tm.record(tm.accum[2 * ti], ss);
-      if (ext || p.lt_lights == 0) launch(wf_accumulate<true>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
-      else launch(wf_accumulate<false>, grid_l, 0, ss, p, sc, Bc, d, o.stats);
+      if (ext || p.lt_lights == 0) launch(wf_accumulate<true>, grid_q, 0, ss, p, sc, Bc, d, o.stats);
+      else launch(wf_accumulate<false>, grid_q, 0, ss, p, sc, Bc, d, o.stats);
       if (rec && tm.accum) tm.record(tm.accum[2 * ti + 1], ss);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
@@ -825,17 +851,17 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       ++tm.n_chunks;
     }
   }
-  if (pipe) {  // the caller's stream resumes after the second slot's last chunk
-    cudaEventRecord(tm.done2_ev, tm.main2);
-    cudaStreamWaitEvent(st0, tm.done2_ev, 0);
+  for (int k = 1; k < nslots; ++k) {  // the caller's stream resumes after every slot's last chunk
+    cudaEventRecord(tm.slot_done[k], tm.slot_main[k]);
+    cudaStreamWaitEvent(st0, tm.slot_done[k], 0);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
-                                    int num_sms, WfBuffers& B, WfTiming& tm, cudaStream_t st) {
-  if (src == SRC_SMEM) return wf_run<SRC_SMEM>(p, sc, o, num_sms, B, tm, st);
-  return wf_run<SRC_GLOBAL>(p, sc, o, num_sms, B, tm, st);
+                                    int num_sms, WfTiming& tm, cudaStream_t st) {
+  if (src == SRC_SMEM) return wf_run<SRC_SMEM>(p, sc, o, num_sms, tm, st);
+  return wf_run<SRC_GLOBAL>(p, sc, o, num_sms, tm, st);
 }
 
 }  // namespace rt

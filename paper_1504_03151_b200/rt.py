@@ -80,6 +80,7 @@ def lib() -> C.CDLL:
         "rt_tonemap_rgba8": [vp, vp, i64, C.c_float, C.c_float],
         "rt_set_integrator": [i32, i32],
         "rt_set_concurrency": [i32],
+        "rt_set_pipeline": [i32],
         "rt_set_graphs": [i32],
         "rt_set_scan_split": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
@@ -171,6 +172,11 @@ def set_variant(name: str):
 def set_concurrency(on: bool):
     """Wavefront: shadow scans concurrent with the next closest scan (default) or all in order."""
     _check("rt_set_concurrency", lib().rt_set_concurrency(1 if on else 0))
+
+
+def set_pipeline(slots: int = 2):
+    """Wavefront: chunk pipelining over 1..4 buffer-set slots (default 2)."""
+    _check("rt_set_pipeline", lib().rt_set_pipeline(int(slots)))
 
 
 def set_graphs(on: bool):

@@ -62,6 +62,47 @@ def test_forced_split_is_bit_identical(name, frame):
                 assert st == ref[3], (split, graphs)
 
 
+@pytest.mark.parametrize("name,frame,world", [("C4", dict(width=480, height=270, spp=4), 1),
+                                              ("C4", dict(width=960, height=540, spp=4), 8)])
+def test_pipeline_slots_bit_identical(name, frame, world):
+    """Chunk pipelining over 1..4 buffer-set slots (rt_set_pipeline) renders the same frame / shard
+    bit for bit, with the same statistics, launched stream by stream and replayed as a graph."""
+    import torch
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get(name).with_frame(**frame)
+    W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
+    rt.set_variant("wavefront")
+    rt.load_scene(sc)
+    tpr, sb = rt.shard_layout(W, H, world)
+    ref = None
+    try:
+        for slots in (1, 2, 3, 4):
+            rt.set_pipeline(slots)
+            rt.set_graphs(True)
+            for rank in (0, world - 1):
+                slab = torch.zeros(sb, dtype=torch.uint8, device="cuda")
+                outs = []
+                for _ in range(3):  # plain, capture, replay
+                    rt.render_shard(W, H, D, S, rank, world, slab)
+                    st = rt.stats()
+                    torch.cuda.synchronize()
+                    outs.append((slab.clone(), {k: st[k] for k in KEYS}))
+                for o, st in outs:
+                    key = (rank,)
+                    if ref is None:
+                        ref = {}
+                    if key not in ref:
+                        ref[key] = (o, st)
+                    assert torch.equal(o, ref[key][0]), (slots, rank)
+                    assert st == ref[key][1], (slots, rank)
+        with pytest.raises(rt.RtError):
+            rt.set_pipeline(0)
+        with pytest.raises(rt.RtError):
+            rt.set_pipeline(5)
+    finally:
+        rt.set_pipeline(2)
+
+
 def test_invalid_split_rejected():
     from paper_1504_03151_b200 import rt
     for bad in (0, 3, 16, -2):

@@ -3,7 +3,9 @@
 renders launch stream by stream, later ones replay the captured CUDA graph), timed with CUDA
 events (median of the timed repeats). Predicts the strong-scaling efficiency before any
 collective: eff(N) = T(1) / (N * max_rank T_rank(N)). Tool only.
-Usage: python tools/shard_scaling.py [C4] [--no-graphs]"""
+Usage: python tools/shard_scaling.py [C4] [--no-graphs] [--variant wavefront|megakernel|auto]
+       [--worlds 1,2,4,8]"""
+import argparse
 import os
 import sys
 
@@ -13,14 +15,23 @@ import torch  # noqa: E402
 import scenegen  # noqa: E402
 from paper_1504_03151_b200 import rt  # noqa: E402
 
-args = [a for a in sys.argv[1:] if not a.startswith("--")]
-name = args[0] if args else "C4"
-rt.set_graphs("--no-graphs" not in sys.argv)
+ap = argparse.ArgumentParser()
+ap.add_argument("config", nargs="?", default="C4")
+ap.add_argument("--no-graphs", action="store_true")
+ap.add_argument("--variant", default="auto")
+ap.add_argument("--worlds", default="1,2,4,8")
+ap.add_argument("--pipeline", type=int, default=0, help="rt_set_pipeline slots (0: library default)")
+a = ap.parse_args()
+if a.pipeline:
+    rt.set_pipeline(a.pipeline)
+name = a.config
+rt.set_graphs(not a.no_graphs)
+rt.set_variant(a.variant)
 sc = scenegen.get(name)
 rt.load_scene(sc)
 W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
 base = None
-for world in (1, 2, 4, 8):
+for world in [int(x) for x in a.worlds.split(",")]:
     tpr, sb = rt.shard_layout(W, H, world)
     slab = torch.empty(sb // 4, dtype=torch.float32, device="cuda")
     ts = []
@@ -37,6 +48,8 @@ for world in (1, 2, 4, 8):
             reps.append(e0.elapsed_time(e1))
         ts.append(sorted(reps)[2])
     worst = max(ts)
-    base = base or worst
-    print(f"{name} world={world}: rank times ms min {min(ts):.3f} max {worst:.3f} -> predicted efficiency "
-          f"{base / (world * worst):.3f}", flush=True)
+    if world == 1:
+        base = worst
+    eff = f"{base / (world * worst):.3f}" if base else "n/a (no world-1 run)"
+    print(f"{name} [{a.variant}{f' pipeline {a.pipeline}' if a.pipeline else ''}] world={world}: rank times ms min {min(ts):.3f} max {worst:.3f} -> predicted "
+          f"efficiency {eff}", flush=True)
