@@ -184,6 +184,12 @@ int rt_set_concurrency(int32_t on);
  * every value. RT_ERR_INVALID_ARG outside 1..4. */
 int rt_set_pipeline(int32_t slots);
 
+/* Wavefront kernels, scenes beyond RT_SMEM_SPHERES (the shared-memory budget): 1 (default) the
+ * long-queue scans stream the sphere pairs through a ring of two TMA-loaded 16 KB tiles per CTA
+ * (cp.async.bulk on mbarriers, a copy in flight while the warps scan the other tile); 0 reads them
+ * from global memory (A/B knob). Same results bit for bit. RT_ERR_INVALID_ARG unless 0/1. */
+int rt_set_tiled_scan(int32_t on);
+
 /* Wavefront kernels: 1 (default) replays a CUDA graph of the launch sequence. The sequence of a
  * render (frame or shard size, max_depth, spp, output pointers, buffers, concurrency) is captured
  * the second time it is requested within the last 8 renders and replayed whenever it comes again

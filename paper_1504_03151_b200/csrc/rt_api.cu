@@ -125,6 +125,7 @@ struct Context {
   // consecutive renders with the same launch key, replayed while the key stays the same
   int graphs = 1;
   int scan_split = -1;  // rt_set_scan_split
+  int tiled = 1;        // scenes beyond shared memory: TMA-tiled scans (1) or global loads (0; A/B)
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
   cudaEvent_t ev_cap = nullptr;
   // a few instantiated graphs, one per launch key (e.g. frames alternating between two output
@@ -450,7 +451,8 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
       tm.chunk_cap = max_chunks;
     }
     CU(cudaEventRecord(c.ev0, c.stream), "cudaEventRecord");
-    const int src = c.smem_scene ? 1 : 0;
+    // the scans' scene source: staged whole in shared memory, else streamed in TMA tiles
+    const int src = c.smem_scene ? 1 : (c.tiled ? 2 : 0);
     {
       const int lrc = launch_wavefront(c, p, sc, o, src, tm);
       if (lrc) return lrc;
@@ -669,6 +671,14 @@ int rt_set_pipeline(int32_t slots) {
   if (rc) return rc;
   if (slots < 1 || slots > Context::kSlots) return fail(RT_ERR_INVALID_ARG, "pipeline slots must be in [1, %d]", Context::kSlots);
   g_ctx.pipeline = slots;
+  return RT_OK;
+}
+
+int rt_set_tiled_scan(int32_t on) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (on != 0 && on != 1) return fail(RT_ERR_INVALID_ARG, "tiled scan must be 0 or 1");
+  g_ctx.tiled = on;
   return RT_OK;
 }
 

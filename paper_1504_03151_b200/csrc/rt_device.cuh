@@ -135,7 +135,7 @@ __device__ __forceinline__ d3 reflect(d3 d, d3 n) { return d - n * (2.0 * dot(d,
 // The pair array (32 B per two spheres) is copied into dynamic shared memory with
 // cp.async.bulk (UBLKCP) completing on an mbarrier; every warp then reads each pair as a
 // warp-uniform LDS.128 broadcast. Scenes larger than the shared-memory budget stay in global
-// memory (uniform LDG through L1).
+// memory in TMA-loaded tiles (SRC_TILE below).
 __device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pairs, uint32_t bytes,
                                             uint64_t* mbar) {
   const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
@@ -167,13 +167,46 @@ __device__ __forceinline__ void stage_scene(float4* s_pairs, const float4* g_pai
 // ---- intersection (a3 closest-hit + a5 any-hit), one loop for the whole warp -----------------
 extern __shared__ float4 s_pairs[];
 
-// where the sphere-pair array is read from inside the scans
-enum : int { SRC_GLOBAL = 0, SRC_SMEM = 1 };
+// where the sphere-pair array is read from inside the scans: the whole scene staged in shared
+// memory (SRC_SMEM), a ring of two TMA-loaded tiles of kTilePairs pairs in shared memory for
+// scenes beyond the shared-memory budget (SRC_TILE: global float4 index i lives at ring slot
+// i mod 4 kTilePairs while its tile is resident), or global memory (SRC_GLOBAL: the short-queue
+// split scans of such scenes)
+enum : int { SRC_GLOBAL = 0, SRC_SMEM = 1, SRC_TILE = 2 };
+constexpr int kTilePairs = 512;  // 16 KB per tile, two tiles in flight per CTA
 
 template <int kSrc>
 __device__ __forceinline__ float4 load_pair(const float4* __restrict__ gp, int i) {
   if constexpr (kSrc == SRC_SMEM) return s_pairs[i];  // warp-uniform address: LDS.128 broadcast
+  else if constexpr (kSrc == SRC_TILE) return s_pairs[i & (4 * kTilePairs - 1)];
   else return __ldg(gp + i);
+}
+
+// ---- tiled staging for scenes beyond shared memory: TMA bulk copies completing on mbarriers ----
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: copy `bytes` (multiple of 16, <= 32 KB) from global to shared memory, completing on mbar
+__device__ __forceinline__ void tile_load(float4* dst, const float4* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(mb), "r"(parity)
+        : "memory");
+  }
 }
 
 // Exact decision for one sphere (float64, from the float inputs): smallest root >= EPS_T of

@@ -671,12 +671,19 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const cudaStream_t st = st0;  // setup launches (debug fill) go on the caller's stream
   const bool dbg = o.dbg_hits != nullptr;
   const bool ext = p.n_emitters > 0 || p.integrator != 0;  // wf_shade with the NEXT-1/NEXT-2 paths
+  // SRC_TILE (scenes beyond shared memory): the long-queue scans stream TMA tiles; the camera-ray
+  // scan and the short-queue split scans read the pairs from global memory
+  constexpr int kScan = kSrc == SRC_TILE ? SRC_GLOBAL : kSrc;
   const size_t smem = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 32u : 0u;
+  const size_t smem_long = kSrc == SRC_TILE ? (size_t)2 * kTilePairs * 32u : smem;
   cudaError_t e;
   int occ_c = 0, occ_s = 0;
   using IsectFn = void (*)(const DevParams, const DevScene, WfBuffers, int);
+  const IsectFn kcl = kSrc == SRC_TILE ? (IsectFn)wf_isect_tiled<false> : (IsectFn)wf_isect<kScan, false>;
+  const IsectFn ksl = kSrc == SRC_TILE ? (IsectFn)wf_isect_tiled<true> : (IsectFn)wf_isect<kScan, true>;
   // camera rays (depth 0): two per thread through the shared-origin filter on the eye's pair table
-  const IsectFn kc0 = wf_isect_eye2<kSrc>;
+  const IsectFn kc0 = kSrc == SRC_TILE ? (IsectFn)wf_isect_eye2_tiled : (IsectFn)wf_isect_eye2<kScan>;
+  const size_t smem_eye = smem_long;
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
   size_t smem_lt = 0;
@@ -693,13 +700,16 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       grid_lt = num_sms * (occ > 0 ? occ : 1);
     }
   }
-  for (auto fn : {(IsectFn)wf_isect<kSrc, false>, (IsectFn)wf_isect<kSrc, true>, kc0, (IsectFn)wf_isect_split<kSrc, false>,
-                  (IsectFn)wf_isect_split<kSrc, true>}) {
+  for (auto fn : {(IsectFn)wf_isect_split<kScan, false>, (IsectFn)wf_isect_split<kScan, true>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, wf_isect<kSrc, false>, 256, smem)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, wf_isect<kSrc, true>, 256, smem)) != cudaSuccess) return e;
+  for (auto fn : {kcl, ksl, kc0}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_long > 0 ? smem_long : 1));
+    if (e != cudaSuccess) return e;
+  }
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kcl, 256, smem_long)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, ksl, 256, smem_long)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
   const int grid_l = num_sms * kLogicGridPerSm;
   // grid for a hinted amount of work: twice the CTAs the hint needs (a stale hint costs speed,
@@ -761,18 +771,18 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const bool rec = ti < tm.cap;
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
-        launch(kc0, grid_c, smem, st, p, sc, Bc, dd);
+        launch(kc0, grid_c, smem_eye, st, p, sc, Bc, dd);
       } else if (hint) {  // one kernel, chosen from the previous frame's queue, on a grid sized to it
         const unsigned tasks = (hint[wf_ctr_q(dd)] + 31u) / 32u;
         const int parts = host_parts(tasks, grid_c);
         WfBuffers Bp = Bs;
         Bp.force_parts = parts;  // the device rule on the smaller grid would pick fewer parts
         const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_c);
-        if (parts > 1) launch(wf_isect_split<kSrc, false>, g, smem, st, p, sc, Bp, dd);
-        else launch(wf_isect<kSrc, false>, g, smem, st, p, sc, Bs, dd);
+        if (parts > 1) launch(wf_isect_split<kScan, false>, g, smem, st, p, sc, Bp, dd);
+        else launch(kcl, g, smem_long, st, p, sc, Bs, dd);
       } else {  // the self-selecting pair: both read the queue length, exactly one works
-        launch(wf_isect<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
-        launch(wf_isect_split<kSrc, false>, grid_c, smem, st, p, sc, Bc, dd);
+        launch(kcl, grid_c, smem_long, st, p, sc, Bc, dd);
+        launch(wf_isect_split<kScan, false>, grid_c, smem, st, p, sc, Bc, dd);
         tm.launches += 1;
       }
       tm.launches += 1;
@@ -818,12 +828,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
           WfBuffers Bp = Bs;
           Bp.force_parts = parts;
           const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_s);
-          if (parts > 1) launch(wf_isect_split<kSrc, true>, g, smem, ss, p, sc, Bp, d);
-          else launch(wf_isect<kSrc, true>, g, smem, ss, p, sc, Bs, d);
+          if (parts > 1) launch(wf_isect_split<kScan, true>, g, smem, ss, p, sc, Bp, d);
+          else launch(ksl, g, smem_long, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch(wf_isect<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
-          launch(wf_isect_split<kSrc, true>, grid_s, smem, ss, p, sc, Bc, d);
+          launch(ksl, grid_s, smem_long, ss, p, sc, Bc, d);
+          launch(wf_isect_split<kScan, true>, grid_s, smem, ss, p, sc, Bc, d);
           scan_launches += 2;
         }
       }
@@ -861,6 +871,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfTiming& tm, cudaStream_t st) {
   if (src == SRC_SMEM) return wf_run<SRC_SMEM>(p, sc, o, num_sms, tm, st);
+  if (src == SRC_TILE) return wf_run<SRC_TILE>(p, sc, o, num_sms, tm, st);
   return wf_run<SRC_GLOBAL>(p, sc, o, num_sms, tm, st);
 }
 

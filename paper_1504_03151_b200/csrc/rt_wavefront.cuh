@@ -541,6 +541,125 @@ wf_isect_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
   wf_isect_split_body<kSrc, kShadow>(P, S, B, d);
 }
 
+// The ring of two TMA-loaded tiles of the pair array (SRC_TILE) a CTA streams through: tile t
+// lives in buffer t & 1 (ring slot i mod 4 kTilePairs of global float4 index i), its copy completes
+// on mbarrier t & 1; the barrier phases are tracked per buffer in registers (CTA-uniform).
+struct TileRing {
+  uint64_t* full;  // [2] mbarriers in shared memory
+  const float4* gp;
+  int n_pairs, ntiles;
+  uint32_t phases;  // bit b: the parity the next completion of buffer b's barrier will have
+  __device__ __forceinline__ void init(uint64_t* bars, const float4* g, int np) {  // every thread
+    full = bars;
+    gp = g;
+    n_pairs = np;
+    ntiles = (np + kTilePairs - 1) / kTilePairs;
+    phases = 0u;
+    if (threadIdx.x == 0) {
+      mbar_init(&full[0]);
+      mbar_init(&full[1]);
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ int begin(int t) const { return t * kTilePairs; }
+  __device__ __forceinline__ int end(int t) const {
+    return (t + 1) * kTilePairs < n_pairs ? (t + 1) * kTilePairs : n_pairs;
+  }
+  __device__ __forceinline__ void issue(int t) const {  // one thread
+    tile_load(s_pairs + 2 * kTilePairs * (t & 1), gp + 2 * begin(t), (uint32_t)(end(t) - begin(t)) * 32u, &full[t & 1]);
+  }
+  __device__ __forceinline__ void wait(int t) {  // every thread
+    mbar_wait(&full[t & 1], (phases >> (t & 1)) & 1u);
+    phases ^= 1u << (t & 1);
+  }
+};
+
+// ---- a3 / a5 for scenes beyond shared memory: the scan over TMA-loaded tiles ------------------
+// A CTA takes 256 rays (8 warps x 32) and streams the pair array through a ring of two tiles of
+// kTilePairs pairs: one elected thread issues the bulk copy of tile t + 2 into the buffer tile t
+// used as soon as every warp is done with it (CTA barrier), so a copy is in flight while the warps
+// scan the other tile. Every warp runs the same FP32 filter over the tile as the staged kernels
+// (isect_scan), so candidate lists, robust occluders and every decision are those of wf_isect.
+// Shadow rays: the CTA stops streaming once none of its rays is active (Alg. 1 `break`).
+template <bool kShadow>
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
+wf_isect_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  __shared__ uint64_t s_full[2];
+  __shared__ unsigned s_task;
+  const unsigned n = kShadow ? B.ctr[wf_ctr_so(d)] : B.ctr[wf_ctr_q(d)];
+  if (!B.solo && split_parts((n + 31u) / 32u, B) > 1) return;  // a short queue: wf_isect_split scans it
+  if ((unsigned long long)blockIdx.x * blockDim.x >= n) return;
+  const float4* gp = S.pairs;
+  TileRing ring;
+  ring.init(s_full, gp, P.n_pairs_pad);
+  const int ntiles = ring.ntiles;
+  unsigned* work = B.ctr + (kShadow ? wf_ctr_ws(d) : wf_ctr_wc(d));
+  const WfQueue Q = B.q[d & 1];
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_task = atomicAdd(work, 256u);
+      ring.issue(0);  // the previous task drained every copy it issued: both buffers are free
+      if (ntiles > 1) ring.issue(1);
+    }
+    __syncthreads();
+    const unsigned e = s_task + threadIdx.x;
+    const bool task_ok = s_task < n;  // CTA-uniform
+    if (!task_ok) {  // drain the copies just issued (the ring must be idle when the kernel exits)
+      ring.wait(0);
+      if (ntiles > 1) ring.wait(1);
+      break;
+    }
+    bool act = e < n;
+    const bool mine = act;
+    d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+    double tl = 0.0;
+    int rob = -1, skip = -1, skip2 = -1;
+    if (act) {
+      if constexpr (kShadow) {
+        o = ld3(B.sray, B.gcap, (int)e, 0);
+        dir = ld3(B.sray, B.gcap, (int)e, 3);
+        tl = B.sray[6 * (size_t)B.gcap + e];
+        skip = B.sskip[e];
+        skip2 = B.sskip2[e];
+        for (int j = 0; j < P.n_planes; ++j) {  // planes first, exactly (FP64), in index order
+          const DevPlane pl = c_planes[j];
+          const double den = pl.nx * dir.x + pl.ny * dir.y + pl.nz * dir.z;
+          if (fabs(den) >= 1e-12) {
+            const double t = (pl.d - (pl.nx * o.x + pl.ny * o.y + pl.nz * o.z)) / den;
+            if (t >= kEps && t < tl) { rob = -2 - j; act = false; break; }
+          }
+        }
+      } else {
+        o = q_origin(P, Q, B.cap, e, d);
+        if (!q_dir(P, B, Q, e, d, dir)) act = false;  // outside the image: no candidates
+        skip = q_skip(Q, e, d);
+      }
+    }
+    RayFilter F;
+    F.init(o, dir, P);
+    float tub = 3.0e38f;
+    int nc = 0;
+    int* cand_row = (kShadow ? B.scand : B.ccand) + (size_t)(mine ? e : 0u) * kCandMax;
+    for (int t = 0; t < ntiles; ++t) {
+      ring.wait(t);
+      isect_scan<SRC_TILE, kShadow>(P, S, gp, F, ring.begin(t), ring.end(t), act, skip, skip2, (float)tl, tub, nc, rob,
+                                    cand_row, nullptr);
+      const bool any_left = kShadow ? (__syncthreads_or(act) != 0) : (__syncthreads(), true);  // buffer t & 1 is free
+      if (any_left) {
+        if (threadIdx.x == 0 && t + 2 < ntiles) ring.issue(t + 2);
+      } else {  // every ray of the CTA is settled: wait for the copy still in flight, then stop
+        if (t + 1 < ntiles) ring.wait(t + 1);
+        break;
+      }
+    }
+    if (mine) {
+      (kShadow ? B.sn : B.cn)[e] = nc;
+      if constexpr (kShadow) B.srob[e] = rob;
+    }
+    __syncthreads();  // s_task and the ring are reused by the next task
+  }
+}
+
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
 // The shared-origin filter needs 4 FMA per sphere, so one ray per thread leaves the kernel
 // co-limited by the shared-memory pipe (2 LDS.128 per 2 spheres). Here every lane carries two
@@ -583,6 +702,53 @@ __device__ __forceinline__ void eye_candidates(const DevParams& P, const float4*
   }
 }
 
+// the shared-origin scan of two camera rays (one thread) over the sphere pairs [pb, pe)
+template <int kSrc>
+__device__ __forceinline__ void eye2_scan(const DevParams& P, const float4* __restrict__ gp, int pb, int pe, EyeRay& Ra,
+                                          EyeRay& Rb, int* rowa, int* rowb) {
+  const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
+  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+  const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
+  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
+  for (int base = pb; base < pe; base += kEyePB) {
+    float2 va[kEyePB], vb[kEyePB];
+#pragma unroll
+    for (int i = 0; i < kEyePB; ++i) {
+      const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
+      const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
+      const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
+      const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
+      const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
+      const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
+      va[i] = __ffma2_rn(ta, ta, S1);
+      vb[i] = __ffma2_rn(tb, tb, S1);
+    }
+    float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+#pragma unroll
+    for (int i = 1; i < kEyePB; ++i) {
+      ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
+      mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+    }
+    const bool ca = Ra.act && ma >= Ra.F.cut, cb = Rb.act && mb >= Rb.F.cut;
+    if (__any_sync(kFull, ca || cb)) {
+      if (ca) {
+        unsigned m = 0u;
+#pragma unroll
+        for (int i = 0; i < kEyePB; ++i)
+          m |= ((va[i].x >= Ra.F.cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= Ra.F.cut) ? 1u : 0u) << (2 * i + 1);
+        eye_candidates<kSrc>(P, gp, m, 2 * base, Ra, rowa);
+      }
+      if (cb) {
+        unsigned m = 0u;
+#pragma unroll
+        for (int i = 0; i < kEyePB; ++i)
+          m |= ((vb[i].x >= Rb.F.cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= Rb.F.cut) ? 1u : 0u) << (2 * i + 1);
+        eye_candidates<kSrc>(P, gp, m, 2 * base, Rb, rowb);
+      }
+    }
+  }
+}
+
 template <int kSrc>
 __global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -613,49 +779,65 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
     }
     Ra.tub = Rb.tub = 3.0e38f;
     Ra.nc = Rb.nc = 0;
-    const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
-    const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
-    const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
-    const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
-    for (int base = 0; base < P.n_pairs_pad; base += kEyePB) {
-      float2 va[kEyePB], vb[kEyePB];
-#pragma unroll
-      for (int i = 0; i < kEyePB; ++i) {
-        const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
-        const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-        const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-        const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
-        const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
-        const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
-        va[i] = __ffma2_rn(ta, ta, S1);
-        vb[i] = __ffma2_rn(tb, tb, S1);
-      }
-      float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
-#pragma unroll
-      for (int i = 1; i < kEyePB; ++i) {
-        ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
-        mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
-      }
-      const bool ca = Ra.act && ma >= Ra.F.cut, cb = Rb.act && mb >= Rb.F.cut;
-      if (__any_sync(kFull, ca || cb)) {
-        if (ca) {
-          unsigned m = 0u;
-#pragma unroll
-          for (int i = 0; i < kEyePB; ++i)
-            m |= ((va[i].x >= Ra.F.cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= Ra.F.cut) ? 1u : 0u) << (2 * i + 1);
-          eye_candidates<kSrc>(P, gp, m, 2 * base, Ra, B.ccand + (size_t)ea * kCandMax);
-        }
-        if (cb) {
-          unsigned m = 0u;
-#pragma unroll
-          for (int i = 0; i < kEyePB; ++i)
-            m |= ((vb[i].x >= Rb.F.cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= Rb.F.cut) ? 1u : 0u) << (2 * i + 1);
-          eye_candidates<kSrc>(P, gp, m, 2 * base, Rb, B.ccand + (size_t)eb * kCandMax);
-        }
-      }
+    eye2_scan<kSrc>(P, gp, 0, P.n_pairs_pad, Ra, Rb, B.ccand + (size_t)ea * kCandMax, B.ccand + (size_t)eb * kCandMax);
+    if (ea < n) B.cn[ea] = Ra.nc;
+    if (eb < n) B.cn[eb] = Rb.nc;
+  }
+}
+
+// camera rays of scenes beyond shared memory: the same two-rays-per-thread scan over the eye's
+// pair table streamed through the TMA tile ring; a CTA takes 512 rays (8 warps x 64)
+__global__ void __launch_bounds__(256, kIsectMinBlocks)
+wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
+  __shared__ uint64_t s_full[2];
+  __shared__ unsigned s_task;
+  const unsigned n = B.ctr[wf_ctr_q(d)];
+  if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
+  const float4* gp = S.pairs_eye;
+  TileRing ring;
+  ring.init(s_full, gp, P.n_pairs_pad);
+  const int ntiles = ring.ntiles;
+  unsigned* work = B.ctr + wf_ctr_wc(d);
+  const WfQueue Q = B.q[d & 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_task = atomicAdd(work, 512u);
+      ring.issue(0);
+      if (ntiles > 1) ring.issue(1);
+    }
+    __syncthreads();
+    const unsigned e0 = s_task + 64u * warp;
+    if (s_task >= n) {  // CTA-uniform: drain the copies just issued
+      ring.wait(0);
+      if (ntiles > 1) ring.wait(1);
+      break;
+    }
+    const unsigned ea = e0 + lane, eb = e0 + 32 + lane;
+    EyeRay Ra, Rb;
+    {
+      d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
+      Ra.act = ea < n;
+      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); Ra.act = q_dir(P, B, Q, ea, d, dir); }
+      Ra.F.init(o, dir, P);
+      o = mk(0, 0, 0); dir = mk(0, 0, 1);
+      Rb.act = eb < n;
+      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
+      Rb.F.init(o, dir, P);
+    }
+    Ra.tub = Rb.tub = 3.0e38f;
+    Ra.nc = Rb.nc = 0;
+    int* rowa = B.ccand + (size_t)(ea < n ? ea : 0u) * kCandMax;
+    int* rowb = B.ccand + (size_t)(eb < n ? eb : 0u) * kCandMax;
+    for (int t = 0; t < ntiles; ++t) {
+      ring.wait(t);
+      eye2_scan<SRC_TILE>(P, gp, ring.begin(t), ring.end(t), Ra, Rb, rowa, rowb);
+      __syncthreads();  // buffer t & 1 is free
+      if (threadIdx.x == 0 && t + 2 < ntiles) ring.issue(t + 2);
     }
     if (ea < n) B.cn[ea] = Ra.nc;
     if (eb < n) B.cn[eb] = Rb.nc;
+    __syncthreads();  // s_task and the ring are reused by the next task
   }
 }
 

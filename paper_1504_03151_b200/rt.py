@@ -81,6 +81,7 @@ def lib() -> C.CDLL:
         "rt_set_integrator": [i32, i32],
         "rt_set_concurrency": [i32],
         "rt_set_pipeline": [i32],
+        "rt_set_tiled_scan": [i32],
         "rt_set_graphs": [i32],
         "rt_set_scan_split": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
@@ -172,6 +173,11 @@ def set_variant(name: str):
 def set_concurrency(on: bool):
     """Wavefront: shadow scans concurrent with the next closest scan (default) or all in order."""
     _check("rt_set_concurrency", lib().rt_set_concurrency(1 if on else 0))
+
+
+def set_tiled_scan(on: bool):
+    """Scenes beyond shared memory: scans over TMA-loaded tiles (default) or global loads."""
+    _check("rt_set_tiled_scan", lib().rt_set_tiled_scan(1 if on else 0))
 
 
 def set_pipeline(slots: int = 2):
