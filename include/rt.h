@@ -190,6 +190,19 @@ int rt_set_pipeline(int32_t slots);
  * from global memory (A/B knob). Same results bit for bit. RT_ERR_INVALID_ARG unless 0/1. */
 int rt_set_tiled_scan(int32_t on);
 
+/* Test support. Schedule fuzzing: seed != 0 makes every later wavefront render that is launched
+ * kernel by kernel (not a graph replay) insert short spin kernels of pseudo-random length (0-40
+ * us, drawn from the seed) on its streams at every fork, join and slot start, so the concurrent
+ * kernels interleave differently; a missing stream dependency then shows up as a different frame
+ * (the results must equal the in-order render bit for bit). 0 (default) turns it off. */
+int rt_set_schedule_jitter(uint64_t seed);
+
+/* Test support. In a library built with -DRT_CHECKS=1 (build.py --checks) every kernel checks its
+ * queue, list and slot indices and capacities; *first_failed receives the id of the first check
+ * that failed since the last call (0 = none) and the record is cleared; *compiled = 1. In the
+ * default build the checks are compiled out: *first_failed = 0, *compiled = 0. */
+int rt_check_status(uint32_t* first_failed, int32_t* compiled);
+
 /* Wavefront kernels: 1 (default) replays a CUDA graph of the launch sequence. The sequence of a
  * render (frame or shard size, max_depth, spp, output pointers, buffers, concurrency) is captured
  * the second time it is requested within the last 8 renders and replayed whenever it comes again

@@ -42,6 +42,16 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+CHECKED_LIB = os.path.join(HERE, "libb200rt_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The checked build (-DRT_CHECKS=1): every kernel checks its queue / list / slot indices and
+    capacities and records the first failure (rt_check_status). Test support (compute-sanitizer
+    is not available on this pool)."""
+    return build(force=force, out=CHECKED_LIB, defines=("RT_CHECKS=1",))
+
+
 FFMA2_PEAK_SRC = os.path.join(ROOT, "tools", "micro", "ffma2_peak.cu")
 FFMA2_PEAK_BIN = os.path.join(ROOT, "tools", "micro", "ffma2_peak")
 

@@ -126,6 +126,7 @@ struct Context {
   int graphs = 1;
   int scan_split = -1;  // rt_set_scan_split
   int tiled = 1;        // scenes beyond shared memory: TMA-tiled scans (1) or global loads (0; A/B)
+  unsigned long long jitter = 0;  // rt_set_schedule_jitter: generator state (0 = off)
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream cannot be captured)
   cudaEvent_t ev_cap = nullptr;
   // a few instantiated graphs, one per launch key (e.g. frames alternating between two output
@@ -327,6 +328,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   // when the launches overlap (their per-launch times would share the GPU anyway)
   if (c.concurrent) tm.cap = 0;
   tm.ext_events = true;
+  tm.jitter = 0;  // a captured graph keeps no spins
   CU(cudaStreamBeginCapture(c.cap_stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
   const cudaError_t le = rt::launch_render_wavefront(p, sc, o, src, c.num_sms, tm, c.cap_stream);
   cudaGraph_t g = nullptr;
@@ -436,6 +438,7 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     tm.cap = pairs;
     tm.shade = c.ev_h.data();
     tm.accum = c.ev_a.data();
+    tm.jitter = c.jitter;
     const bool overlap = host_out != nullptr && p.mode == 0;
     if (overlap) {
       const int max_chunks = n_chunks;
@@ -671,6 +674,26 @@ int rt_set_pipeline(int32_t slots) {
   if (rc) return rc;
   if (slots < 1 || slots > Context::kSlots) return fail(RT_ERR_INVALID_ARG, "pipeline slots must be in [1, %d]", Context::kSlots);
   g_ctx.pipeline = slots;
+  return RT_OK;
+}
+
+int rt_set_schedule_jitter(uint64_t seed) {
+  int rc = ensure_device();
+  if (rc) return rc;
+  g_ctx.jitter = seed;
+  return RT_OK;
+}
+
+int rt_check_status(uint32_t* first_failed, int32_t* compiled) {
+  g_err.clear();
+  int rc = ensure_device();
+  if (rc) return rc;
+  if (!first_failed || !compiled) return fail(RT_ERR_INVALID_ARG, "check_status: NULL argument");
+  CU(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  unsigned v = 0;
+  CU(rt::read_check_status(&v), "read check status");
+  *first_failed = v;
+  *compiled = RT_CHECKS;
   return RT_OK;
 }
 

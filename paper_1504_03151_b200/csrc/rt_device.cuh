@@ -9,6 +9,7 @@
 namespace rt {
 
 __constant__ DevPlane c_planes[kMaxPlanes];
+__device__ unsigned g_rt_check;  // first failed RT_CHECK id (checked builds)
 
 constexpr double kEps = 1e-4;          // EPS_T
 constexpr double kInf = 1.0e300;

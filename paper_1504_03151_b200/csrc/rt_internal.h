@@ -22,6 +22,22 @@
 #include <cuda_runtime.h>
 
 
+// bounds / capacity checks of the checked build (-DRT_CHECKS=1, test support): the first failing
+// check's id is recorded in g_rt_check (rt_check_status); compiled out by default
+#ifndef RT_CHECKS
+#define RT_CHECKS 0
+#endif
+#if RT_CHECKS
+#define RT_CHECK(cond, id)                                                    \
+  do {                                                                        \
+    if (!(cond)) atomicCAS(&::rt::g_rt_check, 0u, (unsigned)(id));          \
+  } while (0)
+#else
+#define RT_CHECK(cond, id) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace rt {
 
 constexpr int kWarp = 32;
@@ -215,6 +231,8 @@ struct WfTiming {
   // while the launch sequence is captured into a CUDA graph, the timing and chunk events become
   // event-record nodes (cudaEventRecordExternal), so every replay records them
   bool ext_events = false;
+  // schedule fuzzing (rt_set_schedule_jitter): state of the generator of the spin lengths, 0 = off
+  unsigned long long jitter = 0;
   void record(cudaEvent_t ev, cudaStream_t s) const {
     cudaEventRecordWithFlags(ev, s, ext_events ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
@@ -228,6 +246,7 @@ int wf_timing_pairs(const DevParams& p, int nslots);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigned long long* stats, cudaStream_t st);
+cudaError_t read_check_status(unsigned* first_failed);
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure,
                            float gamma, cudaStream_t st);
 

@@ -566,6 +566,13 @@ cudaError_t launch_sum_records(const unsigned long long* rec, int world, unsigne
   return cudaGetLastError();
 }
 
+cudaError_t read_check_status(unsigned* first_failed) {
+  cudaError_t e = cudaMemcpyFromSymbol(first_failed, g_rt_check, sizeof(unsigned));
+  if (e != cudaSuccess) return e;
+  const unsigned zero = 0;
+  return cudaMemcpyToSymbol(g_rt_check, &zero, sizeof(unsigned));
+}
+
 cudaError_t launch_tonemap(const float4* rgba, uint8_t* out, int64_t n, float exposure, float gamma,
                            cudaStream_t st) {
   int grid = (int)((n + 255) / 256);
@@ -731,6 +738,13 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   int* db = dbg ? o.dbg_bounces : nullptr;
   const int nslots = tm.nslots;
   const int items_per_chunk = wf_items_per_chunk(p, nslots);
+  // schedule fuzzing: a spin of 0-40 us (or none) on a stream at each fork, join and slot start
+  auto jitter = [&](cudaStream_t s) {
+    if (!tm.jitter || !s) return;
+    tm.jitter = tm.jitter * 6364136223846793005ull + 1442695040888963407ull;
+    const unsigned r = (unsigned)(tm.jitter >> 33);
+    if (r & 1u) launch(spin_ns, 1, 0, s, (r >> 1) % 40000u);
+  };
   tm.n = 0;
   tm.launches = 0;
   tm.n_chunks = 0;
@@ -741,7 +755,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   }
   if (nslots > 1) {  // the other slots' streams start after everything issued on st so far
     cudaEventRecord(tm.start_ev, st);
-    for (int k = 1; k < nslots; ++k) cudaStreamWaitEvent(tm.slot_main[k], tm.start_ev, 0);
+    for (int k = 1; k < nslots; ++k) {
+      cudaStreamWaitEvent(tm.slot_main[k], tm.start_ev, 0);
+      jitter(tm.slot_main[k]);
+    }
   }
   int chunk = 0;
   for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk, ++chunk) {
@@ -802,6 +819,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         cudaEventRecord(fork[d], st);
         cudaStreamWaitEvent(side, fork[d], 0);
         ss = side;
+        jitter(side);
       }
       if (rec) tm.record(tm.shadow[2 * ti], ss);
       int scan_launches = 0;
@@ -846,6 +864,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec && tm.accum) tm.record(tm.accum[2 * ti + 1], ss);
       if (d < p.max_depth) closest_scan(d + 1);
       if (side) {
+        jitter(side);
+        jitter(st);
         cudaEventRecord(join[d], side);
         cudaStreamWaitEvent(st, join[d], 0);
       }

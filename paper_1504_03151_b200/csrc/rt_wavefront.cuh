@@ -884,6 +884,7 @@ __device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, 
   if (valid) {
     dt = B.lt_dir[g];
     const int skip = B.lt_rec[g].y;
+    RT_CHECK(B.lt_rec[g].x >= 0 && B.lt_rec[g].x < B.cap && skip < P.n_spheres, 401);
     if (skip <= -2) {  // plane -2-skip occludes (decided by wf_shade in FP64)
       R.rob = skip;
       R.act = false;
@@ -1038,6 +1039,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
     const int l = li / kLtSub;
     const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
     const unsigned cnt = B.ctr[wf_ctr_lt(d, 0, 0) + li];
+    RT_CHECK(cnt <= (unsigned)B.lt_cap && li < nl, 402);
     const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
     const bool va_ = oa < cnt, vb_ = ob < cnt;
     const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;  // list slots
@@ -1137,6 +1139,7 @@ __device__ __forceinline__ void nearest_sphere(const DevParams& P, const DevScen
   if (nc <= kCandMax) {
     for (int c = 0; c < nc; ++c) {
       const int k = cand[c];
+      RT_CHECK(k >= 0 && k < P.n_spheres, 301);
       const double t = sphere_root(__ldg(S.sph_cr + k), o, d);
       if (t >= kEps && beats(S, t, k, tbest, hp)) { tbest = t; hs = k; hp = -1; }
     }
@@ -1210,6 +1213,7 @@ template <bool kDebug, bool kExt>
 __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, int* dbg_hits, int* dbg_bounces) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
+  RT_CHECK(n <= (unsigned)B.cap, 100);
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
   const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
   const int lane = threadIdx.x & 31;
@@ -1383,12 +1387,16 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
       else if (lane == 30) { ctr = B.ctr + wf_ctr_s(d); cnt = tot_sh; }
       else if (lane == 31) { ctr = B.ctr + wf_ctr_q(d + 1); cnt = (unsigned)__popc(mc); }
       base = (ctr != nullptr && cnt != 0u) ? atomicAdd(ctr, cnt) : 0u;
+      RT_CHECK(lane != 30 || base + cnt <= (unsigned)B.scap, 101);  // shadow entries fit scap
+      RT_CHECK(lane != 31 || base + cnt <= (unsigned)B.cap, 102);   // continuations fit Q[d+1]
+      RT_CHECK(lane >= nres || lane < LT || base + cnt <= (unsigned)B.gcap, 103);  // generic slots fit gcap
       __syncthreads();
       if (threadIdx.x < (unsigned)LT) {  // one atomic per light and CTA; warps in order
         const int l = threadIdx.x;
         unsigned tot = 0;
         for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
         unsigned b0 = tot ? atomicAdd(B.ctr + wf_ctr_lt(d, l, sub), tot) : 0u;
+        RT_CHECK(b0 + tot <= (unsigned)B.lt_cap, 104);  // a light-origin sub-list fits lt_cap
         for (int w = 0; w < 8; ++w) {
           const unsigned c = s_cnt[w][l];
           s_cnt[w][l] = b0;
@@ -1419,6 +1427,7 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
           Qn.skip[slot] = (hs >= 0 && (entering ? dng > 0.0 : dng < 0.0)) ? hs : -1;
           B.nxt[e] = (int)slot;
         } else {  // the path ends here: its radiance (lights of this depth still to come) by path id
+          RT_CHECK(path >= 0 && path < B.cap, 105);
           sf3(B.Lr, B.cap, path, L);
           B.nxt[e] = -1 - path;
         }
@@ -1461,6 +1470,9 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         const float gg = (float)ls.g;
         sf3(B.sq_c, B.scap, (int)k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * gg, fmaf(m.ag, kInvPi, spec) * ls.ig * gg,
                                              fmaf(m.ab, kInvPi, spec) * ls.ib * gg)));
+        RT_CHECK(k < (unsigned)B.scap, 106);
+        RT_CHECK(g < 0 || (g >= (l * kLtSub + sub) * B.lt_cap && g < (l * kLtSub + sub + 1) * B.lt_cap), 107);
+        RT_CHECK(g >= 0 || -2 - g < B.gcap, 108);
         B.spos[k] = g;
         if (g >= 0) {
           d3 ds;
@@ -1514,8 +1526,11 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
       float* Ls = loc >= 0 ? Qn.L : B.Lr;
       const int li = loc >= 0 ? loc : -1 - loc;
       float3 L = lf3(Ls, B.cap, li);
+      RT_CHECK(off >= 0 && off + cnt <= B.scap && li >= 0 && li < B.cap, 201);
       for (int j = off; j < off + cnt; ++j) {
         const int g = B.spos[j];
+        RT_CHECK(g < 0 || g < B.lt_cap * kLtSub * P.lt_lights, 202);
+        RT_CHECK(g >= 0 || -2 - g < B.gcap, 203);
         const bool lt = g >= 0;  // a light-origin list slot, else generic slot o = -2 - g
         const int o = lt ? 0 : -2 - g;
         int rob, nc, skip2 = -1;
@@ -1553,6 +1568,7 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
           ray(os, ds, tl, skip);
           if (nc <= kCandMax) {
             for (int i = 0; i < nc; ++i) {
+              RT_CHECK(cand[i] >= 0 && cand[i] < P.n_spheres, 204);
               const double t = sphere_root(__ldg(S.sph_cr + cand[i]), os, ds);
               if (t >= kEps && t < tl) { first = cand[i]; break; }
             }
@@ -1624,6 +1640,7 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
       continue;
     }
     float3 acc = f3(0.f, 0.f, 0.f);
+    RT_CHECK((i + 1) * P.spp <= B.cap, 501);
     for (int s = 0; s < P.spp; ++s) acc = add(acc, lf3(B.Lr, B.cap, i * P.spp + s));
     const float inv = 1.0f / (float)P.spp;
     const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, 1.0f);
@@ -1647,6 +1664,16 @@ __global__ void __launch_bounds__(256) wf_resolve(const DevParams P, WfBuffers B
     if (P.n_planes) atomicAdd(stats + 4, sec * (unsigned long long)P.n_planes);
     atomicAdd(stats + 5, sec * (unsigned long long)P.n_spheres);
   }
+}
+
+// schedule fuzzing (rt_set_schedule_jitter): one thread spins for `ns` nanoseconds of global time
+__global__ void spin_ns(unsigned ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
 }
 
 __global__ void fill_int(int* p, long long n, int v) {

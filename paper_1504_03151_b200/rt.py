@@ -82,6 +82,8 @@ def lib() -> C.CDLL:
         "rt_set_concurrency": [i32],
         "rt_set_pipeline": [i32],
         "rt_set_tiled_scan": [i32],
+        "rt_set_schedule_jitter": [C.c_uint64],
+        "rt_check_status": [C.POINTER(C.c_uint32), C.POINTER(i32)],
         "rt_set_graphs": [i32],
         "rt_set_scan_split": [i32],
         "rt_render_shard_direct": [i32, i32, i32, i32, i32, i32, vp, vp],
@@ -178,6 +180,18 @@ def set_concurrency(on: bool):
 def set_tiled_scan(on: bool):
     """Scenes beyond shared memory: scans over TMA-loaded tiles (default) or global loads."""
     _check("rt_set_tiled_scan", lib().rt_set_tiled_scan(1 if on else 0))
+
+
+def set_schedule_jitter(seed: int = 0):
+    """Test support: random spin kernels at every stream fork/join of plain launches (0 = off)."""
+    _check("rt_set_schedule_jitter", lib().rt_set_schedule_jitter(int(seed)))
+
+
+def check_status() -> tuple[int, bool]:
+    """Test support: (id of the first failed device check since the last call or 0, checks compiled)."""
+    v, c = C.c_uint32(), C.c_int32()
+    _check("rt_check_status", lib().rt_check_status(C.byref(v), C.byref(c)))
+    return int(v.value), bool(c.value)
 
 
 def set_pipeline(slots: int = 2):
