@@ -52,13 +52,17 @@ class P2PRenderer:
     maps them (peer access over NVLink / NVSwitch). Each frame, every rank's resolve kernel
     stores its pixels straight into rank 0's frame — no slab, no all-gather, no assembly kernel.
 
-    Ordering. With NCCL, one stream-ordered all-reduce of a 4-byte token per frame is the barrier:
-    it completes on every rank only after every rank's render kernels have completed (their peer
-    stores included), and the host never waits. With other backends (gloo, the CPU tests) the
-    host synchronises its stream and calls dist.barrier(). Frames alternate between two buffers,
-    so rank r may start frame i+1 while rank 0 still uses frame i: frame i's buffer is written
-    again only by frame i+2, after the barrier of frame i+1, which rank 0 reaches after it has
-    issued its work on frame i (image valid until the next-but-one render call)."""
+    Ordering. With NCCL, two stream-ordered all-reduces of a 4-byte token per frame order the
+    peer stores, and the host never waits:
+      * the frame barrier (after the render): it completes on every rank only after every rank's
+        render kernels have completed (their peer stores included), so rank 0's work issued after
+        render() returns sees the whole frame;
+      * the release barrier (before the render, when the frame reuses a buffer): frame i + nbuf
+        stores into frame i's buffer only after rank 0's stream has passed everything rank 0
+        issued before that render() call — its reads of frame i included.
+    So the image of frame i stays valid for every read rank 0 issues (on its current stream)
+    before its next-but-one render() call. With other backends (gloo, the CPU tests) the host
+    synchronises its stream and calls dist.barrier() at both points."""
 
     def __init__(self, width: int, height: int, max_depth: int, spp: int, group=None, buffers: int = 2):
         self.W, self.H, self.D, self.spp = width, height, max_depth, spp
@@ -117,8 +121,10 @@ class P2PRenderer:
     def render(self, want_stats: bool = True) -> Frame:
         """Render this rank's tiles of the next frame into rank 0's buffer. Rank 0 gets the image
         (stream-ordered after every rank's stores) and, with want_stats, the summed statistics
-        (a host sync); the image stays valid until the next-but-one call."""
+        (a host sync); reads of the image issued before the next-but-one call are safe."""
         b = self.frames % self.nbuf
+        if self.frames >= self.nbuf:
+            self._barrier()  # release: rank 0's reads of this buffer's previous frame come first
         self.frames += 1
         rt.render_shard_direct(self.W, self.H, self.D, self.spp, self.rank, self.world, self.frame_ptrs[b],
                                self.rec_ptrs[b])
@@ -130,10 +136,8 @@ class P2PRenderer:
         return Frame(None, None)
 
     def release(self):
-        """Kept for callers of the single-buffered version: with two buffers, rank 0 releases a
-        frame by calling render() again, so there is nothing to wait for."""
-        if self.nbuf == 1 and self.world > 1:
-            dist.barrier(group=self.group)
+        """Nothing to do: the release barrier at the start of the render that reuses a buffer
+        orders the new peer stores after rank 0's reads (kept for callers of earlier versions)."""
 
     def close(self):
         self.image = None
