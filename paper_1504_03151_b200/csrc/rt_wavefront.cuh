@@ -63,7 +63,7 @@ __device__ __forceinline__ unsigned warp_reserve1(bool take, unsigned* counter) 
 
 // warp-aggregated statistics for ANY set of active lanes (a butterfly of shuffles would read
 // inactive lanes, e.g. the work items outside the image between valid ones): two 32-bit
-// reductions over the active mask (low 20 bits and the rest; per-lane values < 2^52)
+// reductions over the active mask (low 20 bits and the rest; per-lane values < 2^47)
 __device__ __forceinline__ void warp_stat(unsigned long long* stats, int k, unsigned long long v) {
   const unsigned act = __activemask();
   const unsigned lo = __reduce_add_sync(act, (unsigned)(v & 0xFFFFFull));
@@ -1517,9 +1517,9 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
                                                      unsigned long long* stats) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   const WfQueue Qn = B.q[(d + 1) & 1];
+  unsigned long long st_sph = 0, st_pl = 0;  // this thread's test counts, reduced once at the end
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int cnt = B.shcnt[e];
-    unsigned long long st_sph = 0, st_pl = 0;
     if (cnt > 0) {
       const int off = B.shoff[e];
       const int loc = B.nxt[e];  // where the path's radiance lives now: Q[d+1] slot or Lr[path]
@@ -1601,9 +1601,9 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
       }
       sf3(Ls, B.cap, li, L);
     }
-    warp_stat(stats, 3, st_sph);
-    warp_stat(stats, 4, st_pl);
   }
+  warp_stat(stats, 3, st_sph);
+  warp_stat(stats, 4, st_pl);
 }
 
 // ---- a7: mean over samples in order, 16-byte store ------------------------------------------
