@@ -323,7 +323,7 @@ def run_b200(args):
         extra = (2 if isinstance(rend, ShardedRenderer) else 1) if rank == 0 else 0
         launches_per_step = rt.stats()["launches"] + extra
         del probe
-    fp32 = measure_fp32_peak(gpu) if rank == 0 else None
+    fp32 = measure_fp32_peak(gpu) if rank == 0 and not args.no_fp32_peak else None
     # warm-up (after the probe, so the frame's launch sequence is captured as a CUDA graph here)
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -659,6 +659,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="C4", choices=sorted(scenegen.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32-peak", action="store_true", help="skip the in-run FFMA2 peak measurement "
+                    "(e.g. under ncu, which would profile the microbenchmark too); the derived peak is used")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="core-seconds of oracle work")
     ap.add_argument("--ref-pixels", type=int, default=4096, help="--impl reference: pixels per step")
     ap.add_argument("--strict", action="store_true", default=True)

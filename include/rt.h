@@ -208,8 +208,10 @@ int rt_check_status(uint32_t* first_failed, int32_t* compiled);
  * the second time it is requested within the last 8 renders and replayed whenever it comes again
  * (up to 4 sequences cached, least recently used evicted: e.g. frames alternating between two
  * output buffers), so a frame loop pays one graph launch per frame instead of ~6 kernel launches
- * per depth; scene and camera contents may change between replays (the kernels read them at run
- * time). 0 launches every kernel from the host and empties the cache (calling it with 1 empties
+ * per depth; materials, lights and the environment may change between replays (the kernels read
+ * them at run time; each scan's kernel was chosen from the previous frame's queue lengths, so a
+ * large change costs some speed, never results), while a new camera or new geometry bounds change
+ * the kernel arguments and start a new capture. 0 launches every kernel from the host and empties the cache (calling it with 1 empties
  * it too). Same results bit for bit either way. RT_ERR_INVALID_ARG unless 0/1. */
 int rt_set_graphs(int32_t on);
 

@@ -143,7 +143,8 @@ struct Context {
   std::vector<std::string> recent_keys;
   unsigned long long graph_clock = 0;
   int last_graph = 0;  // how the last wavefront render was launched: 0 plain, 1 captured, 2 replayed
-  std::vector<unsigned> hints[kSlots];  // queue counters of the render before the capture, per slot
+  std::vector<unsigned> hints;     // queue counters of every chunk of the render before a capture
+  DevBuf<unsigned> hint_dev;        // where each render leaves its chunks' counters
 };
 constexpr size_t kGraphCache = 4, kRecentKeys = 8;
 
@@ -240,9 +241,10 @@ int check_frame(int32_t W, int32_t H, int32_t D, int32_t spp) {
   return RT_OK;
 }
 
-// Everything the wavefront launch sequence depends on: the kernel arguments (parameters, scene
-// and output pointers, buffer layout), the scene source, the timing/stream configuration. Scene
-// and camera CONTENTS are read by the kernels at run time and do not enter the key.
+// Everything the wavefront launch sequence depends on: the kernel arguments (parameters — the
+// camera and the geometry's bounds included —, scene and output pointers, buffer layout), the
+// scene source, the timing/stream configuration. The contents behind the scene pointers
+// (materials, lights, sphere data of the same bounds) are read at run time and do not enter it.
 template <class T>
 void key_add(std::string& k, const T& v) {
   k.append(reinterpret_cast<const char*>(&v), sizeof(T));
@@ -316,11 +318,12 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   {
     const size_t nctr = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
     CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
-    for (int k = 0; k < tm.nslots; ++k) {
-      c.hints[k].assign(nctr, 0u);
-      CU(cudaMemcpy(c.hints[k].data(), c.wf_ctr[k].p, nctr * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
-      tm.hint[k] = c.hints[k].data();
-    }
+    (void)nctr;
+    const int ipc = rt::wf_items_per_chunk(p, tm.nslots_req);
+    const size_t n = tm.hint_stride * (size_t)((p.n_items + ipc - 1) / ipc);
+    c.hints.assign(n, 0u);
+    CU(cudaMemcpy(c.hints.data(), c.hint_dev.p, n * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
+    tm.hints = c.hints.data();
   }
   if (!c.cap_stream) CU(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   // per-launch timing events become event-record nodes, which serialise the graph around every
@@ -439,6 +442,10 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     tm.shade = c.ev_h.data();
     tm.accum = c.ev_a.data();
     tm.jitter = c.jitter;
+    tm.nslots_req = nslots;
+    tm.hint_stride = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
+    CU(c.hint_dev.reserve(tm.hint_stride * n_chunks), "cudaMalloc(hints)");
+    tm.hint_dev = c.hint_dev.p;
     const bool overlap = host_out != nullptr && p.mode == 0;
     if (overlap) {
       const int max_chunks = n_chunks;

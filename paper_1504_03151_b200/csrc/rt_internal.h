@@ -223,7 +223,12 @@ struct WfTiming {
   // queue counters of the previous render with the same launch sequence, per buffer set (host
   // copies; null = unknown): each scan is then launched as one kernel, the long-queue scan or
   // its split variant, instead of the pair
-  const unsigned* hint[kMaxSlots] = {};
+  // (hints: host copy, hint_stride counters per chunk, of the chunks' counters saved in hint_dev
+  // by the previous render with this sequence)
+  const unsigned* hints = nullptr;
+  unsigned* hint_dev = nullptr;
+  size_t hint_stride = 0;
+  int nslots_req = 1;  // the slot count the chunking was computed for (wf_items_per_chunk)
   cudaEvent_t* chunk_done = nullptr;
   int* chunk_items = nullptr;
   int chunk_cap = 0;

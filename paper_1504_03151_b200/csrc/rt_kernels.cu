@@ -719,12 +719,6 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, ksl, 256, smem_long)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);
   const int grid_l = num_sms * kLogicGridPerSm;
-  // grid for a hinted amount of work: twice the CTAs the hint needs (a stale hint costs speed,
-  // never results: every kernel loops over whatever its queue holds), at most the full grid
-  auto hinted_grid = [](unsigned work, unsigned per_cta, int full) -> int {
-    const unsigned long long want = 2ull * ((work + per_cta - 1) / per_cta);
-    return (int)(want < 1ull ? 1ull : (want < (unsigned long long)full ? want : (unsigned long long)full));
-  };
   // the device's split_parts (rt_wavefront.cuh) evaluated on a hinted queue length
   auto host_parts = [&](unsigned tasks, int grid) -> int {
     if (grid > B0.xctas) return 1;
@@ -736,8 +730,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
                             : (dbg ? wf_shade<true, false> : wf_shade<false, false>);
   int* dh = dbg ? o.dbg_hits : nullptr;
   int* db = dbg ? o.dbg_bounces : nullptr;
-  const int nslots = tm.nslots;
-  const int items_per_chunk = wf_items_per_chunk(p, nslots);
+  const int nslots = tm.nslots;  // slots that receive chunks (<= the count the chunking used)
+  const int items_per_chunk = wf_items_per_chunk(p, tm.nslots_req);
   // schedule fuzzing: a spin of 0-40 us (or none) on a stream at each fork, join and slot start
   auto jitter = [&](cudaStream_t s) {
     if (!tm.jitter || !s) return;
@@ -768,7 +762,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const cudaStream_t side = tm.slot_side[sl];
     cudaEvent_t* fork = tm.slot_fork[sl];
     cudaEvent_t* join = tm.slot_join[sl];
-    const unsigned* hint = tm.hint[sl];
+    // this chunk's queue counters in the render before the capture (null: launch the pairs)
+    const unsigned* hint = tm.hints ? tm.hints + (size_t)chunk * tm.hint_stride : nullptr;
     WfBuffers Bc = Bset;  // this chunk's launches: the buffer set with the chunk's first sample
     Bc.g0 = (long long)w0 * p.spp;
     WfBuffers Bs = Bc;  // the copy passed to a single (solo) kernel launch
@@ -789,14 +784,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (rec) tm.record(tm.closest[2 * ti], st);
       if (dd == 0) {
         launch(kc0, grid_c, smem_eye, st, p, sc, Bc, dd);
-      } else if (hint) {  // one kernel, chosen from the previous frame's queue, on a grid sized to it
+      } else if (hint) {  // one kernel, chosen from the previous frame's queue of this chunk
+        // (grids stay full: a hint that underestimates the queue, e.g. after a camera move, may
+        // then cost the split kernel's merges, never a starved grid)
         const unsigned tasks = (hint[wf_ctr_q(dd)] + 31u) / 32u;
-        const int parts = host_parts(tasks, grid_c);
-        WfBuffers Bp = Bs;
-        Bp.force_parts = parts;  // the device rule on the smaller grid would pick fewer parts
-        const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_c);
-        if (parts > 1) launch(wf_isect_split<kScan, false>, g, smem, st, p, sc, Bp, dd);
-        else launch(kcl, g, smem_long, st, p, sc, Bs, dd);
+        if (host_parts(tasks, grid_c) > 1) launch(wf_isect_split<kScan, false>, grid_c, smem, st, p, sc, Bs, dd);
+        else launch(kcl, grid_c, smem_long, st, p, sc, Bs, dd);
       } else {  // the self-selecting pair: both read the queue length, exactly one works
         launch(kcl, grid_c, smem_long, st, p, sc, Bc, dd);
         launch(wf_isect_split<kScan, false>, grid_c, smem, st, p, sc, Bc, dd);
@@ -810,8 +803,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const int ti = t0 + d;
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
-      // logic kernels: grid-stride loops, on a grid sized to the hinted queue (no hint: full grid)
-      const int grid_q = hint ? hinted_grid(hint[wf_ctr_q(d)], 256u, grid_l) : grid_l;
+      const int grid_q = grid_l;  // logic kernels: grid-stride loops
       launch(shade, grid_q, 0, st, p, sc, Bc, d, g0, dh, db);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       cudaStream_t ss = st;
@@ -827,11 +819,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         if (hint) {
           unsigned chunks = 0;
           for (int i = 0; i < p.lt_lights * kLtSub; ++i) chunks += (hint[wf_ctr_lt(d, 0, 0) + i] + 63u) / 64u;
-          const int parts = host_parts(chunks, grid_lt);
-          WfBuffers Bp = Bs;
-          Bp.force_parts = parts;
-          launch(parts > 1 ? klts : klt, hinted_grid(chunks * (unsigned)parts, 8u, grid_lt), smem_lt, ss, p, sc,
-                 parts > 1 ? Bp : Bs, d);
+          launch(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
           launch(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
@@ -842,12 +830,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       if (!klt || p.n_emitters > 0) {  // every other shadow ray
         if (hint) {
           const unsigned tasks = (hint[wf_ctr_so(d)] + 31u) / 32u;
-          const int parts = host_parts(tasks, grid_s);
-          WfBuffers Bp = Bs;
-          Bp.force_parts = parts;
-          const int g = hinted_grid(tasks * (unsigned)parts, 8u, grid_s);
-          if (parts > 1) launch(wf_isect_split<kScan, true>, g, smem, ss, p, sc, Bp, d);
-          else launch(ksl, g, smem_long, ss, p, sc, Bs, d);
+          if (host_parts(tasks, grid_s) > 1) launch(wf_isect_split<kScan, true>, grid_s, smem, ss, p, sc, Bs, d);
+          else launch(ksl, grid_s, smem_long, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
           launch(ksl, grid_s, smem_long, ss, p, sc, Bc, d);
@@ -875,6 +859,9 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const int grid_w = (nw + 255) / 256 < grid_l ? (nw + 255) / 256 : grid_l;
     launch(wf_resolve, grid_w, 0, st, p, Bc, w0, nw, o.out, o.accum, o.stats);
     tm.launches += 2;  // wf_q0_len, wf_resolve
+    if (tm.hint_dev)  // keep this chunk's queue counters: the hints of a later capture
+      cudaMemcpyAsync(tm.hint_dev + (size_t)chunk * tm.hint_stride, Bc.ctr, sizeof(unsigned) * tm.hint_stride,
+                      cudaMemcpyDeviceToDevice, st);
     if (tm.chunk_done && tm.n_chunks < tm.chunk_cap) {
       tm.record(tm.chunk_done[tm.n_chunks], st);
       tm.chunk_items[tm.n_chunks] = w0 + nw;

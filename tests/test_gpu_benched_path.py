@@ -59,19 +59,23 @@ def test_benched_render_equals_debug_render(name):
     ref_u = ref.view(torch.int32)
     # device framebuffer: plain launches, capture, then replays of the cached graph
     out = torch.empty_like(ref)
-    modes = []
+    modes, ms = [], []
     for _ in range(4):
         out.fill_(float("nan"))
         rt.render(W, H, D, S, out)
         st = rt.stats()
         torch.cuda.synchronize()
         modes.append(st["graph"])
+        ms.append(st["last_render_ms"])
         assert torch.equal(out.view(torch.int32), ref_u), name
         for k in COUNTS:
             assert st[k] == st_ref[k], (name, k)
         assert st["variant"] == st_ref["variant"]
     if st_ref["variant"] == 1:  # wavefront (C4, C5): the timed frames replay a captured graph
         assert modes[0] == 0 and modes[1] == 1 and modes[2:] == [2, 2], modes
+        # a replay (kernels chosen from the previous frame's per-chunk queue lengths) is never much
+        # slower than the plain launches (round 2 regression: hint-sized grids made C5 36x slower)
+        assert max(ms[2:]) <= 1.25 * ms[0], ms
     # pinned host framebuffer (the e2e leg of bench.py): rows copied while later chunks render
     host = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
     for _ in range(3):
@@ -110,4 +114,43 @@ def test_graph_cache_alternating_buffers():
     torch.cuda.synchronize()
     assert modes[:4] == [0, 0, 1, 1] and modes[4:] == [2, 2, 2, 2], modes
     assert torch.equal(bufs[0], bufs[1])
+    rt.set_variant("auto")
+
+
+def test_stale_hints_after_material_change():
+    """A captured graph keeps its kernel choices (made from the previous frame's per-chunk queue
+    lengths) while the scene's contents change under the same launch key (materials, lights: the
+    kernels read them at run time; the camera and the geometry's bounds are kernel arguments, so
+    changing them starts a new capture). Turning every sphere into a mirror makes every deep queue
+    long where the hints say short: the replay must still render the new scene bit for bit, at a
+    cost close to the plain launches (a grid sized from the hints would starve: round 2 regression)."""
+    import dataclasses
+    import torch
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.get("C4").with_frame(width=960, height=540)
+    W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
+    mirror = dataclasses.replace(sc, mat_kind=np.full_like(sc.mat_kind, scenegen.SPECULAR),
+                                 mat_albedo=np.full_like(sc.mat_albedo, 0.9))
+    rt.set_variant("wavefront")
+    out = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
+    for first, second in ((sc, mirror), (mirror, sc)):
+        rt.set_graphs(True)  # empties the cache: capture with hints from `first`
+        rt.load_scene(first)
+        for _ in range(3):
+            rt.render(W, H, D, S, out)
+        assert rt.stats()["graph"] == 2
+        rt.scene_upload(*rt.pack_scene(second))  # same sizes and bounds: the same launch key
+        rt.render(W, H, D, S, out)
+        st = rt.stats()
+        assert st["graph"] == 2, "expected a replay with stale hints"
+        stale_ms = st["last_render_ms"]
+        torch.cuda.synchronize()
+        rep = out.clone()
+        rt.set_graphs(False)
+        rt.render(W, H, D, S, out)
+        plain_ms = rt.stats()["last_render_ms"]
+        torch.cuda.synchronize()
+        assert torch.equal(out, rep)
+        assert stale_ms <= 1.5 * plain_ms + 0.2, (stale_ms, plain_ms)
+    rt.set_graphs(True)
     rt.set_variant("auto")

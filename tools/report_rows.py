@@ -1,6 +1,6 @@
 """SURVEY §8(d).8 report rows: runs bench.py per config on this GPU and prints a markdown table
 (config | GPUs | Mrays/s | fps | counted TFLOP/s | % FP32 peak | oracle Mrays/s 1 thread / N).
-Usage: python tools/report_rows.py C2 C3 C4 C5 > profiles/r01_report_rows.md"""
+Usage: python tools/report_rows.py C2 C3 C4 C5 > profiles/r02_report_rows.md"""
 import json
 import os
 import subprocess
@@ -14,12 +14,13 @@ for cfg in sys.argv[1:] or ["C2", "C3", "C4", "C5"]:
                           "--warmup", "3", "--cpu-seconds", "10"], capture_output=True, text=True, timeout=1200)
     d = json.loads(out.stdout.strip().splitlines()[-1])
     r, cb, c = d["roofline"], d["cpu_baseline"], d["config"]
-    whole = r.get("whole_frame_achieved", r["achieved"])
+    counted = r.get("whole_frame_counted_tflops", r.get("achieved"))
+    dom = r["kernel"].split(" ")[0]
+    frac = f"{100 * r['frac']:.0f} % ({r['bound']}, {dom})"
     rows.append(f"| {cfg} | {c['width']}x{c['height']}, {c['spheres']} spheres + {c['planes']} planes, "
                 f"{c['lights']} lights, depth {c['max_depth']}, {c['spp']} spp | 1 | {d['value']:.0f} | {d['fps']:.1f} | "
-                f"{whole:.1f} (frame) / {r['achieved']:.1f} ({r['kernel'].split(' ')[0]}) | {100 * whole / r['peak']:.0f} % / "
-                f"{100 * r['frac']:.0f} % | {cb['value_1thread']:.2f} / {cb['value']:.1f} ({cb['cores']} cores) | "
+                f"{counted:.1f} | {frac} | {cb['value_1thread']:.2f} / {cb['value']:.1f} ({cb['cores']} cores) | "
                 f"{d['e2e']['value']:.0f} |")
-print("| config | workload | GPUs | Mrays/s | fps | counted TFLOP/s | % of FP32 peak | oracle Mrays/s 1 thread / all cores | e2e Mrays/s |")
+print("| config | workload | GPUs | Mrays/s | fps | whole-frame counted TFLOP/s | dominant kernel vs its roofline | oracle Mrays/s 1 thread / all cores | e2e Mrays/s |")
 print("|---|---|---|---|---|---|---|---|---|")
 print("\n".join(rows))
