@@ -130,17 +130,20 @@ def measure_fp32_peak(gpu: int) -> dict:
         return {"error": f"{type(ex).__name__}: {ex}"}
 
 
-def _load_profile_traffic(workload: str):
-    """dram bytes per launch of the render kernel from the committed ncu --set full summary."""
+def _load_profile(workload: str) -> dict:
+    """The committed ncu --set full summary of one kernel class (profiles/ncu_render_kernel.json):
+    DRAM bytes per launch, FMA-pipe and issue activity."""
     path = os.path.join(ROOT, "profiles", "ncu_render_kernel.json")
     try:
-        d = json.load(open(path))
-        ent = d.get(workload)
-        if ent and ent.get("dram_bytes_per_launch"):
-            return float(ent["dram_bytes_per_launch"])
+        return json.load(open(path)).get(workload) or {}
     except (OSError, ValueError):
-        pass
-    return None
+        return {}
+
+
+def _load_profile_traffic(workload: str):
+    """dram bytes per launch of a kernel class from the committed ncu --set full summary."""
+    v = _load_profile(workload).get("dram_bytes_per_launch")
+    return float(v) if v else None
 
 
 # ---------------------------------------------------------------------------------------------
@@ -465,6 +468,10 @@ def run_b200(args):
             }
             for k, v in cands.items():
                 v["share_of_frame"] = v["ms"] / kt["frame"]
+                prof = _load_profile(f"{args.config}:{k}")
+                if prof:  # the committed ncu capture of this kernel class (one launch, cold, serialised)
+                    v["ncu"] = {kk: prof.get(kk) for kk in ("fma_pipe_active_pct", "issue_active_pct",
+                                                             "dram_bytes_per_launch", "source")}
                 if v["bound"] == "alu":
                     v["achieved"] = 2 * v["fma_per_test"] * v["tests"] / (v["ms"] * 1e-3) / 1e12
                     v["achieved_counted"] = FLOP_SPHERE * v["tests"] / (v["ms"] * 1e-3) / 1e12

@@ -22,7 +22,8 @@ classes = [("camera", "wf_isect_eye2"), ("shade", "wf_shade"), ("shadow", "wf_is
 
 def val(r, m):
     v = float(r[idx[m]].replace(",", ""))
-    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1, "nsecond": 1e-6}.get(
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1,
+                                     "ns": 1e-6, "nsecond": 1e-6}.get(
         units[idx[m]], 1)
 
 
@@ -33,6 +34,9 @@ for key, pat in classes:
             rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
             out[f"{cfg}:{key}"] = {"kernel": r[idx["Kernel Name"]].split("(")[0], "dram_bytes_per_launch": rd + wr,
                                    "dram_read_bytes": rd, "dram_write_bytes": wr,
-                                   "duration_ms_ncu": val(r, "gpu__time_duration.sum"), "source": note}
+                                   "duration_ms_ncu": val(r, "gpu__time_duration.sum"),
+                                   "fma_pipe_active_pct": val(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                                   "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                   "source": note}
             break
 print(json.dumps(out, indent=1))
