@@ -167,7 +167,7 @@ int rt_set_stream(void* cuda_stream);
  *   RT_VARIANT_WAVEFRONT: queue-based kernels — an FP32 FFMA2 intersection kernel per depth for
  *     closest-hit rays and one for shadow rays, FP64 shade/accumulate kernels between;
  *   RT_VARIANT_MEGAKERNEL: one persistent kernel, each lane carries a pixel's path state;
- *   RT_VARIANT_AUTO (default): wavefront for scenes of >= 384 spheres, else megakernel. */
+ *   RT_VARIANT_AUTO (default): wavefront for scenes of >= 64 spheres, else megakernel. */
 enum { RT_VARIANT_AUTO = -1, RT_VARIANT_MEGAKERNEL = 0, RT_VARIANT_WAVEFRONT = 1 };
 int rt_set_variant(int32_t variant);
 

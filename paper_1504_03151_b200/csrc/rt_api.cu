@@ -149,9 +149,10 @@ struct Context {
 constexpr size_t kGraphCache = 4, kRecentKeys = 8;
 
 Context g_ctx;
-// AUTO picks the wavefront kernels for scenes where the sphere scan dominates (measured on B200:
-// 1000 spheres 10.3 ms wavefront vs 13.3 ms megakernel; 100 spheres 1.43 vs 0.98 ms)
-constexpr int kAutoWavefrontSpheres = 384;
+// AUTO picks the wavefront kernels for scenes where the sphere scan dominates (measured on B200,
+// C4 truncated to n spheres, round 2 kernels, ms per frame wavefront / megakernel: n = 32: 0.67 /
+// 0.43; 64: 0.77 / 0.78; 128: 0.97 / 1.48; 1000: 6.23 / 14.2; C3 (100 spheres): 0.87 / 1.02)
+constexpr int kAutoWavefrontSpheres = 64;
 
 int ensure_device() {
   int dev = 0;
