@@ -174,7 +174,10 @@ struct WfBuffers {
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth
-constexpr int kMaxLtLights = 32;  // point lights scanned from the light (RT_MAX_LIGHTS)
+// point lights scanned from the light: at most 30, lane l of wf_shade's one-round-trip slot
+// reservation takes light l's slots, lanes 30 / 31 the shadow entries / the continuations (more
+// point lights: every shadow ray goes through the general scan)
+constexpr int kMaxLtLights = 30;
 constexpr int kLtSub = 8;         // sub-lists per light (slot reservations spread over 8 counters)
 constexpr int kWfCtrPerDepth = 8 + kMaxLtLights * kLtSub;
 __host__ __device__ constexpr int wf_ctr_q(int d) { return kWfCtrPerDepth * d; }       // closest queue

@@ -104,6 +104,16 @@ def test_interleaved_order_and_tinted_glass(oracle_lib, seed, W, H, D, spp, vari
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("n_lights", [29, 30, 31, 32])
+def test_many_point_lights(oracle_lib, variant, n_lights):
+    """Up to 30 point lights are scanned from the light (one lane each in wf_shade's slot
+    reservation), 31-32 (RT_MAX_LIGHTS) through the general scan: both sides of the limit."""
+    sc = scenegen.random_tiny(40 + n_lights, n_spheres=9, n_planes=1, n_lights=n_lights, width=23, height=11,
+                              max_depth=3, spp=1)
+    _check(oracle_lib, sc, label=f"{n_lights} lights/{variant}", variant=variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 def test_tinted_glass_c2_shaped(oracle_lib, variant):
     """C2-sized frame of a scene with many coloured-glass spheres (every third material glass)."""
     sc = scenegen.random_tiny(31, n_spheres=12, n_planes=1, n_lights=2, width=96, height=64, max_depth=5, spp=1,
