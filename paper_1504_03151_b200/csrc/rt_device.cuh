@@ -279,16 +279,23 @@ struct RayFilter {
     for (int i = 1; i < kPairsPerBatch; ++i) vmax = fmaxf(vmax, fmaxf(v[i].x, v[i].y));
     return vmax;
   }
-  // Camera rays share their origin: s1 = K + 2 c'.o' is then the same for every ray and comes
-  // precomputed per sphere (pairs_eye: {c'x, c'y, c'z, s1} in the pair layout, rt_api.cu), so a
-  // sphere costs tc (3 FMA) + v = tc^2 + s1 (1 FMA) instead of 7 FMA. Same v, same cut; the
-  // precomputed s1 (FP64, rounded once) is more accurate than the FMA chain the slack covers.
+  // Shared-origin scans (camera rays, light-origin shadow rays) test the tangent condition
+  // c'.d - h >= o'.d instead of v >= cut (rt_api.cu neg_tangent: h per sphere precomputed): a hit
+  // at t > 0 from o outside the sphere needs tc >= h, and tc - h is 3 FMA per sphere. Its error
+  // (the FMA chain over |c'| + h <= 2 (cmax + |o'|), c' and d rounded to float, -h and o'.d
+  // rounded) stays below 11 kUlp (cmax + |o'|) <= 2 eta: candidates are the spheres with
+  // c'.d - h >= tangent_cut().
+  __device__ __forceinline__ float tangent_cut() const { return -b1 - 2.0f * eta; }
+  // dd and tc of sphere k for a shared origin whose s1 = K + 2 c'.o' comes precomputed (s1p, one
+  // float2 per pair, FP64 rounded once: more accurate than the FMA chain the slack covers)
   template <int kSrc>
-  __device__ __forceinline__ void sphere_eye(const float4* __restrict__ gp, int k, float& dd, float& tc) const {
+  __device__ __forceinline__ void sphere_s1(const float4* __restrict__ gp, const float2* __restrict__ s1p, int k,
+                                            float& dd, float& tc) const {
     const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
     const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
+    const float2 sv = s1p[k >> 1];
     const bool h = k & 1;
-    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, s1 = h ? pb.w : pb.z;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, s1 = h ? sv.y : sv.x;
     tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
     dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
   }

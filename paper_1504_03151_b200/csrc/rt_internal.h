@@ -95,9 +95,11 @@ struct DevScene {
   const DevMat* mats;
   const DevLight* lights;
   const int* emit_sph;     // [n_emitters] sphere index of emitter e (prim order), or null
-  const float4* pairs_eye; // pair layout with s1 = K + 2 c'.o'(eye) in place of K (camera rays)
-  // light-origin shadow scans: the pair layout followed by s1 = K + 2 c'.o'(P_l) per point light,
-  // float2 per sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy stages both)
+  // camera rays: the pair layout with -h(eye) in place of K (rt_api.cu neg_tangent), followed by
+  // s1 = K + 2 c'.o'(eye), float2 per sphere pair [n_pairs_pad]
+  const float4* pairs_eye;
+  // light-origin shadow scans: the pair layout followed by -h(P_l) per point light, float2 per
+  // sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy stages both)
   const float4* pairs_lt;
 };
 

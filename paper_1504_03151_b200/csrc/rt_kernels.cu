@@ -690,7 +690,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const IsectFn ksl = kSrc == SRC_TILE ? (IsectFn)wf_isect_tiled<true> : (IsectFn)wf_isect<kScan, true>;
   // camera rays (depth 0): two per thread through the shared-origin filter on the eye's pair table
   const IsectFn kc0 = kSrc == SRC_TILE ? (IsectFn)wf_isect_eye2_tiled : (IsectFn)wf_isect_eye2<kScan>;
-  const size_t smem_eye = smem_long;
+  // (shared-memory scene: the eye's table is the pairs plus one float2 s1 per pair)
+  const size_t smem_eye = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 40u : smem_long;
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
   size_t smem_lt = 0;
@@ -711,10 +712,12 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem > 0 ? smem : 1));
     if (e != cudaSuccess) return e;
   }
-  for (auto fn : {kcl, ksl, kc0}) {
+  for (auto fn : {kcl, ksl}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_long > 0 ? smem_long : 1));
     if (e != cudaSuccess) return e;
   }
+  e = cudaFuncSetAttribute(kc0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_eye > 0 ? smem_eye : 1));
+  if (e != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kcl, 256, smem_long)) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, ksl, 256, smem_long)) != cudaSuccess) return e;
   const int grid_c = num_sms * (occ_c > 0 ? occ_c : 1), grid_s = num_sms * (occ_s > 0 ? occ_s : 1);

@@ -661,23 +661,28 @@ wf_isect_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 }
 
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
-// The shared-origin filter needs 4 FMA per sphere, so one ray per thread leaves the kernel
-// co-limited by the shared-memory pipe (2 LDS.128 per 2 spheres). Here every lane carries two
-// camera rays (a warp = 64 rays): each pair of spheres read from shared memory serves both, and
-// the FFMA2 stream is again the only limit. Same filter, same candidate lists as wf_isect.
+// Camera rays share the origin (the eye), so the scan tests the tangent condition
+// c'.d - h >= o'.d (RayFilter::tangent_cut; -h per sphere in the eye's table, rt_api.cu
+// build_eye_pairs): 3 FMA per sphere and ray. One ray per thread would leave the kernel co-limited
+// by the shared-memory pipe (2 LDS.128 per 2 spheres); here every lane carries two camera rays (a
+// warp = 64 rays): each pair of spheres read from shared memory serves both, and the FFMA2 stream
+// is again the only limit. Candidates get the chord bounds of wf_isect (s1 precomputed, one
+// float2 per pair after the pairs), so the candidate lists hold the same decisions.
 constexpr int kEyePB = 8;
 static_assert(kPairsPerBatch % kEyePB == 0, "n_pairs_pad is padded to kPairsPerBatch");
 
 struct EyeRay {
   RayFilter F;
+  float cu;  // F.tangent_cut()
   float tub;
   int nc;
   bool act;
 };
 
 template <int kSrc>
-__device__ __forceinline__ void eye_candidates(const DevParams& P, const float4* __restrict__ gp, unsigned m,
-                                               int kbase, EyeRay& R, int* cand_row) {
+__device__ __forceinline__ void eye_candidates(const DevParams& P, const float4* __restrict__ gp,
+                                               const float2* __restrict__ s1p, unsigned m, int kbase, EyeRay& R,
+                                               int* cand_row) {
   const float eps_f = (float)kEps;
   while (m != 0u) {
     const int i = __ffs(m) - 1;
@@ -685,7 +690,8 @@ __device__ __forceinline__ void eye_candidates(const DevParams& P, const float4*
     const int k = kbase + i;
     if (k >= P.n_spheres) break;
     float dd, tc;
-    R.F.template sphere_eye<kSrc>(gp, k, dd, tc);
+    R.F.template sphere_s1<kSrc>(gp, s1p, k, dd, tc);
+    if (dd < R.F.neg_slack) continue;            // certainly no real root
     const float qh = sqrtf(fmaxf(dd - R.F.neg_slack, 0.f));
     const float ql = sqrtf(fmaxf(dd + R.F.neg_slack, 0.f));
     const bool sure = dd + R.F.neg_slack > 0.f;
@@ -704,46 +710,45 @@ __device__ __forceinline__ void eye_candidates(const DevParams& P, const float4*
 
 // the shared-origin scan of two camera rays (one thread) over the sphere pairs [pb, pe)
 template <int kSrc>
-__device__ __forceinline__ void eye2_scan(const DevParams& P, const float4* __restrict__ gp, int pb, int pe, EyeRay& Ra,
-                                          EyeRay& Rb, int* rowa, int* rowb) {
+__device__ __forceinline__ void eye2_scan(const DevParams& P, const float4* __restrict__ gp,
+                                          const float2* __restrict__ s1p, int pb, int pe, EyeRay& Ra, EyeRay& Rb,
+                                          int* rowa, int* rowb) {
   const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
-  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz);
   const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
-  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
+  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz);
   for (int base = pb; base < pe; base += kEyePB) {
-    float2 va[kEyePB], vb[kEyePB];
+    float2 ua[kEyePB], ub[kEyePB];
 #pragma unroll
     for (int i = 0; i < kEyePB; ++i) {
       const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
       const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
       const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w);
-      const float2 CZ = make_float2(b.x, b.y), S1 = make_float2(b.z, b.w);
-      const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
-      const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
-      va[i] = __ffma2_rn(ta, ta, S1);
-      vb[i] = __ffma2_rn(tb, tb, S1);
+      const float2 CZ = make_float2(b.x, b.y), NH = make_float2(b.z, b.w);
+      ua[i] = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, NH)));  // c'.d - h
+      ub[i] = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, NH)));
     }
-    float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+    float ma = fmaxf(ua[0].x, ua[0].y), mb = fmaxf(ub[0].x, ub[0].y);
 #pragma unroll
     for (int i = 1; i < kEyePB; ++i) {
-      ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
-      mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+      ma = fmaxf(ma, fmaxf(ua[i].x, ua[i].y));
+      mb = fmaxf(mb, fmaxf(ub[i].x, ub[i].y));
     }
-    const bool ca = Ra.act && ma >= Ra.F.cut, cb = Rb.act && mb >= Rb.F.cut;
+    const bool ca = Ra.act && ma >= Ra.cu, cb = Rb.act && mb >= Rb.cu;
     if (__any_sync(kFull, ca || cb)) {
       if (ca) {
         unsigned m = 0u;
 #pragma unroll
         for (int i = 0; i < kEyePB; ++i)
-          m |= ((va[i].x >= Ra.F.cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= Ra.F.cut) ? 1u : 0u) << (2 * i + 1);
-        eye_candidates<kSrc>(P, gp, m, 2 * base, Ra, rowa);
+          m |= ((ua[i].x >= Ra.cu) ? 1u : 0u) << (2 * i) | ((ua[i].y >= Ra.cu) ? 1u : 0u) << (2 * i + 1);
+        eye_candidates<kSrc>(P, gp, s1p, m, 2 * base, Ra, rowa);
       }
       if (cb) {
         unsigned m = 0u;
 #pragma unroll
         for (int i = 0; i < kEyePB; ++i)
-          m |= ((vb[i].x >= Rb.F.cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= Rb.F.cut) ? 1u : 0u) << (2 * i + 1);
-        eye_candidates<kSrc>(P, gp, m, 2 * base, Rb, rowb);
+          m |= ((ub[i].x >= Rb.cu) ? 1u : 0u) << (2 * i) | ((ub[i].y >= Rb.cu) ? 1u : 0u) << (2 * i + 1);
+        eye_candidates<kSrc>(P, gp, s1p, m, 2 * base, Rb, rowb);
       }
     }
   }
@@ -756,7 +761,8 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
   const float4* gp = S.pairs_eye;
-  if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 32u, &s_mbar);
+  if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 40u, &s_mbar);
+  const float2* s1p = reinterpret_cast<const float2*>((kSrc == SRC_SMEM ? s_pairs : gp) + 2 * P.n_pairs_pad);
   unsigned* work = B.ctr + wf_ctr_wc(d);
   const WfQueue Q = B.q[d & 1];
   const int lane = threadIdx.x & 31;
@@ -777,9 +783,12 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
       if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
       Rb.F.init(o, dir, P);
     }
+    Ra.cu = Ra.F.tangent_cut();
+    Rb.cu = Rb.F.tangent_cut();
     Ra.tub = Rb.tub = 3.0e38f;
     Ra.nc = Rb.nc = 0;
-    eye2_scan<kSrc>(P, gp, 0, P.n_pairs_pad, Ra, Rb, B.ccand + (size_t)ea * kCandMax, B.ccand + (size_t)eb * kCandMax);
+    eye2_scan<kSrc>(P, gp, s1p, 0, P.n_pairs_pad, Ra, Rb, B.ccand + (size_t)ea * kCandMax,
+                    B.ccand + (size_t)eb * kCandMax);
     if (ea < n) B.cn[ea] = Ra.nc;
     if (eb < n) B.cn[eb] = Rb.nc;
   }
@@ -794,6 +803,7 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
   const unsigned n = B.ctr[wf_ctr_q(d)];
   if ((unsigned long long)blockIdx.x * blockDim.x * 2ull >= n) return;  // CTAs without work
   const float4* gp = S.pairs_eye;
+  const float2* s1p = reinterpret_cast<const float2*>(gp + 2 * P.n_pairs_pad);  // candidates: from global
   TileRing ring;
   ring.init(s_full, gp, P.n_pairs_pad);
   const int ntiles = ring.ntiles;
@@ -825,13 +835,15 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
       if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
       Rb.F.init(o, dir, P);
     }
+    Ra.cu = Ra.F.tangent_cut();
+    Rb.cu = Rb.F.tangent_cut();
     Ra.tub = Rb.tub = 3.0e38f;
     Ra.nc = Rb.nc = 0;
     int* rowa = B.ccand + (size_t)(ea < n ? ea : 0u) * kCandMax;
     int* rowb = B.ccand + (size_t)(eb < n ? eb : 0u) * kCandMax;
     for (int t = 0; t < ntiles; ++t) {
       ring.wait(t);
-      eye2_scan<SRC_TILE>(P, gp, ring.begin(t), ring.end(t), Ra, Rb, rowa, rowb);
+      eye2_scan<SRC_TILE>(P, gp, s1p, ring.begin(t), ring.end(t), Ra, Rb, rowa, rowb);
       __syncthreads();  // buffer t & 1 is free
       if (threadIdx.x == 0 && t + 2 < ntiles) ring.issue(t + 2);
     }
@@ -844,11 +856,17 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // ---- a5 for point lights: the shadow scan from the light -------------------------------------
 // The segment [p + EPS_T n, P_l) is the same line whichever end it is traced from, and the scan
 // only filters (FP64 decides on the original ray in wf_accumulate). Traced from the light, every
-// shadow ray of light l shares the origin P_l: s1 = K + 2 c'.o'(P_l) comes precomputed per light
-// (S.pairs_lt), so a sphere costs tc' (3 FMA) + v = tc'^2 + s1 (1 FMA) instead of 7, and a thread
-// carries two rays of the same light (one shared-memory read serves both). Work comes in chunks of
-// 64 entries of one list. The chord [tc' - q, tc' + q] along the reversed ray maps back to
-// t = t_l - tc' -/+ q on the original one; the bounds add the error of t_l and of the reversal.
+// shadow ray of light l shares the origin P_l, and an occluder lies on the reversed half-line
+// s = t_l - t > 0: the tangent test c'.d' - h_l >= o'.d' (RayFilter::tangent_cut; -h_l per
+// sphere and light precomputed in S.pairs_lt, rt_api.cu neg_tangent) costs 3 FMA per sphere
+// instead of 7, and a thread carries two rays of the same light (one shared-memory read serves
+// both). Work comes in chunks of 64 entries of one list. The chord [tc' - q, tc' + q] along the
+// reversed ray maps back to t = t_l - tc' -/+ q on the original one; the bounds add the error of
+// t_l and of the reversal.
+// Why the half-line is safe: a sphere the test drops (light outside it by more than 1e-6 S, else
+// it is always a candidate) meets the reversed line, if at all, at s < -(gap)/2 <= -5e-7 S, i.e.
+// at t > t_l + 5e-7 S on the original ray, while the FP64 roots there are off by ~1e-15 (t_l + S);
+// a ray with t_l > 1e6 S (a far plane point) drops nothing (cu = -3e38).
 //
 // Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per CTA iteration,
 // the sub-list chosen by the iteration's 256-path block, so no single hot counter); a
@@ -863,6 +881,7 @@ static_assert(kPairsPerBatch % kLtPB == 0, "n_pairs_pad is padded to kPairsPerBa
 
 struct LtRay {
   RayFilter F;  // filter of the reversed ray (origin P_l, direction -d)
+  float cu;     // F.tangent_cut(), or -3e38 (every sphere a candidate) for t_l > 1e6 S
   float tl_f, tlerr;
   int nc, rob, skip;
   bool act;
@@ -893,13 +912,15 @@ __device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, 
     }
   }
   R.F.init(light_pos(S, l), -dt.x, -dt.y, -dt.z, P);
+  // S = cmax + |o'| + rmax = eta / (8 kUlp) + rmax (RayFilter::init)
+  R.cu = dt.w > 1.0e6f * (R.F.eta * (1.0f / (8.0f * kUlp)) + P.rmax) ? -3.0e38f : R.F.tangent_cut();
   R.tl_f = dt.w;
   R.tlerr = 4.0e-7f * R.tl_f + 1.0e-6f * R.F.eta;  // t_l to float, P_l vs o + t_l d, the subtraction
 }
 
 template <int kSrc>
-__device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ s1p,
-                                              unsigned m, int kbase, LtRay& R, int* cand_row) {
+__device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* __restrict__ gp, unsigned m, int kbase,
+                                              LtRay& R, int* cand_row) {
   const float eps_f = (float)kEps;
   while (m != 0u) {
     const int i = __ffs(m) - 1;
@@ -907,13 +928,9 @@ __device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* 
     const int k = kbase + i;
     if (k >= P.n_spheres) break;
     if (k == R.skip) continue;
-    const float4 pa = load_pair<kSrc>(gp, 2 * (k >> 1));
-    const float4 pb = load_pair<kSrc>(gp, 2 * (k >> 1) + 1);
-    const float2 s1v = s1p[k >> 1];
-    const bool h = k & 1;
-    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, s1 = h ? s1v.y : s1v.x;
-    const float tc = fmaf(cx, R.F.dx, fmaf(cy, R.F.dy, fmaf(cz, R.F.dz, R.F.b1)));  // along -d from P_l
-    const float dd = fmaf(tc, tc, s1) - (R.F.cut - R.F.neg_slack);
+    float dd, tc;  // tc along -d from P_l
+    R.F.template sphere<kSrc>(gp, k, dd, tc);
+    if (dd < R.F.neg_slack) continue;                  // certainly no real root
     const float qh = sqrtf(fmaxf(dd - R.F.neg_slack, 0.f));
     const float ql = sqrtf(fmaxf(dd + R.F.neg_slack, 0.f));
     const bool sure = dd + R.F.neg_slack > 0.f;
@@ -938,47 +955,44 @@ __device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* 
 
 // the light-origin scan of two rays of light l (one thread) over the sphere pairs [pb, pe)
 template <int kSrc>
-__device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ s1p,
+__device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ nhp,
                                         int pb, int pe, LtRay& Ra, LtRay& Rb, int* rowa, int* rowb) {
   const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
-  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz), B1a = make_float2(Ra.F.b1, Ra.F.b1);
+  const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz);
   const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
-  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz), B1b = make_float2(Rb.F.b1, Rb.F.b1);
-  const float cut = Ra.F.cut;  // depends on the origin P_l only: the same for both rays
+  const float2 D3b = make_float2(Rb.F.dz, Rb.F.dz);
   for (int base = pb; base < pe; base += kLtPB) {
-    float2 va[kLtPB], vb[kLtPB];
+    float2 ua[kLtPB], ub[kLtPB];
 #pragma unroll
     for (int i = 0; i < kLtPB; ++i) {
       const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
       const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-      const float2 S1 = s1p[base + i];
+      const float2 NH = nhp[base + i];
       const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w), CZ = make_float2(b.x, b.y);
-      const float2 ta = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, B1a)));
-      const float2 tb = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, B1b)));
-      va[i] = __ffma2_rn(ta, ta, S1);
-      vb[i] = __ffma2_rn(tb, tb, S1);
+      ua[i] = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, NH)));  // c'.d' - h_l
+      ub[i] = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, NH)));
     }
-    float ma = fmaxf(va[0].x, va[0].y), mb = fmaxf(vb[0].x, vb[0].y);
+    float ma = fmaxf(ua[0].x, ua[0].y), mb = fmaxf(ub[0].x, ub[0].y);
 #pragma unroll
     for (int i = 1; i < kLtPB; ++i) {
-      ma = fmaxf(ma, fmaxf(va[i].x, va[i].y));
-      mb = fmaxf(mb, fmaxf(vb[i].x, vb[i].y));
+      ma = fmaxf(ma, fmaxf(ua[i].x, ua[i].y));
+      mb = fmaxf(mb, fmaxf(ub[i].x, ub[i].y));
     }
-    const bool ca = Ra.act && ma >= cut, cb = Rb.act && mb >= cut;
+    const bool ca = Ra.act && ma >= Ra.cu, cb = Rb.act && mb >= Rb.cu;
     if (__any_sync(kFull, ca || cb)) {
       if (ca) {
         unsigned m = 0u;
 #pragma unroll
         for (int i = 0; i < kLtPB; ++i)
-          m |= ((va[i].x >= cut) ? 1u : 0u) << (2 * i) | ((va[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
-        lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Ra, rowa);
+          m |= ((ua[i].x >= Ra.cu) ? 1u : 0u) << (2 * i) | ((ua[i].y >= Ra.cu) ? 1u : 0u) << (2 * i + 1);
+        lt_candidates<kSrc>(P, gp, m, 2 * base, Ra, rowa);
       }
       if (cb) {
         unsigned m = 0u;
 #pragma unroll
         for (int i = 0; i < kLtPB; ++i)
-          m |= ((vb[i].x >= cut) ? 1u : 0u) << (2 * i) | ((vb[i].y >= cut) ? 1u : 0u) << (2 * i + 1);
-        lt_candidates<kSrc>(P, gp, s1p, m, 2 * base, Rb, rowb);
+          m |= ((ub[i].x >= Rb.cu) ? 1u : 0u) << (2 * i) | ((ub[i].y >= Rb.cu) ? 1u : 0u) << (2 * i + 1);
+        lt_candidates<kSrc>(P, gp, m, 2 * base, Rb, rowb);
       }
     }
     if (!__any_sync(kFull, Ra.act || Rb.act)) break;  // Alg. 1 `break`, warp-wide
@@ -1027,7 +1041,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
-  const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
+  const float2* nh_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
   const int lane = threadIdx.x & 31;
   const int nl = P.lt_lights * kLtSub;
   while (true) {
@@ -1046,7 +1060,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
     LtRay Ra, Rb;
     lt_setup(P, S, B, ga, va_, l, Ra);
     lt_setup(P, S, B, gb, vb_, l, Rb);
-    lt_scan<kSrc>(P, gp, s1_all + (size_t)l * P.n_pairs_pad, 0, P.n_pairs_pad, Ra, Rb, B.lt_cand + (size_t)ga * kCandMax,
+    lt_scan<kSrc>(P, gp, nh_all + (size_t)l * P.n_pairs_pad, 0, P.n_pairs_pad, Ra, Rb, B.lt_cand + (size_t)ga * kCandMax,
                   B.lt_cand + (size_t)gb * kCandMax);
     if (va_) B.lt_res[ga] = make_int2(Ra.rob, Ra.nc);
     if (vb_) B.lt_res[gb] = make_int2(Rb.rob, Rb.nc);
@@ -1073,7 +1087,7 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
   if (blockIdx.x >= units) return;  // CTAs without work leave before staging the scene
   stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
   const float4* gp = S.pairs_lt;
-  const float2* s1_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
+  const float2* nh_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
   const int slot = warp / parts, part = warp % parts;
   const int nl = P.lt_lights * kLtSub;
   int pb, pe;
@@ -1098,7 +1112,7 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
     LtRay Ra, Rb;
     lt_setup(P, S, B, ga, va_, l, Ra);
     lt_setup(P, S, B, gb, vb_, l, Rb);
-    lt_scan<kSrc>(P, gp, s1_all + (size_t)l * P.n_pairs_pad, pb, pe, Ra, Rb, xa, xb);
+    lt_scan<kSrc>(P, gp, nh_all + (size_t)l * P.n_pairs_pad, pb, pe, Ra, Rb, xa, xb);
     s_nc[warp][lane] = Ra.nc;
     s_nc[warp][lane + 32] = Rb.nc;
     s_rob[warp][lane] = Ra.rob;

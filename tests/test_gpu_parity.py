@@ -113,6 +113,50 @@ def test_many_point_lights(oracle_lib, variant, n_lights):
     _check(oracle_lib, sc, label=f"{n_lights} lights/{variant}", variant=variant)
 
 
+def _shared_origin_scene(case):
+    """Edge cases of the shared-origin tangent test (camera rays and light-origin shadow scans,
+    rt_api.cu neg_tangent): the eye or a light inside a sphere, exactly on its surface, within
+    1e-6 S of it (always a candidate) and just beyond that; a horizon-grazing ground plane gives
+    shading points at huge t_l (the light-origin scan drops nothing past t_l > 1e6 S)."""
+    g = scenegen.SplitMix64(900 + case)
+    b = scenegen.builder()
+    f32 = lambda x: float(np.float32(x))
+    dif = b.material(scenegen.DIFFUSE, (0.7, 0.6, 0.5), ks=0.3, shininess=20.0, kr=0.2)
+    mir = b.material(scenegen.SPECULAR, (0.9, 0.9, 0.9))
+    gls = b.material(scenegen.REFRACTIVE, (1, 1, 1), ior=1.5)
+    for i in range(40):
+        c = (g.uniform(-6, 6), g.uniform(-2, 4) if case < 3 else g.uniform(1.5, 5), g.uniform(3, 16))
+        b.sphere(tuple(f32(x) for x in c), f32(g.uniform(0.3, 1.2)), (dif, mir, gls)[i % 3])
+    # case 3: a ground plane tilted by 1e-8: the image's centre row (dy = 0) meets it at t ~ 2e8
+    b.plane((0, 1, -1e-8) if case == 3 else (0, 1, 0), -2.0, dif)
+    eye = (0.0, 0.0, 0.0)
+    if case == 0:    # eye inside a glass sphere; a light inside another sphere
+        b.sphere((0.25, 0.0, 0.5), 1.0, gls)
+        b.sphere((5.0, 6.0, 9.0), 0.5, dif)
+        b.light((5.0, 6.0, 9.0), (60, 60, 60))
+    elif case == 1:  # eye exactly on a sphere's surface; a light exactly on another's
+        b.sphere((0.0, 0.0, -1.0), 1.0, dif)
+        b.sphere((3.0, 5.0, 8.0), 1.0, dif)
+        b.light((3.0, 4.0, 8.0), (60, 60, 60))
+    elif case == 2:  # within 1e-6 S (always candidates) and at 1e-4 of the surface (tested)
+        b.sphere((0.0, 0.0, f32(-1.0 - 2e-6)), 1.0, mir)
+        b.sphere((3.0, 5.0, 8.0), 1.0, dif)
+        b.light((3.0, f32(4.0 - 2e-6), 8.0), (60, 60, 60))
+        b.light((-3.0, f32(4.0 - 1e-4), 8.0), (40, 40, 40))
+        b.sphere((-3.0, 5.0, 8.0), 1.0, gls)
+    else:            # far shading points: t_l ~ 2e8 > 1e6 S
+        b.light((0.0, 3.0, 6.0), (80, 80, 80))
+    b.light((-4.0, 8.0, 2.0), (50, 50, 50))
+    return b.build(f"shared-origin-{case}", eye=eye, look_at=(0.0, 0.0, 1.0), up=(0, 1, 0), vfov=60,
+                   width=48, height=33, max_depth=3, spp=1, background=(0.1, 0.2, 0.3))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("case", [0, 1, 2, 3])
+def test_shared_origin_edge_cases(oracle_lib, variant, case):
+    _check(oracle_lib, _shared_origin_scene(case), label=f"shared-origin {case}/{variant}", variant=variant)
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_tinted_glass_c2_shaped(oracle_lib, variant):
     """C2-sized frame of a scene with many coloured-glass spheres (every third material glass)."""
