@@ -423,7 +423,8 @@ def run_b200(args):
         value = rays / (ms_per_step * 1e-3) / 1e6
         # roofline of the dominant kernel (the largest share of the in-order frame):
         #  * scans: bound "alu"; achieved = EXECUTED FP32 flops (the FMAs the filter form needs per
-        #    test: 4 FMA for camera rays and light-origin shadow rays, 7 FMA for secondary rays)
+        #    test: 3 FMA for camera rays and light-origin shadow rays (the tangent test of a shared
+        #    origin), 7 FMA for secondary rays)
         #    per second of the kernel's own launches; peak = the FFMA2 microbenchmark measured on
         #    this box in this run; the counted figure (19 flops per test) beside it;
         #  * wf_shade / wf_accumulate: bound "hbm"; achieved = algorithmic bytes /
@@ -445,14 +446,14 @@ def run_b200(args):
             n_closest = st["closest_sphere_tests"]
             n_eye = st["primary"] * sc.n_spheres
             n_shadow = st["sphere_tests"] - n_closest
-            sh_fma = 4 if sc.n_lights > 0 else 7
+            sh_fma = 3 if 0 < sc.n_lights <= 30 else 7  # light-origin scans for <= 30 point lights
             prim, sec, shd = st["primary"], st["secondary"], st["shadow"]
             cands = {
                 "shadow": {"kernel": "wf_isect_lt (shadow rays to point lights, scanned from the light; FP32 FFMA2, "
                                      "early exit at a certain occluder)", "bound": "alu",
                            "ms": kt["shadow"], "tests": n_shadow, "fma_per_test": sh_fma},
                 "camera": {"kernel": "wf_isect_eye2 (camera rays, shared-origin FP32 FFMA2 scan)", "bound": "alu",
-                           "ms": kt["eye"], "tests": n_eye, "fma_per_test": 4},
+                           "ms": kt["eye"], "tests": n_eye, "fma_per_test": 3},
                 "secondary": {"kernel": "wf_isect<closest> (secondary closest-hit rays, FP32 FFMA2 scan)", "bound": "alu",
                               "ms": kt["closest"] - kt["eye"], "tests": n_closest - n_eye, "fma_per_test": 7},
                 # algorithmic bytes: per shaded path the ray state in (84 B at depth >= 1;
@@ -505,7 +506,8 @@ def run_b200(args):
                     "traffic": traffic, "kernel": kernel, **extra,
                     "peak_basis": peak_basis if bound == "alu" else "MEASURED_PEAKS.json hbm_gbs (burst copy bandwidth)",
                     "fp32_peak_measured": fp32,
-                    "flops_basis": "executed: 4 FMA per camera-ray / light-origin shadow test, 7 per secondary test; "
+                    "flops_basis": "executed: 3 FMA per camera-ray / light-origin shadow test (tangent test), "
+                                   "7 per secondary test; "
                                    "counted: 19 flops/sphere test + 12/plane test (SURVEY 8(d).3)"}
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
