@@ -868,7 +868,7 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // at t > t_l + 5e-7 S on the original ray, while the FP64 roots there are off by ~1e-15 (t_l + S);
 // a ray with t_l > 1e6 S (a far plane point) drops nothing (cu = -3e38).
 //
-// Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per CTA iteration,
+// Input: light l's rays are listed in kLtSub sub-lists (wf_shade reserves slots per warp group,
 // the sub-list chosen by the iteration's 256-path block, so no single hot counter); a
 // slot holds the ray's direction and t_max rounded to float (what the filter reads; wf_shade
 // computed them in FP64) and {shading entry e of Q[d], skip}: skip = the sphere the ray provably
@@ -1208,6 +1208,18 @@ __device__ __forceinline__ void shadow_counts(const DevParams& P, const DevScene
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
 constexpr int kLogicMinBlocks = 4;  // wf_accumulate: 64 registers, 4 CTAs per SM
 constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~190 B spilled, 10 % slower)
+#ifndef RT_RES_WARPS
+#define RT_RES_WARPS 4
+#endif
+// warps that reserve light-origin list slots together (C4 frame: 8 -> 5.842, 4 -> 5.832,
+// 2 -> 5.876, 1 -> 5.907 ms: smaller groups wait less, but their list ranges are less coherent)
+constexpr int kResWarps = RT_RES_WARPS;
+static_assert(8 % kResWarps == 0, "groups of a 256-thread CTA");
+// barrier of the n threads of named barrier `id` (a group of whole warps)
+__device__ __forceinline__ void group_sync(int id, int n) {
+  if (n == 256) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // kExt: the NEXT-1/NEXT-2 extensions (emitters sampled as area lights, the global integrator)
 // are compiled in; the §8(a) hot path (Whitted, point lights) runs the kExt = false instance.
 //
@@ -1219,10 +1231,11 @@ constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~1
 //  * any other source (emitters, or every light when the scene is not in shared memory): a dense
 //    generic slot o (spos[j] = -2 - o) holding the FP64 shadow ray, its skips and the scan results.
 // Every slot a warp needs is reserved in one round trip: lane-parallel atomics for the shadow
-// entries, the continuations and the generic slots; the light-origin lists per CTA (one atomic per
-// light and CTA iteration, warps in order, so a list keeps the CTA's 256 neighbouring paths
-// together: coherent early exits in the scan). The CTA barrier of that reservation sits before the
-// light loop, so warps wait for the slowest warp's hit and bounce, not for its light loop.
+// entries, the continuations and the generic slots; the light-origin lists per group of kResWarps
+// warps (one atomic per light and group iteration, warps in order, so a list keeps the group's
+// 128 neighbouring paths together: coherent early exits in the scan). The group barrier of that
+// reservation sits before the light loop, so warps wait for the slowest warp's hit and bounce,
+// not for its light loop.
 template <bool kDebug, bool kExt>
 __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams P, const DevScene S, WfBuffers B, int d,
                                                 long long g0, int* dbg_hits, int* dbg_bounces) {
@@ -1404,20 +1417,22 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
       RT_CHECK(lane != 30 || base + cnt <= (unsigned)B.scap, 101);  // shadow entries fit scap
       RT_CHECK(lane != 31 || base + cnt <= (unsigned)B.cap, 102);   // continuations fit Q[d+1]
       RT_CHECK(lane >= nres || lane < LT || base + cnt <= (unsigned)B.gcap, 103);  // generic slots fit gcap
-      __syncthreads();
-      if (threadIdx.x < (unsigned)LT) {  // one atomic per light and CTA; warps in order
-        const int l = threadIdx.x;
+      // the group's warps (kResWarps of them, named barrier 1 + group) reserve together
+      const int grp = warp / kResWarps, w0g = grp * kResWarps;
+      group_sync(1 + grp, 32 * kResWarps);
+      if (warp == w0g && lane < LT) {  // one atomic per light and group; warps in order
+        const int l = lane;
         unsigned tot = 0;
-        for (int w = 0; w < 8; ++w) tot += s_cnt[w][l];
+        for (int w = w0g; w < w0g + kResWarps; ++w) tot += s_cnt[w][l];
         unsigned b0 = tot ? atomicAdd(B.ctr + wf_ctr_lt(d, l, sub), tot) : 0u;
         RT_CHECK(b0 + tot <= (unsigned)B.lt_cap, 104);  // a light-origin sub-list fits lt_cap
-        for (int w = 0; w < 8; ++w) {
+        for (int w = w0g; w < w0g + kResWarps; ++w) {
           const unsigned c = s_cnt[w][l];
           s_cnt[w][l] = b0;
           b0 += c;
         }
       }
-      __syncthreads();
+      group_sync(1 + grp, 32 * kResWarps);
       if (lane < LT) base = s_cnt[warp][lane];
       off = __shfl_sync(kFull, base, 30) + pre_sh;
       const unsigned slot = __shfl_sync(kFull, base, 31) + (unsigned)__popc(mc & lt_mask_lane);
