@@ -392,6 +392,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
   return RT_OK;
 }
 
+constexpr int kHostMinChunks = 4;
 // host_out (optional): the caller's host framebuffer for a mode-0 render into the staging buffer
 // `out`; the wavefront variant then copies each chunk's finished rows as soon as it resolves
 // (RT_OK with *copied = true), else the caller copies the whole frame after the render
@@ -411,9 +412,8 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   const bool wavefront = c.variant == RT_VARIANT_WAVEFRONT ||
                          (c.variant == RT_VARIANT_AUTO && (extended || c.n_spheres >= kAutoWavefrontSpheres));
   if (wavefront) {
-    // chunks of whole pixels, at most 2^22 paths each (smaller chunks for host framebuffers hide
-    // more of the row copies but cost more than they hide: C4 e2e 10.6 ms at 2^22, 11.4 at 2^21);
-    // a frame that fills fewer chunks than pipeline slots is cut into one chunk per slot
+    // chunks of whole pixels, at most 2^22 paths each; a frame that fills fewer chunks than
+    // pipeline slots (or than p.min_chunks, host framebuffers) is cut into that many
     const int nslots = c.concurrent ? c.pipeline : 1;
     const int ipc = rt::wf_items_per_chunk(p, nslots);
     const int cap = ipc * p.spp;
@@ -630,6 +630,10 @@ int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba,
   rt::DevParams p = make_params(W, H, D, spp);
   p.mode = 0;
   p.n_items = p.n_tiles * rt::kTilePx;
+  // a host framebuffer: at least kHostMinChunks chunks, so the first chunks' rows are copied
+  // while the last ones render (two chunks start and finish together, and the whole 33 MB D2H of
+  // a C4 frame came after the render: rt_render into pinned memory 6.51 ms -> 6.40 with 4)
+  if (!dev_out && !dbg && !accum) p.min_chunks = kHostMinChunks;
   if (accum) {  // progressive passes (R#42)
     p.jitter = 1;
     p.sample_base = sample_base;

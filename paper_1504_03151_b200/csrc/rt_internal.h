@@ -79,7 +79,7 @@ struct DevParams {
   int lt_lights;      // point lights whose shadow rays are scanned from the light (0 = off)
   int n_emitters;     // emissive spheres sampled as area lights (0 = area lights off)
   int jitter;         // 1: random sub-pixel offsets from RNG streams 1/2 (progressive passes)
-  int pad_;
+  int min_chunks;     // host side: cut the frame into at least this many chunks (0: no minimum)
   long long sample_base;  // global index of sample 0 (pass index of the first pass)
   // job: full frame (mode 0, tile-major work items, row-major output) or shard (mode 1)
   // mode 0: full frame, tile-major items, row-major output; 1: shard, slab output (tile-major);

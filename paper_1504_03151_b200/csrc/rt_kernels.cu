@@ -640,15 +640,16 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int gcap, int lt_list
   B.ctr = ctr;
 }
 
-// work items (pixels) per chunk: at most 2^22 paths per chunk; with nslots > 1 a frame that
-// would fill fewer chunks than slots is cut into nslots chunks (each >= 2^17 paths), so the chunks
-// overlap (DESIGN.md §7 "chunk pipelining")
+// work items (pixels) per chunk: at most 2^22 paths per chunk; a frame that would fill fewer
+// chunks than max(slots, p.min_chunks) is cut into that many (each >= 2^17 paths), so the chunks
+// overlap (DESIGN.md §7 "chunk pipelining"; min_chunks: host framebuffers)
 int wf_items_per_chunk(const DevParams& p, int nslots) {
   const long long paths = (long long)p.n_items * p.spp;
   const int max_items = (1 << 22) / p.spp > 0 ? (1 << 22) / p.spp : 1;
   long long chunks = (p.n_items + max_items - 1) / max_items;
-  if (nslots > 1 && chunks < nslots) {
-    long long want = nslots;
+  const long long want_min = nslots > p.min_chunks ? nslots : p.min_chunks;
+  if (want_min > 1 && chunks < want_min) {
+    long long want = want_min;
     while (want > 1 && paths / want < (1 << 17)) --want;
     if (want > chunks) chunks = want;
   }
