@@ -83,8 +83,6 @@ struct Context {
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt;
   int lt_lights = 0;  // point lights with light-origin shadow scans (0 = off)
-  std::vector<float4> pairs_host, pairs_eye_host;  // expanded-form pairs; the camera-ray table
-  std::vector<float4> sph_host;                    // {c, r} per sphere (float inputs), host copy
   bool eye_ready = false;
   DevBuf<int> sph_prim, sph_mat, emit_sph;
   int n_emitters = 0;  // emissive spheres (prim order)
@@ -211,51 +209,26 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   return p;
 }
 
-// Tangent test of a shared origin o (rt_wavefront.cuh eye2_scan, lt_scan). For a sphere {c, r}
-// with o outside it, a ray o + t d (|d| = 1) meets the sphere at some t > 0 iff
-// (c - o).d >= h, h = sqrt(|c - o|^2 - r^2) the distance from o to the tangent points (Eq. 11:
-// the roots t = tc -/+ sqrt(tc^2 - h^2) are real iff |tc| >= h and share the sign of tc). The
-// table holds -h (FP64 from the float inputs, rounded once); a sphere that contains o or whose
-// surface passes within 1e-6 S of it (S = cmax + |o'| + rmax bounds the scene seen from o) gets
-// +3e38: always a candidate, the chord bounds decide.
-static float neg_tangent(const float4& cr, const double o[3], double S) {
-  const double x = (double)cr.x - o[0], y = (double)cr.y - o[1], z = (double)cr.z - o[2];
-  const double dist = std::sqrt(x * x + y * y + z * z), r = cr.w;
-  if (dist - r <= 1e-6 * S) return 3.0e38f;
-  return (float)-std::sqrt((dist - r) * (dist + r));
-}
+// Shared-origin tables (rt_wavefront.cuh eye2_scan, lt_scan): built on the device from the
+// uploaded pairs and spheres (rt_kernels.cu build_eye_table / build_light_tables: -h of the
+// tangent test per sphere, FP64 rounded once). S = cmax + |o'| + rmax bounds the
+// scene seen from o.
 static double view_scale(const Context& c, const double o[3]) {
   const double x = o[0] - c.centre[0], y = o[1] - c.centre[1], z = o[2] - c.centre[2];
   return (double)c.cmax + std::sqrt(x * x + y * y + z * z) + (double)c.rmax;
 }
 
 // Camera rays share the origin `eye`. The table (wf_isect_eye2): the pair layout with -h of the
-// eye (neg_tangent) in place of K, then s1 = K + 2 c'.o'(eye) per sphere (one float2 per pair,
-// FP64 rounded once) for the candidates' chord bounds.
+// eye in place of K, then s1 = K + 2 c'.o'(eye) per sphere (one float2 per pair) for the
+// candidates' chord bounds.
 int build_eye_pairs() {
   Context& c = g_ctx;
   c.eye_ready = false;
-  if (!c.has_scene || !c.has_camera || c.pairs_host.empty()) return RT_OK;
-  const double ox = c.eye[0] - c.centre[0], oy = c.eye[1] - c.centre[1], oz = c.eye[2] - c.centre[2];
-  const size_t npp = c.pairs_host.size() / 2;
-  const double S = view_scale(c, c.eye);
-  c.pairs_eye_host.assign(2 * npp + (npp + 1) / 2, make_float4(0.f, 0.f, 0.f, 0.f));
-  std::memcpy(c.pairs_eye_host.data(), c.pairs_host.data(), sizeof(float4) * 2 * npp);
-  float2* s1 = reinterpret_cast<float2*>(c.pairs_eye_host.data() + 2 * npp);
-  for (size_t q = 0; q < npp; ++q) {
-    const float4 a = c.pairs_host[2 * q], b = c.pairs_host[2 * q + 1];
-    float4& be = c.pairs_eye_host[2 * q + 1];
-    s1[q] = make_float2((float)((double)b.z + 2.0 * ((double)a.x * ox + (double)a.z * oy + (double)b.x * oz)),
-                        (float)((double)b.w + 2.0 * ((double)a.y * ox + (double)a.w * oy + (double)b.y * oz)));
-    for (int h = 0; h < 2; ++h) {
-      const size_t k = 2 * q + h;
-      (h ? be.w : be.z) = k < c.sph_host.size() ? neg_tangent(c.sph_host[k], c.eye, S) : -1e30f;  // dummies never pass
-    }
-  }
-  CU(c.pairs_eye.reserve(c.pairs_eye_host.size()), "cudaMalloc(eye pairs)");
-  CU(cudaMemcpyAsync(c.pairs_eye.p, c.pairs_eye_host.data(), sizeof(float4) * c.pairs_eye_host.size(),
-                     cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // the host copy may change next call
+  if (!c.has_scene || !c.has_camera || c.n_pairs_pad == 0) return RT_OK;
+  const int npp = c.n_pairs_pad;
+  CU(c.pairs_eye.reserve(2 * (size_t)npp + (npp + 1) / 2), "cudaMalloc(eye pairs)");
+  CU(rt::launch_eye_table(c.pairs.p, c.sph_cr.p, c.n_spheres, npp, c.eye, c.centre, view_scale(c, c.eye),
+                          c.pairs_eye.p, c.stream), "eye table kernel");
   c.eye_ready = true;
   return RT_OK;
 }
@@ -914,7 +887,8 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
   const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
   CU(rt::upload_planes(planes.data(), np, c.stream), "constant upload (planes)");
-  CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");  // host vectors die at return
+  // (no stream sync: an async copy from pageable memory returns once the data is staged, so the
+  // host vectors may die at return; the tables below are built on the device from these copies)
   c.smem_scene = in_smem;
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
   for (int k = 0; k < 3; ++k) c.centre[k] = centre[k];
@@ -930,27 +904,16 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     c.amb[k] = env ? env->ambient[k] : 0.f;
   }
   c.has_scene = true;
-  c.pairs_host = pairs;
-  c.sph_host.assign(cr.begin(), cr.begin() + ns);
   // light-origin shadow scans (rt_wavefront.cuh wf_isect_lt): after a copy of the pairs, -h of
-  // each point light per sphere (neg_tangent, one float2 per pair and light); on while the
-  // tables fit 64 KB of shared memory
+  // each point light per sphere (one float2 per pair and light, built on the device); on while
+  // the tables fit 64 KB of shared memory
   c.lt_lights = 0;
   const size_t lt_bytes = (size_t)n_lights * npairs_pad * 8;
   if (n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
       lt_bytes <= 65536 && in_smem) {
-    std::vector<float4> lt(2 * (size_t)npairs_pad + lt_bytes / 16 + 1);
-    std::memcpy(lt.data(), pairs.data(), sizeof(float4) * pairs.size());
-    float* nh = reinterpret_cast<float*>(lt.data() + 2 * (size_t)npairs_pad);
-    for (int l = 0; l < n_lights; ++l) {
-      const double pl[3] = {lights[l].position[0], lights[l].position[1], lights[l].position[2]};
-      const double S = view_scale(c, pl);
-      for (int k = 0; k < 2 * npairs_pad; ++k)
-        nh[(size_t)l * 2 * npairs_pad + k] = k < ns ? neg_tangent(cr[k], pl, S) : -1e30f;  // dummies never pass
-    }
-    CU(c.pairs_lt.reserve(lt.size()), "cudaMalloc(light pairs)");
-    CU(cudaMemcpyAsync(c.pairs_lt.p, lt.data(), sizeof(float4) * lt.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-    CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
+    CU(c.pairs_lt.reserve(2 * (size_t)npairs_pad + lt_bytes / 16 + 1), "cudaMalloc(light pairs)");
+    CU(rt::launch_light_tables(c.pairs.p, c.sph_cr.p, c.lights.p, ns, npairs_pad, n_lights, c.centre, c.cmax, c.rmax,
+                               c.pairs_lt.p, c.stream), "light table kernel");
     c.lt_lights = n_lights;
   }
   return build_eye_pairs();

@@ -498,6 +498,65 @@ __global__ void tonemap_kernel(const float4* __restrict__ in, uchar4* __restrict
   }
 }
 
+// ---- shared-origin tables (rt_api.cu: the eye's after rt_camera_set, the lights' after upload) -
+// Tangent test: -h = -sqrt((|c - o| - r)(|c - o| + r)) per sphere in FP64 from the
+// float inputs, rounded once; +3e38 (always a candidate) when o is inside the sphere or within
+// 1e-6 S of its surface; -1e30 for the padding slots (never a candidate).
+__device__ __forceinline__ float neg_tangent(const float4 cr, double ox, double oy, double oz, double S) {
+  const double x = (double)cr.x - ox, y = (double)cr.y - oy, z = (double)cr.z - oz;
+  const double dist = sqrt(x * x + y * y + z * z), r = cr.w;
+  if (dist - r <= 1e-6 * S) return 3.0e38f;
+  return (float)-sqrt((dist - r) * (dist + r));
+}
+// The eye's table: pair q = {c'x, c'y | c'z, -h}, then s1 = K + 2 c'.o' (FP64, rounded once) for
+// the candidates' chord bounds. One thread per pair.
+__global__ void build_eye_table(const float4* __restrict__ pairs, const float4* __restrict__ sph_cr, int ns, int npp,
+                                double ox, double oy, double oz, double cx, double cy, double cz, double S,
+                                float4* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npp) return;
+  const float4 a = pairs[2 * q], b = pairs[2 * q + 1];
+  const double px = ox - cx, py = oy - cy, pz = oz - cz;  // o' = o - centre
+  float4 nb = b;
+  nb.z = 2 * q < ns ? neg_tangent(sph_cr[2 * q], ox, oy, oz, S) : -1e30f;
+  nb.w = 2 * q + 1 < ns ? neg_tangent(sph_cr[2 * q + 1], ox, oy, oz, S) : -1e30f;
+  out[2 * q] = a;
+  out[2 * q + 1] = nb;
+  float2* s1 = reinterpret_cast<float2*>(out + 2 * npp);
+  s1[q] = make_float2((float)((double)b.z + 2.0 * ((double)a.x * px + (double)a.z * py + (double)b.x * pz)),
+                      (float)((double)b.w + 2.0 * ((double)a.y * px + (double)a.w * py + (double)b.y * pz)));
+}
+// The light-origin tables: the pairs, then -h of light l for every sphere slot k
+// (out + 2 npp as floats, [l][2 npp]). One thread per (light, sphere slot).
+__global__ void build_light_tables(const float4* __restrict__ pairs, const float4* __restrict__ sph_cr,
+                                   const DevLight* __restrict__ lights, int ns, int npp, int n_lights, double cx,
+                                   double cy, double cz, float cmax, float rmax, float4* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 2 * npp) out[i] = pairs[i];
+  if (i >= n_lights * 2 * npp) return;
+  const int l = i / (2 * npp), k = i - l * 2 * npp;
+  const DevLight L = lights[l];
+  const double ox = L.px, oy = L.py, oz = L.pz;
+  const double px = ox - cx, py = oy - cy, pz = oz - cz;
+  const double S = (double)cmax + sqrt(px * px + py * py + pz * pz) + (double)rmax;
+  reinterpret_cast<float*>(out + 2 * npp)[i] = k < ns ? neg_tangent(sph_cr[k], ox, oy, oz, S) : -1e30f;
+}
+
+cudaError_t launch_eye_table(const float4* pairs, const float4* sph_cr, int ns, int npp, const double o[3],
+                             const double centre[3], double S, float4* out, cudaStream_t st) {
+  build_eye_table<<<(npp + 255) / 256, 256, 0, st>>>(pairs, sph_cr, ns, npp, o[0], o[1], o[2], centre[0], centre[1],
+                                                     centre[2], S, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_light_tables(const float4* pairs, const float4* sph_cr, const DevLight* lights, int ns, int npp,
+                                int n_lights, const double centre[3], float cmax, float rmax, float4* out,
+                                cudaStream_t st) {
+  const int n = (n_lights > 1 ? n_lights : 1) * 2 * npp;
+  build_light_tables<<<(n + 255) / 256, 256, 0, st>>>(pairs, sph_cr, lights, ns, npp, n_lights, centre[0], centre[1],
+                                                      centre[2], cmax, rmax, out);
+  return cudaGetLastError();
+}
+
 // ---- launchers ------------------------------------------------------------------------------
 cudaError_t upload_planes(const DevPlane* planes, int n_planes, cudaStream_t st) {
   if (n_planes <= 0) return cudaSuccess;
