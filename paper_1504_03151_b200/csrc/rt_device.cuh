@@ -288,7 +288,7 @@ struct RayFilter {
     return max16(v);
   }
   // Shared-origin scans (camera rays, light-origin shadow rays) test the tangent condition
-  // c'.d - h >= o'.d instead of v >= cut (rt_api.cu neg_tangent: h per sphere precomputed): a hit
+  // c'.d - h >= o'.d instead of v >= cut (rt_kernels.cu neg_tangent: h per sphere precomputed): a hit
   // at t > 0 from o outside the sphere needs tc >= h, and tc - h is 3 FMA per sphere. Its error
   // (the FMA chain over |c'| + h <= 2 (cmax + |o'|), c' and d rounded to float, -h and o'.d
   // rounded) stays below 11 kUlp (cmax + |o'|) <= 2 eta: candidates are the spheres with

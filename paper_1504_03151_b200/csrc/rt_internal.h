@@ -95,7 +95,7 @@ struct DevScene {
   const DevMat* mats;
   const DevLight* lights;
   const int* emit_sph;     // [n_emitters] sphere index of emitter e (prim order), or null
-  // camera rays: the pair layout with -h(eye) in place of K (rt_api.cu neg_tangent), followed by
+  // camera rays: the pair layout with -h(eye) in place of K (rt_kernels.cu neg_tangent), followed by
   // s1 = K + 2 c'.o'(eye), float2 per sphere pair [n_pairs_pad]
   const float4* pairs_eye;
   // light-origin shadow scans: the pair layout followed by -h(P_l) per point light, float2 per

@@ -663,7 +663,7 @@ wf_isect_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
 // Camera rays share the origin (the eye), so the scan tests the tangent condition
 // c'.d - h >= o'.d (RayFilter::tangent_cut; -h per sphere in the eye's table, rt_api.cu
-// build_eye_pairs): 3 FMA per sphere and ray. One ray per thread would leave the kernel co-limited
+// build_eye_table): 3 FMA per sphere and ray. One ray per thread would leave the kernel co-limited
 // by the shared-memory pipe (2 LDS.128 per 2 spheres); here every lane carries two camera rays (a
 // warp = 64 rays): each pair of spheres read from shared memory serves both, and the FFMA2 stream
 // is again the only limit. Candidates get the chord bounds of wf_isect (s1 precomputed, one
@@ -858,7 +858,7 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // only filters (FP64 decides on the original ray in wf_accumulate). Traced from the light, every
 // shadow ray of light l shares the origin P_l, and an occluder lies on the reversed half-line
 // s = t_l - t > 0: the tangent test c'.d' - h_l >= o'.d' (RayFilter::tangent_cut; -h_l per
-// sphere and light precomputed in S.pairs_lt, rt_api.cu neg_tangent) costs 3 FMA per sphere
+// sphere and light precomputed in S.pairs_lt, rt_kernels.cu neg_tangent) costs 3 FMA per sphere
 // instead of 7, and a thread carries two rays of the same light (one shared-memory read serves
 // both). Work comes in chunks of 64 entries of one list. The chord [tc' - q, tc' + q] along the
 // reversed ray maps back to t = t_l - tc' -/+ q on the original one; the bounds add the error of

@@ -115,7 +115,7 @@ def test_many_point_lights(oracle_lib, variant, n_lights):
 
 def _shared_origin_scene(case):
     """Edge cases of the shared-origin tangent test (camera rays and light-origin shadow scans,
-    rt_api.cu neg_tangent): the eye or a light inside a sphere, the eye exactly on a surface, a
+    rt_kernels.cu neg_tangent): the eye or a light inside a sphere, the eye exactly on a surface, a
     light within 1e-6 S of one (always a candidate), 1e-4 and 1e-3 off one (tested); a ground
     plane tilted by 1e-8 gives shading points at t ~ 2e8 (the light-origin scan drops nothing
     past t_l > 1e6 S)."""
