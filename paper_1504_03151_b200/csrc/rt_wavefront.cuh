@@ -662,7 +662,7 @@ wf_isect_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 
 // ---- a3 for camera rays, two rays per thread --------------------------------------------------
 // Camera rays share the origin (the eye), so the scan tests the tangent condition
-// c'.d - h >= o'.d (RayFilter::tangent_cut; -h per sphere in the eye's table, rt_api.cu
+// c'.d - h >= o'.d (RayFilter::tangent_cut; -h per sphere in the eye's table, rt_kernels.cu
 // build_eye_table): 3 FMA per sphere and ray. One ray per thread would leave the kernel co-limited
 // by the shared-memory pipe (2 LDS.128 per 2 spheres); here every lane carries two camera rays (a
 // warp = 64 rays): each pair of spheres read from shared memory serves both, and the FFMA2 stream
