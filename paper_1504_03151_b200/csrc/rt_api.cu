@@ -321,8 +321,7 @@ int launch_wavefront(Context& c, const rt::DevParams& p, const rt::DevScene& sc,
     const size_t nctr = (size_t)rt::kWfCtrPerDepth * (p.max_depth + 2);
     CU(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize");
     (void)nctr;
-    const int ipc = rt::wf_items_per_chunk(p, tm.nslots_req);
-    const size_t n = tm.hint_stride * (size_t)((p.n_items + ipc - 1) / ipc);
+    const size_t n = tm.hint_stride * (size_t)rt::wf_chunk_count(p, tm.nslots_req);
     c.hints.assign(n, 0u);
     CU(cudaMemcpy(c.hints.data(), c.hint_dev.p, n * sizeof(unsigned), cudaMemcpyDeviceToHost), "counters D2H");
     tm.hints = c.hints.data();
@@ -388,15 +387,14 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
     // chunks of whole pixels, at most 2^22 paths each; a frame that fills fewer chunks than
     // pipeline slots (or than p.min_chunks, host framebuffers) is cut into that many
     const int nslots = c.concurrent ? c.pipeline : 1;
-    const int ipc = rt::wf_items_per_chunk(p, nslots);
-    const int cap = ipc * p.spp;
+    const int cap = rt::wf_chunk_max_items(p, nslots) * p.spp;
     const int n_src = p.n_lights + p.n_emitters;  // shadow rays per shading point <= n_src
     const int scap = cap * (n_src > 0 ? n_src : 1);
     // point lights with light-origin scans get list slots; every other source a generic slot
     const int n_gen = n_src - p.lt_lights;
     const int gcap = cap * (n_gen > 0 ? n_gen : 1);
     const int lt_lists = p.lt_lights * rt::kLtSub;
-    const int n_chunks = (p.n_items + ipc - 1) / ipc;
+    const int n_chunks = rt::wf_chunk_count(p, nslots);
     const int used = n_chunks < nslots ? n_chunks : nslots;  // slots that receive a chunk
     rt::WfTiming tm{nullptr, nullptr, 0, 0, 0};
     tm.nslots = used;
@@ -603,9 +601,10 @@ int render_common(int32_t W, int32_t H, int32_t D, int32_t spp, float* out_rgba,
   rt::DevParams p = make_params(W, H, D, spp);
   p.mode = 0;
   p.n_items = p.n_tiles * rt::kTilePx;
-  // a host framebuffer: at least kHostMinChunks chunks, so the first chunks' rows are copied
-  // while the last ones render (two chunks start and finish together, and the whole 33 MB D2H of
-  // a C4 frame came after the render: rt_render into pinned memory 6.51 ms -> 6.40 with 4)
+  // a host framebuffer: at least kHostMinChunks chunks of falling size (rt_kernels.cu
+  // wf_chunk_begin), so the first chunks' rows are copied while the last ones render (two equal
+  // chunks start and finish together, and the whole 33 MB D2H of a C4 frame came after the
+  // render: rt_render into pinned memory 6.51 ms -> 6.40 with 4 equal chunks, 6.17 falling)
   if (!dev_out && !dbg && !accum) p.min_chunks = kHostMinChunks;
   if (accum) {  // progressive passes (R#42)
     p.jitter = 1;

@@ -238,7 +238,7 @@ struct WfTiming {
   const unsigned* hints = nullptr;
   unsigned* hint_dev = nullptr;
   size_t hint_stride = 0;
-  int nslots_req = 1;  // the slot count the chunking was computed for (wf_items_per_chunk)
+  int nslots_req = 1;  // the slot count the chunking was computed for (wf_chunk_count / _begin)
   cudaEvent_t* chunk_done = nullptr;
   int* chunk_items = nullptr;
   int chunk_cap = 0;
@@ -256,7 +256,9 @@ struct WfTiming {
 cudaError_t launch_render_wavefront(const DevParams& p, const DevScene& sc, const DevOutputs& o, int src,
                                     int num_sms, WfTiming& tm, cudaStream_t st);
 // work items (pixels) per chunk of a frame rendered over nslots buffer-set slots
-int wf_items_per_chunk(const DevParams& p, int nslots);
+int wf_chunk_count(const DevParams& p, int nslots);
+int wf_chunk_begin(const DevParams& p, int nslots, int k);
+int wf_chunk_max_items(const DevParams& p, int nslots);
 int wf_timing_pairs(const DevParams& p, int nslots);
 cudaError_t launch_assemble(const float4* gathered, int W, int H, int world, int tiles_per_rank,
                             float4* out, unsigned long long* stats, cudaStream_t st);

@@ -699,10 +699,15 @@ void wf_carve(WfBuffers& B, void* base, int cap, int scap, int gcap, int lt_list
   B.ctr = ctr;
 }
 
-// work items (pixels) per chunk: at most 2^22 paths per chunk; a frame that would fill fewer
-// chunks than max(slots, p.min_chunks) is cut into that many (each >= 2^17 paths), so the chunks
-// overlap (DESIGN.md §7 "chunk pipelining"; min_chunks: host framebuffers)
-int wf_items_per_chunk(const DevParams& p, int nslots) {
+// Chunks of whole work items (pixels): at most 2^22 paths per chunk; a frame that would fill
+// fewer chunks than max(slots, p.min_chunks) is cut into that many (each >= 2^17 paths), so the
+// chunks overlap (DESIGN.md §7 "chunk pipelining"). A host framebuffer (p.min_chunks > 0) cut
+// into exactly 2 x slots chunks gets chunks of falling size (the first `slots` chunks share
+// kHostHead of the frame): their rows are copied while the smaller last ones render (C4,
+// rt_render into pinned memory: head 0.5 (uniform) / 0.7 / 0.8 / 0.9 / 0.95 -> 6.39 / 6.29 /
+// 6.24 / 6.17 / 6.32 ms; device-buffer renders keep uniform chunks).
+constexpr double kHostHead = 0.9;
+static long long wf_uniform_chunks(const DevParams& p, int nslots) {
   const long long paths = (long long)p.n_items * p.spp;
   const int max_items = (1 << 22) / p.spp > 0 ? (1 << 22) / p.spp : 1;
   long long chunks = (p.n_items + max_items - 1) / max_items;
@@ -712,16 +717,42 @@ int wf_items_per_chunk(const DevParams& p, int nslots) {
     while (want > 1 && paths / want < (1 << 17)) --want;
     if (want > chunks) chunks = want;
   }
-  if (chunks < 1) chunks = 1;
+  return chunks < 1 ? 1 : chunks;
+}
+int wf_chunk_count(const DevParams& p, int nslots) {
+  const long long chunks = wf_uniform_chunks(p, nslots);
   const long long items = (p.n_items + chunks - 1) / chunks;
-  return items > 0 ? (int)items : 1;
+  return (int)((p.n_items + items - 1) / items);
+}
+// first work item of chunk k (k = wf_chunk_count: n_items)
+int wf_chunk_begin(const DevParams& p, int nslots, int k) {
+  const long long chunks = wf_uniform_chunks(p, nslots);
+  const long long items = (p.n_items + chunks - 1) / chunks;
+  const int n = (int)((p.n_items + items - 1) / items);
+  if (k >= n) return p.n_items;
+  const long long rows = p.n_items / ((long long)p.tiles_x * kTilePx);
+  if (p.min_chunks > 0 && nslots > 1 && n == 2 * nslots && kHostHead > 0.0 && rows >= 8LL * n) {
+    // falling sizes, boundaries on whole tile rows
+    const long long row = (long long)p.tiles_x * kTilePx;
+    const double f = k <= nslots ? kHostHead * k / nslots : kHostHead + (1.0 - kHostHead) * (k - nslots) / nslots;
+    long long b = (long long)(f * (double)p.n_items / (double)row + 0.5) * row;
+    return (int)(b < p.n_items ? b : p.n_items);
+  }
+  const long long b = (long long)k * items;
+  return (int)(b < p.n_items ? b : p.n_items);
+}
+// the largest chunk (the buffer sets' capacity)
+int wf_chunk_max_items(const DevParams& p, int nslots) {
+  const int n = wf_chunk_count(p, nslots);
+  int m = 1;
+  for (int k = 0; k < n; ++k) {
+    const int w = wf_chunk_begin(p, nslots, k + 1) - wf_chunk_begin(p, nslots, k);
+    if (w > m) m = w;
+  }
+  return m;
 }
 
-int wf_timing_pairs(const DevParams& p, int nslots) {
-  const int items_per_chunk = wf_items_per_chunk(p, nslots);
-  const int chunks = (p.n_items + items_per_chunk - 1) / items_per_chunk;
-  return chunks * (p.max_depth + 1);
-}
+int wf_timing_pairs(const DevParams& p, int nslots) { return wf_chunk_count(p, nslots) * (p.max_depth + 1); }
 
 template <typename... KArgs, typename... Args>
 static void launch(void (*k)(KArgs...), int grid, size_t smem, cudaStream_t st, Args... args) {
@@ -794,7 +825,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   int* dh = dbg ? o.dbg_hits : nullptr;
   int* db = dbg ? o.dbg_bounces : nullptr;
   const int nslots = tm.nslots;  // slots that receive chunks (<= the count the chunking used)
-  const int items_per_chunk = wf_items_per_chunk(p, tm.nslots_req);
+  const int n_chunks_plan = wf_chunk_count(p, tm.nslots_req);
   // schedule fuzzing: a spin of 0-40 us (or none) on a stream at each fork, join and slot start
   auto jitter = [&](cudaStream_t s) {
     if (!tm.jitter || !s) return;
@@ -818,7 +849,8 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     }
   }
   int chunk = 0;
-  for (int w0 = 0; w0 < p.n_items; w0 += items_per_chunk, ++chunk) {
+  for (; chunk < n_chunks_plan; ++chunk) {
+    const int w0 = wf_chunk_begin(p, tm.nslots_req, chunk);
     const int sl = chunk % nslots;
     WfBuffers& Bset = *tm.slot_B[sl];
     const cudaStream_t st = sl == 0 ? st0 : tm.slot_main[sl];
@@ -831,7 +863,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     Bc.g0 = (long long)w0 * p.spp;
     WfBuffers Bs = Bc;  // the copy passed to a single (solo) kernel launch
     Bs.solo = 1;
-    const int nw = (p.n_items - w0) < items_per_chunk ? (p.n_items - w0) : items_per_chunk;
+    const int nw = wf_chunk_begin(p, tm.nslots_req, chunk + 1) - w0;
     const int npaths = nw * p.spp;
     const long long g0 = (long long)w0 * p.spp;
     if ((e = cudaMemsetAsync(Bc.ctr, 0, sizeof(unsigned) * kWfCtrPerDepth * (p.max_depth + 2), st)) != cudaSuccess) return e;
