@@ -103,6 +103,27 @@ def test_interleaved_order_and_tinted_glass(oracle_lib, seed, W, H, D, spp, vari
     _check(oracle_lib, sc, label=f"interleaved{seed}/{variant}", variant=variant)
 
 
+def _sweep_cases():
+    """Seeded sweep over the scene shapes the kernels branch on: sphere counts around the pair /
+    batch / AUTO boundaries (1, 2, 15, 16, 17, 63, 64, 65, 150, 300; dense, so the eye often sits
+    inside spheres), 0-2 planes, planes-first or interleaved orders, 0-30 point lights (light-origin
+    scans up to 30), depths 0-6, 1-5 spp, ragged frames."""
+    g = np.random.default_rng(2024)
+    cases = []
+    for i, ns in enumerate([1, 2, 15, 16, 17, 63, 64, 65, 150, 300, 40, 9]):
+        cases.append(dict(seed=300 + i, n_spheres=ns, n_planes=int(g.integers(0, 3)), n_lights=int(g.choice([0, 1, 5, 12, 30])),
+                          width=int(g.integers(5, 19)), height=int(g.integers(3, 13)), max_depth=int(g.integers(0, 7)),
+                          spp=int(g.integers(1, 6)), glass_tint=bool(g.integers(0, 2)), interleave=bool(g.integers(0, 2))))
+    return cases
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"s{c['seed']}-n{c['n_spheres']}-l{c['n_lights']}")
+def test_random_sweep(oracle_lib, variant, case):
+    sc = scenegen.random_tiny(**case)
+    _check(oracle_lib, sc, label=f"sweep {case['seed']}/{variant}", variant=variant)
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("n_lights", [29, 30, 31, 32])
 def test_many_point_lights(oracle_lib, variant, n_lights):
