@@ -176,12 +176,13 @@ int rt_set_variant(int32_t variant);
  * the library stream (same results bit for bit; used to time each kernel alone). */
 int rt_set_concurrency(int32_t on);
 
-/* Wavefront kernels: chunk pipelining over `slots` buffer sets (1..4, default 2). A frame is cut
+/* Wavefront kernels: chunk pipelining over `slots` buffer sets (1..4; 0 = AUTO, the default: 2, or
+ * 3 when the frame has at least 8 chunks of 2^22 paths). A frame is cut
  * into chunks of at most 2^22 paths, and into at least `slots` chunks when it has >= 2^17 paths
  * per chunk; chunk i runs on slot i % slots, each slot with its own buffers and stream pair, so
  * one chunk's short deep-depth queues overlap the next chunks' dense first depths. 1 renders the
  * chunks one after another. Ignored (1) when concurrency is off. Same results bit for bit for
- * every value. RT_ERR_INVALID_ARG outside 1..4. */
+ * every value. RT_ERR_INVALID_ARG outside 0..4. */
 int rt_set_pipeline(int32_t slots);
 
 /* Wavefront kernels, scenes beyond RT_SMEM_SPHERES (the shared-memory budget): 1 (default) the

@@ -194,8 +194,9 @@ def check_status() -> tuple[int, bool]:
     return int(v.value), bool(c.value)
 
 
-def set_pipeline(slots: int = 2):
-    """Wavefront: chunk pipelining over 1..4 buffer-set slots (default 2)."""
+def set_pipeline(slots: int = 0):
+    """Wavefront: chunk pipelining over 1..4 buffer-set slots; 0 = AUTO (the default: 2, or 3 for
+    frames of >= 8 chunks)."""
     _check("rt_set_pipeline", lib().rt_set_pipeline(int(slots)))
 
 

@@ -81,7 +81,7 @@ def test_schedule_fuzzing_bit_identical(name, frame):
                 assert {k: st[k] for k in KEYS} == ref_st, (slots, seed)
     finally:
         rt.set_schedule_jitter(0)
-        rt.set_pipeline(2)
+        rt.set_pipeline(0)
         rt.set_concurrency(True)
         rt.set_graphs(True)
         rt.set_variant("auto")

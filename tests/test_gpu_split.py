@@ -96,11 +96,11 @@ def test_pipeline_slots_bit_identical(name, frame, world):
                     assert torch.equal(o, ref[key][0]), (slots, rank)
                     assert st == ref[key][1], (slots, rank)
         with pytest.raises(rt.RtError):
-            rt.set_pipeline(0)
+            rt.set_pipeline(-1)
         with pytest.raises(rt.RtError):
             rt.set_pipeline(5)
     finally:
-        rt.set_pipeline(2)
+        rt.set_pipeline(0)
 
 
 def test_invalid_split_rejected():

@@ -3,7 +3,7 @@
 configuration (concurrent streams, graph replay, L2 flushed before every frame, CUDA events) and
 the in-order per-kernel times (library events, rt_set_concurrency(0)).
 
-    python tools/ab_frame.py [--config C4] [--frames 30] [--rounds 2] [--pipeline K] LIB.so [LIB2.so ...]
+    python tools/ab_frame.py [--config C4] [--frames 30] [--rounds 2] [--pipeline K] [--variant V] LIB.so [LIB2.so ...]
 
 Each measurement runs in its own process (B200RT_LIB selects the build); builds alternate over
 the rounds so clock drift hits every build alike. Tool only.
@@ -18,7 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(config, frames, pipeline=0):
+def child(config, frames, pipeline=0, variant="auto"):
     sys.path.insert(0, ROOT)
     import torch
     import scenegen
@@ -29,6 +29,7 @@ def child(config, frames, pipeline=0):
     rt.load_scene(sc)
     if pipeline:
         rt.set_pipeline(pipeline)
+    rt.set_variant(variant)
     out = torch.empty((sc.height, sc.width, 4), dtype=torch.float32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     W, H, D, S = sc.width, sc.height, sc.max_depth, sc.spp
@@ -68,16 +69,17 @@ def main():
     ap.add_argument("--frames", type=int, default=30)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--pipeline", type=int, default=0, help="rt_set_pipeline slots (0: the library default)")
+    ap.add_argument("--variant", default="auto", help="auto | wavefront | megakernel")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
-        return child(a.config, a.frames, a.pipeline)
+        return child(a.config, a.frames, a.pipeline, a.variant)
     libs = a.libs or [os.path.join(ROOT, "paper_1504_03151_b200", "libb200rt.so")]
     res = {lib: [] for lib in libs}
     for _ in range(a.rounds):
         for lib in libs:
             out = subprocess.run([sys.executable, __file__, "--child", "--config", a.config, "--frames", str(a.frames),
-                                  "--pipeline", str(a.pipeline)],
+                                  "--pipeline", str(a.pipeline), "--variant", a.variant],
                                  env=dict(os.environ, B200RT_LIB=os.path.abspath(lib)), capture_output=True, text=True)
             line = [ln for ln in out.stdout.splitlines() if ln.startswith("RESULT ")]
             if not line:

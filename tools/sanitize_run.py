@@ -44,7 +44,7 @@ def main():
     for slots in (1, 2, 3, 4):
         rt.set_pipeline(slots)
         frames(c4, 2)
-    rt.set_pipeline(2)
+    rt.set_pipeline(0)
     for split in (2, 8):
         rt.set_scan_split(split)
         frames(c4, 2)
