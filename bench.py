@@ -457,11 +457,14 @@ def run_b200(args):
                 "secondary": {"kernel": "wf_isect<closest> (secondary closest-hit rays, FP32 FFMA2 scan)", "bound": "alu",
                               "ms": kt["closest"] - kt["eye"], "tests": n_closest - n_eye, "fma_per_test": 7},
                 # algorithmic bytes: per shaded path the ray state in (84 B at depth >= 1;
-                # camera rays are implicit) + its candidate count (4 B); per continuation the next state
-                # out (84 B); per ended path its radiance (12 B); per shadow ray the FP64 shadow ray and
-                # its contribution out (68 B)
+                # camera rays are implicit), its candidate count in (4 B) and its entry range and next
+                # position out (12 B); per continuation the next state out (84 B); per ended path its
+                # radiance (12 B); per shadow ray its scan record (24 B: float direction and t_max,
+                # entry, skip), its contribution (12 B) and its slot (4 B) out (round 1 wrote the 56-B
+                # FP64 ray instead of the record: 68 B per shadow ray)
                 "shade": {"kernel": "wf_shade (FP64 nearest hit, shading, shadow-ray set-up, bounce)", "bound": "hbm",
-                          "ms": kt["shade"], "bytes": 84 * sec + 4 * (prim + sec) + 84 * sec + 12 * prim + 68 * shd},
+                          "ms": kt["shade"],
+                          "bytes": 84 * sec + 16 * (prim + sec) + 84 * sec + 12 * prim + 40 * shd},
                 # per shadow ray its decision inputs (status 8 B) and contribution (12 B); per shading
                 # path the entry range (8 B) and the radiance read and written (24 B)
                 "accumulate": {"kernel": "wf_accumulate (FP64 occlusion decisions, radiance sums)", "bound": "hbm",
