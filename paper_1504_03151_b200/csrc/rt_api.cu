@@ -94,6 +94,7 @@ struct Context {
   DevBuf<unsigned long long> stats;
   DevBuf<int> dbg_hits, dbg_bounces;
   // wavefront variant
+  int off_spp = 0;  // spp whose sub-pixel offsets are in the constant table (0: none)
   int variant = RT_VARIANT_AUTO;
   int concurrent = 1;  // shadow scans || next closest scan on a side stream (rt_set_concurrency)
   // chunk pipelining over buffer-set slots (rt_set_pipeline): chunk i on slot i % pipeline, each
@@ -372,6 +373,10 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
                float* host_out = nullptr, bool* copied = nullptr) {
   if (copied) *copied = false;
   Context& c = g_ctx;
+  if (c.off_spp != p.spp) {  // stream-ordered before this render's launches (or graph replay)
+    CU(rt::upload_sample_offsets(p.spp, c.stream), "constant upload (sample offsets)");
+    c.off_spp = p.spp;
+  }
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
   rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p,

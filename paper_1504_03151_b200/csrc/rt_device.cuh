@@ -9,6 +9,10 @@
 namespace rt {
 
 __constant__ DevPlane c_planes[kMaxPlanes];
+// sub-pixel offsets {ox, oy} of samples 0..spp-1 for spp <= kOffTable (sample_offset's values,
+// computed on the host with the same IEEE double operations: rt_kernels.cu upload_sample_offsets)
+constexpr int kOffTable = 256;
+__constant__ double2 c_sample_off[kOffTable];
 __device__ unsigned g_rt_check;  // first failed RT_CHECK id (checked builds)
 
 constexpr double kEps = 1e-4;          // EPS_T
@@ -79,8 +83,22 @@ __device__ __forceinline__ d3 cosine_dir(d3 n, double u1, double u2) {
   return t1 * (rr * cp) + t2 * (rr * sp) + n * sqrt(fmax(0.0, 1.0 - u1));
 }
 
+// Phong lobe max(0, r.wo)^s (Eq. 5, R#3) for alpha in [0, 1], s >= 1: exp2(s log2 alpha) with the
+// accurate (non-intrinsic) log2f / exp2f. The relative error stays below ln2 |s log2 alpha| 2^-23
+// <= 1e-5 over the range before underflow (|s log2 alpha| <= 126), inside the 1e-4 radiance
+// tolerance; powf's extended-precision log and special cases cost twice the instructions.
+__device__ __forceinline__ float phong_lobe(float alpha, float s) {
+  return alpha > 0.f ? exp2f(s * log2f(alpha)) : 0.f;
+}
+
 // ---- ray generation (a2): §8(c).1 steps 1-2 ------------------------------------
 __device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double& oy) {
+  if (spp <= kOffTable) {  // the same values, precomputed per spp (no divisions here)
+    const double2 o = c_sample_off[s];
+    ox = o.x;
+    oy = o.y;
+    return;
+  }
   int n = 1;
   while ((n + 1) * (n + 1) <= spp) ++n;
   if (n * n == spp) {

@@ -195,6 +195,7 @@ constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
 // launchers (rt_kernels.cu)
 cudaError_t upload_planes(const DevPlane* planes, int n_planes, cudaStream_t st);
+cudaError_t upload_sample_offsets(int spp, cudaStream_t st);
 cudaError_t launch_eye_table(const float4* pairs, const float4* sph_cr, int ns, int npp, const double o[3],
                              const double centre[3], double S, float4* out, cudaStream_t st);
 cudaError_t launch_light_tables(const float4* pairs, const float4* sph_cr, const DevLight* lights, int ns, int npp,

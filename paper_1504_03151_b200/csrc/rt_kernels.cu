@@ -16,6 +16,7 @@
 // Paper: "each kernel thread traces a single light"; recursion becomes iteration
 // (P:226); ray–sphere per Eq. 9–12; shading per Eq. 3–7 for point
 // lights; Alg. 1 any-hit with early exit.
+#include <cmath>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -319,7 +320,7 @@ __device__ void next_light_or_bounce(Lane& L, const DevParams& P, const DevScene
       L.n_shadow++;
       const d3 rl = L.n * (2.0 * ls.cos_s) - ls.wi;
       const float alpha = (float)fmax(0.0, -dot(rl, L.d));
-      const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+      const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * phong_lobe(alpha, m.shin);
       const float g = (float)ls.g;
       L.contrib = mul(L.T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * g, fmaf(m.ag, kInvPi, spec) * ls.ig * g,
                               fmaf(m.ab, kInvPi, spec) * ls.ib * g));
@@ -348,7 +349,7 @@ __device__ void next_light_or_bounce(Lane& L, const DevParams& P, const DevScene
       // f_r = rho/pi + ks (s+2)/(2 pi) max(0, r.wo)^s (Eq. 5, R#3); E = I cos / d^2 (Eq. 3)
       const d3 rl = L.n * (2.0 * cosT) - wi;
       const float alpha = (float)fmax(0.0, -dot(rl, L.d));
-      const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+      const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * phong_lobe(alpha, m.shin);
       const float g = (float)(cosT / d2);
       L.contrib = mul(L.T, f3(fmaf(m.ar, kInvPi, spec) * lt.ix * g, fmaf(m.ag, kInvPi, spec) * lt.iy * g,
                               fmaf(m.ab, kInvPi, spec) * lt.iz * g));
@@ -555,6 +556,28 @@ cudaError_t launch_light_tables(const float4* pairs, const float4* sph_cr, const
   build_light_tables<<<(n + 255) / 256, 256, 0, st>>>(pairs, sph_cr, lights, ns, npp, n_lights, centre[0], centre[1],
                                                       centre[2], cmax, rmax, out);
   return cudaGetLastError();
+}
+
+// sample_offset's values for spp <= kOffTable, in the same IEEE double operations (x86-64 SSE2,
+// no FMA contraction: the device table then holds exactly what sample_offset computes)
+cudaError_t upload_sample_offsets(int spp, cudaStream_t st) {
+  if (spp < 1 || spp > kOffTable) return cudaSuccess;
+  static double2 off[kOffTable];
+  int n = 1;
+  while ((n + 1) * (n + 1) <= spp) ++n;
+  for (int s = 0; s < spp; ++s) {
+    if (n * n == spp) {
+      const int i = s % n, j = s / n;
+      off[s] = make_double2((i + 0.5) / n, (j + 0.5) / n);
+    } else {
+      unsigned v = (unsigned)s, r = 0;
+      for (int b = 0; b < 32; ++b) { r = (r << 1) | (v & 1u); v >>= 1; }
+      const double radinv = (double)r * (1.0 / 4294967296.0);
+      const double y = radinv + 0.5 / spp;
+      off[s] = make_double2((s + 0.5) / spp, y - std::floor(y));
+    }
+  }
+  return cudaMemcpyToSymbolAsync(c_sample_off, off, sizeof(double2) * spp, 0, cudaMemcpyHostToDevice, st);
 }
 
 // ---- launchers ------------------------------------------------------------------------------

@@ -1495,7 +1495,7 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         // or L_e cos_s cos_l / (d^2 pdf) for an emitter sample (Eq. 8, R#41)
         const d3 rl = nrm * (2.0 * ls.cos_s) - ls.wi;
         const float alpha = (float)fmax(0.0, -dot(rl, dir));
-        const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * powf(alpha, m.shin);
+        const float spec = m.ks * (m.shin + 2.0f) * kInv2Pi * phong_lobe(alpha, m.shin);
         const float gg = (float)ls.g;
         sf3(B.sq_c, B.scap, (int)k, mul(T, f3(fmaf(m.ar, kInvPi, spec) * ls.ir * gg, fmaf(m.ag, kInvPi, spec) * ls.ig * gg,
                                              fmaf(m.ab, kInvPi, spec) * ls.ib * gg)));
