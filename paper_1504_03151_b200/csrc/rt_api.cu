@@ -207,6 +207,8 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   p.lt_lights = (c.smem_scene && p.n_lights + p.n_emitters <= 64) ? c.lt_lights : 0;
   p.tiles_x = (W + rt::kTileW - 1) / rt::kTileW;
   p.n_tiles = p.tiles_x * ((H + rt::kTileH - 1) / rt::kTileH);
+  p.div_spp = rt::make_fastdiv((unsigned)spp);
+  p.div_tiles_x = rt::make_fastdiv((unsigned)p.tiles_x);
   return p;
 }
 

@@ -143,8 +143,9 @@ __device__ __forceinline__ bool item_pixel(const DevParams& P, int w, int& px, i
     t = rank_tile(t, P.rank, P.world);
     if (t >= P.n_tiles) return false;
   }
-  px = (t % P.tiles_x) * kTileW + (i % kTileW);
-  py = (t / P.tiles_x) * kTileH + (i / kTileW);
+  const int ty = (int)fdiv(P.div_tiles_x, (unsigned)t);  // t / tiles_x
+  px = (t - ty * P.tiles_x) * kTileW + (i % kTileW);
+  py = ty * kTileH + (i / kTileW);
   return px < P.W && py < P.H;
 }
 

@@ -64,6 +64,29 @@ struct DevMat {
   float pad;
 };
 
+// Exact unsigned 32-bit division by a runtime divisor d >= 1 (Granlund-Montgomery, round-up
+// multiplier): t = umulhi(x, m), q = (t + ((x - t) >> 1)) >> (l - 1), l = ceil(log2 d), for every
+// 32-bit x; d = 1 passes x through. Host-initialised once per render (DevParams).
+struct FastDiv {
+  unsigned d, m, s;
+};
+inline FastDiv make_fastdiv(unsigned d) {
+  FastDiv f{d, 0u, 0u};
+  if (d <= 1u) return f;
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;  // l = ceil(log2 d) >= 1
+  f.m = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1ull);
+  f.s = l - 1u;
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned fdiv(const FastDiv& f, unsigned x) {
+  if (f.d <= 1u) return x;
+  const unsigned t = __umulhi(x, f.m);
+  return (t + ((x - t) >> 1)) >> f.s;
+}
+#endif
+
 struct DevParams {
   // camera (basis in double): d = normalize(F + (2sx-1) R + (1-2sy) U)
   double eye[3], F[3], R[3], U[3];
@@ -85,6 +108,7 @@ struct DevParams {
   // mode 0: full frame, tile-major items, row-major output; 1: shard, slab output (tile-major);
   // 2: direct shard, the rank's tiles stored row-major into a (possibly peer) frame
   int mode, rank, world, tiles_x, n_tiles, n_items;
+  FastDiv div_spp, div_tiles_x;  // exact divisions by spp and tiles_x (camera rays, pixels)
 };
 
 struct DevScene {
@@ -172,7 +196,8 @@ struct WfBuffers {
   int force_parts;
   // set per chunk on the copies passed to its launches: global sample index of the chunk's path 0
   // (the camera rays of depth 0 are implicit: entry e of Q[0] is path e, its ray computed on use)
-  long long g0;
+  long long g0;    // the chunk's first path (w0 * spp)
+  int w0;          // the chunk's first work item
 };
 
 // counter layout (zeroed per chunk): queue lengths and persistent-kernel work heads per depth

@@ -72,8 +72,9 @@ __device__ __forceinline__ bool start_item(Lane& L, const DevParams& P, int w, f
       return false;
     }
   }
-  const int px = (t % P.tiles_x) * kTileW + (i % kTileW);
-  const int py = (t / P.tiles_x) * kTileH + (i / kTileW);
+  const int ty = (int)fdiv(P.div_tiles_x, (unsigned)t);  // t / tiles_x
+  const int px = (t - ty * P.tiles_x) * kTileW + (i % kTileW);
+  const int py = ty * kTileH + (i / kTileW);
   if (px >= P.W || py >= P.H) {
     if (P.mode == 1) out[w] = make_float4(0.f, 0.f, 0.f, 0.f);
     return false;
@@ -884,6 +885,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
     const unsigned* hint = tm.hints ? tm.hints + (size_t)chunk * tm.hint_stride : nullptr;
     WfBuffers Bc = Bset;  // this chunk's launches: the buffer set with the chunk's first sample
     Bc.g0 = (long long)w0 * p.spp;
+    Bc.w0 = w0;
     WfBuffers Bs = Bc;  // the copy passed to a single (solo) kernel launch
     Bs.solo = 1;
     const int nw = wf_chunk_begin(p, tm.nslots_req, chunk + 1) - w0;

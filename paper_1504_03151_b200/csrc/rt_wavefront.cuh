@@ -91,10 +91,10 @@ __device__ __forceinline__ int q_skip(const WfQueue& Q, unsigned e, int d) { ret
 __device__ __forceinline__ bool q_dir(const DevParams& P, const WfBuffers& B, const WfQueue& Q, unsigned e, int d,
                                       d3& dir) {
   if (d == 0) {
-    const long long g = B.g0 + e;
+    const unsigned we = fdiv(P.div_spp, e);  // g0 + e = (w0 + we) * spp + sample
     int px = 0, py = 0;
-    if (!item_pixel(P, (int)(g / P.spp), px, py)) return false;
-    dir = camera_dir(P, px, py, (int)(g % P.spp));
+    if (!item_pixel(P, B.w0 + (int)we, px, py)) return false;
+    dir = camera_dir(P, px, py, (int)(e - we * (unsigned)P.spp));
     return true;
   }
   dir = ld3(Q.ray, B.cap, (int)e, 3);
@@ -1242,7 +1242,7 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
   const unsigned n = B.ctr[wf_ctr_q(d)];
   RT_CHECK(n <= (unsigned)B.cap, 100);
   const WfQueue Q = B.q[d & 1], Qn = B.q[(d + 1) & 1];
-  const int w0 = (int)(g0 / P.spp);  // first work item of the chunk (g0 = w0 * spp)
+  const int w0 = B.w0;  // first work item of the chunk (g0 = w0 * spp)
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask_lane = lanemask_lt();
   const int n_src = P.n_lights + (kExt ? P.n_emitters : 0);  // point lights, then emitters (R#41)
@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
     unsigned long long pix = 0;
     unsigned sg = 0;
     auto pixel_sample = [&]() {
-      const int wl = path / P.spp;
+      const int wl = (int)fdiv(P.div_spp, (unsigned)path);
       int px = 0, py = 0;
       item_pixel(P, w0 + wl, px, py);
       pix = (unsigned long long)py * P.W + px;
