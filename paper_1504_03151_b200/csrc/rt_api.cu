@@ -209,6 +209,8 @@ rt::DevParams make_params(int W, int H, int max_depth, int spp) {
   p.n_tiles = p.tiles_x * ((H + rt::kTileH - 1) / rt::kTileH);
   p.div_spp = rt::make_fastdiv((unsigned)spp);
   p.div_tiles_x = rt::make_fastdiv((unsigned)p.tiles_x);
+  p.inv_w = 1.0 / W;
+  p.inv_h = 1.0 / H;
   return p;
 }
 

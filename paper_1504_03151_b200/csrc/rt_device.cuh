@@ -114,8 +114,8 @@ __device__ __forceinline__ void sample_offset(int s, int spp, double& ox, double
 }
 
 // camera ray of sample s of pixel (px, py): d = normalize(F + (2sx-1) R + (1-2sy) U)
-__device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int s) {
-  double ox, oy;
+// sub-pixel position of sample s of pixel (px, py)
+__device__ __forceinline__ void sample_xy(const DevParams& P, int px, int py, int s, double& ox, double& oy) {
   if (P.jitter) {  // progressive passes: random offset of sample (pass) sample_base + s (R#42)
     const unsigned long long pix = (unsigned long long)py * P.W + px;
     const unsigned sg = (unsigned)(P.sample_base + s);
@@ -124,10 +124,31 @@ __device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int
   } else {
     sample_offset(s, P.spp, ox, oy);
   }
+}
+__device__ __forceinline__ d3 camera_dir(const DevParams& P, int px, int py, int s) {
+  double ox, oy;
+  sample_xy(P, px, py, s, ox, oy);
   const double sx = (px + ox) / P.W, sy = (py + oy) / P.H;
   const double a = 2.0 * sx - 1.0, b = 1.0 - 2.0 * sy;
   return normalize(mk(P.F[0] + a * P.R[0] + b * P.U[0], P.F[1] + a * P.R[1] + b * P.U[1],
                       P.F[2] + a * P.R[2] + b * P.U[2]));
+}
+
+// The same camera ray for a float filter only (the camera-ray scan): the divisions by W and H
+// become products with 1/W, 1/H and the normalisation an FP64 rsqrt, so the direction is within
+// a few FP64 ulps of camera_dir's — far inside the filter's bound for d rounded to float (eta,
+// slack: 2^-24 per component), while every decision uses camera_dir itself (wf_shade).
+__device__ __forceinline__ void camera_dir_filter(const DevParams& P, int px, int py, int s, float& dx, float& dy,
+                                                  float& dz) {
+  double ox, oy;
+  sample_xy(P, px, py, s, ox, oy);
+  const double a = 2.0 * ((px + ox) * P.inv_w) - 1.0, b = 1.0 - 2.0 * ((py + oy) * P.inv_h);
+  const double vx = P.F[0] + a * P.R[0] + b * P.U[0], vy = P.F[1] + a * P.R[1] + b * P.U[1],
+               vz = P.F[2] + a * P.R[2] + b * P.U[2];
+  const double k = rsqrt(vx * vx + vy * vy + vz * vz);
+  dx = (float)(vx * k);
+  dy = (float)(vy * k);
+  dz = (float)(vz * k);
 }
 
 // global tile of a rank's local tile j: one tile of every group of `world` consecutive tiles,

@@ -109,6 +109,7 @@ struct DevParams {
   // 2: direct shard, the rank's tiles stored row-major into a (possibly peer) frame
   int mode, rank, world, tiles_x, n_tiles, n_items;
   FastDiv div_spp, div_tiles_x;  // exact divisions by spp and tiles_x (camera rays, pixels)
+  double inv_w, inv_h;           // 1/W, 1/H: the camera-ray scan's filter directions (not decisions)
 };
 
 struct DevScene {

@@ -100,6 +100,16 @@ __device__ __forceinline__ bool q_dir(const DevParams& P, const WfBuffers& B, co
   dir = ld3(Q.ray, B.cap, (int)e, 3);
   return true;
 }
+// the camera-ray scan's filter direction of path e of the chunk (camera_dir_filter); false for a
+// work item outside the image
+__device__ __forceinline__ bool eye_filter_dir(const DevParams& P, const WfBuffers& B, unsigned e, float& dx, float& dy,
+                                               float& dz) {
+  const unsigned we = fdiv(P.div_spp, e);
+  int px = 0, py = 0;
+  if (!item_pixel(P, B.w0 + (int)we, px, py)) return false;
+  camera_dir_filter(P, px, py, (int)(e - we * (unsigned)P.spp), dx, dy, dz);
+  return true;
+}
 __device__ __forceinline__ int q_path(const WfQueue& Q, unsigned e, int d) {
   return d == 0 ? (int)e : Q.path[e];
 }
@@ -764,8 +774,7 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
   const float4* gp = S.pairs_eye;
   if constexpr (kSrc == SRC_SMEM) stage_scene(s_pairs, gp, (uint32_t)P.n_pairs_pad * 40u, &s_mbar);
   const float2* s1p = reinterpret_cast<const float2*>((kSrc == SRC_SMEM ? s_pairs : gp) + 2 * P.n_pairs_pad);
-  unsigned* work = B.ctr + wf_ctr_wc(d);
-  const WfQueue Q = B.q[d & 1];
+  unsigned* work = B.ctr + wf_ctr_wc(d);  // (camera rays: d == 0, the implicit queue)
   const int lane = threadIdx.x & 31;
   while (true) {
     unsigned e0 = 0;
@@ -774,15 +783,13 @@ wf_isect_eye2(const DevParams P, const DevScene S, WfBuffers B, int d) {
     if (e0 >= n) break;
     const unsigned ea = e0 + lane, eb = e0 + 32 + lane;
     EyeRay Ra, Rb;
-    {
-      d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
-      Ra.act = ea < n;
-      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); Ra.act = q_dir(P, B, Q, ea, d, dir); }
-      Ra.F.init(o, dir, P);
-      o = mk(0, 0, 0); dir = mk(0, 0, 1);
-      Rb.act = eb < n;
-      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
-      Rb.F.init(o, dir, P);
+    {  // camera rays (depth 0): the eye and the filter direction (decisions: wf_shade, camera_dir)
+      const d3 o = mk(P.eye[0], P.eye[1], P.eye[2]);
+      float ax = 0.f, ay = 0.f, az = 1.f, bx = 0.f, by = 0.f, bz = 1.f;
+      Ra.act = ea < n && eye_filter_dir(P, B, ea, ax, ay, az);
+      Rb.act = eb < n && eye_filter_dir(P, B, eb, bx, by, bz);
+      Ra.F.init(o, ax, ay, az, P);
+      Rb.F.init(o, bx, by, bz, P);
     }
     Ra.cu = Ra.F.tangent_cut();
     Rb.cu = Rb.F.tangent_cut();
@@ -808,8 +815,7 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
   TileRing ring;
   ring.init(s_full, gp, P.n_pairs_pad);
   const int ntiles = ring.ntiles;
-  unsigned* work = B.ctr + wf_ctr_wc(d);
-  const WfQueue Q = B.q[d & 1];
+  unsigned* work = B.ctr + wf_ctr_wc(d);  // (camera rays: d == 0, the implicit queue)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     if (threadIdx.x == 0) {
@@ -826,15 +832,13 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
     }
     const unsigned ea = e0 + lane, eb = e0 + 32 + lane;
     EyeRay Ra, Rb;
-    {
-      d3 o = mk(0, 0, 0), dir = mk(0, 0, 1);
-      Ra.act = ea < n;
-      if (Ra.act) { o = q_origin(P, Q, B.cap, ea, d); Ra.act = q_dir(P, B, Q, ea, d, dir); }
-      Ra.F.init(o, dir, P);
-      o = mk(0, 0, 0); dir = mk(0, 0, 1);
-      Rb.act = eb < n;
-      if (Rb.act) { o = q_origin(P, Q, B.cap, eb, d); Rb.act = q_dir(P, B, Q, eb, d, dir); }
-      Rb.F.init(o, dir, P);
+    {  // camera rays (depth 0): the eye and the filter direction (decisions: wf_shade, camera_dir)
+      const d3 o = mk(P.eye[0], P.eye[1], P.eye[2]);
+      float ax = 0.f, ay = 0.f, az = 1.f, bx = 0.f, by = 0.f, bz = 1.f;
+      Ra.act = ea < n && eye_filter_dir(P, B, ea, ax, ay, az);
+      Rb.act = eb < n && eye_filter_dir(P, B, eb, bx, by, bz);
+      Ra.F.init(o, ax, ay, az, P);
+      Rb.F.init(o, bx, by, bz, P);
     }
     Ra.cu = Ra.F.tangent_cut();
     Rb.cu = Rb.F.tangent_cut();
