@@ -1509,20 +1509,35 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
         RT_CHECK(g >= 0 || -2 - g < B.gcap, 108);
         B.spos[k] = g;
         if (g >= 0) {
-          d3 ds;
-          double tl;
           const d3 os = p + nrm * kEps;
-          shadow_dir(os, ls.x, ds, tl);
-          int skip = shadow_skip(out_sph, nrm, ds);
-          for (int q = 0; q < P.n_planes; ++q) {  // planes first, exactly (FP64), in index order
-            const DevPlane pl = c_planes[q];
-            const double den = pl.nx * ds.x + pl.ny * ds.y + pl.nz * ds.z;
-            if (fabs(den) >= 1e-12) {
-              const double t = (pl.d - (pl.nx * os.x + pl.ny * os.y + pl.nz * os.z)) / den;
-              if (t >= kEps && t < tl) { skip = -2 - q; break; }
+          const d3 ws = ls.x - os;
+          float4 rec;
+          int skip = -1;
+          const double t_n = dot(nrm, ws);  // the sign of n.d_s (shadow_skip) is the sign of n.w_s...
+          const double band = 1e-14 * (fabs(ws.x) + fabs(ws.y) + fabs(ws.z));
+          if (P.n_planes == 0 && (out_sph < 0 || fabs(t_n) > band)) {
+            // ...outside the rounding band (sends_shadow_ray's argument); with no plane to decide
+            // in FP64 the direction only feeds the float record, which the filter's bounds cover
+            // within a few FP64 ulps: an FP64 rsqrt instead of shadow_dir's sqrt and division
+            const double d2 = dot(ws, ws), k = rsqrt(d2);
+            rec = make_float4((float)(ws.x * k), (float)(ws.y * k), (float)(ws.z * k), (float)(d2 * k));
+            skip = (out_sph >= 0 && t_n > 0.0) ? out_sph : -1;
+          } else {
+            d3 ds;
+            double tl;
+            shadow_dir(os, ls.x, ds, tl);
+            skip = shadow_skip(out_sph, nrm, ds);
+            for (int q = 0; q < P.n_planes; ++q) {  // planes first, exactly (FP64), in index order
+              const DevPlane pl = c_planes[q];
+              const double den = pl.nx * ds.x + pl.ny * ds.y + pl.nz * ds.z;
+              if (fabs(den) >= 1e-12) {
+                const double t = (pl.d - (pl.nx * os.x + pl.ny * os.y + pl.nz * os.z)) / den;
+                if (t >= kEps && t < tl) { skip = -2 - q; break; }
+              }
             }
+            rec = make_float4((float)ds.x, (float)ds.y, (float)ds.z, (float)tl);
           }
-          B.lt_dir[g] = make_float4((float)ds.x, (float)ds.y, (float)ds.z, (float)tl);
+          B.lt_dir[g] = rec;
           B.lt_rec[g] = make_int2((int)e, skip);
         } else {
           const int o = -2 - g;
