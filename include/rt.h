@@ -122,7 +122,7 @@ typedef struct {
   double shade_ms;               /* wavefront: summed device time of the wf_shade launches (a4/a6:
                                     FP64 nearest hit, shading, shadow set-up, bounce) */
   double isect_eye_ms;           /* wavefront: the part of isect_closest_ms spent on camera rays
-                                    (depth 0, shared-origin filter) */
+                                    (depth 0, shared-origin tangent test) */
   int32_t graph;                 /* wavefront launch of the call: 0 kernel by kernel, 1 captured
                                     into a CUDA graph and launched, 2 replay of a cached graph
                                     (rt_set_graphs; up to 4 launch keys are cached) */

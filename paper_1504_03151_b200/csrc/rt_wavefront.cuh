@@ -9,13 +9,13 @@
 //   it is used (wf_isect_eye2, wf_shade at depth 0)                                 (a2)
 //   per depth d = 0..max_depth:
 //     isect_closest   Q[d]: FP32 FFMA2 filter over all spheres -> candidate lists     (a3)
-//                     (depth 0: two camera rays per thread, shared-origin filter)
+//                     (depth 0: two camera rays per thread, shared-origin tangent test)
 //     shade           Q[d]: FP64 nearest hit (planes + candidates), emission/ambient,
 //                     shadow entries with their Lambert/Phong contribution, bounce   (a4, a6)
 //                     -> Q[d+1]
 //     isect_shadow    shadow entries: FP64 planes, FP32 filter with early exit on a
 //                     robust (float-certain) occluder -> candidate lists; point
-//                     lights' rays are scanned from the light (wf_isect_lt)           (a5)
+//                     lights' rays are scanned from the light, tangent test (wf_isect_lt) (a5)
 //     accumulate      Q[d]: FP64 occlusion decisions in light order, L += contribution
 //   resolve           sum of the spp sample radiances in order s = 0..spp-1 -> float4 (a7)
 //
