@@ -1211,7 +1211,10 @@ __device__ __forceinline__ void shadow_counts(const DevParams& P, const DevScene
 }
 
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
-constexpr int kLogicMinBlocks = 4;  // wf_accumulate: 64 registers, 4 CTAs per SM
+// wf_accumulate: 40 registers (32 B spilled), 6 CTAs per SM = the logic kernels' grid of 6 CTAs
+// per SM in one wave (C4 in order: 4 CTAs / 64 registers 0.550 ms, 5 / 48 (1.2 waves) 0.589,
+// 6 / 40 0.514, 8 / 32 (52 B spilled) 0.555)
+constexpr int kLogicMinBlocks = 6;
 constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~190 B spilled, 10 % slower)
 #ifndef RT_RES_WARPS
 #define RT_RES_WARPS 4
