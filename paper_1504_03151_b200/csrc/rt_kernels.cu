@@ -924,7 +924,10 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
       const bool rec = ti < tm.cap;
       if (rec && tm.shade) tm.record(tm.shade[2 * ti], st);
       const int grid_q = grid_l;  // logic kernels: grid-stride loops
-      launch(shade, grid_q, 0, st, p, sc, Bc, d, g0, dh, db);
+      // wf_shade: one wave of its resident CTAs for large chunks (C4: 3 / 6 / 9 / 12 CTAs per SM
+      // 5.603 / 5.618 / 5.629 / 5.633 ms per frame), the logic grid for small ones (a world-8 shard
+      // is 0.8 % slower with one wave)
+      launch(shade, npaths >= (1 << 21) ? num_sms * kShadeMinBlocks : grid_q, 0, st, p, sc, Bc, d, g0, dh, db);
       if (rec && tm.shade) tm.record(tm.shade[2 * ti + 1], st);
       cudaStream_t ss = st;
       if (side) {
