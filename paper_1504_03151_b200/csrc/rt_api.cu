@@ -81,7 +81,7 @@ struct Context {
   float cmax = 0.f, rmax = 0.f;
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
-  DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt;
+  DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt, pairs_ltl;
   int lt_lights = 0;  // point lights with light-origin shadow scans (0 = off)
   bool eye_ready = false;
   DevBuf<int> sph_prim, sph_mat, emit_sph;
@@ -384,7 +384,8 @@ int run_render(const rt::DevParams& p, float4* out, int* dbg_hits, int* dbg_boun
   CU(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream), "cudaMemsetAsync");
   CU(cudaMemsetAsync(c.stats.p, 0, sizeof(unsigned long long) * 8, c.stream), "cudaMemsetAsync");
   rt::DevScene sc{c.pairs.p, c.sph_cr.p, c.sph_prim.p, c.sph_mat.p, c.mats.p, c.lights.p, c.emit_sph.p,
-                  c.eye_ready ? c.pairs_eye.p : nullptr, c.lt_lights > 0 ? c.pairs_lt.p : nullptr};
+                  c.eye_ready ? c.pairs_eye.p : nullptr, c.lt_lights > 0 ? c.pairs_lt.p : nullptr,
+                  c.lt_lights > 0 ? c.pairs_ltl.p : nullptr};
   rt::DevOutputs o{out, c.counter.p, c.stats.p, dbg_hits, dbg_bounces, accum};
   // AUTO: the wavefront kernels for large scenes, and for the NEXT-1 / NEXT-2 modes, whose long
   // divergent paths (every diffuse hit continues; one lane per pixel walks all its passes) leave
@@ -922,8 +923,9 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   if (n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
       lt_bytes <= 65536 && in_smem) {
     CU(c.pairs_lt.reserve(2 * (size_t)npairs_pad + lt_bytes / 16 + 1), "cudaMalloc(light pairs)");
+    CU(c.pairs_ltl.reserve((size_t)rt::lt_table_stride(npairs_pad) * n_lights), "cudaMalloc(light pairs)");
     CU(rt::launch_light_tables(c.pairs.p, c.sph_cr.p, c.lights.p, ns, npairs_pad, n_lights, c.centre, c.cmax, c.rmax,
-                               c.pairs_lt.p, c.stream), "light table kernel");
+                               c.pairs_lt.p, c.pairs_ltl.p, c.stream), "light table kernel");
     c.lt_lights = n_lights;
   }
   return build_eye_pairs();

@@ -347,6 +347,20 @@ struct RayFilter {
     tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
     dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
   }
+  // the same as sphere() for a table whose K slots hold something else (a light's -h): c' from
+  // the table gt (kSrc), K from the float2-per-pair column kp
+  template <int kSrc>
+  __device__ __forceinline__ void sphere_k(const float4* __restrict__ gt, const float2* __restrict__ kp, int k,
+                                           float& dd, float& tc) const {
+    const float4 pa = load_pair<kSrc>(gt, 2 * (k >> 1));
+    const float4 pb = load_pair<kSrc>(gt, 2 * (k >> 1) + 1);
+    const float2 kk = kp[k >> 1];
+    const bool h = k & 1;
+    const float cx = h ? pa.y : pa.x, cy = h ? pa.w : pa.z, cz = h ? pb.y : pb.x, w = h ? kk.y : kk.x;
+    const float s1 = fmaf(cx, a1, fmaf(cy, a2, fmaf(cz, a3, w)));
+    tc = fmaf(cx, dx, fmaf(cy, dy, fmaf(cz, dz, b1)));
+    dd = fmaf(tc, tc, s1) - (cut - neg_slack);  // v - |o'|^2
+  }
   // float discriminant estimate dd (|dd - disc| <= slack) and chord centre tc (|err| <= eta) of
   // one sphere k (rare path)
   template <int kSrc>

@@ -126,7 +126,13 @@ struct DevScene {
   // light-origin shadow scans: the pair layout followed by -h(P_l) per point light, float2 per
   // sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy stages both)
   const float4* pairs_lt;
+  // per point light l: the pair layout with -h(P_l) in place of K, followed by K as one float2 per
+  // pair (for the candidates' chord bounds): lt_table_stride(n_pairs_pad) float4 per light; the
+  // long-list light-origin scan stages one light's table at a time
+  const float4* pairs_ltl;
 };
+
+__host__ __device__ constexpr int lt_table_stride(int npp) { return 2 * npp + (npp + 1) / 2; }  // float4 per light
 
 struct DevOutputs {
   float4* out;                  // framebuffer (mode 0) or slab (mode 1)
@@ -207,7 +213,7 @@ struct WfBuffers {
 // point lights: every shadow ray goes through the general scan)
 constexpr int kMaxLtLights = 30;
 constexpr int kLtSub = 8;         // sub-lists per light (slot reservations spread over 8 counters)
-constexpr int kWfCtrPerDepth = 8 + kMaxLtLights * kLtSub;
+constexpr int kWfCtrPerDepth = 8 + kMaxLtLights * kLtSub + 32;
 __host__ __device__ constexpr int wf_ctr_q(int d) { return kWfCtrPerDepth * d; }       // closest queue
 __host__ __device__ constexpr int wf_ctr_s(int d) { return kWfCtrPerDepth * d + 1; }   // shadow entries
 __host__ __device__ constexpr int wf_ctr_wc(int d) { return kWfCtrPerDepth * d + 2; }  // work heads
@@ -216,6 +222,9 @@ __host__ __device__ constexpr int wf_ctr_so(int d) { return kWfCtrPerDepth * d +
 __host__ __device__ constexpr int wf_ctr_wlt(int d) { return kWfCtrPerDepth * d + 5; } // light-scan chunks
 __host__ __device__ constexpr int wf_ctr_lt(int d, int l, int sub) {  // light l's sub-list `sub`
   return kWfCtrPerDepth * d + 8 + l * kLtSub + sub;
+}
+__host__ __device__ constexpr int wf_ctr_wltl(int d, int l) {  // light l's chunk head (wf_isect_lt)
+  return kWfCtrPerDepth * d + 8 + kMaxLtLights * kLtSub + l;
 }
 constexpr int kPrevDiffuse = 0x100;  // flag in WfBuffers::depth (R#43)
 
@@ -226,7 +235,7 @@ cudaError_t launch_eye_table(const float4* pairs, const float4* sph_cr, int ns, 
                              const double centre[3], double S, float4* out, cudaStream_t st);
 cudaError_t launch_light_tables(const float4* pairs, const float4* sph_cr, const DevLight* lights, int ns, int npp,
                                 int n_lights, const double centre[3], float cmax, float rmax, float4* out,
-                                cudaStream_t st);
+                                float4* out_per_light, cudaStream_t st);
 cudaError_t launch_render(const DevParams& p, const DevScene& sc, const DevOutputs& o,
                           bool smem_scene, int num_sms, cudaStream_t st);
 // buffer sizes of one chunk: cap paths, scap = cap x sources shadow entries, gcap generic

@@ -529,10 +529,13 @@ __global__ void build_eye_table(const float4* __restrict__ pairs, const float4* 
                       (float)((double)b.w + 2.0 * ((double)a.y * px + (double)a.w * py + (double)b.y * pz)));
 }
 // The light-origin tables: the pairs, then -h of light l for every sphere slot k
-// (out + 2 npp as floats, [l][2 npp]). One thread per (light, sphere slot).
+// (out + 2 npp as floats, [l][2 npp]: the short-list scan stages all of them); and per light the
+// pair layout with -h in place of K (out_pl, [l][2 npp] float4: the long-list scan stages one).
+// One thread per (light, sphere slot).
 __global__ void build_light_tables(const float4* __restrict__ pairs, const float4* __restrict__ sph_cr,
                                    const DevLight* __restrict__ lights, int ns, int npp, int n_lights, double cx,
-                                   double cy, double cz, float cmax, float rmax, float4* __restrict__ out) {
+                                   double cy, double cz, float cmax, float rmax, float4* __restrict__ out,
+                                   float4* __restrict__ out_pl) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 2 * npp) out[i] = pairs[i];
   if (i >= n_lights * 2 * npp) return;
@@ -541,7 +544,18 @@ __global__ void build_light_tables(const float4* __restrict__ pairs, const float
   const double ox = L.px, oy = L.py, oz = L.pz;
   const double px = ox - cx, py = oy - cy, pz = oz - cz;
   const double S = (double)cmax + sqrt(px * px + py * py + pz * pz) + (double)rmax;
-  reinterpret_cast<float*>(out + 2 * npp)[i] = k < ns ? neg_tangent(sph_cr[k], ox, oy, oz, S) : -1e30f;
+  const float nh = k < ns ? neg_tangent(sph_cr[k], ox, oy, oz, S) : -1e30f;
+  reinterpret_cast<float*>(out + 2 * npp)[i] = nh;
+  // per-light pair layout: pair q = k / 2, float4 {cx0, cx1, cy0, cy1} then {cz0, cz1, nh0, nh1};
+  // after the 2 npp float4, K as {K0, K1} per pair
+  const int q = k >> 1, h = k & 1;
+  float4* T = out_pl + (size_t)l * lt_table_stride(npp);
+  if (h == 0) T[2 * q] = pairs[2 * q];
+  float* b = reinterpret_cast<float*>(&T[2 * q + 1]);
+  const float* pb = reinterpret_cast<const float*>(&pairs[2 * q + 1]);
+  b[h] = pb[h];  // c'z
+  b[2 + h] = nh;
+  reinterpret_cast<float*>(T + 2 * npp)[k] = pb[2 + h];  // K
 }
 
 cudaError_t launch_eye_table(const float4* pairs, const float4* sph_cr, int ns, int npp, const double o[3],
@@ -552,10 +566,10 @@ cudaError_t launch_eye_table(const float4* pairs, const float4* sph_cr, int ns, 
 }
 cudaError_t launch_light_tables(const float4* pairs, const float4* sph_cr, const DevLight* lights, int ns, int npp,
                                 int n_lights, const double centre[3], float cmax, float rmax, float4* out,
-                                cudaStream_t st) {
+                                float4* out_per_light, cudaStream_t st) {
   const int n = (n_lights > 1 ? n_lights : 1) * 2 * npp;
   build_light_tables<<<(n + 255) / 256, 256, 0, st>>>(pairs, sph_cr, lights, ns, npp, n_lights, centre[0], centre[1],
-                                                      centre[2], cmax, rmax, out);
+                                                      centre[2], cmax, rmax, out, out_per_light);
   return cudaGetLastError();
 }
 
@@ -809,17 +823,18 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const size_t smem_eye = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 40u : smem_long;
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
-  size_t smem_lt = 0;
+  size_t smem_lt = 0, smem_ltl = 0;  // the split scan stages every light's -h column, the long one a light's table
   int grid_lt = 0;
   if constexpr (kSrc == SRC_SMEM) {
     if (p.lt_lights > 0) {
       klt = wf_isect_lt<kSrc>;
       klts = wf_isect_lt_split<kSrc>;
       smem_lt = (size_t)p.n_pairs_pad * 32u + (size_t)p.lt_lights * p.n_pairs_pad * 8u;
-      if ((e = cudaFuncSetAttribute(klt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
+      smem_ltl = (size_t)lt_table_stride(p.n_pairs_pad) * 16u;
+      if ((e = cudaFuncSetAttribute(klt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ltl)) != cudaSuccess) return e;
       if ((e = cudaFuncSetAttribute(klts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
       int occ = 0;
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, klt, 256, smem_lt)) != cudaSuccess) return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, klt, 256, smem_ltl)) != cudaSuccess) return e;
       grid_lt = num_sms * (occ > 0 ? occ : 1);
     }
   }
@@ -942,10 +957,11 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
         if (hint) {
           unsigned chunks = 0;
           for (int i = 0; i < p.lt_lights * kLtSub; ++i) chunks += (hint[wf_ctr_lt(d, 0, 0) + i] + 63u) / 64u;
-          launch(host_parts(chunks, grid_lt) > 1 ? klts : klt, grid_lt, smem_lt, ss, p, sc, Bs, d);
+          if (host_parts(chunks, grid_lt) > 1) launch(klts, grid_lt, smem_lt, ss, p, sc, Bs, d);
+          else launch(klt, grid_lt, smem_ltl, ss, p, sc, Bs, d);
           scan_launches += 1;
         } else {
-          launch(klt, grid_lt, smem_lt, ss, p, sc, Bc, d);
+          launch(klt, grid_lt, smem_ltl, ss, p, sc, Bc, d);
           launch(klts, grid_lt, smem_lt, ss, p, sc, Bc, d);
           scan_launches += 2;
         }

@@ -923,9 +923,12 @@ __device__ __forceinline__ void lt_setup(const DevParams& P, const DevScene& S, 
   R.tlerr = 4.0e-7f * R.tl_f + 1.0e-6f * R.F.eta;  // t_l to float, P_l vs o + t_l d, the subtraction
 }
 
+// gk == nullptr: gp is the shared pair layout (K in place); else gp is a light's table (-h in
+// place of K) and K comes from the float2-per-pair column gk
 template <int kSrc>
-__device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* __restrict__ gp, unsigned m, int kbase,
-                                              LtRay& R, int* cand_row) {
+__device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* __restrict__ gp,
+                                              const float2* __restrict__ gk, unsigned m, int kbase, LtRay& R,
+                                              int* cand_row) {
   const float eps_f = (float)kEps;
   while (m != 0u) {
     const int i = __ffs(m) - 1;
@@ -934,7 +937,8 @@ __device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* 
     if (k >= P.n_spheres) break;
     if (k == R.skip) continue;
     float dd, tc;  // tc along -d from P_l
-    R.F.template sphere<kSrc>(gp, k, dd, tc);
+    if (gk) R.F.template sphere_k<kSrc>(gp, gk, k, dd, tc);
+    else R.F.template sphere<kSrc>(gp, k, dd, tc);
     if (dd < R.F.neg_slack) continue;                  // certainly no real root
     const float qh = sqrtf(fmaxf(dd - R.F.neg_slack, 0.f));
     const float ql = sqrtf(fmaxf(dd + R.F.neg_slack, 0.f));
@@ -958,10 +962,14 @@ __device__ __forceinline__ void lt_candidates(const DevParams& P, const float4* 
   }
 }
 
-// the light-origin scan of two rays of light l (one thread) over the sphere pairs [pb, pe)
-template <int kSrc>
+// the light-origin scan of two rays of light l (one thread) over the sphere pairs [pb, pe):
+// kTable = false: the shared pair layout gp + light l's -h column nhp (the short-list scan stages
+// every light's column); true: light l's own table gp ({c'x, c'y | c'z, -h}, two LDS.128 per pair
+// like the camera-ray scan), K for the candidates from its column gk
+template <int kSrc, bool kTable = false>
 __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __restrict__ gp, const float2* __restrict__ nhp,
-                                        int pb, int pe, LtRay& Ra, LtRay& Rb, int* rowa, int* rowb) {
+                                        const float2* __restrict__ gk, int pb, int pe, LtRay& Ra, LtRay& Rb, int* rowa,
+                                        int* rowb) {
   const float2 D1a = make_float2(Ra.F.dx, Ra.F.dx), D2a = make_float2(Ra.F.dy, Ra.F.dy);
   const float2 D3a = make_float2(Ra.F.dz, Ra.F.dz);
   const float2 D1b = make_float2(Rb.F.dx, Rb.F.dx), D2b = make_float2(Rb.F.dy, Rb.F.dy);
@@ -972,7 +980,7 @@ __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __rest
     for (int i = 0; i < kLtPB; ++i) {
       const float4 a = load_pair<kSrc>(gp, 2 * (base + i));
       const float4 b = load_pair<kSrc>(gp, 2 * (base + i) + 1);
-      const float2 NH = nhp[base + i];
+      const float2 NH = kTable ? make_float2(b.z, b.w) : nhp[base + i];
       const float2 CX = make_float2(a.x, a.y), CY = make_float2(a.z, a.w), CZ = make_float2(b.x, b.y);
       ua[i] = __ffma2_rn(CX, D1a, __ffma2_rn(CY, D2a, __ffma2_rn(CZ, D3a, NH)));  // c'.d' - h_l
       ub[i] = __ffma2_rn(CX, D1b, __ffma2_rn(CY, D2b, __ffma2_rn(CZ, D3b, NH)));
@@ -990,14 +998,14 @@ __device__ __forceinline__ void lt_scan(const DevParams& P, const float4* __rest
 #pragma unroll
         for (int i = 0; i < kLtPB; ++i)
           m |= ((ua[i].x >= Ra.cu) ? 1u : 0u) << (2 * i) | ((ua[i].y >= Ra.cu) ? 1u : 0u) << (2 * i + 1);
-        lt_candidates<kSrc>(P, gp, m, 2 * base, Ra, rowa);
+        lt_candidates<kSrc>(P, gp, kTable ? gk : nullptr, m, 2 * base, Ra, rowa);
       }
       if (cb) {
         unsigned m = 0u;
 #pragma unroll
         for (int i = 0; i < kLtPB; ++i)
           m |= ((ub[i].x >= Rb.cu) ? 1u : 0u) << (2 * i) | ((ub[i].y >= Rb.cu) ? 1u : 0u) << (2 * i + 1);
-        lt_candidates<kSrc>(P, gp, m, 2 * base, Rb, rowb);
+        lt_candidates<kSrc>(P, gp, kTable ? gk : nullptr, m, 2 * base, Rb, rowb);
       }
     }
     if (!__any_sync(kFull, Ra.act || Rb.act)) break;  // Alg. 1 `break`, warp-wide
@@ -1034,6 +1042,44 @@ __device__ __forceinline__ int lt_list_of(const unsigned* s_end, int nl, unsigne
   return lo;
 }
 
+// thread 0 of wf_isect_lt: the next light (after *light) whose chunks are not all taken, its
+// chunk range, and its table staged on the barrier (the previous table is free: every warp
+// passed the CTA barrier); *light = -1 when every light's chunks are taken. Out of line: the
+// scan's registers are not spent on it.
+__device__ __noinline__ void lt_pick_stage(const DevParams& P, const DevScene& S, const WfBuffers& B, int d,
+                                           const unsigned* s_chunk_end, uint64_t* mbar, int* light, unsigned* lo_out,
+                                           unsigned* hi_out) {
+  const int LT = P.lt_lights;
+  int pick = -1;
+  unsigned plo = 0u, phi = 0u;
+  for (int t = 1; t <= LT && pick < 0; ++t) {
+    const int l = (*light + t) % LT;
+    const unsigned lo = l > 0 ? s_chunk_end[l * kLtSub - 1] : 0u, hi = s_chunk_end[l * kLtSub + kLtSub - 1];
+    if (*(volatile unsigned*)(B.ctr + wf_ctr_wltl(d, l)) < hi - lo) { pick = l; plo = lo; phi = hi; }
+  }
+  *light = pick;
+  *lo_out = plo;
+  *hi_out = phi;
+  if (pick < 0) return;
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  const uint32_t table_bytes = (uint32_t)lt_table_stride(P.n_pairs_pad) * 16u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(table_bytes) : "memory");
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_pairs);
+  const char* src = reinterpret_cast<const char*>(S.pairs_ltl + (size_t)pick * lt_table_stride(P.n_pairs_pad));
+  constexpr uint32_t kChunk = 1u << 15;
+  for (uint32_t off = 0; off < table_bytes; off += kChunk) {
+    const uint32_t n = (table_bytes - off) < kChunk ? (table_bytes - off) : kChunk;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+                 "l"(src + off), "r"(n), "r"(mb)
+                 : "memory");
+  }
+}
+
+// Long lists: a CTA works on one light at a time and stages only that light's table (the pair
+// layout with -h in place of K: two LDS.128 per pair and no column load, 32 B per pair of shared
+// memory whatever the number of lights). It starts on light blockIdx % lights, takes 64-entry
+// chunks of that light's sub-lists (one head per light) and, when they run out, moves to the next
+// light with chunks left, restaging after a CTA barrier.
 template <int kSrc>
 __global__ void __launch_bounds__(256, kIsectMinBlocks)
 wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
@@ -1041,34 +1087,69 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights * kLtSub];
   __shared__ unsigned s_warp[8];
+  __shared__ int s_light;                  // the light being scanned (thread 0 picks it), -1: done
+  __shared__ unsigned s_lo, s_hi, s_phase;  // its chunk range, the staging barrier's parity
   const unsigned n_chunks = lt_chunk_prefix(P, B, d, s_chunk_end, s_warp);
   if (!B.solo && split_parts(n_chunks, B) > 1) return;  // a short list: wf_isect_lt_split scans it
   if ((unsigned long long)blockIdx.x * (blockDim.x / 32u) >= n_chunks) return;  // CTAs without work
-  stage_scene(s_pairs, S.pairs_lt, (uint32_t)P.n_pairs_pad * 32u + (uint32_t)P.lt_lights * P.n_pairs_pad * 8u, &s_mbar);
-  const float4* gp = S.pairs_lt;
-  const float2* nh_all = reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad);
   const int lane = threadIdx.x & 31;
-  const int nl = P.lt_lights * kLtSub;
+  if (threadIdx.x == 0) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_light = (int)(blockIdx.x % (unsigned)P.lt_lights) - 1;  // the first pick starts at blockIdx % lights
+    s_phase = 0u;
+  }
+  __syncthreads();
   while (true) {
-    unsigned k = 0;
-    if (lane == 0) k = atomicAdd(B.ctr + wf_ctr_wlt(d), 1u);
-    k = __shfl_sync(kFull, k, 0);
-    if (k >= n_chunks) break;
-    const int li = lt_list_of(s_chunk_end, nl, k);
-    const int l = li / kLtSub;
-    const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
-    const unsigned cnt = B.ctr[wf_ctr_lt(d, 0, 0) + li];
-    RT_CHECK(cnt <= (unsigned)B.lt_cap && li < nl, 402);
-    const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
-    const bool va_ = oa < cnt, vb_ = ob < cnt;
-    const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;  // list slots
-    LtRay Ra, Rb;
-    lt_setup(P, S, B, ga, va_, l, Ra);
-    lt_setup(P, S, B, gb, vb_, l, Rb);
-    lt_scan<kSrc>(P, gp, nh_all + (size_t)l * P.n_pairs_pad, 0, P.n_pairs_pad, Ra, Rb, B.lt_cand + (size_t)ga * kCandMax,
-                  B.lt_cand + (size_t)gb * kCandMax);
-    if (va_) B.lt_res[ga] = make_int2(Ra.rob, Ra.nc);
-    if (vb_) B.lt_res[gb] = make_int2(Rb.rob, Rb.nc);
+    if (threadIdx.x == 0) lt_pick_stage(P, S, B, d, s_chunk_end, &s_mbar, &s_light, &s_lo, &s_hi);
+    __syncthreads();
+    const int L = s_light;
+    if (L < 0) break;
+    mbar_wait(&s_mbar, s_phase);
+#if RT_CHECKS
+    for (int q = threadIdx.x; q < P.n_pairs_pad; q += blockDim.x) {
+      const float4 a = s_pairs[2 * q], b = s_pairs[2 * q + 1], ga = S.pairs[2 * q], gb = S.pairs[2 * q + 1];
+      const float2 nh = reinterpret_cast<const float2*>(S.pairs_lt + 2 * P.n_pairs_pad)[(size_t)L * P.n_pairs_pad + q];
+      RT_CHECK(a.x == ga.x && a.y == ga.y && a.z == ga.z && a.w == ga.w, 405);
+      RT_CHECK(b.x == gb.x && b.y == gb.y, 406);
+      RT_CHECK(b.z == nh.x && b.w == nh.y, 407);
+    }
+#endif
+    while (true) {
+      unsigned k = 0;
+      if (lane == 0) k = atomicAdd(B.ctr + wf_ctr_wltl(d, L), 1u);
+      k = __shfl_sync(kFull, k, 0) + s_lo;  // a chunk of light L's sub-lists
+      if (k >= s_hi) break;
+      const int li = lt_list_of(s_chunk_end, P.lt_lights * kLtSub, k);
+      const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
+      const unsigned cnt = B.ctr[wf_ctr_lt(d, 0, 0) + li];
+      RT_CHECK(cnt <= (unsigned)B.lt_cap && li / kLtSub == L, 402);
+      const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
+      const bool va_ = oa < cnt, vb_ = ob < cnt;
+      const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;  // list slots
+      LtRay Ra, Rb;
+      lt_setup(P, S, B, ga, va_, L, Ra);
+      lt_setup(P, S, B, gb, vb_, L, Rb);
+      lt_scan<kSrc, true>(P, s_pairs, nullptr, reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad), 0,
+                          P.n_pairs_pad, Ra, Rb, B.lt_cand + (size_t)ga * kCandMax, B.lt_cand + (size_t)gb * kCandMax);
+#if RT_CHECKS
+      {  // the same rays through the shared-layout scan from global memory
+        LtRay Ra2, Rb2;
+        lt_setup(P, S, B, ga, va_, L, Ra2);
+        lt_setup(P, S, B, gb, vb_, L, Rb2);
+        int* xa = B.xcand_s + ((size_t)(blockIdx.x * 8 + (threadIdx.x >> 5)) * 64 + lane) * kCandMax;
+        lt_scan<SRC_GLOBAL, false>(P, S.pairs_lt, reinterpret_cast<const float2*>(S.pairs_lt + 2 * P.n_pairs_pad) +
+                                   (size_t)L * P.n_pairs_pad, nullptr, 0, P.n_pairs_pad, Ra2, Rb2, xa, xa + 32 * kCandMax);
+        RT_CHECK(!va_ || (Ra.rob == Ra2.rob && Ra.nc == Ra2.nc), 408);
+        RT_CHECK(!vb_ || (Rb.rob == Rb2.rob && Rb.nc == Rb2.nc), 409);
+      }
+#endif
+      if (va_) B.lt_res[ga] = make_int2(Ra.rob, Ra.nc);
+      if (vb_) B.lt_res[gb] = make_int2(Rb.rob, Rb.nc);
+    }
+    __syncthreads();  // every warp is done with light L's table (and has read s_phase)
+    if (threadIdx.x == 0) s_phase ^= 1u;
   }
 }
 
@@ -1117,7 +1198,7 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
     LtRay Ra, Rb;
     lt_setup(P, S, B, ga, va_, l, Ra);
     lt_setup(P, S, B, gb, vb_, l, Rb);
-    lt_scan<kSrc>(P, gp, nh_all + (size_t)l * P.n_pairs_pad, pb, pe, Ra, Rb, xa, xb);
+    lt_scan<kSrc>(P, gp, nh_all + (size_t)l * P.n_pairs_pad, nullptr, pb, pe, Ra, Rb, xa, xb);
     s_nc[warp][lane] = Ra.nc;
     s_nc[warp][lane + 32] = Rb.nc;
     s_rob[warp][lane] = Ra.rob;
@@ -1542,6 +1623,9 @@ __global__ void __launch_bounds__(256, kShadeMinBlocks) wf_shade(const DevParams
           }
           B.lt_dir[g] = rec;
           B.lt_rec[g] = make_int2((int)e, skip);
+#if RT_CHECKS
+          B.lt_res[g] = make_int2(-77, -77);  // every slot must be scanned before wf_accumulate reads it
+#endif
         } else {
           const int o = -2 - g;
           d3 os2, ds;
@@ -1589,6 +1673,7 @@ __global__ void __launch_bounds__(256, kLogicMinBlocks) wf_accumulate(const DevP
         const int* cand;
         if (lt) {
           const int2 r = B.lt_res[g];
+          RT_CHECK(r.x != -77, 205);
           rob = r.x;
           nc = r.y;
           cand = B.lt_cand + (size_t)g * kCandMax;
