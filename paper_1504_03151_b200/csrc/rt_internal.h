@@ -123,8 +123,9 @@ struct DevScene {
   // camera rays: the pair layout with -h(eye) in place of K (rt_kernels.cu neg_tangent), followed by
   // s1 = K + 2 c'.o'(eye), float2 per sphere pair [n_pairs_pad]
   const float4* pairs_eye;
-  // light-origin shadow scans: the pair layout followed by -h(P_l) per point light, float2 per
-  // sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy stages both)
+  // light-origin shadow scans of short lists (wf_isect_lt_split): the pair layout followed by
+  // -h(P_l) per point light, float2 per sphere pair, [lt_lights][n_pairs_pad] (one TMA bulk copy
+  // stages both)
   const float4* pairs_lt;
   // per point light l: the pair layout with -h(P_l) in place of K, followed by K as one float2 per
   // pair (for the candidates' chord bounds): lt_table_stride(n_pairs_pad) float4 per light; the

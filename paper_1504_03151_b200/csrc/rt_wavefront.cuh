@@ -863,9 +863,10 @@ wf_isect_eye2_tiled(const DevParams P, const DevScene S, WfBuffers B, int d) {
 // only filters (FP64 decides on the original ray in wf_accumulate). Traced from the light, every
 // shadow ray of light l shares the origin P_l, and an occluder lies on the reversed half-line
 // s = t_l - t > 0: the tangent test c'.d' - h_l >= o'.d' (RayFilter::tangent_cut; -h_l per
-// sphere and light precomputed in S.pairs_lt, rt_kernels.cu neg_tangent) costs 3 FMA per sphere
-// instead of 7, and a thread carries two rays of the same light (one shared-memory read serves
-// both). Work comes in chunks of 64 entries of one list. The chord [tc' - q, tc' + q] along the
+// sphere and light precomputed, rt_kernels.cu neg_tangent: light l's own table in S.pairs_ltl for
+// the long lists, every light's column after the pairs in S.pairs_lt for the short-list split
+// scan) costs 3 FMA per sphere instead of 7, and a thread carries two rays of the same light (one
+// shared-memory read serves both). Work comes in chunks of 64 entries of one list. The chord [tc' - q, tc' + q] along the
 // reversed ray maps back to t = t_l - tc' -/+ q on the original one; the bounds add the error of
 // t_l and of the reversal.
 // Why the half-line is safe: a sphere the test drops (light outside it by more than 1e-6 S, else
