@@ -819,8 +819,7 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const IsectFn ksl = kSrc == SRC_TILE ? (IsectFn)wf_isect_tiled<true> : (IsectFn)wf_isect<kScan, true>;
   // camera rays (depth 0): two per thread through the shared-origin filter on the eye's pair table
   const IsectFn kc0 = kSrc == SRC_TILE ? (IsectFn)wf_isect_eye2_tiled : (IsectFn)wf_isect_eye2<kScan>;
-  // (shared-memory scene: the eye's table is the pairs plus one float2 s1 per pair)
-  const size_t smem_eye = kSrc == SRC_SMEM ? (size_t)p.n_pairs_pad * 40u : smem_long;
+  const size_t smem_eye = smem_long;  // the eye's pairs (its s1 column stays in global memory)
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
   size_t smem_lt = 0, smem_ltl = 0;  // the split scan stages every light's -h column, the long one a light's table
