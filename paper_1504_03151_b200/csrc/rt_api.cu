@@ -69,6 +69,34 @@ struct DevBuf {
   }
 };
 
+// pinned host staging for the scene copies: from pinned memory an async copy is a plain DMA
+// (from pageable memory every call first copies into a driver buffer); the next upload waits for
+// the previous one's copies before it rewrites the buffer
+struct PinnedStage {
+  char* p = nullptr;
+  size_t n = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  cudaError_t reserve(size_t bytes) {
+    if (pending) {
+      cudaError_t e = cudaEventSynchronize(done);
+      if (e != cudaSuccess) return e;
+      pending = false;
+    }
+    if (!done) {
+      cudaError_t e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&p), bytes ? bytes : 1);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+};
+
 struct Context {
   int device = -1;
   int num_sms = 0;
@@ -82,6 +110,7 @@ struct Context {
   double centre[3] = {0, 0, 0};
   float bg[3] = {0, 0, 0}, amb[3] = {0, 0, 0};
   DevBuf<float4> pairs, sph_cr, stage, pairs_eye, pairs_lt, pairs_ltl;
+  PinnedStage upload;  // host staging of rt_scene_upload's copies
   int lt_lights = 0;  // point lights with light-origin shadow scans (0 = off)
   bool eye_ready = false;
   DevBuf<int> sph_prim, sph_mat, emit_sph;
@@ -894,18 +923,32 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
   CU(c.mats.reserve(dm.size()), "cudaMalloc(materials)");
   CU(c.lights.reserve(dl.size()), "cudaMalloc(lights)");
   CU(c.emit_sph.reserve(emit.size() > 0 ? emit.size() : 1), "cudaMalloc(emitters)");
-  if (!emit.empty())
-    CU(cudaMemcpyAsync(c.emit_sph.p, emit.data(), sizeof(int) * emit.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.pairs.p, pairs.data(), sizeof(float4) * pairs.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.sph_cr.p, cr.data(), sizeof(float4) * cr.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.sph_prim.p, sprim.data(), sizeof(int) * sprim.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.sph_mat.p, smat.data(), sizeof(int) * smat.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
-  CU(cudaMemcpyAsync(c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size(), cudaMemcpyHostToDevice, c.stream), "H2D");
+  {  // every array through the pinned staging buffer, then async copies (no stream sync: the
+     // tables below are built on the device from these copies)
+    struct Part { void* dst; const void* src; size_t bytes; };
+    const Part parts[] = {{c.pairs.p, pairs.data(), sizeof(float4) * pairs.size()},
+                          {c.sph_cr.p, cr.data(), sizeof(float4) * cr.size()},
+                          {c.sph_prim.p, sprim.data(), sizeof(int) * sprim.size()},
+                          {c.sph_mat.p, smat.data(), sizeof(int) * smat.size()},
+                          {c.mats.p, dm.data(), sizeof(rt::DevMat) * dm.size()},
+                          {c.lights.p, dl.data(), sizeof(rt::DevLight) * dl.size()},
+                          {c.emit_sph.p, emit.data(), sizeof(int) * emit.size()},
+                          {nullptr, planes.data(), sizeof(rt::DevPlane) * (size_t)np}};
+    size_t total = 0;
+    for (const Part& q : parts) total += (q.bytes + 255) & ~size_t(255);
+    CU(c.upload.reserve(total), "cudaMallocHost(upload staging)");
+    size_t off = 0;
+    for (const Part& q : parts) {
+      if (q.bytes == 0) continue;
+      std::memcpy(c.upload.p + off, q.src, q.bytes);
+      if (q.dst) CU(cudaMemcpyAsync(q.dst, c.upload.p + off, q.bytes, cudaMemcpyHostToDevice, c.stream), "H2D");
+      else CU(rt::upload_planes(reinterpret_cast<const rt::DevPlane*>(c.upload.p + off), np, c.stream), "constant upload (planes)");
+      off += (q.bytes + 255) & ~size_t(255);
+    }
+    CU(cudaEventRecord(c.upload.done, c.stream), "cudaEventRecord");
+    c.upload.pending = true;
+  }
   const bool in_smem = npairs_pad <= rt::kMaxSmemPairs;
-  CU(rt::upload_planes(planes.data(), np, c.stream), "constant upload (planes)");
-  // (no stream sync: an async copy from pageable memory returns once the data is staged, so the
-  // host vectors may die at return; the tables below are built on the device from these copies)
   c.smem_scene = in_smem;
   c.cmax = (float)(cmax * (1.0 + 1e-6));  // rounded up: the float filter bound must not shrink
   for (int k = 0; k < 3; ++k) c.centre[k] = centre[k];
