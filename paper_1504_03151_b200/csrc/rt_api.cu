@@ -964,13 +964,13 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
     c.amb[k] = env ? env->ambient[k] : 0.f;
   }
   c.has_scene = true;
-  // light-origin shadow scans (rt_wavefront.cuh wf_isect_lt): after a copy of the pairs, -h of
-  // each point light per sphere (one float2 per pair and light, built on the device); on while
-  // the tables fit 64 KB of shared memory
+  // light-origin shadow scans (rt_wavefront.cuh wf_isect_lt / _split): per point light its own
+  // table (the pairs with -h in place of K, then K; the scans stage one light's at a time), and
+  // the pairs followed by every light's -h column (the checked build's reference); built on the
+  // device; on for up to 30 point lights (wf_shade's reservation lanes) in a shared-memory scene
   c.lt_lights = 0;
   const size_t lt_bytes = (size_t)n_lights * npairs_pad * 8;
-  if (n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 &&
-      lt_bytes <= 65536 && in_smem) {
+  if (n_lights > 0 && n_lights <= rt::kMaxLtLights && ns > 0 && in_smem) {
     CU(c.pairs_lt.reserve(2 * (size_t)npairs_pad + lt_bytes / 16 + 1), "cudaMalloc(light pairs)");
     CU(c.pairs_ltl.reserve((size_t)rt::lt_table_stride(npairs_pad) * n_lights), "cudaMalloc(light pairs)");
     CU(rt::launch_light_tables(c.pairs.p, c.sph_cr.p, c.lights.p, ns, npairs_pad, n_lights, c.centre, c.cmax, c.rmax,

@@ -822,14 +822,16 @@ static cudaError_t wf_run(const DevParams& p, const DevScene& sc, const DevOutpu
   const size_t smem_eye = smem_long;  // the eye's pairs (its s1 column stays in global memory)
   // point lights' shadow rays scanned from the light (shared-memory scene with the light tables)
   IsectFn klt = nullptr, klts = nullptr;
-  size_t smem_lt = 0, smem_ltl = 0;  // the split scan stages every light's -h column, the long one a light's table
+  size_t smem_lt = 0, smem_ltl = 0;  // the short-list scan's staging, the long-list scan's (one light's table)
   int grid_lt = 0;
   if constexpr (kSrc == SRC_SMEM) {
     if (p.lt_lights > 0) {
       klt = wf_isect_lt<kSrc>;
-      klts = wf_isect_lt_split<kSrc>;
-      smem_lt = (size_t)p.n_pairs_pad * 32u + (size_t)p.lt_lights * p.n_pairs_pad * 8u;
-      smem_ltl = (size_t)lt_table_stride(p.n_pairs_pad) * 16u;
+      // short lists: every light's column beside the pairs while they fit 64 KB, else light by light
+      const bool cols = (size_t)p.lt_lights * p.n_pairs_pad * 8u <= 65536u;
+      klts = cols ? (IsectFn)wf_isect_lt_split<kSrc, false> : (IsectFn)wf_isect_lt_split<kSrc, true>;
+      smem_ltl = (size_t)lt_table_stride(p.n_pairs_pad) * 16u;  // one light's table
+      smem_lt = cols ? (size_t)p.n_pairs_pad * 32u + (size_t)p.lt_lights * p.n_pairs_pad * 8u : smem_ltl;
       if ((e = cudaFuncSetAttribute(klt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ltl)) != cudaSuccess) return e;
       if ((e = cudaFuncSetAttribute(klts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lt)) != cudaSuccess) return e;
       int occ = 0;

@@ -1051,14 +1051,14 @@ __device__ __forceinline__ int lt_list_of(const unsigned* s_end, int nl, unsigne
 // scan's registers are not spent on it.
 __device__ __noinline__ void lt_pick_stage(const DevParams& P, const DevScene& S, const WfBuffers& B, int d,
                                            const unsigned* s_chunk_end, uint64_t* mbar, int* light, unsigned* lo_out,
-                                           unsigned* hi_out) {
+                                           unsigned* hi_out, unsigned tpc) {
   const int LT = P.lt_lights;
   int pick = -1;
   unsigned plo = 0u, phi = 0u;
-  for (int t = 1; t <= LT && pick < 0; ++t) {
+  for (int t = 1; t <= LT && pick < 0; ++t) {  // the light's head counts units of tpc chunks
     const int l = (*light + t) % LT;
     const unsigned lo = l > 0 ? s_chunk_end[l * kLtSub - 1] : 0u, hi = s_chunk_end[l * kLtSub + kLtSub - 1];
-    if (*(volatile unsigned*)(B.ctr + wf_ctr_wltl(d, l)) < hi - lo) { pick = l; plo = lo; phi = hi; }
+    if (*(volatile unsigned*)(B.ctr + wf_ctr_wltl(d, l)) < (hi - lo + tpc - 1u) / tpc) { pick = l; plo = lo; phi = hi; }
   }
   *light = pick;
   *lo_out = plo;
@@ -1105,7 +1105,7 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
   }
   __syncthreads();
   while (true) {
-    if (threadIdx.x == 0) lt_pick_stage(P, S, B, d, s_chunk_end, &s_mbar, &s_light, &s_lo, &s_hi);
+    if (threadIdx.x == 0) lt_pick_stage(P, S, B, d, s_chunk_end, &s_mbar, &s_light, &s_lo, &s_hi, 1u);
     __syncthreads();
     const int L = s_light;
     if (L < 0) break;
@@ -1158,8 +1158,11 @@ wf_isect_lt(const DevParams P, const DevScene S, WfBuffers B, int d) {
 
 // the light-origin scan of a short list: parts warps of a CTA share a 64-entry chunk (sphere
 // ranges), merged in part order as in wf_isect_split
+// Two organisations of the short-list scan: every light's -h column staged beside the pairs (a
+// CTA unit may mix lights; up to 64 KB of columns: C4 frame 5.490 vs 5.501 ms, world-8 shard
+// 0.93 vs 0.95 ms), or one light's table at a time (any number of lights x spheres)
 template <int kSrc>
-__device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
+__device__ __forceinline__ void wf_isect_lt_split_cols(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
   static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
   __shared__ uint64_t s_mbar;
   __shared__ unsigned s_chunk_end[kMaxLtLights * kLtSub];
@@ -1225,9 +1228,93 @@ __device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const
 }
 
 template <int kSrc>
+__device__ __forceinline__ void wf_isect_lt_split_body(const DevParams& P, const DevScene& S, const WfBuffers& B, int d) {
+  static_assert(kSrc == SRC_SMEM, "light-origin scan stages the light tables in smem");
+  __shared__ uint64_t s_mbar;
+  __shared__ unsigned s_chunk_end[kMaxLtLights * kLtSub];
+  __shared__ unsigned s_warp[8];
+  __shared__ int s_nc[8][64];
+  __shared__ int s_rob[8][64];
+  __shared__ unsigned s_unit;
+  __shared__ int s_light;                  // as in wf_isect_lt: one light's table at a time
+  __shared__ unsigned s_lo, s_hi, s_phase;
+  const unsigned n_chunks = lt_chunk_prefix(P, B, d, s_chunk_end, s_warp);
+  const int parts = split_parts(n_chunks, B);
+  if (parts == 1 && !B.solo) return;  // a long list: wf_isect_lt scans it (solo: one part here)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tpc = 8 / parts;  // chunks per CTA unit (units never straddle two lights)
+  if (blockIdx.x >= (n_chunks + tpc - 1) / tpc + (unsigned)P.lt_lights) return;  // CTAs without work
+  const int slot = warp / parts, part = warp % parts;
+  const int nl = P.lt_lights * kLtSub;
+  int pb, pe;
+  split_range(P, part, parts, pb, pe);
+  const size_t xs = (size_t)64 * kCandMax;
+  int* xa = B.xcand_s + ((size_t)(blockIdx.x * 8 + warp) * 64 + lane) * kCandMax;
+  int* xb = xa + 32 * kCandMax;
+  if (threadIdx.x == 0) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_light = (int)(blockIdx.x % (unsigned)P.lt_lights) - 1;
+    s_phase = 0u;
+  }
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) lt_pick_stage(P, S, B, d, s_chunk_end, &s_mbar, &s_light, &s_lo, &s_hi, (unsigned)tpc);
+    __syncthreads();
+    const int l = s_light;
+    if (l < 0) break;
+    mbar_wait(&s_mbar, s_phase);
+    const unsigned units = (s_hi - s_lo + tpc - 1) / tpc;
+    while (true) {
+      if (threadIdx.x == 0) s_unit = atomicAdd(B.ctr + wf_ctr_wltl(d, l), 1u);
+      __syncthreads();
+      const unsigned u = s_unit;
+      if (u >= units) break;  // CTA-uniform
+      const unsigned k = s_lo + u * tpc + slot;
+      const bool valid_chunk = k < s_hi;
+      const int li = valid_chunk ? lt_list_of(s_chunk_end, nl, k) : l * kLtSub;
+      RT_CHECK(li / kLtSub == l, 404);
+      const unsigned c = k - (li > 0 ? s_chunk_end[li - 1] : 0u);
+      const unsigned cnt = valid_chunk ? B.ctr[wf_ctr_lt(d, 0, 0) + li] : 0u;
+      const unsigned oa = 64u * c + (unsigned)lane, ob = oa + 32u;
+      const bool va_ = oa < cnt, vb_ = ob < cnt;
+      const unsigned ga = (unsigned)li * B.lt_cap + oa, gb = ga + 32u;
+      LtRay Ra, Rb;
+      lt_setup(P, S, B, ga, va_, l, Ra);
+      lt_setup(P, S, B, gb, vb_, l, Rb);
+      lt_scan<kSrc, true>(P, s_pairs, nullptr, reinterpret_cast<const float2*>(s_pairs + 2 * P.n_pairs_pad), pb, pe, Ra,
+                          Rb, xa, xb);
+      s_nc[warp][lane] = Ra.nc;
+      s_nc[warp][lane + 32] = Rb.nc;
+      s_rob[warp][lane] = Ra.rob;
+      s_rob[warp][lane + 32] = Rb.rob;
+      __syncthreads();
+      if (part == 0) {
+        int nco, robo;
+        if (va_) {
+          split_merge_shadow(parts, &s_nc[warp][lane], &s_rob[warp][lane], 64, xa, xs, B.lt_cand + (size_t)ga * kCandMax,
+                             nco, robo);
+          B.lt_res[ga] = make_int2(robo, nco);
+        }
+        if (vb_) {
+          split_merge_shadow(parts, &s_nc[warp][lane + 32], &s_rob[warp][lane + 32], 64, xb, xs,
+                             B.lt_cand + (size_t)gb * kCandMax, nco, robo);
+          B.lt_res[gb] = make_int2(robo, nco);
+        }
+      }
+      __syncthreads();  // s_unit / s_nc / s_rob / scratch rows are rewritten by the next unit
+    }
+    __syncthreads();  // every warp is done with light l's table (and has read s_phase)
+    if (threadIdx.x == 0) s_phase ^= 1u;
+  }
+}
+
+template <int kSrc, bool kPerLight>
 __global__ void __launch_bounds__(256, 2)  // two rays per thread plus the merge: no spills at 2 CTAs/SM
 wf_isect_lt_split(const DevParams P, const DevScene S, WfBuffers B, int d) {
-  wf_isect_lt_split_body<kSrc>(P, S, B, d);
+  if constexpr (kPerLight) wf_isect_lt_split_body<kSrc>(P, S, B, d);
+  else wf_isect_lt_split_cols<kSrc>(P, S, B, d);
 }
 
 // FP64 nearest sphere among the candidate list (index order, strict <), or a full scan when

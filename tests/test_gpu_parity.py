@@ -182,6 +182,20 @@ def test_shared_origin_edge_cases(oracle_lib, variant, case):
     _check(oracle_lib, _shared_origin_scene(case), label=f"shared-origin {case}/{variant}", variant=variant)
 
 
+@pytest.mark.parametrize("split", [-1, 2, 8])
+def test_light_origin_tables_beyond_64k(oracle_lib, split):
+    """16 point lights x 1100 spheres: the lights' -h columns (70 KB) no longer fit the short-list
+    scan's staging, which then works light by light like the long-list scan; forced splits (2, 8
+    parts) run that path on every list. Full-frame parity with exact counts."""
+    from paper_1504_03151_b200 import rt
+    sc = scenegen.random_tiny(77, n_spheres=1100, n_planes=1, n_lights=16, width=20, height=12, max_depth=3, spp=2)
+    rt.set_scan_split(split)
+    try:
+        _check(oracle_lib, sc, label=f"16 lights x 1100 spheres, split {split}", variant="wavefront")
+    finally:
+        rt.set_scan_split(-1)
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_tinted_glass_c2_shaped(oracle_lib, variant):
     """C2-sized frame of a scene with many coloured-glass spheres (every third material glass)."""
