@@ -6,7 +6,8 @@ CUDA-graph capture and replays run too (VERDICT r1 "race and sync-ch
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
 
 Cases: C2 (512x256, wavefront, concurrency + 2-slot pipelining + graphs; in-order; megakernel),
-C4 (240x135, 4 spp, the light-origin shadow scans and split scans, 1-4 pipeline slots), an
+C4 (240x135, 4 spp, the light-origin shadow scans and split scans, 1-4 pipeline slots), 16 lights x
+1100 spheres (light-origin scans light by light, forced splits), an
 interleaved sphere/plane scene with coloured glass, progressive passes with the global integrator
 and area lights, shards of world 3 + assembly, and the tone map. Tool only.
 """
@@ -48,6 +49,12 @@ def main():
     for split in (2, 8):
         rt.set_scan_split(split)
         frames(c4, 2)
+    rt.set_scan_split(-1)
+    many = scenegen.random_tiny(77, n_spheres=1100, n_planes=1, n_lights=16, width=40, height=24, max_depth=3, spp=2)
+    rt.load_scene(many)  # light-origin columns beyond 64 KB: the short-list scan works light by light
+    for split in (-1, 2, 8):
+        rt.set_scan_split(split)
+        frames(many, 2)
     rt.set_scan_split(-1)
     tiny = scenegen.random_tiny(20, n_spheres=8, n_planes=2, n_lights=3, width=33, height=17, max_depth=5, spp=2,
                                 glass_tint=True, interleave=True)
