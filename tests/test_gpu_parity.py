@@ -182,6 +182,14 @@ def test_shared_origin_edge_cases(oracle_lib, variant, case):
     _check(oracle_lib, _shared_origin_scene(case), label=f"shared-origin {case}/{variant}", variant=variant)
 
 
+@pytest.mark.parametrize("spp", [255, 256, 257, 300])
+def test_sub_pixel_offsets_table_and_computed(oracle_lib, spp):
+    """spp <= 256 reads the sub-pixel offsets from the constant table, beyond that they are
+    computed per sample (the same IEEE values): both against the oracle."""
+    sc = scenegen.random_tiny(91, n_spheres=6, n_planes=1, n_lights=2, width=3, height=2, max_depth=2, spp=spp)
+    _check(oracle_lib, sc, label=f"spp {spp}", variant="wavefront")
+
+
 @pytest.mark.parametrize("split", [-1, 2, 8])
 def test_light_origin_tables_beyond_64k(oracle_lib, split):
     """16 point lights x 1100 spheres: the lights' -h columns (70 KB) no longer fit the short-list
