@@ -1382,17 +1382,14 @@ __device__ __forceinline__ void shadow_counts(const DevParams& P, const DevScene
 }
 
 // ---- a4 + a6: nearest hit, emission/ambient, shadow entries, continuation -------------------
-// wf_accumulate: 40 registers (32 B spilled), 6 CTAs per SM = the logic kernels' grid of 6 CTAs
+// wf_accumulate: 40 registers (160 B spilled: the rare FP64 decisions), 6 CTAs per SM = the logic kernels' grid of 6 CTAs
 // per SM in one wave (C4 in order: 4 CTAs / 64 registers 0.550 ms, 5 / 48 (1.2 waves) 0.589,
 // 6 / 40 0.514, 8 / 32 (52 B spilled) 0.555)
 constexpr int kLogicMinBlocks = 6;
 constexpr int kShadeMinBlocks = 3;  // wf_shade: 80 registers, no spills (64: ~190 B spilled, 10 % slower)
-#ifndef RT_RES_WARPS
-#define RT_RES_WARPS 4
-#endif
 // warps that reserve light-origin list slots together (C4 frame: 8 -> 5.842, 4 -> 5.832,
 // 2 -> 5.876, 1 -> 5.907 ms: smaller groups wait less, but their list ranges are less coherent)
-constexpr int kResWarps = RT_RES_WARPS;
+constexpr int kResWarps = 4;
 static_assert(8 % kResWarps == 0, "groups of a 256-thread CTA");
 // barrier of the n threads of named barrier `id` (a group of whole warps)
 __device__ __forceinline__ void group_sync(int id, int n) {
