@@ -475,7 +475,7 @@ def run_b200(args):
                 prof = _load_profile(f"{args.config}:{k}")
                 if prof:  # the committed ncu capture of this kernel class (one launch, cold, serialised)
                     v["ncu"] = {kk: prof.get(kk) for kk in ("fma_pipe_active_pct", "issue_active_pct",
-                                                             "dram_bytes_per_launch", "source")}
+                                                             "warp_efficiency_pct", "dram_bytes_per_launch", "source")}
                 if v["bound"] == "alu":
                     v["achieved"] = 2 * v["fma_per_test"] * v["tests"] / (v["ms"] * 1e-3) / 1e12
                     v["achieved_counted"] = FLOP_SPHERE * v["tests"] / (v["ms"] * 1e-3) / 1e12

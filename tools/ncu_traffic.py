@@ -37,6 +37,9 @@ for key, pat in classes:
                                    "duration_ms_ncu": val(r, "gpu__time_duration.sum"),
                                    "fma_pipe_active_pct": val(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                                    "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                   # active lanes per executed warp instruction / 32
+                                   "warp_efficiency_pct": 100.0 / 32.0 * val(
+                                       r, "smsp__thread_inst_executed_per_inst_executed.ratio"),
                                    "source": note}
             break
 print(json.dumps(out, indent=1))
