@@ -355,6 +355,23 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
+    per_rank = None
+    if world > 1:  # every rank's step time and its last shard render (imbalance)
+        # this rank's shard render alone, once more after the timed region (rank 0's statistics
+        # above are the assembly's, which times no render)
+        probe = torch.empty(rt.shard_layout(W, H, world)[1], dtype=torch.uint8, device=dev)
+        rt.render_shard(W, H, D, S, rank, world, probe)
+        shard_ms = float(rt.stats()["last_render_ms"])
+        del probe
+        cdev = dev if backend == "nccl" else torch.device("cpu")
+        mine = torch.tensor([my_total / args.steps, shard_ms], dtype=torch.float64, device=cdev)
+        allt = torch.empty(2 * world, dtype=torch.float64, device=cdev)
+        dist.all_gather_into_tensor(allt, mine)
+        rows = allt.view(world, 2).tolist()
+        per_rank = {"step_ms": [round(r[0], 4) for r in rows], "shard_render_ms": [round(r[1], 4) for r in rows],
+                    "note": "step = shard render + the frame's collective (CUDA events, mean over the timed "
+                            "steps); shard_render = the library's own events around one more render of this "
+                            "rank's shard after the timed region"}
 
     # per-kernel times for the roofline: the same frames with every wavefront launch in order on
     # one stream (the timed frames overlap a depth's shadow scan with the next closest-hit scan,
@@ -528,6 +545,8 @@ def run_b200(args):
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
         }
+        if per_rank:
+            line["per_rank"] = per_rank
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args.config, target_core_s=args.cpu_seconds)
         print(json.dumps(line), flush=True)
