@@ -24,13 +24,14 @@ def test_bench_two_ranks_share_one_gpu():
     env = dict(os.environ, B200RT_DIST_BACKEND="gloo", B200RT_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--config", "C2", "--steps",
-           "3", "--warmup", "3", "--no-cpu-baseline", "--no-fp32-peak"]
+           "3", "--warmup", "1", "--no-cpu-baseline", "--no-fp32-peak"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
+    assert d["warmup"] == 3  # at least 3 warm-up steps run (and are reported) whatever --warmup says
     assert d["config"]["workload"] == "C2" and d["config"]["parallelism"] == "tiles2"
     pr = d["per_rank"]
     assert len(pr["step_ms"]) == 2 and len(pr["shard_render_ms"]) == 2
