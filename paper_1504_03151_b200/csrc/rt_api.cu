@@ -3,6 +3,7 @@
 // Every computational step of the path runs in the kernels of rt_kernels.cu; this file only
 // validates, packs and launches.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -18,6 +19,15 @@
 namespace {
 
 thread_local std::string g_err;
+
+// an NVTX range around each public call (named in ncu --nvtx / nsys timelines; no cost without
+// a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -707,6 +717,7 @@ int rt_set_integrator(int32_t integrator, int32_t area_lights) {
 
 int rt_render_passes(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin, int32_t n_passes,
                      double* accum_rgb, float* out_rgba) {
+  NvtxRange nvtx_range("rt_render_passes");
   g_err.clear();
   if (!accum_rgb) return fail(RT_ERR_INVALID_ARG, "accum_rgb is NULL");
   return render_common(width, height, max_depth, n_passes, out_rgba, nullptr, nullptr, accum_rgb, pass_begin);
@@ -714,6 +725,7 @@ int rt_render_passes(int32_t width, int32_t height, int32_t max_depth, int64_t p
 
 int rt_render_passes_debug(int32_t width, int32_t height, int32_t max_depth, int64_t pass_begin, int32_t n_passes,
                            double* accum_rgb, float* out_rgba, int32_t* hit_ids, int32_t* bounces) {
+  NvtxRange nvtx_range("rt_render_passes_debug");
   g_err.clear();
   if (!accum_rgb) return fail(RT_ERR_INVALID_ARG, "accum_rgb is NULL");
   if (!out_rgba || !hit_ids || !bounces) return fail(RT_ERR_INVALID_ARG, "out_rgba/hit_ids/bounces must not be NULL");
@@ -791,6 +803,7 @@ int rt_set_seed(uint64_t seed) {
 
 int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_material* mats, int32_t n_mats,
                     const rt_light* lights, int32_t n_lights, const rt_env* env) {
+  NvtxRange nvtx_range("rt_scene_upload");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
@@ -981,6 +994,7 @@ int rt_scene_upload(const rt_primitive* prims, int32_t n_prims, const rt_materia
 }
 
 int rt_camera_set(const float eye[3], const float look_at[3], const float up[3], float vfov_deg) {
+  NvtxRange nvtx_range("rt_camera_set");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
@@ -1007,12 +1021,14 @@ int rt_camera_set(const float eye[3], const float look_at[3], const float up[3],
 }
 
 int rt_render(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba) {
+  NvtxRange nvtx_range("rt_render");
   g_err.clear();
   return render_common(width, height, max_depth, spp, out_rgba, nullptr, nullptr);
 }
 
 int rt_render_debug(int32_t width, int32_t height, int32_t max_depth, int32_t spp, float* out_rgba,
                     int32_t* hit_ids, int32_t* bounces) {
+  NvtxRange nvtx_range("rt_render_debug");
   g_err.clear();
   if (!hit_ids || !bounces) return fail(RT_ERR_INVALID_ARG, "hit_ids/bounces must not be NULL");
   return render_common(width, height, max_depth, spp, out_rgba, hit_ids, bounces);
@@ -1041,6 +1057,7 @@ int rt_shard_layout(int32_t width, int32_t height, int32_t world, int32_t* tiles
 
 int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank, int32_t world,
                     float* slab_dev) {
+  NvtxRange nvtx_range("rt_render_shard");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
@@ -1068,6 +1085,7 @@ int rt_render_shard(int32_t width, int32_t height, int32_t max_depth, int32_t sp
 
 int rt_render_shard_direct(int32_t width, int32_t height, int32_t max_depth, int32_t spp, int32_t rank,
                            int32_t world, float* frame_dev, uint64_t* records_dev) {
+  NvtxRange nvtx_range("rt_render_shard_direct");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
@@ -1150,6 +1168,7 @@ int rt_ipc_free(void* dev_ptr) {
 }
 
 int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, int32_t world, float* out_rgba_dev) {
+  NvtxRange nvtx_range("rt_assemble_tiles");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
@@ -1166,6 +1185,7 @@ int rt_assemble_tiles(const float* gathered_dev, int32_t width, int32_t height, 
 }
 
 int rt_tonemap_rgba8(const float* rgba, uint8_t* out, int64_t n_px, float exposure, float gamma) {
+  NvtxRange nvtx_range("rt_tonemap_rgba8");
   g_err.clear();
   int rc = ensure_device();
   if (rc) return rc;
